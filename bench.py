@@ -1,0 +1,460 @@
+#!/usr/bin/env python
+"""Benchmark of the restricted-domain dual iteration on B200 (BASELINE.json metric).
+
+Workload (default): C3 = BASELINE.json configs[3], the headline -- 4096x4096 Voronoi image
+(200 cells, sigma 0.15), Chan-Vese f (c1=.8, c2=.2), lambda=5, theta=.1, tau=.125,
+K=1000 iterations, delta in {0.1, 0.2, 0.4, inf} * max|f|.  One step = the whole hot path
+(fused fitting/band/init, tile compaction, K iterations, output u/mask, energy and gap) for
+every delta of the sweep.
+
+Metric: active Gpixel-iter/s = sum over the sweep of (pixels in active 32x32 tiles) x K,
+divided by the step time; higher is better.  Also reported: RD-pixel-iter/s, restricted vs
+full speedup per delta, the stencil kernel's roofline, the CPU oracle baseline, e2e through
+the C ABI with host buffers, clocks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 (torchrun): replicas only -- every rank solves the same workload on its own GPU, no
+data-path collective; value = all ranks' work / max-over-ranks time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+from paper_1807_11534_b200 import workloads as wl  # noqa: E402
+
+METRIC = "active Gpixel-iter/s at 4096^2 fp32 (restricted-domain dual iteration, C3 delta sweep)"
+UNIT = "Gpixel-iter/s"
+BYTES_PER_PX_ITER = 28  # read rho1, rho2, v, c (16 B) + write rho1, rho2, v (12 B)
+FLOPS_PER_PX_ITER = 26  # algorithmic FP32 operations of one iteration
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--kf", type=int, default=0, help="iterations per HBM round trip (0=lib default)")
+    ap.add_argument("--rows", type=int, default=0, help="rows per work item (0=lib default)")
+    ap.add_argument("--iters", type=int, default=0, help="override K (diagnostics only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------------
+# distributed plumbing (replicas)
+# ------------------------------------------------------------------------------------------
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as dist
+
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            backend = "nccl" if _cuda() else "gloo"
+            dist.init_process_group(backend)
+            self.pg = dist
+
+    def barrier(self):
+        if self.pg:
+            import torch
+
+            if _cuda():
+                self.pg.barrier(device_ids=[self.local])
+            else:
+                self.pg.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if _cuda() else "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.pg:
+            return x
+        import torch
+
+        t = torch.tensor([x], dtype=torch.float64, device="cuda" if _cuda() else "cpu")
+        self.pg.all_reduce(t, op=self.pg.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.pg:
+            self.pg.destroy_process_group()
+
+
+def _cuda():
+    import torch
+
+    return torch.cuda.is_available()
+
+
+# ------------------------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ------------------------------------------------------------------------------------------
+
+class Clocks:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle baseline / reference arm
+# ------------------------------------------------------------------------------------------
+
+def oracle_rate(cfg, z, P, deltas_rel, seconds, iters_hint=None):
+    """Time the oracle (as it stands) on the full image with a bounded iteration count.
+    Returns (px-iter/s counted like the GPU metric, cores, sample description)."""
+    import oracle
+
+    f = oracle.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    am = oracle.absmax(f)
+    lam = cfg.lambdas[0]
+    # calibrate: 1 iteration at delta=inf
+    t0 = time.perf_counter()
+    oracle.solve(f, np.inf, lam, np.float32(cfg.theta), cfg.tau, 1)
+    t1 = time.perf_counter() - t0
+    per_delta = max(1, int(seconds / max(t1, 1e-6) / len(deltas_rel)))
+    if iters_hint:
+        per_delta = iters_hint
+    work = 0
+    t0 = time.perf_counter()
+    for dr in deltas_rel:
+        delta = wl.band_delta(dr, am)
+        lab = oracle.labels(f, delta)
+        n_act = len(oracle.tiles(lab, 32, 32)) * 32 * 32
+        oracle.solve(f, delta, lam, np.float32(cfg.theta), cfg.tau, per_delta)
+        work += min(n_act, cfg.H * cfg.W) * per_delta
+    dt = time.perf_counter() - t0
+    sample = (f"oracle fp64 on the full {cfg.H}x{cfg.W} {cfg.name} image, {per_delta} "
+              f"iterations per delta for delta_rel in {list(deltas_rel)} (of K={cfg.iters})")
+    return work / dt, oracle.get_threads(), sample, dt
+
+
+def run_reference(args, dist):
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    if dist.rank != 0:
+        return
+    cfg = wl.CONFIGS[args.config]
+    z, P = wl.make_image(cfg)
+    import oracle
+
+    oracle.build()
+    # each step: a bounded sample (2 iterations per delta on the full image)
+    for _ in range(args.warmup):
+        oracle_rate(cfg, z, P, cfg.delta_rels, 0, iters_hint=1)
+    times, works = [], []
+    for _ in range(args.steps):
+        r, cores, sample, dt = oracle_rate(cfg, z, P, cfg.delta_rels, 0, iters_hint=2)
+        times.append(dt)
+        works.append(r * dt)
+    value = sum(works) / sum(times) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.desc}", "delta_rels": _js(cfg.delta_rels),
+                   "iters_per_step_per_delta": 2, "iters_of_config": cfg.iters},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def _js(xs):
+    return [("inf" if (isinstance(x, float) and math.isinf(x)) else x) for x in xs]
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+
+def run_ours(args, dist):
+    import torch
+
+    assert torch.cuda.is_available(), "bench.py --impl ours needs a CUDA device"
+    torch.cuda.set_device(dist.local)
+    from paper_1807_11534_b200 import rds
+
+    cfg = wl.CONFIGS[args.config]
+    K = args.iters or cfg.iters
+    lam = cfg.lambdas[0]
+    z, P = wl.make_image(cfg)
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
+    s = rds.Solver(cfg.H, cfg.W, stream=sp, k_fuse=args.kf, item_rows=args.rows, timing=True)
+    zt = torch.from_numpy(z).cuda()
+    Pt = torch.from_numpy(P).cuda() if P is not None else None
+    s.set_image(zt)
+    s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, Pt)
+    am = s.absmax()
+    deltas = [wl.band_delta(dr, am) for dr in cfg.delta_rels]
+
+    def step(collect=None):
+        for dr, d in zip(cfg.delta_rels, deltas):
+            s.solve(lam, cfg.theta, cfg.tau, d, K)
+            e = s.energy()  # S8, synchronises the stream
+            if collect is not None:
+                st = s.stats()
+                collect.append((dr, st, e))
+
+    # warm-up (also captures the K-loop graphs)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    # per-delta characterisation (untimed pass with per-solve event times)
+    info = []
+    step(info)
+    torch.cuda.synchronize()
+
+    clocks = Clocks(dist.local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    loop_ms = []
+    with torch.cuda.stream(stream):
+        ev0.record(stream)
+        for _ in range(args.steps):
+            for dr, d in zip(cfg.delta_rels, deltas):
+                s.solve(lam, cfg.theta, cfg.tau, d, K)
+                s.energy()
+                loop_ms.append((dr, s.stats()))
+        ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ck = clocks.stop()
+    t_ms = dist.max(ev0.elapsed_time(ev1))
+
+    # work accounting
+    act_px = {dr: st["n_active_tiles"] * 32 * 32 for dr, st, _ in info}
+    act_px = {dr: min(v, cfg.H * cfg.W) for dr, v in act_px.items()}  # ragged tiles clipped
+    rd_px = {dr: st["n_rd"] for dr, st, _ in info}
+    work_step = sum(act_px[dr] for dr in cfg.delta_rels) * K
+    rd_step = sum(rd_px[dr] for dr in cfg.delta_rels) * K
+    total_work = dist.sum(work_step * args.steps)
+    value = total_work / (t_ms * 1e-3) / 1e9
+    ms_per_step = t_ms / args.steps
+
+    # stencil roofline: the K-loop is only stencil launches; average per-launch duration
+    per = {}
+    for dr, st in loop_ms:
+        per.setdefault(dr, []).append(st)
+    per_delta = []
+    t_full = statistics.median(x["loop_ms"] for x in per[cfg.delta_rels[-1]]) \
+        if math.isinf(cfg.delta_rels[-1]) else None
+    launch_ms_all, bytes_all, flops_all = [], [], []
+    for dr, st, e in info:
+        lm = statistics.median(x["loop_ms"] for x in per[dr])
+        sm = statistics.median(x["setup_ms"] for x in per[dr])
+        n_items = st["n_active_items"]
+        item_px = n_items * st["item_rows"] * st["item_cols"]
+        launches = st["launches"]
+        launch_ms_all.append(lm / launches)
+        px = act_px[dr]
+        bytes_all.append(BYTES_PER_PX_ITER * px * K / launches)
+        flops_all.append(FLOPS_PER_PX_ITER * px * K / launches)
+        per_delta.append({
+            "delta_rel": "inf" if math.isinf(dr) else dr,
+            "loop_ms": lm, "setup_ms": sm,
+            "active_tile_frac": st["n_active_tiles"] / st["n_tiles"],
+            "rd_frac": st["n_rd"] / (cfg.H * cfg.W),
+            "active_item_frac": n_items / st["n_items"],
+            "tile_gpix_iter_s": px * K / (lm * 1e-3) / 1e9,
+            "rd_gpix_iter_s": st["n_rd"] * K / (lm * 1e-3) / 1e9,
+            "speedup_vs_full": (t_full / lm) if t_full else None,
+            "gap": e["gap"], "E_v": e["E_v"],
+        })
+    launch_ms = statistics.mean(launch_ms_all)
+    bytes_per_launch = statistics.mean(bytes_all)
+    achieved_gbs = bytes_per_launch / (launch_ms * 1e-3) / 1e9
+    peaks = _peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    clock_mhz = ck.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * clock_mhz * 1e6 / 1e12  # TFLOP/s at the observed SM clock
+    achieved_tf = statistics.mean(flops_all) / (launch_ms * 1e-3) / 1e12
+    st0 = info[0][1]
+    roofline = {
+        "bound": "hbm", "kernel": "k_stencil", "achieved": achieved_gbs, "peak": hbm_peak,
+        "unit": "GB/s", "frac": achieved_gbs / hbm_peak,
+        "traffic": _traffic_from_profile(),
+        "basis": (f"{BYTES_PER_PX_ITER} B per active pixel-iteration x (active px x "
+                  f"{st0['k_fuse']} fused iterations) per launch / mean launch time "
+                  f"{launch_ms:.4f} ms; peak = MEASURED_PEAKS.json hbm_gbs (measured copy)"),
+        "k_fuse": st0["k_fuse"],
+        "alu": {"achieved_tflops": achieved_tf, "peak_tflops": fp32_peak,
+                "frac": achieved_tf / fp32_peak,
+                "basis": f"{FLOPS_PER_PX_ITER} algorithmic FP32 ops per px-iter; peak = 148 SM x "
+                         f"128 FP32 lanes x 2 x {clock_mhz:.0f} MHz"},
+    }
+
+    launches_per_step = sum(st["launches"] + 4 + 2 for _, st, _ in info)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.desc}", "H": cfg.H, "W": cfg.W, "iters": K,
+                   "lambda": lam, "theta": cfg.theta, "tau": cfg.tau,
+                   "delta_rels": _js(cfg.delta_rels), "k_fuse": st0["k_fuse"],
+                   "item_rows": st0["item_rows"], "item_cols": st0["item_cols"],
+                   "l2": "no flush: per-iteration working set 448 MiB > 126 MB L2",
+                   "parallelism": f"replicas x{dist.world}"},
+        "rd_gpix_iter_s": dist.sum(rd_step * args.steps) / (t_ms * 1e-3) / 1e9,
+        "per_delta": per_delta,
+        "roofline": roofline,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": ck,
+    }
+    if not args.no_e2e:
+        line["e2e"] = e2e(args, s, cfg, z, P, deltas, K, lam, dist, work_step)
+    s.close()
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        r, cores, sample, _ = oracle_rate(cfg, z, P, cfg.delta_rels, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": r / 1e9, "unit": UNIT, "cores": cores,
+                                "kind": "oracle", "sample": sample}
+    if dist.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def e2e(args, s, cfg, z, P, deltas, K, lam, dist, work_step):
+    """Same metric through the C ABI with HOST buffers: each step copies z (and P) from
+    pinned host memory, solves every delta and reads back each mask and the energies."""
+    import torch
+
+    zh = torch.from_numpy(z).pin_memory()
+    Ph = torch.from_numpy(P).pin_memory() if P is not None else None
+    masks = [torch.empty((cfg.H, cfg.W), dtype=torch.uint8).pin_memory() for _ in deltas]
+    h2d = z.nbytes + (P.nbytes if P is not None else 0)
+    d2h = sum(m.numel() for m in masks) + 6 * 8 * len(deltas)
+
+    def one():
+        s.set_image(zh.numpy())
+        s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, Ph.numpy() if Ph is not None else None)
+        for d, m in zip(deltas, masks):
+            s.solve(lam, cfg.theta, cfg.tau, d, K)
+            s.mask(m.numpy())
+            s.energy()
+
+    one()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    torch.cuda.synchronize()
+    dt = dist.max(time.perf_counter() - t0)
+    value = dist.sum(work_step * args.steps) / dt / 1e9
+    return {"value": value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": 1e3 * dt / args.steps,
+            "path": "rds_set_image/rds_set_fitting (pinned host) -> rds_solve -> rds_get_mask "
+                    "(host) + rds_energy per delta"}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return {}
+
+
+def _traffic_from_profile():
+    path = os.path.join(ROOT, "profiles", "stencil_dram_bytes.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    args = parse()
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_ours(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

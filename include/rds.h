@@ -1,0 +1,178 @@
+/*
+ * rds.h -- C ABI of librds: the restricted-domain dual iteration of arXiv 1807.11534
+ * ("A Restricted-Domain Dual Formulation for Two-Phase Image Segmentation") on one B200
+ * (sm_100a).  Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ *
+ * The method (PAPER.md line numbers, section / equation):
+ *   fitting term   f = (z - c1)^2 - (z - c2)^2 + gamma P          PAPER.md:31-37 (Eq. 2, 3)
+ *   partition      Fg = {f <= -delta}, Bg = {f >= delta}, RD = rest  PAPER.md:74-83 (§3)
+ *                  (RD <=> |f| < delta; reading R-C7)
+ *   init           u0 = v0 = H(-f) (H(0) = 1), rho0 = 0
+ *   rho-step (RD)  rho <- (rho + tau grad w) / (1 + tau |grad w|),
+ *                  w = div rho - v/theta; rho = 0 on Fg u Bg       PAPER.md:129-141 (Eq. 8)
+ *   u-step         u = v - theta div rho on RD; 1 on Fg; 0 on Bg   PAPER.md:119-128 (Eq. 7)
+ *   v-step         v = min(max(u - theta lambda f, 0), 1) on RD;
+ *                  1 on Fg; 0 on Bg                                 PAPER.md:146-155 (Eq. 9)
+ *   threshold      mask = [u > 0.5]
+ *   Discrete grad = forward differences with zero last row/col, div = -grad^T
+ *   (PAPER.md:70 defers to Chambolle 2004; reading R-C6).
+ *
+ * Layout conventions: every image argument is H x W, row-major (row i, column j), densely
+ * packed (row stride W elements).  `on_device` = 1 means the pointer is CUDA device memory
+ * (e.g. a torch CUDA tensor's data_ptr), 0 means host memory.  The library copies inputs into
+ * its own storage; the caller keeps ownership of every pointer it passes and may reuse it as
+ * soon as the call returns (host copies are synchronous; device copies are stream-ordered on
+ * the handle's stream, so a device buffer must stay valid until that stream reaches the copy).
+ *
+ * Errors: every call returns an int, RDS_OK (0) or a negative code; no call throws across the
+ * ABI.  rds_last_error() gives a message for the last failure on that handle.  A handle is not
+ * thread-safe; distinct handles are independent.  Results are deterministic: identical inputs
+ * produce bit-identical outputs (no atomics on any output path).
+ */
+#ifndef RDS_H_
+#define RDS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RDS_OK 0
+#define RDS_EINVAL (-1)  /* invalid argument (NULL, size, parameter range, non-finite data) */
+#define RDS_ESTATE (-2)  /* call out of order (e.g. solve before image/fitting, get before solve) */
+#define RDS_ECUDA (-3)   /* a CUDA runtime call or kernel launch failed */
+#define RDS_ENOMEM (-4)  /* device allocation failed */
+
+/* Pixel labels: 0 = Bg (pinned u = v = 0), 1 = Fg (pinned u = v = 1),
+ * 2 = RD (iterated). */
+#define RDS_LABEL_BG 0
+#define RDS_LABEL_FG 1
+#define RDS_LABEL_RD 2
+
+/* Active-tile granularity exported by rds_get_active_tiles (see rds_tile_shape). */
+#define RDS_TILE_H 32
+#define RDS_TILE_W 32
+
+typedef struct rds_handle rds_t;
+
+/* Energies of the current state, all double (rds_energy).
+ *  E_v   = TV(v) + lambda sum f v            (Eq. 4, at w = v)
+ *  E_u   = TV(c(u)) + lambda sum f c(u),     c(u) = min(max(u,0),1)
+ *  D_p   = sum min(0, lambda f + div rho)    (Lagrangian dual of Eq. 4 over u in [0,1])
+ *  gap   = E_v - D_p  (>= 0 by weak duality whenever |rho| <= 1)
+ *  TV_v, fit_v = lambda sum f v : the two parts of E_v. */
+typedef struct {
+    double E_v, E_u, D_p, gap, TV_v, fit_v;
+} rds_energy_t;
+
+/* Statistics of the last rds_solve. Times are CUDA-event times on the handle's stream and are
+ * only filled when RDS_OPT_TIMING is on (else -1). */
+typedef struct {
+    int64_t H, W;
+    int64_t n_rd;            /* pixels in RD (label 2) */
+    int64_t n_tiles;         /* 32x32 tiles covering the image */
+    int64_t n_active_tiles;  /* tiles containing an RD pixel */
+    int64_t n_items;         /* stencil work items (strip x row-chunk) covering the image */
+    int64_t n_active_items;  /* items overlapping an active tile (launched work) */
+    int32_t iters;           /* K of the last solve */
+    int32_t k_fuse;          /* iterations fused per HBM round trip */
+    int32_t launches;        /* stencil launches in the K-loop */
+    int32_t item_rows;       /* output rows per work item */
+    int32_t item_cols;       /* output columns per work item */
+    int32_t pad_;
+    float setup_ms;          /* fused fitting/band/init + compaction */
+    float loop_ms;           /* the K-loop (all stencil launches) */
+} rds_stats_t;
+
+/* Options (rds_set_option). */
+#define RDS_OPT_KFUSE 1      /* iterations per HBM round trip; 0 = library default; allowed
+                                values are listed by rds_kfuse_supported */
+#define RDS_OPT_ITEM_ROWS 2  /* output rows per stencil work item; 0 = default */
+#define RDS_OPT_TIMING 3     /* 1 = record setup/loop CUDA-event times in rds_stats_t */
+#define RDS_OPT_SKIP 4       /* 1 (default) = launch only items overlapping active tiles;
+                                0 = process every item (restriction without tile skipping) */
+#define RDS_OPT_GRAPH 5      /* 1 (default) = replay the K-loop as a CUDA graph */
+
+/* Create a solver for an H x W image; allocates all device state on the current device.
+ * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */
+int rds_create(int64_t H, int64_t W, rds_t **out);
+
+/* Free everything; NULL is a no-op.  Synchronises the handle's stream first. */
+int rds_destroy(rds_t *h);
+
+/* All later work is ordered on `stream` (a cudaStream_t, e.g.
+ * torch.cuda.current_stream().cuda_stream).  NULL selects the handle's private stream. */
+int rds_set_stream(rds_t *h, void *stream);
+
+/* Set an option (RDS_OPT_*). RDS_EINVAL on unknown key or unsupported value. */
+int rds_set_option(rds_t *h, int key, int64_t value);
+
+/* Copy the image z (H x W float32).  Synchronous; checks finiteness.
+ * Errors: RDS_EINVAL on NULL or any non-finite value. */
+int rds_set_image(rds_t *h, const float *z, int on_device);
+
+/* Fitting constants and the selection map P (H x W float32; may be NULL iff
+ * gamma == 0).  Errors: RDS_EINVAL if c1 == c2, gamma < 0 or not finite, P == NULL with
+ * gamma > 0, or P non-finite. */
+int rds_set_fitting(rds_t *h, float c1, float c2, float gamma, const float *P, int on_device);
+
+/* Optional warm start for the NEXT rds_solve only: v, rho1, rho2 (H x W float32 each).  Used
+ * on RD pixels; pinned pixels still start at u0 / 0; rho1 on the last row and rho2 on the last
+ * column are zeroed (they are identically 0 under the iteration).  Errors: RDS_EINVAL on NULL. */
+int rds_set_state(rds_t *h, const float *v, const float *rho1, const float *rho2,
+                  int on_device);
+
+/* Exact float32 max |f| of the current image/fitting (for delta = delta_rel * max|f|).
+ * Errors: RDS_ESTATE if image or fitting unset; RDS_EINVAL on NULL. Synchronous. */
+int rds_fitting_absmax(rds_t *h, float *out);
+
+/* Run the whole method: fused fitting + band test + init, active-tile compaction, `iters`
+ * outer iterations (rho-step, u-step, v-step) over the active work items, and the output
+ * u = v_{K-1} - theta div rho_K on RD (u0 elsewhere) with its mask.  delta is the absolute
+ * band threshold (INFINITY = unrestricted, 0 = pure thresholding); iters = 0 yields u = H(-f).
+ * Asynchronous on the handle's stream.
+ * Errors: RDS_EINVAL if lambda <= 0, theta <= 0, tau not in (0, 1/8], delta < 0 or NaN,
+ * iters < 0, or any parameter non-finite (delta may be +inf); RDS_ESTATE if image or fitting
+ * unset. */
+int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32_t iters);
+
+/* Getters: copy H x W results into `out` (host copies synchronise the handle's stream).
+ * Errors: RDS_ESTATE before the first solve; RDS_EINVAL on NULL. */
+int rds_get_u(rds_t *h, float *out, int on_device);          /* u_K */
+int rds_get_mask(rds_t *h, uint8_t *out, int on_device);     /* [u_K > 0.5] as 0/1 */
+int rds_get_v(rds_t *h, float *out, int on_device);          /* v_K */
+int rds_get_p(rds_t *h, float *rho1, float *rho2, int on_device); /* rho_K */
+int rds_get_fitting(rds_t *h, float *out, int on_device);    /* f of the last solve */
+int rds_get_labels(rds_t *h, uint8_t *out, int on_device);   /* RDS_LABEL_* per pixel */
+
+/* Ascending list of active tile indices t = ti * ceil(W/tw) + tj (a tile is active iff it
+ * contains an RD pixel).  *count always receives the number of active tiles; RDS_EINVAL if
+ * cap < count (nothing written then) or count == NULL.  Synchronous. */
+int rds_get_active_tiles(rds_t *h, int32_t *out, int64_t cap, int64_t *count);
+
+/* Tile shape used by rds_get_active_tiles (RDS_TILE_H x RDS_TILE_W). */
+int rds_tile_shape(int *th, int *tw);
+
+/* Energies of the current (v, rho, u) with the lambda of the last solve (see rds_energy_t).
+ * Deterministic two-pass reduction; synchronous.  Errors: RDS_ESTATE before a solve. */
+int rds_energy(rds_t *h, rds_energy_t *out);
+
+/* Statistics of the last solve (synchronises the stream). */
+int rds_get_stats(rds_t *h, rds_stats_t *out);
+
+/* Supported RDS_OPT_KFUSE values: writes up to cap values into out, returns how many exist. */
+int rds_kfuse_supported(int32_t *out, int cap);
+
+/* Message for the last failure on h ("" if none); h == NULL gives the last global failure
+ * (e.g. from rds_create). Valid until the next call on that handle. */
+const char *rds_last_error(rds_t *h);
+
+/* Library version string. */
+const char *rds_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RDS_H_ */

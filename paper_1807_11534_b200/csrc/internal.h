@@ -1,0 +1,91 @@
+// internal.h -- shared declarations of the librds CUDA product path (not part of the ABI).
+//
+// Device-memory layout ("padded planes"): every per-pixel array is a plane of
+// (H + 2*PAD_R) rows x pitch elements; pixel (i, j) lives at element
+//     origin + i * pitch + j,   origin = PAD_R * pitch + PAD_C.
+// The frame outside the image holds *pinned background* values (rho = 0, v = 0,
+// c = +inf) that the iteration reproduces exactly, so the stencil needs no bounds tests on
+// loads: only the two Neumann conditions (grad_1 = 0 on row H-1, grad_2 = 0 on column W-1)
+// are explicit.  pitch is a multiple of 32 elements (128 B rows for float planes).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rds {
+
+constexpr int PAD_R = 16;      // >= KF + 1 rows of halo above / below (KF <= 15)
+constexpr int PAD_C = 32;      // left frame, keeps column 0 16-byte aligned
+constexpr int PAD_C_RIGHT = 128;  // a warp strip may read up to 127 columns past its start
+constexpr int TILE_H = 32, TILE_W = 32;
+constexpr int STENCIL_WARPS = 4;  // warps per CTA of the stencil kernel (one item per warp)
+
+// Column geometry of a stencil warp for KF fused iterations: the warp loads 128 columns
+// (float4 per lane); the valid output columns are [LH, LH + WV) of those.  The dependency
+// cone of KF iterations reaches KF+1 columns to the left and KF to the right
+// (DESIGN.md §5), rounded up to whole float4 lanes.
+__host__ __device__ constexpr int lh_of(int kf) { return 4 * ((kf + 1 + 3) / 4); }
+__host__ __device__ constexpr int rh_of(int kf) { return 4 * ((kf + 3) / 4); }
+__host__ __device__ constexpr int wv_of(int kf) { return 128 - lh_of(kf) - rh_of(kf); }
+
+struct StencilArgs {
+    const float *p1_in, *p2_in, *v_in;   // plane origins (pixel (0,0))
+    const float *c;                      // theta*lambda*f on RD, -inf on Fg, +inf on Bg/frame
+    float *p1_out, *p2_out, *v_out;
+    float *u_out;                        // only written when WRITE_U
+    uint8_t *mask_out;                   // only written when WRITE_U
+    const int32_t *items;                // active items, ascending (chunk-major)
+    const int32_t *n_items;              // device count
+    int64_t pitch;
+    int H, W;
+    int rows;                            // output rows per item
+    int n_strips;
+    float tau, theta, inv_theta;
+};
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_fill_frame(float *plane, int64_t n, float value, cudaStream_t s);
+cudaError_t launch_check_finite(const float *a, int64_t pitch, int H, int W, int *flag,
+                                cudaStream_t s);
+cudaError_t launch_absmax(const float *z, const float *P, int64_t pitch, int H, int W,
+                          float c1, float c2, float gamma, unsigned *out_bits,
+                          cudaStream_t s);
+
+struct SetupArgs {
+    const float *z, *P;                 // P may be null when gamma == 0
+    const float *wv, *wp1, *wp2;        // warm start (null = none)
+    float *f, *c, *u;
+    float *v0, *v1, *p10, *p11, *p20, *p21;
+    uint8_t *lab, *mask;
+    int32_t *tile_rd;                   // RD pixels per 32x32 tile
+    int64_t pitch;
+    int H, W;
+    float c1, c2, gamma, delta, theta_lambda;
+};
+cudaError_t launch_setup(const SetupArgs &a, cudaStream_t s);
+
+// Deterministic ballot/prefix-sum compaction of flags[i] != 0 into an ascending index list.
+// counts[0] = number of nonzero flags; if sum_out != null also the int64 sum of the values.
+cudaError_t launch_compact(const int32_t *flags, int n, int32_t *list, int32_t *count,
+                           long long *sum_out, cudaStream_t s);
+cudaError_t launch_item_flags(const int32_t *tile_rd, int H, int W, int rows, int wv,
+                              int n_strips, int n_chunks, int skip, int32_t *item_flag,
+                              cudaStream_t s);
+
+cudaError_t launch_stencil(int kf, int stages, bool write_u, const StencilArgs &a,
+                           int grid, cudaStream_t s);
+bool kf_supported(int kf);
+int kf_list(int32_t *out, int cap);
+
+struct EnergyArgs {
+    const float *f, *u, *v, *p1, *p2;
+    int64_t pitch;
+    int H, W;
+    double *partials;   // [n_blocks * 5]
+    double *out;        // [5]: TV_v, sum f v, TV_cu, sum f cu, sum min(0, lambda f + div p)
+    float lambda;
+};
+constexpr int ENERGY_BLOCKS = 592;  // 4 x 148 SMs
+cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s);
+
+}  // namespace rds

@@ -1,0 +1,89 @@
+// k_energy.cu -- K5: energies and primal-dual gap of the current state (sm_100a).
+//
+//   TV(w)  = sum |grad w| (forward differences, zero on row H-1 / column W-1)
+//   fit(w) = sum f w
+//   D(rho) = sum min(0, lambda f + div rho)   (Lagrangian dual of Eq. 4 over u in [0,1])
+// for w = v and w = clamp(u, 0, 1).  Per-pixel terms in float32, per-thread/warp/block sums
+// in float64; the grid has a fixed size and a fixed pixel -> thread assignment and the two
+// passes combine partials in a fixed order, so the result is bit-reproducible.
+#include "internal.h"
+
+namespace rds {
+
+constexpr int NE = 5;
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+__device__ __forceinline__ float clamp01(float x) { return fminf(fmaxf(x, 0.0f), 1.0f); }
+
+__global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
+    const int64_t n = (int64_t)a.H * a.W;
+    const int64_t pitch = a.pitch;
+    double acc[NE] = {0, 0, 0, 0, 0};
+    for (int64_t k = blockIdx.x * 256 + threadIdx.x; k < n; k += (int64_t)gridDim.x * 256) {
+        const int i = (int)(k / a.W), j = (int)(k - (int64_t)i * a.W);
+        const int64_t o = (int64_t)i * pitch + j;
+        const bool down = i < a.H - 1, right = j < a.W - 1;
+        const float v = a.v[o];
+        const float gv1 = down ? a.v[o + pitch] - v : 0.0f;
+        const float gv2 = right ? a.v[o + 1] - v : 0.0f;
+        const float cu = clamp01(a.u[o]);
+        const float gu1 = down ? clamp01(a.u[o + pitch]) - cu : 0.0f;
+        const float gu2 = right ? clamp01(a.u[o + 1]) - cu : 0.0f;
+        const float f = a.f[o];
+        // rho1 on row H-1 and rho2 on column W-1 are identically 0; the frame holds 0
+        const float dv = a.p1[o] - a.p1[o - pitch] + a.p2[o] - a.p2[o - 1];
+        const float t = a.lambda * f + dv;
+        acc[0] += (double)sqrtf(gv1 * gv1 + gv2 * gv2);
+        acc[1] += (double)f * (double)v;
+        acc[2] += (double)sqrtf(gu1 * gu1 + gu2 * gu2);
+        acc[3] += (double)f * (double)cu;
+        acc[4] += (double)fminf(t, 0.0f);
+    }
+    __shared__ double sh[8][NE];
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+        const double s = warp_sum(acc[q]);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5][q] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < NE) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += sh[w][threadIdx.x];
+        a.partials[blockIdx.x * NE + threadIdx.x] = s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_energy_final(const double *partials, int nb,
+                                                      double *out) {
+    __shared__ double sh[8][NE];
+    double acc[NE] = {0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < nb; b += 256)
+#pragma unroll
+        for (int q = 0; q < NE; ++q) acc[q] += partials[b * NE + q];
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+        const double s = warp_sum(acc[q]);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5][q] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < NE) {
+        double s = 0.0;
+        for (int w = 0; w < 8; ++w) s += sh[w][threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+}
+
+cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s) {
+    k_energy_partial<<<ENERGY_BLOCKS, 256, 0, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_energy_final<<<1, 256, 0, s>>>(a.partials, ENERGY_BLOCKS, a.out);
+    return cudaGetLastError();
+}
+
+}  // namespace rds

@@ -1,0 +1,627 @@
+// rds_api.cu -- host side of librds: the C ABI declared in include/rds.h.
+//
+// Handles own all device state in "padded planes" (internal.h).  rds_solve enqueues, on the
+// handle's stream:  K1 fused fitting/band/init -> K2 tile compaction (+ RD count) -> item
+// flags -> K2 item compaction -> ceil(K/KF) launches of K3 (ping-pong buffers; the last one
+// also writes u and the mask), optionally replayed from a cached CUDA graph.  No host
+// synchronisation happens inside rds_solve.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "internal.h"
+#include "rds.h"
+
+using namespace rds;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+constexpr int kDefaultKF = 7;
+constexpr int kDefaultRows = 128;
+
+}  // namespace
+
+struct rds_handle {
+    int64_t H = 0, W = 0;
+    int64_t pitch = 0;     // elements per padded row (multiple of 32)
+    int64_t rows_alloc = 0;
+    int64_t plane = 0;     // elements per plane
+    int64_t origin = 0;    // element offset of pixel (0,0)
+
+    // float planes (base pointers)
+    float *z = nullptr, *P = nullptr, *f = nullptr, *c = nullptr, *u = nullptr;
+    float *p1[2] = {nullptr, nullptr}, *p2[2] = {nullptr, nullptr}, *v[2] = {nullptr, nullptr};
+    float *wv = nullptr, *wp1 = nullptr, *wp2 = nullptr;  // warm start (lazy)
+    uint8_t *lab = nullptr, *mask = nullptr;
+    // tiles / items
+    int n_tiles = 0;
+    int32_t *tile_rd = nullptr, *tile_list = nullptr;
+    int32_t *item_flag = nullptr, *item_list = nullptr;
+    int items_cap = 0;
+    int32_t *counts = nullptr;       // [0] active tiles, [1] active items
+    long long *n_rd_dev = nullptr;
+    unsigned *absmax_bits = nullptr;
+    int *flag = nullptr;
+    double *e_partials = nullptr, *e_out = nullptr;
+
+    cudaStream_t own_stream = nullptr, stream = nullptr;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+
+    bool have_image = false, have_fitting = false, solved = false, warm_pending = false;
+    bool image_ok = true, p_ok = true;
+    float c1 = 0, c2 = 0, gamma = 0;
+    float lambda = 0, theta = 0;
+    int cur = 0;  // ping-pong buffer holding the latest state
+
+    int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1;
+    rds_stats_t stats{};
+
+    // cached CUDA graph of the K-loop
+    cudaGraphExec_t graph = nullptr;
+    struct Key {
+        int kf, rows, iters, cur0, n_strips, n_chunks;
+        float tau, theta;
+        bool operator==(const Key &o) const { return memcmp(this, &o, sizeof(Key)) == 0; }
+    } gkey{};
+
+    std::string err;
+
+    float *at(float *base) const { return base + origin; }
+    uint8_t *at(uint8_t *base) const { return base + origin; }
+};
+
+static int fail(rds_t *h, int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (h) h->err = buf;
+    g_last_error = buf;
+    return code;
+}
+
+#define CK(h, call)                                                                       \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail((h), e_ == cudaErrorMemoryAllocation ? RDS_ENOMEM : RDS_ECUDA,    \
+                        "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, \
+                        __LINE__);                                                        \
+    } while (0)
+
+static void free_all(rds_t *h) {
+    float *fl[] = {h->z,  h->P,     h->f,     h->c,     h->u,   h->p1[0], h->p1[1],
+                   h->p2[0], h->p2[1], h->v[0], h->v[1], h->wv, h->wp1,   h->wp2};
+    for (float *p : fl)
+        if (p) cudaFree(p);
+    void *other[] = {h->lab,      h->mask,      h->tile_rd, h->tile_list,   h->item_flag,
+                     h->item_list, h->counts,   h->n_rd_dev, h->absmax_bits, h->flag,
+                     h->e_partials, h->e_out};
+    for (void *p : other)
+        if (p) cudaFree(p);
+    if (h->graph) cudaGraphExecDestroy(h->graph);
+    for (auto &e : h->ev)
+        if (e) cudaEventDestroy(e);
+    if (h->own_stream) cudaStreamDestroy(h->own_stream);
+}
+
+static cudaError_t alloc_plane(rds_t *h, float **p, float frame_value) {
+    cudaError_t e = cudaMalloc(p, sizeof(float) * h->plane);
+    if (e != cudaSuccess) return e;
+    if (frame_value == 0.0f) return cudaMemsetAsync(*p, 0, sizeof(float) * h->plane, h->stream);
+    return launch_fill_frame(*p, h->plane, frame_value, h->stream);
+}
+
+extern "C" {
+
+int rds_create(int64_t H, int64_t W, rds_t **out) {
+    if (!out) return fail(nullptr, RDS_EINVAL, "rds_create: out is NULL");
+    *out = nullptr;
+    if (H < 1 || W < 1) return fail(nullptr, RDS_EINVAL, "rds_create: H=%lld W=%lld must be >= 1",
+                                    (long long)H, (long long)W);
+    if (H * W > (int64_t(1) << 31) || H > (1 << 30) || W > (1 << 30))
+        return fail(nullptr, RDS_EINVAL, "rds_create: image too large (H*W > 2^31)");
+    rds_t *h = new (std::nothrow) rds_t();
+    if (!h) return fail(nullptr, RDS_ENOMEM, "rds_create: host allocation failed");
+    h->H = H;
+    h->W = W;
+    h->pitch = ((PAD_C + W + PAD_C_RIGHT) + 31) / 32 * 32;
+    h->rows_alloc = H + 2 * PAD_R;
+    h->plane = h->pitch * h->rows_alloc;
+    h->origin = PAD_R * h->pitch + PAD_C;
+    h->n_tiles = (int)(((H + TILE_H - 1) / TILE_H) * ((W + TILE_W - 1) / TILE_W));
+    cudaError_t e = cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        int rc = fail(nullptr, RDS_ECUDA, "rds_create: cudaStreamCreate: %s", cudaGetErrorString(e));
+        delete h;
+        return rc;
+    }
+    h->stream = h->own_stream;
+#define A(call)                                                                        \
+    do {                                                                               \
+        cudaError_t e_ = (call);                                                       \
+        if (e_ != cudaSuccess) {                                                       \
+            int rc_ = fail(nullptr, e_ == cudaErrorMemoryAllocation ? RDS_ENOMEM : RDS_ECUDA, \
+                           "rds_create: %s: %s", #call, cudaGetErrorString(e_));        \
+            free_all(h);                                                               \
+            delete h;                                                                  \
+            return rc_;                                                                \
+        }                                                                              \
+    } while (0)
+    A(alloc_plane(h, &h->z, 0.0f));
+    A(alloc_plane(h, &h->f, 0.0f));
+    A(alloc_plane(h, &h->c, INFINITY));
+    A(alloc_plane(h, &h->u, 0.0f));
+    for (int b = 0; b < 2; ++b) {
+        A(alloc_plane(h, &h->p1[b], 0.0f));
+        A(alloc_plane(h, &h->p2[b], 0.0f));
+        A(alloc_plane(h, &h->v[b], 0.0f));
+    }
+    A(cudaMalloc(&h->lab, h->plane));
+    A(cudaMemsetAsync(h->lab, 0, h->plane, h->stream));
+    A(cudaMalloc(&h->mask, h->plane));
+    A(cudaMemsetAsync(h->mask, 0, h->plane, h->stream));
+    A(cudaMalloc(&h->tile_rd, sizeof(int32_t) * h->n_tiles));
+    A(cudaMalloc(&h->tile_list, sizeof(int32_t) * h->n_tiles));
+    A(cudaMalloc(&h->counts, sizeof(int32_t) * 4));
+    A(cudaMemsetAsync(h->counts, 0, sizeof(int32_t) * 4, h->stream));
+    A(cudaMalloc(&h->n_rd_dev, sizeof(long long)));
+    A(cudaMalloc(&h->absmax_bits, sizeof(unsigned)));
+    A(cudaMalloc(&h->flag, sizeof(int)));
+    A(cudaMalloc(&h->e_partials, sizeof(double) * ENERGY_BLOCKS * 5));
+    A(cudaMalloc(&h->e_out, sizeof(double) * 5));
+    for (auto &ev : h->ev) A(cudaEventCreate(&ev));
+    A(cudaStreamSynchronize(h->stream));
+#undef A
+    *out = h;
+    return RDS_OK;
+}
+
+int rds_destroy(rds_t *h) {
+    if (!h) return RDS_OK;
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    free_all(h);
+    delete h;
+    return RDS_OK;
+}
+
+int rds_set_stream(rds_t *h, void *stream) {
+    if (!h) return fail(nullptr, RDS_EINVAL, "rds_set_stream: NULL handle");
+    cudaStream_t s = stream ? (cudaStream_t)stream : h->own_stream;
+    if (s != h->stream) {
+        // order the switch: work already queued on the old stream completes first
+        CK(h, cudaStreamSynchronize(h->stream));
+        h->stream = s;
+        if (h->graph) {
+            cudaGraphExecDestroy(h->graph);
+            h->graph = nullptr;
+        }
+    }
+    return RDS_OK;
+}
+
+int rds_set_option(rds_t *h, int key, int64_t value) {
+    if (!h) return fail(nullptr, RDS_EINVAL, "rds_set_option: NULL handle");
+    switch (key) {
+        case RDS_OPT_KFUSE:
+            if (value != 0 && !kf_supported((int)value))
+                return fail(h, RDS_EINVAL, "rds_set_option: k_fuse=%lld unsupported",
+                            (long long)value);
+            h->opt_kf = (int)value;
+            return RDS_OK;
+        case RDS_OPT_ITEM_ROWS:
+            if (value < 0 || value > (1 << 20))
+                return fail(h, RDS_EINVAL, "rds_set_option: item_rows=%lld", (long long)value);
+            h->opt_rows = (int)value;
+            return RDS_OK;
+        case RDS_OPT_TIMING:
+            h->opt_timing = value != 0;
+            return RDS_OK;
+        case RDS_OPT_SKIP:
+            h->opt_skip = value != 0;
+            return RDS_OK;
+        case RDS_OPT_GRAPH:
+            h->opt_graph = value != 0;
+            return RDS_OK;
+        default:
+            return fail(h, RDS_EINVAL, "rds_set_option: unknown key %d", key);
+    }
+}
+
+static int copy_in(rds_t *h, float *plane, const float *src, int on_device) {
+    cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(h, cudaMemcpy2DAsync(h->at(plane), sizeof(float) * h->pitch, src, sizeof(float) * h->W,
+                            sizeof(float) * h->W, h->H, kind, h->stream));
+    return RDS_OK;
+}
+
+static int check_finite(rds_t *h, const float *plane, bool *ok) {
+    CK(h, cudaMemsetAsync(h->flag, 0, sizeof(int), h->stream));
+    CK(h, launch_check_finite(h->at(const_cast<float *>(plane)), h->pitch, (int)h->H, (int)h->W,
+                              h->flag, h->stream));
+    int bad = 0;
+    CK(h, cudaMemcpyAsync(&bad, h->flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    *ok = bad == 0;
+    return RDS_OK;
+}
+
+int rds_set_image(rds_t *h, const float *z, int on_device) {
+    if (!h || !z) return fail(h, RDS_EINVAL, "rds_set_image: NULL argument");
+    int rc = copy_in(h, h->z, z, on_device);
+    if (rc) return rc;
+    bool ok = true;
+    if ((rc = check_finite(h, h->z, &ok))) return rc;
+    h->image_ok = ok;
+    h->have_image = true;
+    if (!ok) return fail(h, RDS_EINVAL, "rds_set_image: image has non-finite values");
+    return RDS_OK;
+}
+
+int rds_set_fitting(rds_t *h, float c1, float c2, float gamma, const float *P, int on_device) {
+    if (!h) return fail(nullptr, RDS_EINVAL, "rds_set_fitting: NULL handle");
+    if (!isfinite(c1) || !isfinite(c2) || c1 == c2)
+        return fail(h, RDS_EINVAL, "rds_set_fitting: need finite c1 != c2 (got %g, %g)", c1, c2);
+    if (!isfinite(gamma) || gamma < 0.0f)
+        return fail(h, RDS_EINVAL, "rds_set_fitting: gamma=%g must be finite and >= 0", gamma);
+    if (gamma > 0.0f && !P)
+        return fail(h, RDS_EINVAL, "rds_set_fitting: P is NULL but gamma > 0");
+    if (gamma > 0.0f) {
+        if (!h->P) {
+            CK(h, alloc_plane(h, &h->P, 0.0f));
+        }
+        int rc = copy_in(h, h->P, P, on_device);
+        if (rc) return rc;
+        bool ok = true;
+        if ((rc = check_finite(h, h->P, &ok))) return rc;
+        h->p_ok = ok;
+        if (!ok) {
+            h->have_fitting = false;
+            return fail(h, RDS_EINVAL, "rds_set_fitting: P has non-finite values");
+        }
+    }
+    h->c1 = c1;
+    h->c2 = c2;
+    h->gamma = gamma;
+    h->have_fitting = true;
+    return RDS_OK;
+}
+
+int rds_set_state(rds_t *h, const float *v, const float *rho1, const float *rho2,
+                  int on_device) {
+    if (!h || !v || !rho1 || !rho2) return fail(h, RDS_EINVAL, "rds_set_state: NULL argument");
+    if (!h->wv) {
+        CK(h, alloc_plane(h, &h->wv, 0.0f));
+        CK(h, alloc_plane(h, &h->wp1, 0.0f));
+        CK(h, alloc_plane(h, &h->wp2, 0.0f));
+    }
+    int rc;
+    if ((rc = copy_in(h, h->wv, v, on_device))) return rc;
+    if ((rc = copy_in(h, h->wp1, rho1, on_device))) return rc;
+    if ((rc = copy_in(h, h->wp2, rho2, on_device))) return rc;
+    h->warm_pending = true;
+    return RDS_OK;
+}
+
+int rds_fitting_absmax(rds_t *h, float *out) {
+    if (!h || !out) return fail(h, RDS_EINVAL, "rds_fitting_absmax: NULL argument");
+    if (!h->have_image || !h->have_fitting || !h->image_ok)
+        return fail(h, RDS_ESTATE, "rds_fitting_absmax: image and fitting must be set");
+    CK(h, cudaMemsetAsync(h->absmax_bits, 0, sizeof(unsigned), h->stream));
+    CK(h, launch_absmax(h->at(h->z), h->gamma != 0.0f ? h->at(h->P) : nullptr, h->pitch,
+                        (int)h->H, (int)h->W, h->c1, h->c2, h->gamma, h->absmax_bits, h->stream));
+    unsigned bits = 0;
+    CK(h, cudaMemcpyAsync(&bits, h->absmax_bits, sizeof bits, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    memcpy(out, &bits, sizeof bits);
+    return RDS_OK;
+}
+
+// Enqueue the K-loop: ceil(iters/kf) stencil launches (the last one writes u and mask).
+static cudaError_t enqueue_loop(rds_t *h, int kf, int rows, int iters, int n_strips,
+                                int n_chunks, float tau, float theta) {
+    StencilArgs a{};
+    a.c = h->at(h->c);
+    a.u_out = h->at(h->u);
+    a.mask_out = h->at(h->mask);
+    a.items = h->item_list;
+    a.n_items = h->counts + 1;
+    a.pitch = h->pitch;
+    a.H = (int)h->H;
+    a.W = (int)h->W;
+    a.rows = rows;
+    a.n_strips = n_strips;
+    a.tau = tau;
+    a.theta = theta;
+    a.inv_theta = 1.0f / theta;
+    const int grid = (n_strips * n_chunks + STENCIL_WARPS - 1) / STENCIL_WARPS;
+    int done = 0, cur = h->cur;
+    while (done < iters) {
+        const int stages = (iters - done) >= kf ? kf : (iters - done);
+        const bool last = done + stages == iters;
+        a.p1_in = h->at(h->p1[cur]);
+        a.p2_in = h->at(h->p2[cur]);
+        a.v_in = h->at(h->v[cur]);
+        a.p1_out = h->at(h->p1[cur ^ 1]);
+        a.p2_out = h->at(h->p2[cur ^ 1]);
+        a.v_out = h->at(h->v[cur ^ 1]);
+        cudaError_t e = launch_stencil(kf, stages, last, a, grid, h->stream);
+        if (e != cudaSuccess) return e;
+        cur ^= 1;
+        done += stages;
+    }
+    return cudaSuccess;
+}
+
+int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32_t iters) {
+    if (!h) return fail(nullptr, RDS_EINVAL, "rds_solve: NULL handle");
+    if (!(lambda > 0.0f) || !isfinite(lambda))
+        return fail(h, RDS_EINVAL, "rds_solve: lambda=%g must be finite and > 0", lambda);
+    if (!(theta > 0.0f) || !isfinite(theta))
+        return fail(h, RDS_EINVAL, "rds_solve: theta=%g must be finite and > 0", theta);
+    if (!(tau > 0.0f) || !(tau <= 0.125f))
+        return fail(h, RDS_EINVAL, "rds_solve: tau=%g must be in (0, 1/8]", tau);
+    if (isnan(delta) || delta < 0.0f)
+        return fail(h, RDS_EINVAL, "rds_solve: delta=%g must be >= 0 (inf allowed)", delta);
+    if (iters < 0) return fail(h, RDS_EINVAL, "rds_solve: iters=%d must be >= 0", iters);
+    if (!h->have_image || !h->have_fitting)
+        return fail(h, RDS_ESTATE, "rds_solve: image and fitting must be set first");
+    if (!h->image_ok || !h->p_ok)
+        return fail(h, RDS_EINVAL, "rds_solve: image or P has non-finite values");
+
+    const int kf = h->opt_kf ? h->opt_kf : kDefaultKF;
+    const int rows = h->opt_rows ? h->opt_rows : kDefaultRows;
+    const int wv = wv_of(kf);
+    const int n_strips = (int)((h->W + wv - 1) / wv);
+    const int n_chunks = (int)((h->H + rows - 1) / rows);
+    const int n_items = n_strips * n_chunks;
+    if (n_items > h->items_cap) {
+        if (h->item_flag) cudaFree(h->item_flag);
+        if (h->item_list) cudaFree(h->item_list);
+        h->item_flag = h->item_list = nullptr;
+        h->items_cap = 0;
+        CK(h, cudaMalloc(&h->item_flag, sizeof(int32_t) * n_items));
+        CK(h, cudaMalloc(&h->item_list, sizeof(int32_t) * n_items));
+        h->items_cap = n_items;
+        if (h->graph) {
+            cudaGraphExecDestroy(h->graph);
+            h->graph = nullptr;
+        }
+    }
+
+    if (h->opt_timing) CK(h, cudaEventRecord(h->ev[0], h->stream));
+    SetupArgs s{};
+    s.z = h->at(h->z);
+    s.P = h->gamma != 0.0f ? h->at(h->P) : nullptr;
+    if (h->warm_pending) {
+        s.wv = h->at(h->wv);
+        s.wp1 = h->at(h->wp1);
+        s.wp2 = h->at(h->wp2);
+    }
+    s.f = h->at(h->f);
+    s.c = h->at(h->c);
+    s.u = h->at(h->u);
+    s.v0 = h->at(h->v[0]);
+    s.v1 = h->at(h->v[1]);
+    s.p10 = h->at(h->p1[0]);
+    s.p11 = h->at(h->p1[1]);
+    s.p20 = h->at(h->p2[0]);
+    s.p21 = h->at(h->p2[1]);
+    s.lab = h->at(h->lab);
+    s.mask = h->at(h->mask);
+    s.tile_rd = h->tile_rd;
+    s.pitch = h->pitch;
+    s.H = (int)h->H;
+    s.W = (int)h->W;
+    s.c1 = h->c1;
+    s.c2 = h->c2;
+    s.gamma = h->gamma;
+    s.delta = delta;
+    s.theta_lambda = theta * lambda;
+    CK(h, launch_setup(s, h->stream));
+    CK(h, launch_compact(h->tile_rd, h->n_tiles, h->tile_list, h->counts + 0, h->n_rd_dev,
+                         h->stream));
+    CK(h, launch_item_flags(h->tile_rd, (int)h->H, (int)h->W, rows, wv, n_strips, n_chunks,
+                            h->opt_skip, h->item_flag, h->stream));
+    CK(h, launch_compact(h->item_flag, n_items, h->item_list, h->counts + 1, nullptr,
+                         h->stream));
+    h->warm_pending = false;
+    h->cur = 0;
+    if (h->opt_timing) CK(h, cudaEventRecord(h->ev[1], h->stream));
+
+    if (iters > 0) {
+        rds_handle::Key key{kf, rows, iters, h->cur, n_strips, n_chunks, tau, theta};
+        const int launches = (iters + kf - 1) / kf;
+        if (h->opt_graph && launches > 1) {
+            if (!h->graph || !(h->gkey == key)) {
+                if (h->graph) {
+                    cudaGraphExecDestroy(h->graph);
+                    h->graph = nullptr;
+                }
+                cudaStream_t cap;
+                CK(h, cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+                cudaGraph_t g = nullptr;
+                cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+                if (e == cudaSuccess) {
+                    cudaStream_t keep = h->stream;
+                    h->stream = cap;
+                    cudaError_t e2 = enqueue_loop(h, kf, rows, iters, n_strips, n_chunks, tau,
+                                                  theta);
+                    h->stream = keep;
+                    e = cudaStreamEndCapture(cap, &g);
+                    if (e == cudaSuccess) e = e2;
+                }
+                if (e == cudaSuccess) e = cudaGraphInstantiate(&h->graph, g, 0);
+                if (g) cudaGraphDestroy(g);
+                cudaStreamDestroy(cap);
+                if (e != cudaSuccess)
+                    return fail(h, RDS_ECUDA, "rds_solve: graph capture failed: %s",
+                                cudaGetErrorString(e));
+                h->gkey = key;
+            }
+            CK(h, cudaGraphLaunch(h->graph, h->stream));
+        } else {
+            CK(h, enqueue_loop(h, kf, rows, iters, n_strips, n_chunks, tau, theta));
+        }
+        if (launches & 1) h->cur ^= 1;
+    }
+    if (h->opt_timing) CK(h, cudaEventRecord(h->ev[2], h->stream));
+
+    h->lambda = lambda;
+    h->theta = theta;
+    h->solved = true;
+    rds_stats_t &st = h->stats;
+    memset(&st, 0, sizeof st);
+    st.H = h->H;
+    st.W = h->W;
+    st.n_tiles = h->n_tiles;
+    st.n_items = n_items;
+    st.iters = iters;
+    st.k_fuse = kf;
+    st.launches = (iters + kf - 1) / kf;
+    st.item_rows = rows;
+    st.item_cols = wv;
+    st.setup_ms = st.loop_ms = -1.0f;
+    return RDS_OK;
+}
+
+static int copy_out(rds_t *h, void *dst, const void *plane_origin, size_t elt, int on_device) {
+    cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CK(h, cudaMemcpy2DAsync(dst, elt * h->W, plane_origin, elt * h->pitch, elt * h->W, h->H,
+                            kind, h->stream));
+    if (!on_device) CK(h, cudaStreamSynchronize(h->stream));
+    return RDS_OK;
+}
+
+#define NEED_SOLVED(name)                                                          \
+    if (!h) return fail(nullptr, RDS_EINVAL, name ": NULL handle");                \
+    if (!h->solved) return fail(h, RDS_ESTATE, name ": no solve has run yet");
+
+int rds_get_u(rds_t *h, float *out, int on_device) {
+    NEED_SOLVED("rds_get_u");
+    if (!out) return fail(h, RDS_EINVAL, "rds_get_u: NULL out");
+    return copy_out(h, out, h->at(h->u), sizeof(float), on_device);
+}
+
+int rds_get_mask(rds_t *h, uint8_t *out, int on_device) {
+    NEED_SOLVED("rds_get_mask");
+    if (!out) return fail(h, RDS_EINVAL, "rds_get_mask: NULL out");
+    return copy_out(h, out, h->at(h->mask), 1, on_device);
+}
+
+int rds_get_v(rds_t *h, float *out, int on_device) {
+    NEED_SOLVED("rds_get_v");
+    if (!out) return fail(h, RDS_EINVAL, "rds_get_v: NULL out");
+    return copy_out(h, out, h->at(h->v[h->cur]), sizeof(float), on_device);
+}
+
+int rds_get_p(rds_t *h, float *rho1, float *rho2, int on_device) {
+    NEED_SOLVED("rds_get_p");
+    if (!rho1 || !rho2) return fail(h, RDS_EINVAL, "rds_get_p: NULL out");
+    int rc = copy_out(h, rho1, h->at(h->p1[h->cur]), sizeof(float), on_device);
+    if (rc) return rc;
+    return copy_out(h, rho2, h->at(h->p2[h->cur]), sizeof(float), on_device);
+}
+
+int rds_get_fitting(rds_t *h, float *out, int on_device) {
+    NEED_SOLVED("rds_get_fitting");
+    if (!out) return fail(h, RDS_EINVAL, "rds_get_fitting: NULL out");
+    return copy_out(h, out, h->at(h->f), sizeof(float), on_device);
+}
+
+int rds_get_labels(rds_t *h, uint8_t *out, int on_device) {
+    NEED_SOLVED("rds_get_labels");
+    if (!out) return fail(h, RDS_EINVAL, "rds_get_labels: NULL out");
+    return copy_out(h, out, h->at(h->lab), 1, on_device);
+}
+
+int rds_get_active_tiles(rds_t *h, int32_t *out, int64_t cap, int64_t *count) {
+    NEED_SOLVED("rds_get_active_tiles");
+    if (!count) return fail(h, RDS_EINVAL, "rds_get_active_tiles: NULL count");
+    int32_t n = 0;
+    CK(h, cudaMemcpyAsync(&n, h->counts, sizeof n, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    *count = n;
+    if (cap < n) return fail(h, RDS_EINVAL, "rds_get_active_tiles: cap %lld < count %d",
+                             (long long)cap, n);
+    if (n > 0) {
+        if (!out) return fail(h, RDS_EINVAL, "rds_get_active_tiles: NULL out");
+        CK(h, cudaMemcpyAsync(out, h->tile_list, sizeof(int32_t) * n, cudaMemcpyDeviceToHost,
+                              h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+    }
+    return RDS_OK;
+}
+
+int rds_tile_shape(int *th, int *tw) {
+    if (!th || !tw) return fail(nullptr, RDS_EINVAL, "rds_tile_shape: NULL argument");
+    *th = TILE_H;
+    *tw = TILE_W;
+    return RDS_OK;
+}
+
+int rds_energy(rds_t *h, rds_energy_t *out) {
+    NEED_SOLVED("rds_energy");
+    if (!out) return fail(h, RDS_EINVAL, "rds_energy: NULL out");
+    EnergyArgs a{};
+    a.f = h->at(h->f);
+    a.u = h->at(h->u);
+    a.v = h->at(h->v[h->cur]);
+    a.p1 = h->at(h->p1[h->cur]);
+    a.p2 = h->at(h->p2[h->cur]);
+    a.pitch = h->pitch;
+    a.H = (int)h->H;
+    a.W = (int)h->W;
+    a.partials = h->e_partials;
+    a.out = h->e_out;
+    a.lambda = h->lambda;
+    CK(h, launch_energy(a, h->stream));
+    double s[5];
+    CK(h, cudaMemcpyAsync(s, h->e_out, sizeof s, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    const double lam = (double)h->lambda;
+    out->TV_v = s[0];
+    out->fit_v = lam * s[1];
+    out->E_v = s[0] + lam * s[1];
+    out->E_u = s[2] + lam * s[3];
+    out->D_p = s[4];
+    out->gap = out->E_v - out->D_p;
+    return RDS_OK;
+}
+
+int rds_get_stats(rds_t *h, rds_stats_t *out) {
+    NEED_SOLVED("rds_get_stats");
+    if (!out) return fail(h, RDS_EINVAL, "rds_get_stats: NULL out");
+    int32_t cnt[2];
+    long long nrd = 0;
+    CK(h, cudaMemcpyAsync(cnt, h->counts, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(&nrd, h->n_rd_dev, sizeof nrd, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    h->stats.n_active_tiles = cnt[0];
+    h->stats.n_active_items = cnt[1];
+    h->stats.n_rd = nrd;
+    if (h->opt_timing) {
+        CK(h, cudaEventElapsedTime(&h->stats.setup_ms, h->ev[0], h->ev[1]));
+        CK(h, cudaEventElapsedTime(&h->stats.loop_ms, h->ev[1], h->ev[2]));
+    }
+    *out = h->stats;
+    return RDS_OK;
+}
+
+int rds_kfuse_supported(int32_t *out, int cap) { return kf_list(out, cap); }
+
+const char *rds_last_error(rds_t *h) {
+    if (h) return h->err.c_str();
+    return g_last_error.c_str();
+}
+
+const char *rds_version(void) { return "librds 0.1 (sm_100a)"; }
+
+}  // extern "C"

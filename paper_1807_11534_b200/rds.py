@@ -1,0 +1,345 @@
+"""Thin Python binding of librds (include/rds.h) via ctypes -- argument marshalling only.
+
+Every computation runs in the CUDA kernels of ``librds.so``; this module only converts
+numpy arrays (host, ``on_device=0``) or torch CUDA tensors (device, ``on_device=1``) to
+pointers and checks return codes.  There is no CPU fallback: if the library is missing this
+module raises at import time.
+
+Function names mirror the C ABI (``rds_create``, ``rds_solve``, ...).  ``Solver`` is a small
+convenience wrapper around a handle.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "librds.so")
+
+RDS_OK, RDS_EINVAL, RDS_ESTATE, RDS_ECUDA, RDS_ENOMEM = 0, -1, -2, -3, -4
+RDS_LABEL_BG, RDS_LABEL_FG, RDS_LABEL_RD = 0, 1, 2
+RDS_OPT_KFUSE, RDS_OPT_ITEM_ROWS, RDS_OPT_TIMING, RDS_OPT_SKIP, RDS_OPT_GRAPH = 1, 2, 3, 4, 5
+
+EXPORTS = (
+    "rds_create", "rds_destroy", "rds_set_stream", "rds_set_option", "rds_set_image",
+    "rds_set_fitting", "rds_set_state", "rds_fitting_absmax", "rds_solve", "rds_get_u",
+    "rds_get_mask", "rds_get_v", "rds_get_p", "rds_get_fitting", "rds_get_labels",
+    "rds_get_active_tiles", "rds_tile_shape", "rds_energy", "rds_get_stats",
+    "rds_kfuse_supported", "rds_last_error", "rds_version",
+)
+
+
+class RdsError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"rds error {code}: {msg}")
+        self.code = code
+
+
+class rds_energy_t(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_double) for k in ("E_v", "E_u", "D_p", "gap", "TV_v", "fit_v")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class rds_stats_t(ctypes.Structure):
+    _fields_ = [("H", ctypes.c_int64), ("W", ctypes.c_int64), ("n_rd", ctypes.c_int64),
+                ("n_tiles", ctypes.c_int64), ("n_active_tiles", ctypes.c_int64),
+                ("n_items", ctypes.c_int64), ("n_active_items", ctypes.c_int64),
+                ("iters", ctypes.c_int32), ("k_fuse", ctypes.c_int32),
+                ("launches", ctypes.c_int32), ("item_rows", ctypes.c_int32),
+                ("item_cols", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("setup_ms", ctypes.c_float), ("loop_ms", ctypes.c_float)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; "
+                          f"g.build()'` (no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, i64, i32, f, i = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float, ctypes.c_int
+    sig = {
+        "rds_create": [i64, i64, ctypes.POINTER(P)],
+        "rds_destroy": [P],
+        "rds_set_stream": [P, P],
+        "rds_set_option": [P, i, i64],
+        "rds_set_image": [P, P, i],
+        "rds_set_fitting": [P, f, f, f, P, i],
+        "rds_set_state": [P, P, P, P, i],
+        "rds_fitting_absmax": [P, ctypes.POINTER(f)],
+        "rds_solve": [P, f, f, f, f, i32],
+        "rds_get_u": [P, P, i],
+        "rds_get_mask": [P, P, i],
+        "rds_get_v": [P, P, i],
+        "rds_get_p": [P, P, P, i],
+        "rds_get_fitting": [P, P, i],
+        "rds_get_labels": [P, P, i],
+        "rds_get_active_tiles": [P, P, i64, ctypes.POINTER(i64)],
+        "rds_tile_shape": [ctypes.POINTER(i), ctypes.POINTER(i)],
+        "rds_energy": [P, ctypes.POINTER(rds_energy_t)],
+        "rds_get_stats": [P, ctypes.POINTER(rds_stats_t)],
+        "rds_kfuse_supported": [ctypes.POINTER(i32), i],
+        "rds_last_error": [P],
+        "rds_version": [],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.rds_last_error.restype = ctypes.c_char_p
+    lib.rds_version.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = _load()
+
+
+def _check(rc, h=None):
+    if rc != RDS_OK:
+        raise RdsError(rc, _lib.rds_last_error(h).decode())
+    return rc
+
+
+def _buf(a, dtype, shape, writable=False):
+    """(pointer, on_device, keepalive) for a numpy array or torch tensor of `dtype`/`shape`."""
+    if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):  # torch tensor
+        import torch
+
+        tdt = {np.float32: torch.float32, np.uint8: torch.uint8, np.int32: torch.int32}[dtype]
+        if a.dtype != tdt or tuple(a.shape) != tuple(shape) or not a.is_contiguous():
+            raise ValueError(f"expected contiguous {tdt} tensor of shape {shape}")
+        return ctypes.c_void_p(a.data_ptr()), int(a.is_cuda), a
+    arr = np.asarray(a)
+    if arr.dtype != dtype or arr.shape != tuple(shape) or not arr.flags.c_contiguous or \
+            (writable and not arr.flags.writeable):
+        raise ValueError(f"expected C-contiguous {np.dtype(dtype)} array of shape {shape}")
+    return ctypes.c_void_p(arr.ctypes.data), 0, arr
+
+
+# ------------------------------------------------------------------------------------------
+# C-ABI mirror
+# ------------------------------------------------------------------------------------------
+
+def rds_create(H, W):
+    h = ctypes.c_void_p()
+    _check(_lib.rds_create(int(H), int(W), ctypes.byref(h)))
+    return h
+
+
+def rds_destroy(h):
+    _check(_lib.rds_destroy(h))
+
+
+def rds_set_stream(h, stream_ptr):
+    _check(_lib.rds_set_stream(h, ctypes.c_void_p(stream_ptr or None)), h)
+
+
+def rds_set_option(h, key, value):
+    _check(_lib.rds_set_option(h, int(key), int(value)), h)
+
+
+def rds_set_image(h, z, shape):
+    p, dev, _keep = _buf(z, np.float32, shape)
+    _check(_lib.rds_set_image(h, p, dev), h)
+
+
+def rds_set_fitting(h, c1, c2, gamma, P, shape):
+    if P is None:
+        p, dev = None, 0
+    else:
+        p, dev, _keep = _buf(P, np.float32, shape)
+    _check(_lib.rds_set_fitting(h, float(c1), float(c2), float(gamma), p, dev), h)
+
+
+def rds_set_state(h, v, rho1, rho2, shape):
+    pv, dev, _k1 = _buf(v, np.float32, shape)
+    p1, dev1, _k2 = _buf(rho1, np.float32, shape)
+    p2, dev2, _k3 = _buf(rho2, np.float32, shape)
+    if not (dev == dev1 == dev2):
+        raise ValueError("v, rho1, rho2 must all be host or all device")
+    _check(_lib.rds_set_state(h, pv, p1, p2, dev), h)
+
+
+def rds_fitting_absmax(h):
+    out = ctypes.c_float()
+    _check(_lib.rds_fitting_absmax(h, ctypes.byref(out)), h)
+    return np.float32(out.value)
+
+
+def rds_solve(h, lam, theta, tau, delta, iters):
+    _check(_lib.rds_solve(h, float(lam), float(theta), float(tau), float(delta), int(iters)), h)
+
+
+def _get(fn, h, out, dtype, shape):
+    p, dev, _keep = _buf(out, dtype, shape, writable=True)
+    _check(fn(h, p, dev), h)
+    return out
+
+
+def rds_get_u(h, out, shape):
+    return _get(_lib.rds_get_u, h, out, np.float32, shape)
+
+
+def rds_get_mask(h, out, shape):
+    return _get(_lib.rds_get_mask, h, out, np.uint8, shape)
+
+
+def rds_get_v(h, out, shape):
+    return _get(_lib.rds_get_v, h, out, np.float32, shape)
+
+
+def rds_get_fitting(h, out, shape):
+    return _get(_lib.rds_get_fitting, h, out, np.float32, shape)
+
+
+def rds_get_labels(h, out, shape):
+    return _get(_lib.rds_get_labels, h, out, np.uint8, shape)
+
+
+def rds_get_p(h, rho1, rho2, shape):
+    p1, dev1, _k1 = _buf(rho1, np.float32, shape, writable=True)
+    p2, dev2, _k2 = _buf(rho2, np.float32, shape, writable=True)
+    if dev1 != dev2:
+        raise ValueError("rho1 and rho2 must both be host or both device")
+    _check(_lib.rds_get_p(h, p1, p2, dev1), h)
+    return rho1, rho2
+
+
+def rds_get_active_tiles(h):
+    cnt = ctypes.c_int64()
+    rc = _lib.rds_get_active_tiles(h, None, 0, ctypes.byref(cnt))
+    if rc not in (RDS_OK, RDS_EINVAL):
+        _check(rc, h)
+    out = np.empty(max(cnt.value, 1), dtype=np.int32)
+    _check(_lib.rds_get_active_tiles(h, ctypes.c_void_p(out.ctypes.data), out.size,
+                                     ctypes.byref(cnt)), h)
+    return out[: cnt.value].copy()
+
+
+def rds_tile_shape():
+    th, tw = ctypes.c_int(), ctypes.c_int()
+    _check(_lib.rds_tile_shape(ctypes.byref(th), ctypes.byref(tw)))
+    return th.value, tw.value
+
+
+def rds_energy(h):
+    e = rds_energy_t()
+    _check(_lib.rds_energy(h, ctypes.byref(e)), h)
+    return e.as_dict()
+
+
+def rds_get_stats(h):
+    s = rds_stats_t()
+    _check(_lib.rds_get_stats(h, ctypes.byref(s)), h)
+    return s.as_dict()
+
+
+def rds_kfuse_supported():
+    buf = (ctypes.c_int32 * 64)()
+    n = _lib.rds_kfuse_supported(buf, 64)
+    return [buf[i] for i in range(min(n, 64))]
+
+
+def rds_last_error(h=None):
+    return _lib.rds_last_error(h).decode()
+
+
+def rds_version():
+    return _lib.rds_version().decode()
+
+
+# ------------------------------------------------------------------------------------------
+# convenience wrapper
+# ------------------------------------------------------------------------------------------
+
+class Solver:
+    """One librds handle for an H x W image.  Host (numpy) or device (torch) buffers."""
+
+    def __init__(self, H, W, stream=None, k_fuse=0, item_rows=0, timing=False, skip=True,
+                 graph=True):
+        self.shape = (int(H), int(W))
+        self.h = rds_create(H, W)
+        if stream is not None:
+            rds_set_stream(self.h, stream)
+        if k_fuse:
+            rds_set_option(self.h, RDS_OPT_KFUSE, k_fuse)
+        if item_rows:
+            rds_set_option(self.h, RDS_OPT_ITEM_ROWS, item_rows)
+        rds_set_option(self.h, RDS_OPT_TIMING, int(timing))
+        rds_set_option(self.h, RDS_OPT_SKIP, int(skip))
+        rds_set_option(self.h, RDS_OPT_GRAPH, int(graph))
+
+    def close(self):
+        if self.h is not None:
+            rds_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_stream(self, stream_ptr):
+        rds_set_stream(self.h, stream_ptr)
+
+    def set_option(self, key, value):
+        rds_set_option(self.h, key, value)
+
+    def set_image(self, z):
+        rds_set_image(self.h, z, self.shape)
+
+    def set_fitting(self, c1, c2, gamma=0.0, P=None):
+        rds_set_fitting(self.h, c1, c2, gamma, P, self.shape)
+
+    def set_state(self, v, rho1, rho2):
+        rds_set_state(self.h, v, rho1, rho2, self.shape)
+
+    def absmax(self):
+        return rds_fitting_absmax(self.h)
+
+    def solve(self, lam, theta, tau, delta, iters):
+        rds_solve(self.h, lam, theta, tau, math.inf if delta is None else delta, iters)
+
+    def _out(self, dtype, out):
+        return np.empty(self.shape, dtype=dtype) if out is None else out
+
+    def u(self, out=None):
+        return rds_get_u(self.h, self._out(np.float32, out), self.shape)
+
+    def mask(self, out=None):
+        return rds_get_mask(self.h, self._out(np.uint8, out), self.shape)
+
+    def v(self, out=None):
+        return rds_get_v(self.h, self._out(np.float32, out), self.shape)
+
+    def p(self):
+        return rds_get_p(self.h, np.empty(self.shape, np.float32),
+                         np.empty(self.shape, np.float32), self.shape)
+
+    def fitting(self, out=None):
+        return rds_get_fitting(self.h, self._out(np.float32, out), self.shape)
+
+    def labels(self, out=None):
+        return rds_get_labels(self.h, self._out(np.uint8, out), self.shape)
+
+    def active_tiles(self):
+        return rds_get_active_tiles(self.h)
+
+    def energy(self):
+        return rds_energy(self.h)
+
+    def stats(self):
+        return rds_get_stats(self.h)

@@ -1,0 +1,346 @@
+"""GPU parity of librds (through the C ABI) against the CPU oracle on seeded inputs.
+
+Bars (BASELINE.json north_star): labels / active tiles / f bit-exact; u and rho within 5e-4
+max-abs after the stated iteration count; thresholded mask disagreeing on <= 0.05% of pixels.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1807_11534_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+TOL = 5e-4          # u, rho max-abs (north_star)
+MASK_FRAC = 5e-4    # <= 0.05% mask disagreement
+
+
+@pytest.fixture(scope="module")
+def rds():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1807_11534_b200 import _build
+
+    _build.build()
+    from paper_1807_11534_b200 import rds as _rds
+
+    return _rds
+
+
+def gpu_solve(rds, z, P, c1, c2, gamma, lam, theta, tau, delta, iters, init=None, **opt):
+    H, W = z.shape
+    s = rds.Solver(H, W, **opt)
+    s.set_image(z)
+    s.set_fitting(c1, c2, gamma, P)
+    if init is not None:
+        s.set_state(*init)
+    s.solve(lam, theta, tau, delta, iters)
+    p1, p2 = s.p()
+    out = dict(u=s.u(), v=s.v(), p1=p1, p2=p2, mask=s.mask(), labels=s.labels(),
+               f=s.fitting(), tiles=s.active_tiles(), stats=s.stats(), solver=s)
+    return out
+
+
+def compare(g, o, lab=None, tol=TOL, mask_frac=MASK_FRAC, ctx=""):
+    for k in ("u", "v", "p1", "p2"):
+        err = np.abs(g[k].astype(np.float64) - o[k]).max() if g[k].size else 0.0
+        assert err <= tol, f"{ctx} {k} max-abs {err:.3g} > {tol}"
+    dis = np.mean(g["mask"] != (o["u"] > 0.5)) if g["mask"].size else 0.0
+    assert dis <= mask_frac, f"{ctx} mask disagreement {dis:.3g}"
+
+
+def _params(cfg):
+    return dict(c1=cfg.c1, c2=cfg.c2, gamma=cfg.gamma, theta=cfg.theta, tau=cfg.tau)
+
+
+# ------------------------------------------------------------------------------------------
+# K1 / K2: fitting, labels, tiles bit-exact (all configs at full size, C4 included)
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["C0", "C1", "C2", "C3"])
+def test_setup_bitexact(rds, orc, name):
+    cfg = wl.CONFIGS[name]
+    z, P = wl.make_image(cfg)
+    f_o = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    am = orc.absmax(f_o)
+    s = rds.Solver(cfg.H, cfg.W)
+    s.set_image(z)
+    s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
+    assert s.absmax() == am
+    for dr in cfg.delta_rels:
+        delta = wl.band_delta(dr, am)
+        s.solve(cfg.lambdas[0], cfg.theta, cfg.tau, delta, 0)
+        assert np.array_equal(s.fitting(), f_o)
+        lab_o = orc.labels(f_o, delta)
+        assert np.array_equal(s.labels(), lab_o)
+        assert np.array_equal(s.active_tiles(), orc.tiles(lab_o, 32, 32))
+        st = s.stats()
+        assert st["n_rd"] == int((lab_o == 2).sum())
+        h = (f_o <= 0)
+        assert np.array_equal(s.u(), h.astype(np.float32))          # K = 0 -> u = H(-f)
+        assert np.array_equal(s.mask(), h.astype(np.uint8))
+    s.close()
+
+
+@pytest.mark.slow
+def test_setup_bitexact_c4(rds, orc):
+    cfg = wl.CONFIGS["C4"]
+    z, P = wl.make_image(cfg)
+    f_o = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    am = orc.absmax(f_o)
+    s = rds.Solver(cfg.H, cfg.W)
+    s.set_image(z)
+    s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
+    assert s.absmax() == am
+    delta = wl.band_delta(0.2, am)
+    s.solve(5.0, cfg.theta, cfg.tau, delta, 0)
+    lab_o = orc.labels(f_o, delta)
+    assert np.array_equal(s.labels(), lab_o)
+    assert np.array_equal(s.active_tiles(), orc.tiles(lab_o, 32, 32))
+    s.close()
+
+
+# ------------------------------------------------------------------------------------------
+# K3: the iteration on small and ragged shapes, every fusion depth, warm starts
+# ------------------------------------------------------------------------------------------
+
+SHAPES = [(1, 1), (1, 7), (9, 1), (5, 3), (33, 129), (100, 77), (130, 250), (257, 131)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_ragged_shapes(rds, orc, shape):
+    H, W = shape
+    z = wl.random_image(H, W, seed=H * 1000 + W)
+    for dr in (0.0, 0.3, math.inf):
+        f = orc.fitting(z, 0.8, 0.2)
+        delta = wl.band_delta(dr, orc.absmax(f))
+        for iters in (1, 8, 23):
+            g = gpu_solve(rds, z, None, 0.8, 0.2, 0.0, 5.0, 0.1, 0.125, delta, iters)
+            o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, iters)
+            assert np.array_equal(g["labels"], o["labels"])
+            compare(g, o, tol=1e-5, mask_frac=0.0 if H * W < 2000 else MASK_FRAC,
+                    ctx=f"{shape} d={dr} K={iters}")
+
+
+@pytest.mark.parametrize("kf", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_every_fusion_depth(rds, orc, kf):
+    """Each KF (iterations per HBM round trip) and each remainder stage count matches the
+    oracle; item rows small so many chunk seams are crossed."""
+    H, W = 150, 300
+    z = wl.random_image(H, W, seed=kf)
+    f = orc.fitting(z, 0.75, 0.25)
+    delta = wl.band_delta(0.4, orc.absmax(f))
+    for iters in (kf, 2 * kf + 1, 3 * kf + kf - 1):
+        g = gpu_solve(rds, z, None, 0.75, 0.25, 0.0, 2.0, 0.1, 0.125, delta, iters, k_fuse=kf,
+                      item_rows=40)
+        o = orc.solve(f, delta, 2.0, np.float32(0.1), 0.125, iters)
+        compare(g, o, tol=1e-5, ctx=f"kf={kf} K={iters}")
+
+
+def test_warm_start_random_state(rds, orc):
+    """One and several iterations from a random (v, rho) state: exercises every term of the
+    update with O(1) values, not just the smooth evolution from H(-f)."""
+    H, W = 96, 200
+    z = wl.random_image(H, W, seed=77)
+    f = orc.fitting(z, 0.8, 0.2)
+    v, p1, p2 = wl.random_state(H, W, 78)
+    for dr in (0.5, math.inf):
+        delta = wl.band_delta(dr, orc.absmax(f))
+        for iters in (1, 2, 9):
+            g = gpu_solve(rds, z, None, 0.8, 0.2, 0.0, 5.0, 0.1, 0.125, delta, iters,
+                          init=(v, p1, p2))
+            o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, iters,
+                          init=(v.astype(np.float64), p1.astype(np.float64),
+                                p2.astype(np.float64)))
+            compare(g, o, tol=2e-5, mask_frac=1e-3, ctx=f"warm d={dr} K={iters}")
+
+
+def test_fusion_depth_equivalence(rds):
+    """k=1 and k=KF run the same per-pixel arithmetic: results agree to float32 rounding."""
+    cfg = wl.CONFIGS["C1"]
+    z, P = wl.make_image(cfg)
+    res = []
+    for kf in (1, 3, 7):
+        g = gpu_solve(rds, z, P, cfg.c1, cfg.c2, cfg.gamma, 5.0, cfg.theta, cfg.tau,
+                      np.float32(0.2), 23, k_fuse=kf)
+        res.append(g)
+    for g in res[1:]:
+        for k in ("u", "v", "p1", "p2"):
+            assert np.abs(g[k] - res[0][k]).max() <= 1e-6
+
+
+def test_skip_equivalence_and_determinism(rds):
+    """Tile skipping never changes the result (pinned pixels are fixed points), and repeated
+    solves are bit-identical."""
+    cfg = wl.CONFIGS["C2"]
+    z, P = wl.make_image(cfg)
+    am = np.float32(0)
+    s = rds.Solver(cfg.H, cfg.W)
+    s.set_image(z)
+    s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
+    am = s.absmax()
+    delta = wl.band_delta(0.2, am)
+    outs = []
+    for skip in (1, 1, 0):
+        s.set_option(rds.RDS_OPT_SKIP, skip)
+        s.solve(5.0, cfg.theta, cfg.tau, delta, 40)
+        p1, p2 = s.p()
+        outs.append((s.u(), s.v(), p1, p2))
+    st = s.stats()
+    assert st["n_active_items"] == st["n_items"]  # last run: skip off
+    for o in outs[1:]:
+        for a, b in zip(outs[0], o):
+            assert a.tobytes() == b.tobytes()
+    s.close()
+
+
+# ------------------------------------------------------------------------------------------
+# configs at their stated sizes / iteration counts
+# ------------------------------------------------------------------------------------------
+
+def _run_cfg(rds, orc, name, lam, dr, iters=None):
+    cfg = wl.CONFIGS[name]
+    z, P = wl.make_image(cfg)
+    f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    delta = wl.band_delta(dr, orc.absmax(f))
+    K = cfg.iters if iters is None else iters
+    g = gpu_solve(rds, z, P, cfg.c1, cfg.c2, cfg.gamma, lam, cfg.theta, cfg.tau, delta, K)
+    o = orc.solve(f, delta, lam, np.float32(cfg.theta), cfg.tau, K)
+    assert np.array_equal(g["labels"], o["labels"])
+    assert np.array_equal(g["tiles"], orc.tiles(o["labels"], 32, 32))
+    compare(g, o, ctx=f"{name} lam={lam} d={dr} K={K}")
+    return g, o
+
+
+@pytest.mark.parametrize("dr", [0.2, math.inf])
+def test_c0(rds, orc, dr):
+    g, o = _run_cfg(rds, orc, "C0", 5.0, dr)
+
+
+@pytest.mark.parametrize("lam,dr", [(5.0, 0.05), (5.0, 0.1), (5.0, 0.2), (5.0, 0.4),
+                                    (2.0, 0.2), (10.0, 0.2), (5.0, math.inf)])
+def test_c1(rds, orc, lam, dr):
+    _run_cfg(rds, orc, "C1", lam, dr)
+
+
+@pytest.mark.parametrize("dr", [0.05, 0.2, math.inf])
+def test_c2(rds, orc, dr):
+    _run_cfg(rds, orc, "C2", 5.0, dr)
+
+
+@pytest.mark.parametrize("dr", [0.1, math.inf])
+def test_c3_reduced_iters(rds, orc, dr):
+    """C3 at full size in the bench's launch configuration, K=60 (oracle cost bound)."""
+    _run_cfg(rds, orc, "C3", 5.0, dr, iters=60)
+
+
+@pytest.mark.slow
+def test_c3_full(rds, orc):
+    """C3 at full size and full K=1000 (headline config), delta = 0.1 max|f|."""
+    _run_cfg(rds, orc, "C3", 5.0, 0.1)
+
+
+def test_c3_full_properties(rds, orc):
+    """Headline config, full K: properties that hold at any size -- |rho| <= 1, v in [0,1],
+    exact pinning, Neumann zeros, weak-duality gap >= 0 (GPU energy), labels bit-exact."""
+    cfg = wl.CONFIGS["C3"]
+    z, P = wl.make_image(cfg)
+    f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    am = orc.absmax(f)
+    for dr in (0.1, math.inf):
+        delta = wl.band_delta(dr, am)
+        g = gpu_solve(rds, z, P, cfg.c1, cfg.c2, cfg.gamma, 5.0, cfg.theta, cfg.tau, delta,
+                      cfg.iters)
+        lab = orc.labels(f, delta)
+        assert np.array_equal(g["labels"], lab)
+        pn = np.sqrt(g["p1"].astype(np.float64) ** 2 + g["p2"].astype(np.float64) ** 2)
+        assert pn.max() <= 1 + 1e-6
+        assert g["v"].min() >= 0 and g["v"].max() <= 1
+        off = lab != 2
+        u0 = (f <= 0).astype(np.float32)
+        assert np.array_equal(g["u"][off], u0[off]) and np.array_equal(g["v"][off], u0[off])
+        assert not g["p1"][off].any() and not g["p2"][off].any()
+        assert not g["p1"][-1].any() and not g["p2"][:, -1].any()
+        e = g["solver"].energy()
+        assert e["gap"] >= -1e-6 * abs(e["E_v"])
+        g["solver"].close()
+
+
+# ------------------------------------------------------------------------------------------
+# K5 energy, API behaviour
+# ------------------------------------------------------------------------------------------
+
+def test_energy_matches_oracle(rds, orc):
+    """GPU energies equal the oracle's energies evaluated on the GPU's own state."""
+    cfg = wl.CONFIGS["C1"]
+    z, P = wl.make_image(cfg)
+    for dr in (0.2, math.inf):
+        g = gpu_solve(rds, z, P, cfg.c1, cfg.c2, cfg.gamma, 5.0, cfg.theta, cfg.tau,
+                      wl.band_delta(dr, np.float32(0.7637)), 50)
+        e_g = g["solver"].energy()
+        e_o = orc.energy(g["f"], 5.0, g["u"], g["v"], g["p1"], g["p2"])
+        for k in ("E_v", "E_u", "D_p", "TV_v", "fit_v"):
+            assert abs(e_g[k] - e_o[k]) <= 1e-5 * max(1.0, abs(e_o[k])), (k, e_g[k], e_o[k])
+        assert e_g["gap"] >= 0
+        assert abs(e_g["gap"] - e_o["gap"]) <= 1e-5 * abs(e_o["E_v"])
+        g["solver"].close()
+
+
+def test_errors(rds):
+    s = rds.Solver(16, 16)
+    with pytest.raises(rds.RdsError) as ei:
+        s.u()
+    assert ei.value.code == rds.RDS_ESTATE
+    with pytest.raises(rds.RdsError) as ei:
+        s.solve(5.0, 0.1, 0.125, 0.1, 10)
+    assert ei.value.code == rds.RDS_ESTATE
+    z = np.zeros((16, 16), np.float32)
+    s.set_image(z)
+    with pytest.raises(rds.RdsError):
+        s.set_fitting(0.5, 0.5)
+    with pytest.raises(rds.RdsError):
+        s.set_fitting(0.8, 0.2, 1.0, None)
+    s.set_fitting(0.8, 0.2)
+    for bad in [(0.0, 0.1, 0.125, 0.1, 1), (5.0, 0.0, 0.125, 0.1, 1), (5.0, 0.1, 0.2, 0.1, 1),
+                (5.0, 0.1, 0.125, -1.0, 1), (5.0, 0.1, 0.125, float("nan"), 1),
+                (5.0, 0.1, 0.125, 0.1, -1)]:
+        with pytest.raises(rds.RdsError) as ei:
+            s.solve(*bad)
+        assert ei.value.code == rds.RDS_EINVAL
+    zn = z.copy()
+    zn[3, 3] = np.nan
+    with pytest.raises(rds.RdsError):
+        s.set_image(zn)
+    with pytest.raises(rds.RdsError):
+        s.solve(5.0, 0.1, 0.125, 0.1, 1)
+    s.set_image(z)
+    s.solve(5.0, 0.1, 0.125, 0.1, 1)
+    s.close()
+
+
+def test_device_buffers_and_stream(rds, orc):
+    """torch CUDA tensors in/out (on_device=1) on a user stream give the same bytes as the
+    host path."""
+    import torch
+
+    cfg = wl.CONFIGS["C0"]
+    z, _ = wl.make_image(cfg)
+    host = gpu_solve(rds, z, None, cfg.c1, cfg.c2, 0.0, 5.0, cfg.theta, cfg.tau, np.inf, 200)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        zt = torch.from_numpy(z).cuda()
+        s = rds.Solver(*z.shape, stream=st.cuda_stream)
+        s.set_image(zt)
+        s.set_fitting(cfg.c1, cfg.c2)
+        s.solve(5.0, cfg.theta, cfg.tau, np.inf, 200)
+        ut = torch.empty(z.shape, dtype=torch.float32, device="cuda")
+        mt = torch.empty(z.shape, dtype=torch.uint8, device="cuda")
+        s.u(ut)
+        s.mask(mt)
+    st.synchronize()
+    assert ut.cpu().numpy().tobytes() == host["u"].tobytes()
+    assert mt.cpu().numpy().tobytes() == host["mask"].tobytes()
+    s.close()
