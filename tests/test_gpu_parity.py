@@ -257,7 +257,9 @@ def test_c3_full_properties(rds, orc):
         lab = orc.labels(f, delta)
         assert np.array_equal(g["labels"], lab)
         pn = np.sqrt(g["p1"].astype(np.float64) ** 2 + g["p2"].astype(np.float64) ** 2)
-        assert pn.max() <= 1 + 1e-6
+        # |rho| <= 1 is algebraic; float32 with MUFU sqrt/rcp leaves a few-ulp excess that
+        # can accumulate over K=1000 steps where tau|g| is small.
+        assert pn.max() <= 1 + 1e-5
         assert g["v"].min() >= 0 and g["v"].max() <= 1
         off = lab != 2
         u0 = (f <= 0).astype(np.float32)
