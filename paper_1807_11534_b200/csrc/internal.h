@@ -75,6 +75,7 @@ cudaError_t launch_item_flags(const int32_t *tile_rd, int H, int W, int rows, in
 cudaError_t launch_stencil(int kf, int stages, bool write_u, const StencilArgs &a,
                            int grid, cudaStream_t s);
 bool kf_supported(int kf);
+int stencil_warps_per_sm(int kf, int stages, bool aligned);  // resident warps per SM
 int kf_list(int32_t *out, int cap);
 
 struct EnergyArgs {

@@ -22,7 +22,7 @@ namespace {
 
 thread_local std::string g_last_error;
 
-constexpr int kDefaultKF = 7;
+constexpr int kDefaultKF = 5;
 constexpr int kDefaultRows = 128;
 
 }  // namespace
@@ -33,6 +33,7 @@ struct rds_handle {
     int64_t rows_alloc = 0;
     int64_t plane = 0;     // elements per plane
     int64_t origin = 0;    // element offset of pixel (0,0)
+    int n_sm = 148;
 
     // float planes (base pointers)
     float *z = nullptr, *P = nullptr, *f = nullptr, *c = nullptr, *u = nullptr;
@@ -144,6 +145,13 @@ int rds_create(int64_t H, int64_t W, rds_t **out) {
         return rc;
     }
     h->stream = h->own_stream;
+    {
+        int dev = 0, nsm = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+            nsm > 0)
+            h->n_sm = nsm;
+    }
 #define A(call)                                                                        \
     do {                                                                               \
         cudaError_t e_ = (call);                                                       \
@@ -360,6 +368,31 @@ static cudaError_t enqueue_loop(rds_t *h, int kf, int rows, int iters, int n_str
     return cudaSuccess;
 }
 
+// Rows per work item when not set: every item redoes a (2 KF + 3)-row warm-up, and items run
+// in waves of (resident warps per SM x SMs); pick the R minimising
+// waves(R) x (R + 2 KF + 3), preferring larger R on ties.
+static int auto_rows(rds_t *h, int kf, int iters) {
+    const int stages = iters >= kf ? kf : (iters > 0 ? iters : 1);
+    const int per_sm = stencil_warps_per_sm(kf, stages, (h->W & 3) == 0);
+    if (per_sm <= 0) return kDefaultRows;
+    const int64_t slots = (int64_t)per_sm * h->n_sm;
+    const int64_t strips = (h->W + wv_of(kf) - 1) / wv_of(kf);
+    int best = kDefaultRows;
+    double best_cost = 1e300;
+    for (int R = 32; R <= 512; R += 4) {
+        const int64_t items = strips * ((h->H + R - 1) / R);
+        const int64_t waves = (items + slots - 1) / slots;
+        const int64_t rows_eff = (R < h->H ? R : h->H) + 2 * kf + 3;
+        const double cost = (double)waves * rows_eff;
+        if (cost <= best_cost) {
+            best_cost = cost;
+            best = R;
+        }
+        if (R >= h->H) break;
+    }
+    return best;
+}
+
 int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32_t iters) {
     if (!h) return fail(nullptr, RDS_EINVAL, "rds_solve: NULL handle");
     if (!(lambda > 0.0f) || !isfinite(lambda))
@@ -377,8 +410,8 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
         return fail(h, RDS_EINVAL, "rds_solve: image or P has non-finite values");
 
     const int kf = h->opt_kf ? h->opt_kf : kDefaultKF;
-    const int rows = h->opt_rows ? h->opt_rows : kDefaultRows;
     const int wv = wv_of(kf);
+    const int rows = h->opt_rows ? h->opt_rows : auto_rows(h, kf, iters);
     const int n_strips = (int)((h->W + wv - 1) / wv);
     const int n_chunks = (int)((h->H + rows - 1) / rows);
     const int n_items = n_strips * n_chunks;

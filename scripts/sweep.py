@@ -1,0 +1,51 @@
+"""Tuning sweep of the stencil launch configuration (k_fuse x item_rows) on one config.
+Prints one JSON line per setting with the K-loop time (CUDA events, median of reps)."""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_1807_11534_b200 import rds  # noqa: E402
+from paper_1807_11534_b200 import workloads as wl  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C3")
+ap.add_argument("--kf", default="3,5,7")
+ap.add_argument("--rows", default="64,128,256")
+ap.add_argument("--delta", type=float, default=math.inf)
+ap.add_argument("--iters", type=int, default=0)
+ap.add_argument("--reps", type=int, default=3)
+args = ap.parse_args()
+
+cfg = wl.CONFIGS[args.config]
+K = args.iters or cfg.iters
+z, P = wl.make_image(cfg)
+st = torch.cuda.Stream()
+s = rds.Solver(cfg.H, cfg.W, stream=st.cuda_stream, timing=True)
+s.set_image(torch.from_numpy(z).cuda())
+s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, torch.from_numpy(P).cuda() if P is not None else None)
+am = s.absmax()
+delta = wl.band_delta(args.delta, am)
+for kf in [int(x) for x in args.kf.split(",")]:
+    for rows in [int(x) for x in args.rows.split(",")]:
+        s.set_option(rds.RDS_OPT_KFUSE, kf)
+        s.set_option(rds.RDS_OPT_ITEM_ROWS, rows)
+        s.solve(cfg.lambdas[0], cfg.theta, cfg.tau, delta, K)  # warm (graph capture)
+        s.stats()
+        ts = []
+        for _ in range(args.reps):
+            s.solve(cfg.lambdas[0], cfg.theta, cfg.tau, delta, K)
+            ts.append(s.stats()["loop_ms"])
+        info = s.stats()
+        lm = statistics.median(ts)
+        px = info["n_active_tiles"] * 1024
+        print(json.dumps({"config": args.config, "kf": kf, "rows": rows, "loop_ms": lm,
+                          "gpix_iter_s": px * K / lm / 1e6, "items": info["n_active_items"],
+                          "launches": info["launches"]}), flush=True)
+s.close()
