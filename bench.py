@@ -39,7 +39,7 @@ from paper_1807_11534_b200 import workloads as wl  # noqa: E402
 METRIC = "active Gpixel-iter/s at 4096^2 fp32 (restricted-domain dual iteration, C3 delta sweep)"
 UNIT = "Gpixel-iter/s"
 BYTES_PER_PX_ITER = 28  # read rho1, rho2, v, c (16 B) + write rho1, rho2, v (12 B)
-FLOPS_PER_PX_ITER = 26  # algorithmic FP32 operations of one iteration
+FLOPS_PER_PX_ITER = 24  # algorithmic FP32 operations of one iteration
 
 
 def parse():
@@ -112,6 +112,11 @@ def _cuda():
     import torch
 
     return torch.cuda.is_available()
+
+
+def throughput(total_work: float, t_ms: float) -> float:
+    """Whole-job Gpixel-iter/s: work summed over ranks / max-over-ranks device time."""
+    return total_work / (t_ms * 1e-3) / 1e9
 
 
 # ------------------------------------------------------------------------------------------
@@ -309,7 +314,7 @@ def run_ours(args, dist):
     work_step = sum(act_px[dr] for dr in cfg.delta_rels) * K
     rd_step = sum(rd_px[dr] for dr in cfg.delta_rels) * K
     total_work = dist.sum(work_step * args.steps)
-    value = total_work / (t_ms * 1e-3) / 1e9
+    value = throughput(total_work, t_ms)
     ms_per_step = t_ms / args.steps
 
     # stencil roofline: the K-loop is only stencil launches; average per-launch duration
@@ -350,10 +355,12 @@ def run_ours(args, dist):
     fp32_peak = 148 * 128 * 2 * clock_mhz * 1e6 / 1e12  # TFLOP/s at the observed SM clock
     achieved_tf = statistics.mean(flops_all) / (launch_ms * 1e-3) / 1e12
     st0 = info[0][1]
+    traffic = _traffic_from_profile(st0["k_fuse"])
     roofline = {
         "bound": "hbm", "kernel": "k_stencil", "achieved": achieved_gbs, "peak": hbm_peak,
         "unit": "GB/s", "frac": achieved_gbs / hbm_peak,
-        "traffic": _traffic_from_profile(),
+        "traffic": traffic,
+        "dram_frac": (traffic / (launch_ms * 1e-3) / 1e9 / hbm_peak) if traffic else None,
         "basis": (f"{BYTES_PER_PX_ITER} B per active pixel-iteration x (active px x "
                   f"{st0['k_fuse']} fused iterations) per launch / mean launch time "
                   f"{launch_ms:.4f} ms; peak = MEASURED_PEAKS.json hbm_gbs (measured copy)"),
@@ -435,13 +442,18 @@ def _peaks():
         return {}
 
 
-def _traffic_from_profile():
+def _traffic_from_profile(kf):
+    """dram__bytes_read.sum + dram__bytes_write.sum per stencil launch from the committed
+    ncu --set full capture of the same configuration (profiles/stencil_dram_bytes.json)."""
     path = os.path.join(ROOT, "profiles", "stencil_dram_bytes.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get("dram_bytes_per_launch")
+            d = json.load(fh)
+        if int(d.get("k_fuse", -1)) == int(kf):
+            return d.get("dram_bytes_per_launch")
     except Exception:
-        return None
+        pass
+    return None
 
 
 def main():

@@ -1,4 +1,5 @@
 """Summarise an ncu report: key throughput metrics, stall breakdown, SASS op mix."""
+import builtins
 import collections
 import csv
 import io
@@ -19,7 +20,13 @@ def run(cmd):
     return subprocess.run(cmd, capture_output=True, text=True).stdout
 
 
-def main(rep):
+def main(rep, out=None):
+    lines = []
+
+    def print(*a):  # noqa: A001 - tee into the summary file
+        builtins.print(*a)
+        lines.append(" ".join(str(x) for x in a))
+
     raw = list(csv.reader(io.StringIO(run(['ncu', '-i', rep, '--page', 'raw', '--csv']))))
     hdr, units, vals = raw[0], raw[1], raw[2]
     print(f"== {rep}: {vals[hdr.index('Kernel Name')][:90]}")
@@ -48,8 +55,37 @@ def main(rep):
     tot = sum(ops.values())
     print("  op mix (% of warp instr):", ", ".join(f"{k} {100*v/tot:.1f}" for k, v in ops.most_common(14)))
     print(f"  warp instructions executed: {tot/1e6:.2f} M")
+    get = {h: vals[i] for i, h in enumerate(hdr)}
+    res = {"kernel": get.get("Kernel Name"),
+           "gpu_time_us": float(get["gpu__time_duration.sum"]),
+           "dram_bytes_per_launch": (float(get["dram__bytes_read.sum"]) +
+                                     float(get["dram__bytes_write.sum"])) * _scale(units[hdr.index("dram__bytes_read.sum")]),
+           "issue_active_pct": float(get.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0) or 0),
+           "registers": int(float(get["launch__registers_per_thread"]))}
+    if out:
+        with open(out, "w") as fh:
+            fh.write("\n".join(lines) + "\n")
+    return res
+
+
+def _scale(unit):
+    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
 
 
 if __name__ == '__main__':
-    for rep in sys.argv[1:]:
-        main(rep)
+    import argparse
+    import json
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("reports", nargs="+")
+    ap.add_argument("--out", help="write the text summary of the (single) report here")
+    ap.add_argument("--json", help="write dram bytes per launch here (profiles/stencil_dram_bytes.json)")
+    ap.add_argument("--kf", type=int, default=0)
+    ap.add_argument("--config", default="")
+    a = ap.parse_args()
+    for rep in a.reports:
+        res = main(rep, a.out)
+        if a.json:
+            res.update({"k_fuse": a.kf, "config": a.config, "report": rep})
+            with open(a.json, "w") as fh:
+                json.dump(res, fh, indent=1)
