@@ -328,7 +328,7 @@ def run_ours(args, dist):
     for dr, st, e in info:
         lm = statistics.median(x["loop_ms"] for x in per[dr])
         sm = statistics.median(x["setup_ms"] for x in per[dr])
-        n_items = st["n_active_items"]
+        n_items = st["n_active_cells"]
         item_px = n_items * st["item_rows"] * st["item_cols"]
         launches = st["launches"]
         launch_ms_all.append(lm / launches)
@@ -340,7 +340,7 @@ def run_ours(args, dist):
             "loop_ms": lm, "setup_ms": sm,
             "active_tile_frac": st["n_active_tiles"] / st["n_tiles"],
             "rd_frac": st["n_rd"] / (cfg.H * cfg.W),
-            "active_item_frac": n_items / st["n_items"],
+            "active_cell_frac": n_items / st["n_items"], "work_items": st["n_active_items"],
             "tile_gpix_iter_s": px * K / (lm * 1e-3) / 1e9,
             "rd_gpix_iter_s": st["n_rd"] * K / (lm * 1e-3) / 1e9,
             "speedup_vs_full": (t_full / lm) if t_full else None,

@@ -73,13 +73,14 @@ typedef struct {
     int64_t n_rd;            /* pixels in RD (label 2) */
     int64_t n_tiles;         /* 32x32 tiles covering the image */
     int64_t n_active_tiles;  /* tiles containing an RD pixel */
-    int64_t n_items;         /* stencil work items (strip x row-chunk) covering the image */
-    int64_t n_active_items;  /* items overlapping an active tile (launched work) */
+    int64_t n_items;         /* strip x 32-row band cells covering the image */
+    int64_t n_active_items;  /* stencil work items launched (runs of active cells, split) */
+    int64_t n_active_cells;  /* strip x band cells overlapping an active tile */
     int32_t iters;           /* K of the last solve */
     int32_t k_fuse;          /* iterations fused per HBM round trip */
     int32_t launches;        /* stencil launches in the K-loop */
-    int32_t item_rows;       /* output rows per work item */
-    int32_t item_cols;       /* output columns per work item */
+    int32_t item_rows;       /* maximum output rows per work item (chosen per solve) */
+    int32_t item_cols;       /* output columns per work item (strip width) */
     int32_t pad_;
     float setup_ms;          /* fused fitting/band/init + compaction */
     float loop_ms;           /* the K-loop (all stencil launches) */
@@ -88,10 +89,13 @@ typedef struct {
 /* Options (rds_set_option). */
 #define RDS_OPT_KFUSE 1      /* iterations per HBM round trip; 0 = library default; allowed
                                 values are listed by rds_kfuse_supported */
-#define RDS_OPT_ITEM_ROWS 2  /* output rows per stencil work item; 0 = default */
+#define RDS_OPT_ITEM_ROWS 2  /* maximum output rows per stencil work item (rounded up to a
+                                multiple of 32); 0 = automatic (about one item per resident
+                                warp, 64..512 rows) */
 #define RDS_OPT_TIMING 3     /* 1 = record setup/loop CUDA-event times in rds_stats_t */
-#define RDS_OPT_SKIP 4       /* 1 (default) = launch only items overlapping active tiles;
-                                0 = process every item (restriction without tile skipping) */
+#define RDS_OPT_SKIP 4       /* 1 (default) = work only on strip x band cells overlapping
+                                active tiles; 0 = process every cell (restriction without
+                                tile skipping) */
 #define RDS_OPT_GRAPH 5      /* 1 (default) = replay the K-loop as a CUDA graph */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.

@@ -28,18 +28,24 @@ __host__ __device__ constexpr int lh_of(int kf) { return 4 * ((kf + 1 + 3) / 4);
 __host__ __device__ constexpr int rh_of(int kf) { return 4 * ((kf + 3) / 4); }
 __host__ __device__ constexpr int wv_of(int kf) { return 128 - lh_of(kf) - rh_of(kf); }
 
+// A stencil work item: output columns [strip*WV, (strip+1)*WV) and output rows
+// [b0*TILE_H, min(H, b1*TILE_H)) -- a piece of a vertical run of active 32-row bands.
+struct Item {
+    int32_t strip;
+    int32_t bands;  // b0 | (b1 << 16)
+};
+
 struct StencilArgs {
     const float *p1_in, *p2_in, *v_in;   // plane origins (pixel (0,0))
     const float *c;                      // theta*lambda*f on RD, -inf on Fg, +inf on Bg/frame
     float *p1_out, *p2_out, *v_out;
     float *u_out;                        // only written when WRITE_U
     uint8_t *mask_out;                   // only written when WRITE_U
-    const int32_t *items;                // active items, ascending (chunk-major)
+    const Item *items;                   // active items (strip-major, runs split in chunks)
     const int32_t *n_items;              // device count
+    int32_t *queue;                      // this launch's work counter (zeroed before the loop)
     int64_t pitch;
     int H, W;
-    int rows;                            // output rows per item
-    int n_strips;
     float tau, theta, inv_theta;
 };
 
@@ -68,14 +74,22 @@ cudaError_t launch_setup(const SetupArgs &a, cudaStream_t s);
 // counts[0] = number of nonzero flags; if sum_out != null also the int64 sum of the values.
 cudaError_t launch_compact(const int32_t *flags, int n, int32_t *list, int32_t *count,
                            long long *sum_out, cudaStream_t s);
-cudaError_t launch_item_flags(const int32_t *tile_rd, int H, int W, int rows, int wv,
-                              int n_strips, int n_chunks, int skip, int32_t *item_flag,
-                              cudaStream_t s);
+// band_flag[s * n_bands + b] = 1 iff strip s (output columns [s*wv, (s+1)*wv)) overlaps an
+// active 32x32 tile in tile row b (skip = 0 marks everything active).
+cudaError_t launch_band_flags(const int32_t *tile_rd, int H, int W, int wv, int n_strips,
+                              int skip, int32_t *band_flag, cudaStream_t s);
+// Work items from the band flags: maximal vertical runs of active bands per strip, each split
+// into near-equal pieces of <= chunk bands.  chunk = fixed_chunk if > 0, else the chunk in
+// [1, 16] minimising max(items, slots) * (32 chunk + warmup_rows) (makespan model).
+// out: items, counts[1] = number of items, counts[2] = chunk used, counts[3] = active cells.
+cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands,
+                               int slots, int fixed_chunk, int warmup_rows, Item *items,
+                               int32_t *counts, cudaStream_t s);
 
 cudaError_t launch_stencil(int kf, int stages, bool write_u, const StencilArgs &a,
                            int grid, cudaStream_t s);
+int stencil_blocks_per_sm(int kf, int stages, bool aligned);
 bool kf_supported(int kf);
-int stencil_warps_per_sm(int kf, int stages, bool aligned);  // resident warps per SM
 int kf_list(int32_t *out, int cap);
 
 struct EnergyArgs {

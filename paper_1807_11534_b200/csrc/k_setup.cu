@@ -1,7 +1,8 @@
 // k_setup.cu -- per-solve setup kernels of librds (sm_100a):
 //   K1 k_setup      fused fitting term + band test + initialisation + per-tile RD counts
-//   K2 k_compact    warp-ballot / prefix-sum compaction of tile and work-item flags
-//      k_item_flags work item (strip x row chunk) is active iff it overlaps an active tile
+//   K2 k_compact    warp-ballot / prefix-sum compaction of the active-tile list
+//      k_band_flags / k_build_items: stencil work items = runs of active 32-row bands per
+//                   column strip, split into near-equal pieces
 //   plus the absmax reduction (delta = delta_rel * max|f|) and the finiteness check.
 //
 // PAPER.md references: fitting term Eq. 2-3; partition;
@@ -231,38 +232,141 @@ cudaError_t launch_compact(const int32_t *flags, int n, int32_t *list, int32_t *
     return cudaGetLastError();
 }
 
-// Work item (chunk b, strip s) covers output rows [b*rows, (b+1)*rows) and columns
-// [s*wv, (s+1)*wv); it is active iff one of the 32x32 tiles it overlaps holds an RD pixel.
-// Processing a pinned pixel reproduces its value exactly, so any superset of the needed
-// items gives the same result; skip = 0 marks every item active.
-__global__ void k_item_flags(const int32_t *tile_rd, int H, int W, int rows, int wv,
-                             int n_strips, int n_chunks, int skip, int32_t *item_flag) {
+// A strip's band b is active iff one of the 32x32 tiles its output columns overlap in tile
+// row b holds an RD pixel.  Processing a pinned pixel reproduces its value exactly, so any
+// superset of the needed work gives the same result; skip = 0 marks every band active.
+__global__ void k_band_flags(const int32_t *tile_rd, int H, int W, int wv, int n_strips,
+                             int skip, int32_t *band_flag) {
+    const int n_bands = (H + TILE_H - 1) / TILE_H;
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (it >= n_strips * n_chunks) return;
-    const int b = it / n_strips, s = it - b * n_strips;
+    if (it >= n_strips * n_bands) return;
+    const int s = it / n_bands, b = it - s * n_bands;
     if (!skip) {
-        item_flag[it] = 1;
+        band_flag[it] = 1;
         return;
     }
     const int ntj = (W + TILE_W - 1) / TILE_W;
-    const int i0 = b * rows, i1 = min(H, (b + 1) * rows) - 1;
     const int j0 = s * wv, j1 = min(W, (s + 1) * wv) - 1;
     int on = 0;
-    for (int ti = i0 / TILE_H; ti <= i1 / TILE_H && !on; ++ti)
-        for (int tj = j0 / TILE_W; tj <= j1 / TILE_W; ++tj)
-            if (tile_rd[ti * ntj + tj]) {
-                on = 1;
-                break;
-            }
-    item_flag[it] = on;
+    for (int tj = j0 / TILE_W; tj <= j1 / TILE_W; ++tj) on |= tile_rd[b * ntj + tj] != 0;
+    band_flag[it] = on;
 }
 
-cudaError_t launch_item_flags(const int32_t *tile_rd, int H, int W, int rows, int wv,
-                              int n_strips, int n_chunks, int skip, int32_t *item_flag,
-                              cudaStream_t s) {
-    const int n = n_strips * n_chunks;
-    k_item_flags<<<(n + 255) / 256, 256, 0, s>>>(tile_rd, H, W, rows, wv, n_strips, n_chunks,
-                                                  skip, item_flag);
+cudaError_t launch_band_flags(const int32_t *tile_rd, int H, int W, int wv, int n_strips,
+                              int skip, int32_t *band_flag, cudaStream_t s) {
+    const int n = n_strips * ((H + TILE_H - 1) / TILE_H);
+    k_band_flags<<<(n + 255) / 256, 256, 0, s>>>(tile_rd, H, W, wv, n_strips, skip, band_flag);
+    return cudaGetLastError();
+}
+
+// Runs of active bands in strip s, split into pieces; emit == false only counts.
+__device__ int strip_items(const int32_t *flags, int n_bands, int chunk, int s, Item *out) {
+    int n = 0, b = 0;
+    while (b < n_bands) {
+        if (!flags[b]) {
+            ++b;
+            continue;
+        }
+        int e = b;
+        while (e < n_bands && flags[e]) ++e;
+        const int len = e - b, pieces = (len + chunk - 1) / chunk;
+        for (int k = 0; k < pieces; ++k) {
+            if (out) {
+                const int p0 = b + (int)((int64_t)k * len / pieces);
+                const int p1 = b + (int)((int64_t)(k + 1) * len / pieces);
+                out[n] = Item{s, p0 | (p1 << 16)};
+            }
+            ++n;
+        }
+        b = e;
+    }
+    return n;
+}
+
+// Single CTA: total active bands -> chunk; per-strip item counts -> block exclusive scan ->
+// items written in strip-major, ascending-row order (deterministic, no atomics).
+__global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, int n_strips,
+                                                      int n_bands, int slots, int fixed_chunk,
+                                                      int warmup_rows, Item *items,
+                                                      int32_t *counts) {
+    __shared__ long long red[32];
+    __shared__ int off[32];
+    __shared__ int chunk_s, base_s;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    long long tot = 0;
+    for (int i = tid; i < n_strips * n_bands; i += 1024) tot += band_flag[i] != 0;
+    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) red[wid] = tot;
+    __syncthreads();
+    if (tid == 0) {
+        long long t = 0;
+        for (int w = 0; w < 32; ++w) t += red[w];
+        int c = fixed_chunk;
+        if (c <= 0) {
+            // makespan model: items ~ t / c, each costing the chunk's rows plus the pipeline
+            // warm-up (2 KF + 4 rows)
+            const long long sl = slots > 0 ? slots : 1;
+            long long best = -1;
+            for (int cc = 1; cc <= 16; ++cc) {
+                // fractional rounds once over-subscribed (the queue is work-conserving), one
+                // latency-bound round below that
+                const long long items = (t + cc - 1) / cc;
+                const long long cost = (items > sl ? items : sl) * (cc * TILE_H + warmup_rows);
+                if (best < 0 || cost < best) {
+                    best = cost;
+                    c = cc;
+                }
+            }
+        }
+        chunk_s = c;
+        base_s = 0;
+    }
+    __syncthreads();
+    const int chunk = chunk_s;
+    for (int s0 = 0; s0 < n_strips; s0 += 1024) {
+        const int s = s0 + tid;
+        const int cnt = s < n_strips ? strip_items(band_flag + (int64_t)s * n_bands, n_bands,
+                                                   chunk, s, nullptr)
+                                     : 0;
+        // block exclusive scan of cnt
+        int incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) off[wid] = incl;
+        __syncthreads();
+        if (wid == 0) {
+            const int t = off[lane];
+            int in2 = t;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, in2, o);
+                if (lane >= o) in2 += y;
+            }
+            off[lane] = in2 - t;
+        }
+        __syncthreads();
+        const int start = base_s + off[wid] + incl - cnt;
+        if (s < n_strips)
+            strip_items(band_flag + (int64_t)s * n_bands, n_bands, chunk, s, items + start);
+        __syncthreads();
+        if (tid == 1023) base_s = start + cnt;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        counts[1] = base_s;
+        counts[2] = chunk;
+        long long t = 0;
+        for (int w = 0; w < 32; ++w) t += red[w];
+        counts[3] = (int32_t)t;
+    }
+}
+
+cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands,
+                               int slots, int fixed_chunk, int warmup_rows, Item *items,
+                               int32_t *counts, cudaStream_t s) {
+    k_build_items<<<1, 1024, 0, s>>>(band_flag, n_strips, n_bands, slots, fixed_chunk,
+                                     warmup_rows, items, counts);
     return cudaGetLastError();
 }
 

@@ -264,55 +264,59 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
     constexpr int LH = lh_of(KF), WV = wv_of(KF);
     constexpr int SP = Split<S>::value;
     extern __shared__ float4 smem[];  // [warps][RING][3][32] then [warps][2 CR][32]
-    float4 *ring = smem;
-    float4 *cring = smem + STENCIL_WARPS * RING * 96;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int widx = blockIdx.x * STENCIL_WARPS + warp;
-    if (widx >= *a.n_items) return;  // warp-uniform exit
-    const int item = a.items[widx];
-    const int b = item / a.n_strips, s = item - b * a.n_strips;
+    const int n_items = *a.n_items;
     Ctx x;
-    x.R0 = b * a.rows;
-    x.Rend = min(x.R0 + a.rows, a.H);
-    x.col = s * WV - LH + 4 * lane;
-    x.store_lane = (4 * lane >= LH) && (4 * lane < LH + WV);
-    x.right_edge = (x.col + 3 == a.W - 1);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) x.kx[e] = (x.col + e == a.W - 1) ? 0.0f : 1.0f;
     x.pitch = a.pitch;
     x.H = a.H;
     x.tau = a.tau;
     x.theta = a.theta;
     x.inv_theta = a.inv_theta;
-    x.p1i = a.p1_in + x.col;
-    x.p2i = a.p2_in + x.col;
-    x.vi = a.v_in + x.col;
-    x.ci = a.c + x.col;
     x.p1o = a.p1_out;
     x.p2o = a.p2_out;
     x.vo = a.v_out;
     x.uo = a.u_out;
     x.mo = a.mask_out;
-    x.ring = ring + warp * RING * 96 + lane;
-    x.cring = cring + warp * 2 * CR * 32 + lane;
-
-    // input rows [n, n_last]; the cone reaches S+1 rows up and S rows down, the delay
-    // buffer adds one row of latency.  The step count is made even (one extra warm-up row)
-    // for the two-state unrolled loop.
-    x.n_last = x.Rend - 1 + S + (SP ? 1 : 0);
-    int n = x.R0 - (S + 1);
-    if (((x.n_last - n + 1) & 1) != 0) --n;
+    x.ring = smem + warp * RING * 96 + lane;
+    x.cring = smem + STENCIL_WARPS * RING * 96 + warp * 2 * CR * 32 + lane;
+    // persistent warps: fetch items from this launch's queue until it is drained
+    for (;;) {
+        int it = 0;
+        if (lane == 0) it = atomicAdd(a.queue, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= n_items) break;  // warp-uniform
+        const Item item = a.items[it];
+        const int b0 = item.bands & 0xffff, b1 = item.bands >> 16;
+        x.R0 = b0 * TILE_H;
+        x.Rend = min(b1 * TILE_H, a.H);
+        x.col = item.strip * WV - LH + 4 * lane;
+        x.store_lane = (4 * lane >= LH) && (4 * lane < LH + WV);
+        x.right_edge = (x.col + 3 == a.W - 1);
 #pragma unroll
-    for (int r = 0; r < RING; ++r) {
-        if (n + r <= x.n_last) stage_row(x, n + r);
-        cp_async_commit();
+        for (int e = 0; e < 4; ++e) x.kx[e] = (x.col + e == a.W - 1) ? 0.0f : 1.0f;
+        x.p1i = a.p1_in + x.col;
+        x.p2i = a.p2_in + x.col;
+        x.vi = a.v_in + x.col;
+        x.ci = a.c + x.col;
+        // input rows [n, n_last]; the cone reaches S+1 rows up and S rows down, the delay
+        // buffer adds one row of latency.  The step count is made even (one extra warm-up
+        // row) for the two-state unrolled loop.
+        x.n_last = x.Rend - 1 + S + (SP ? 1 : 0);
+        int n = x.R0 - (S + 1);
+        if (((x.n_last - n + 1) & 1) != 0) --n;
+#pragma unroll
+        for (int r = 0; r < RING; ++r) {
+            if (n + r <= x.n_last) stage_row(x, n + r);
+            cp_async_commit();
+        }
+        // the Neumann row H-1 matters whenever the march (cone included) reaches it
+        if (x.n_last >= a.H - 1)
+            march<S, WRITE_U, ALIGNED, true>(x, n);
+        else
+            march<S, WRITE_U, ALIGNED, false>(x, n);
+        cp_async_wait<0>();
+        __syncwarp();
     }
-    // the Neumann row H-1 matters whenever the march (cone included) reaches it
-    if (x.n_last >= a.H - 1)
-        march<S, WRITE_U, ALIGNED, true>(x, n);
-    else
-        march<S, WRITE_U, ALIGNED, false>(x, n);
-    cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -372,14 +376,14 @@ int kf_list(int32_t *out, int cap) {
     return n;
 }
 
-int stencil_warps_per_sm(int kf, int stages, bool aligned) {
+int stencil_blocks_per_sm(int kf, int stages, bool aligned) {
     StencilFn fn = lookup(kf, stages, false, aligned);
     if (!fn) return 0;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, STENCIL_WARPS * 32,
                                                       STENCIL_SMEM) != cudaSuccess)
         return 0;
-    return nb * STENCIL_WARPS;
+    return nb;
 }
 
 cudaError_t launch_stencil(int kf, int stages, bool write_u, const StencilArgs &a, int grid,

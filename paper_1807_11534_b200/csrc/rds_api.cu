@@ -22,8 +22,7 @@ namespace {
 
 thread_local std::string g_last_error;
 
-constexpr int kDefaultKF = 5;
-constexpr int kDefaultRows = 128;
+constexpr int kDefaultKF = 6;
 
 }  // namespace
 
@@ -43,9 +42,12 @@ struct rds_handle {
     // tiles / items
     int n_tiles = 0;
     int32_t *tile_rd = nullptr, *tile_list = nullptr;
-    int32_t *item_flag = nullptr, *item_list = nullptr;
-    int items_cap = 0;
-    int32_t *counts = nullptr;       // [0] active tiles, [1] active items
+    int32_t *band_flag = nullptr;    // [strip][band] active flags
+    Item *items = nullptr;           // stencil work items
+    int32_t *queue = nullptr;        // per-launch work counters
+    size_t band_bytes = 0, items_bytes = 0, queue_bytes = 0;
+    int bps[16][16] = {};            // cached stencil CTAs per SM [kf][stages]
+    int32_t *counts = nullptr;       // [0] active tiles, [1] items, [2] chunk (bands)
     long long *n_rd_dev = nullptr;
     unsigned *absmax_bits = nullptr;
     int *flag = nullptr;
@@ -66,7 +68,7 @@ struct rds_handle {
     // cached CUDA graph of the K-loop
     cudaGraphExec_t graph = nullptr;
     struct Key {
-        int kf, rows, iters, cur0, n_strips, n_chunks;
+        int kf, iters, cur0, max_items;
         float tau, theta;
         bool operator==(const Key &o) const { return memcmp(this, &o, sizeof(Key)) == 0; }
     } gkey{};
@@ -102,9 +104,9 @@ static void free_all(rds_t *h) {
                    h->p2[0], h->p2[1], h->v[0], h->v[1], h->wv, h->wp1,   h->wp2};
     for (float *p : fl)
         if (p) cudaFree(p);
-    void *other[] = {h->lab,      h->mask,      h->tile_rd, h->tile_list,   h->item_flag,
-                     h->item_list, h->counts,   h->n_rd_dev, h->absmax_bits, h->flag,
-                     h->e_partials, h->e_out};
+    void *other[] = {h->lab,     h->mask,        h->tile_rd, h->tile_list, h->band_flag,
+                     h->items,   h->queue,       h->counts,  h->n_rd_dev,  h->absmax_bits,
+                     h->flag,    h->e_partials,  h->e_out};
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -332,25 +334,34 @@ int rds_fitting_absmax(rds_t *h, float *out) {
     return RDS_OK;
 }
 
-// Enqueue the K-loop: ceil(iters/kf) stencil launches (the last one writes u and mask).
-static cudaError_t enqueue_loop(rds_t *h, int kf, int rows, int iters, int n_strips,
-                                int n_chunks, float tau, float theta) {
+// Resident stencil CTAs per SM for (kf, stages), cached (occupancy API).
+static int blocks_per_sm(rds_t *h, int kf, int stages) {
+    const bool aligned = (h->W & 3) == 0;
+    int &slot = h->bps[kf][stages];
+    if (slot <= 0) slot = stencil_blocks_per_sm(kf, stages, aligned);
+    return slot > 0 ? slot : 1;
+}
+
+// Enqueue the K-loop: zero the per-launch work queues, then ceil(iters/kf) persistent
+// stencil launches on ping-pong buffers (the last one also writes u and mask).
+static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, float tau,
+                                float theta) {
+    const int launches = (iters + kf - 1) / kf;
+    cudaError_t e = cudaMemsetAsync(h->queue, 0, sizeof(int32_t) * launches, h->stream);
+    if (e != cudaSuccess) return e;
     StencilArgs a{};
     a.c = h->at(h->c);
     a.u_out = h->at(h->u);
     a.mask_out = h->at(h->mask);
-    a.items = h->item_list;
+    a.items = h->items;
     a.n_items = h->counts + 1;
     a.pitch = h->pitch;
     a.H = (int)h->H;
     a.W = (int)h->W;
-    a.rows = rows;
-    a.n_strips = n_strips;
     a.tau = tau;
     a.theta = theta;
     a.inv_theta = 1.0f / theta;
-    const int grid = (n_strips * n_chunks + STENCIL_WARPS - 1) / STENCIL_WARPS;
-    int done = 0, cur = h->cur;
+    int done = 0, cur = h->cur, l = 0;
     while (done < iters) {
         const int stages = (iters - done) >= kf ? kf : (iters - done);
         const bool last = done + stages == iters;
@@ -360,37 +371,27 @@ static cudaError_t enqueue_loop(rds_t *h, int kf, int rows, int iters, int n_str
         a.p1_out = h->at(h->p1[cur ^ 1]);
         a.p2_out = h->at(h->p2[cur ^ 1]);
         a.v_out = h->at(h->v[cur ^ 1]);
-        cudaError_t e = launch_stencil(kf, stages, last, a, grid, h->stream);
+        a.queue = h->queue + l;
+        int grid = h->n_sm * blocks_per_sm(h, kf, stages);
+        const int need = (max_items + STENCIL_WARPS - 1) / STENCIL_WARPS;
+        if (grid > need) grid = need;
+        e = launch_stencil(kf, stages, last, a, grid, h->stream);
         if (e != cudaSuccess) return e;
         cur ^= 1;
         done += stages;
+        ++l;
     }
     return cudaSuccess;
 }
 
-// Rows per work item when not set: every item redoes a (2 KF + 3)-row warm-up, and items run
-// in waves of (resident warps per SM x SMs); pick the R minimising
-// waves(R) x (R + 2 KF + 3), preferring larger R on ties.
-static int auto_rows(rds_t *h, int kf, int iters) {
-    const int stages = iters >= kf ? kf : (iters > 0 ? iters : 1);
-    const int per_sm = stencil_warps_per_sm(kf, stages, (h->W & 3) == 0);
-    if (per_sm <= 0) return kDefaultRows;
-    const int64_t slots = (int64_t)per_sm * h->n_sm;
-    const int64_t strips = (h->W + wv_of(kf) - 1) / wv_of(kf);
-    int best = kDefaultRows;
-    double best_cost = 1e300;
-    for (int R = 32; R <= 512; R += 4) {
-        const int64_t items = strips * ((h->H + R - 1) / R);
-        const int64_t waves = (items + slots - 1) / slots;
-        const int64_t rows_eff = (R < h->H ? R : h->H) + 2 * kf + 3;
-        const double cost = (double)waves * rows_eff;
-        if (cost <= best_cost) {
-            best_cost = cost;
-            best = R;
-        }
-        if (R >= h->H) break;
-    }
-    return best;
+static cudaError_t grow(void **p, size_t *cap, size_t bytes) {
+    if (bytes <= *cap) return cudaSuccess;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    *cap = 0;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaSuccess) *cap = bytes;
+    return e;
 }
 
 int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32_t iters) {
@@ -411,19 +412,22 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
 
     const int kf = h->opt_kf ? h->opt_kf : kDefaultKF;
     const int wv = wv_of(kf);
-    const int rows = h->opt_rows ? h->opt_rows : auto_rows(h, kf, iters);
     const int n_strips = (int)((h->W + wv - 1) / wv);
-    const int n_chunks = (int)((h->H + rows - 1) / rows);
-    const int n_items = n_strips * n_chunks;
-    if (n_items > h->items_cap) {
-        if (h->item_flag) cudaFree(h->item_flag);
-        if (h->item_list) cudaFree(h->item_list);
-        h->item_flag = h->item_list = nullptr;
-        h->items_cap = 0;
-        CK(h, cudaMalloc(&h->item_flag, sizeof(int32_t) * n_items));
-        CK(h, cudaMalloc(&h->item_list, sizeof(int32_t) * n_items));
-        h->items_cap = n_items;
-        if (h->graph) {
+    const int n_bands = (int)((h->H + TILE_H - 1) / TILE_H);
+    const int max_items = n_strips * n_bands;
+    const int fixed_chunk = h->opt_rows ? (h->opt_rows + TILE_H - 1) / TILE_H : 0;
+    const int launches = (iters + kf - 1) / kf;
+    {
+        void *pf = h->band_flag, *pi = h->items, *pq = h->queue;
+        const bool realloc_items = sizeof(Item) * (size_t)max_items > h->items_bytes;
+        const bool realloc_queue = sizeof(int32_t) * (size_t)(launches + 1) > h->queue_bytes;
+        CK(h, grow(&pf, &h->band_bytes, sizeof(int32_t) * (size_t)max_items));
+        CK(h, grow(&pi, &h->items_bytes, sizeof(Item) * (size_t)max_items));
+        CK(h, grow(&pq, &h->queue_bytes, sizeof(int32_t) * (size_t)(launches + 1)));
+        h->band_flag = (int32_t *)pf;
+        h->items = (Item *)pi;
+        h->queue = (int32_t *)pq;
+        if ((realloc_items || realloc_queue) && h->graph) {
             cudaGraphExecDestroy(h->graph);
             h->graph = nullptr;
         }
@@ -461,17 +465,19 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
     CK(h, launch_setup(s, h->stream));
     CK(h, launch_compact(h->tile_rd, h->n_tiles, h->tile_list, h->counts + 0, h->n_rd_dev,
                          h->stream));
-    CK(h, launch_item_flags(h->tile_rd, (int)h->H, (int)h->W, rows, wv, n_strips, n_chunks,
-                            h->opt_skip, h->item_flag, h->stream));
-    CK(h, launch_compact(h->item_flag, n_items, h->item_list, h->counts + 1, nullptr,
-                         h->stream));
+    CK(h, launch_band_flags(h->tile_rd, (int)h->H, (int)h->W, wv, n_strips, h->opt_skip,
+                            h->band_flag, h->stream));
+    {
+        const int slots = h->n_sm * blocks_per_sm(h, kf, kf) * STENCIL_WARPS;
+        CK(h, launch_build_items(h->band_flag, n_strips, n_bands, slots, fixed_chunk,
+                                 2 * kf + 4, h->items, h->counts, h->stream));
+    }
     h->warm_pending = false;
     h->cur = 0;
     if (h->opt_timing) CK(h, cudaEventRecord(h->ev[1], h->stream));
 
     if (iters > 0) {
-        rds_handle::Key key{kf, rows, iters, h->cur, n_strips, n_chunks, tau, theta};
-        const int launches = (iters + kf - 1) / kf;
+        rds_handle::Key key{kf, iters, h->cur, max_items, tau, theta};
         if (h->opt_graph && launches > 1) {
             if (!h->graph || !(h->gkey == key)) {
                 if (h->graph) {
@@ -485,8 +491,7 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
                 if (e == cudaSuccess) {
                     cudaStream_t keep = h->stream;
                     h->stream = cap;
-                    cudaError_t e2 = enqueue_loop(h, kf, rows, iters, n_strips, n_chunks, tau,
-                                                  theta);
+                    cudaError_t e2 = enqueue_loop(h, kf, iters, max_items, tau, theta);
                     h->stream = keep;
                     e = cudaStreamEndCapture(cap, &g);
                     if (e == cudaSuccess) e = e2;
@@ -501,7 +506,7 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
             }
             CK(h, cudaGraphLaunch(h->graph, h->stream));
         } else {
-            CK(h, enqueue_loop(h, kf, rows, iters, n_strips, n_chunks, tau, theta));
+            CK(h, enqueue_loop(h, kf, iters, max_items, tau, theta));
         }
         if (launches & 1) h->cur ^= 1;
     }
@@ -515,11 +520,11 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
     st.H = h->H;
     st.W = h->W;
     st.n_tiles = h->n_tiles;
-    st.n_items = n_items;
+    st.n_items = max_items;
     st.iters = iters;
     st.k_fuse = kf;
     st.launches = (iters + kf - 1) / kf;
-    st.item_rows = rows;
+    st.item_rows = 0;  // filled by rds_get_stats (chosen on the device)
     st.item_cols = wv;
     st.setup_ms = st.loop_ms = -1.0f;
     return RDS_OK;
@@ -632,13 +637,15 @@ int rds_energy(rds_t *h, rds_energy_t *out) {
 int rds_get_stats(rds_t *h, rds_stats_t *out) {
     NEED_SOLVED("rds_get_stats");
     if (!out) return fail(h, RDS_EINVAL, "rds_get_stats: NULL out");
-    int32_t cnt[2];
+    int32_t cnt[4];
     long long nrd = 0;
     CK(h, cudaMemcpyAsync(cnt, h->counts, sizeof cnt, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaMemcpyAsync(&nrd, h->n_rd_dev, sizeof nrd, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     h->stats.n_active_tiles = cnt[0];
     h->stats.n_active_items = cnt[1];
+    h->stats.item_rows = cnt[2] * TILE_H;
+    h->stats.n_active_cells = cnt[3];
     h->stats.n_rd = nrd;
     if (h->opt_timing) {
         CK(h, cudaEventElapsedTime(&h->stats.setup_ms, h->ev[0], h->ev[1]));

@@ -49,6 +49,7 @@ class rds_stats_t(ctypes.Structure):
     _fields_ = [("H", ctypes.c_int64), ("W", ctypes.c_int64), ("n_rd", ctypes.c_int64),
                 ("n_tiles", ctypes.c_int64), ("n_active_tiles", ctypes.c_int64),
                 ("n_items", ctypes.c_int64), ("n_active_items", ctypes.c_int64),
+                ("n_active_cells", ctypes.c_int64),
                 ("iters", ctypes.c_int32), ("k_fuse", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("item_rows", ctypes.c_int32),
                 ("item_cols", ctypes.c_int32), ("pad_", ctypes.c_int32),

@@ -56,7 +56,7 @@ for skip in (1, 0):
             "iters": K, "loop_ms": lm, "setup_ms": sm, "speedup_vs_full": full / lm,
             "rd_frac": x["n_rd"] / (cfg.H * cfg.W),
             "tile_frac": x["n_active_tiles"] / x["n_tiles"],
-            "item_frac": x["n_active_items"] / x["n_items"], "items": x["n_items"],
+            "cell_frac": x["n_active_cells"] / x["n_items"], "items": x["n_active_items"],
             "item_rows": x["item_rows"], "k_fuse": x["k_fuse"],
             "tile_gpix_iter_s": x["n_active_tiles"] * 1024 * K / lm / 1e6,
             "rd_gpix_iter_s": x["n_rd"] * K / lm / 1e6}), flush=True)
