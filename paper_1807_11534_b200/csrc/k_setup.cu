@@ -122,7 +122,10 @@ __global__ void __launch_bounds__(256) k_setup(SetupArgs a) {
                 const float u0 = fg ? 1.0f : 0.0f;
                 f[e] = fe;
                 lab[e] = rd ? 2 : (fg ? 1 : 0);
-                c[e] = rd ? __fmul_rn(a.theta_lambda, fe) : (fg ? -INFINITY : INFINITY);
+                // RD: theta*lambda*f clamped to +-2^20 (the v-step saturates far earlier:
+                // |u| <= max|v| + 4 theta), so |c| * 2^-120 is negligible in the stencil
+                c[e] = rd ? fminf(fmaxf(__fmul_rn(a.theta_lambda, fe), -0x1p20f), 0x1p20f)
+                          : (fg ? -INFINITY : INFINITY);
                 u[e] = u0;
                 msk[e] = fg ? 1 : 0;
                 const bool warm = rd && a.wv != nullptr;

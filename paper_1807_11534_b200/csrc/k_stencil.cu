@@ -9,7 +9,8 @@
 // with grad = forward differences (zero on row H-1 / column W-1) and div = -grad^T
 // (reading R-C6).  The label and theta*lambda*f are folded into one float c per pixel:
 // c = theta*lambda*f on RD, -inf on Fg, +inf on Bg and on the frame, so
-// sat(u - c) (FADD.SAT) reproduces the pinned u0 exactly and "RD" is |c| < inf.
+// sat(u - c) (FADD.SAT) reproduces the pinned u0 exactly, and |c| * 2^-120 under the
+// square root of |grad w| makes rho's update factor exactly 0 off RD.
 //
 // Execution model.  Each warp owns one work item: a strip of 128 columns
 // (4 per lane, float4 loads/stores, 512 B per row per array) of which WV = wv_of(KF) are
@@ -135,10 +136,12 @@ __device__ __forceinline__ void stage(const float (&ap1)[4], const float (&ap2)[
         if (LAST) g1 = last_row ? 0.0f : g1;
         float g2 = (e < 3 ? aw[e + 1] : wr) - aw[e];
         if (!ALIGNED) g2 *= x.kx[e];
-        float rr = rcp_approx(fmaf(x.tau, sqrt_approx(fmaf(g1, g1, g2 * g2)), 1.0f));
-        // rho = 0 off RD: c = +-inf there, so c*0 = NaN and max(NaN, 0) = 0; on RD
-        // c*0 + rr = rr (no predicate registers needed)
-        rr = fmaxf(fmaf(cc[e], 0.0f, rr), 0.0f);
+        // rho = 0 off RD without predicates: c = +-inf there, so |c| * 2^-120 = inf enters
+        // the square root and rr = 1 / (1 + tau inf) = 0.  On RD |c| <= 2^20 (clamped in K1),
+        // so the added |c| * 2^-120 <= 2^-100 is far below float32 resolution of g^2 + ...
+        const float e_rd = fabsf(cc[e]) * 0x1p-120f;
+        const float rr =
+            rcp_approx(fmaf(x.tau, sqrt_approx(fmaf(g1, g1, fmaf(g2, g2, e_rd))), 1.0f));
         o1[e] = fmaf(x.tau, g1, ap1[e]) * rr;
         o2[e] = fmaf(x.tau, g2, ap2[e]) * rr;
     }
