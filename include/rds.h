@@ -131,6 +131,18 @@ int rds_set_state(rds_t *h, const float *v, const float *rho1, const float *rho2
  * Errors: RDS_ESTATE if image or fitting unset; RDS_EINVAL on NULL. Synchronous. */
 int rds_fitting_absmax(rds_t *h, float *out);
 
+/* The q -> q^ search of PAPER.md:74-84 (§3): "q^ is initially 0 and is increased until the
+ * selected value of q is satisfied".  Writes the smallest float32 delta such that the band
+ * RD = {|f| < delta} holds at least ceil(q * H * W) pixels (pixels tied at the k-th smallest
+ * |f| all join RD): delta = nextafter(k-th smallest |f|, +inf); q = 0 gives 0
+ * (RD empty, pure thresholding), q = 1 makes every pixel RD.  Exact (4-pass radix select on
+ * the bit patterns of |f|, integer histograms); synchronous.
+ * Errors: RDS_EINVAL if q not in [0, 1] or delta_out NULL; RDS_ESTATE if image/fitting unset. */
+int rds_band_for_fraction(rds_t *h, double q, float *delta_out);
+
+/* rds_band_for_fraction(q) followed by rds_solve with that delta (the paper's control knob). */
+int rds_solve_q(rds_t *h, float lambda, float theta, float tau, double q, int32_t iters);
+
 /* Run the whole method: fused fitting + band test + init, active-tile compaction, `iters`
  * outer iterations (rho-step, u-step, v-step) over the active work items, and the output
  * u = v_{K-1} - theta div rho_K on RD (u0 elsewhere) with its mask.  delta is the absolute

@@ -74,6 +74,8 @@ def _load():
         lib.orc_solve_plain.restype = i
         lib.orc_inner.argtypes = [P, i64, i64, f, d, d, i, P, P, P, P]
         lib.orc_inner.restype = i
+        lib.orc_band_for_fraction.argtypes = [P, i64, d]
+        lib.orc_band_for_fraction.restype = f
         lib.orc_ntrace.restype = i
         assert lib.orc_ntrace() == NTRACE
         _lib = lib
@@ -127,6 +129,12 @@ def labels(f, delta):
     out = np.empty(f.shape, dtype=np.uint8)
     _load().orc_labels(_ptr(f), f.size, np.float32(delta), _ptr(out))
     return out
+
+
+def band_for_fraction(f, q) -> np.float32:
+    """q -> q^: smallest float32 q^ with #{|f| < q^} >= ceil(q N)."""
+    f = _f32(f)
+    return np.float32(_load().orc_band_for_fraction(_ptr(f), f.size, float(q)))
 
 
 def tiles(lab, th=32, tw=32):

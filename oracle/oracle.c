@@ -116,6 +116,27 @@ int64_t orc_tiles(const uint8_t *lab, int64_t H, int64_t W, int th, int tw, int3
     return cnt;
 }
 
+/* q -> q^ ("q^ is initially 0 and is increased until the selected value of */
+/* q is satisfied").  Returns the smallest float32 q^ with #{|f| < q^} >= k, k = ceil(q n)     */
+/* (double): q^ = nextafter(a_(k), +inf) with a_(k) the k-th smallest |f| (so pixels tied at   */
+/* a_(k) join RD); q^ = 0 for k = 0.  Plain sort.                                 */
+static int cmp_float(const void *a, const void *b) {
+    float x = *(const float *)a, y = *(const float *)b;
+    return (x > y) - (x < y);
+}
+
+float orc_band_for_fraction(const float *f, int64_t n, double q) {
+    int64_t k = (int64_t)ceil(q * (double)n);
+    if (k > n) k = n;
+    if (k <= 0) return 0.0f;
+    float *a = (float *)malloc(sizeof(float) * (size_t)n);
+    for (int64_t i = 0; i < n; ++i) a[i] = fabsf(f[i]);
+    qsort(a, (size_t)n, sizeof(float), cmp_float);
+    float r = nextafterf(a[k - 1], INFINITY);
+    free(a);
+    return r;
+}
+
 /* ---------------------------------------------------------------------------------------- */
 /* Discrete operators.  PAPER.md:70 defers them to Chambolle (2004) (not in the container);  */
 /* reading R-C6 = SPEC.md:42, 51: forward-difference gradient with zero last row / column,   */

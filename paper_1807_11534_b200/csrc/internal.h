@@ -57,6 +57,10 @@ cudaError_t launch_absmax(const float *z, const float *P, int64_t pitch, int H, 
                           float c1, float c2, float gamma, unsigned *out_bits,
                           cudaStream_t s);
 
+cudaError_t launch_abs_hist(const float *z, const float *P, int64_t pitch, int H, int W,
+                            float c1, float c2, float gamma, unsigned prefix, unsigned mask,
+                            int shift, unsigned *hist, cudaStream_t s);
+
 struct SetupArgs {
     const float *z, *P;                 // P may be null when gamma == 0
     const float *wv, *wp1, *wp2;        // warm start (null = none)

@@ -80,6 +80,38 @@ cudaError_t launch_absmax(const float *z, const float *P, int64_t pitch, int H, 
     return cudaGetLastError();
 }
 
+// Radix-select pass for the q -> q^ search: histogram of byte `shift` of the
+// bit pattern of |f| over the pixels whose higher bytes equal `prefix` (under `mask`).
+// Non-negative floats order like their bit patterns, so 4 passes find the k-th smallest |f|
+// exactly; integer counts make the result independent of the atomic order.
+__global__ void k_abs_hist(const float *z, const float *P, int64_t pitch, int H, int W,
+                           float c1, float c2, float gamma, unsigned prefix, unsigned mask,
+                           int shift, unsigned *hist) {
+    __shared__ unsigned sh[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const int64_t n = (int64_t)H * W;
+    const bool use_p = gamma != 0.0f;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = k / W, j = k - i * W, o = i * pitch + j;
+        const float f = fitting_term(z[o], use_p ? P[o] : 0.0f, c1, c2, gamma, use_p);
+        const unsigned b = __float_as_uint(fabsf(f));
+        if ((b & mask) == prefix) atomicAdd(&sh[(b >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+        if (sh[i]) atomicAdd(&hist[i], sh[i]);
+}
+
+cudaError_t launch_abs_hist(const float *z, const float *P, int64_t pitch, int H, int W,
+                            float c1, float c2, float gamma, unsigned prefix, unsigned mask,
+                            int shift, unsigned *hist, cudaStream_t s) {
+    k_abs_hist<<<148 * 4, 256, 0, s>>>(z, P, pitch, H, W, c1, c2, gamma, prefix, mask, shift,
+                                        hist);
+    return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------------------
 // K1: one CTA per 32x32 tile, 256 threads, 4 consecutive pixels (one float4) per thread.
 // Writes f, the label byte, c (theta*lambda*f on RD, -inf on Fg, +inf on Bg), u = mask = u0,

@@ -52,6 +52,7 @@ struct rds_handle {
     unsigned *absmax_bits = nullptr;
     int *flag = nullptr;
     double *e_partials = nullptr, *e_out = nullptr;
+    unsigned *hist = nullptr;        // radix-select histogram (rds_band_for_fraction)
 
     cudaStream_t own_stream = nullptr, stream = nullptr;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -106,7 +107,7 @@ static void free_all(rds_t *h) {
         if (p) cudaFree(p);
     void *other[] = {h->lab,     h->mask,        h->tile_rd, h->tile_list, h->band_flag,
                      h->items,   h->queue,       h->counts,  h->n_rd_dev,  h->absmax_bits,
-                     h->flag,    h->e_partials,  h->e_out};
+                     h->flag,    h->e_partials,  h->e_out,   h->hist};
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -332,6 +333,53 @@ int rds_fitting_absmax(rds_t *h, float *out) {
     CK(h, cudaStreamSynchronize(h->stream));
     memcpy(out, &bits, sizeof bits);
     return RDS_OK;
+}
+
+int rds_band_for_fraction(rds_t *h, double q, float *delta_out) {
+    if (!h || !delta_out) return fail(h, RDS_EINVAL, "rds_band_for_fraction: NULL argument");
+    if (!(q >= 0.0 && q <= 1.0))
+        return fail(h, RDS_EINVAL, "rds_band_for_fraction: q=%g must be in [0, 1]", q);
+    if (!h->have_image || !h->have_fitting || !h->image_ok || !h->p_ok)
+        return fail(h, RDS_ESTATE, "rds_band_for_fraction: image and fitting must be set");
+    const int64_t N = h->H * h->W;
+    int64_t k = (int64_t)ceil(q * (double)N);  // k = ceil(q N), evaluated in double
+    if (k > N) k = N;
+    if (k <= 0) {  // q = 0: q^ = 0, RD = {|f| < 0} = empty
+        *delta_out = 0.0f;
+        return RDS_OK;
+    }
+    if (!h->hist) CK(h, cudaMalloc(&h->hist, sizeof(unsigned) * 256));
+    unsigned prefix = 0, mask = 0;
+    int64_t rank = k;  // 1-based rank of the wanted |f| among the pixels matching prefix
+    for (int shift = 24; shift >= 0; shift -= 8) {
+        unsigned hh[256];
+        CK(h, cudaMemsetAsync(h->hist, 0, sizeof hh, h->stream));
+        CK(h, launch_abs_hist(h->at(h->z), h->gamma != 0.0f ? h->at(h->P) : nullptr, h->pitch,
+                              (int)h->H, (int)h->W, h->c1, h->c2, h->gamma, prefix, mask, shift,
+                              h->hist, h->stream));
+        CK(h, cudaMemcpyAsync(hh, h->hist, sizeof hh, cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+        int d = 0;
+        for (; d < 256; ++d) {
+            if (rank <= (int64_t)hh[d]) break;
+            rank -= hh[d];
+        }
+        if (d == 256) return fail(h, RDS_ECUDA, "rds_band_for_fraction: histogram inconsistent");
+        prefix |= (unsigned)d << shift;
+        mask |= 255u << shift;
+    }
+    float a;  // the k-th smallest |f|
+    memcpy(&a, &prefix, sizeof a);
+    // smallest float32 q^ with #{|f| < q^} >= k: the next float above a (ties at a join RD)
+    *delta_out = nextafterf(a, INFINITY);
+    return RDS_OK;
+}
+
+int rds_solve_q(rds_t *h, float lambda, float theta, float tau, double q, int32_t iters) {
+    float delta = 0.0f;
+    const int rc = rds_band_for_fraction(h, q, &delta);
+    if (rc) return rc;
+    return rds_solve(h, lambda, theta, tau, delta, iters);
 }
 
 // Resident stencil CTAs per SM for (kf, stages), cached (occupancy API).

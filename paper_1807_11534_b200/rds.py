@@ -28,7 +28,8 @@ EXPORTS = (
     "rds_set_fitting", "rds_set_state", "rds_fitting_absmax", "rds_solve", "rds_get_u",
     "rds_get_mask", "rds_get_v", "rds_get_p", "rds_get_fitting", "rds_get_labels",
     "rds_get_active_tiles", "rds_tile_shape", "rds_energy", "rds_get_stats",
-    "rds_kfuse_supported", "rds_last_error", "rds_version",
+    "rds_kfuse_supported", "rds_last_error", "rds_version", "rds_band_for_fraction",
+    "rds_solve_q",
 )
 
 
@@ -88,6 +89,8 @@ def _load():
         "rds_kfuse_supported": [ctypes.POINTER(i32), i],
         "rds_last_error": [P],
         "rds_version": [],
+        "rds_band_for_fraction": [P, ctypes.c_double, ctypes.POINTER(f)],
+        "rds_solve_q": [P, f, f, f, ctypes.c_double, i32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -171,6 +174,16 @@ def rds_fitting_absmax(h):
     out = ctypes.c_float()
     _check(_lib.rds_fitting_absmax(h, ctypes.byref(out)), h)
     return np.float32(out.value)
+
+
+def rds_band_for_fraction(h, q):
+    out = ctypes.c_float()
+    _check(_lib.rds_band_for_fraction(h, float(q), ctypes.byref(out)), h)
+    return np.float32(out.value)
+
+
+def rds_solve_q(h, lam, theta, tau, q, iters):
+    _check(_lib.rds_solve_q(h, float(lam), float(theta), float(tau), float(q), int(iters)), h)
 
 
 def rds_solve(h, lam, theta, tau, delta, iters):
@@ -310,6 +323,12 @@ class Solver:
 
     def absmax(self):
         return rds_fitting_absmax(self.h)
+
+    def band_for_fraction(self, q):
+        return rds_band_for_fraction(self.h, q)
+
+    def solve_q(self, lam, theta, tau, q, iters):
+        rds_solve_q(self.h, lam, theta, tau, q, iters)
 
     def solve(self, lam, theta, tau, delta, iters):
         rds_solve(self.h, lam, theta, tau, math.inf if delta is None else delta, iters)

@@ -347,3 +347,28 @@ def test_device_buffers_and_stream(rds, orc):
     assert ut.cpu().numpy().tobytes() == host["u"].tobytes()
     assert mt.cpu().numpy().tobytes() == host["mask"].tobytes()
     s.close()
+
+
+# ------------------------------------------------------------------------------------------
+# q -> q^, NEXT item f1
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["C0", "C2", "C3"])
+def test_band_for_fraction_exact(rds, orc, name):
+    """GPU radix select of the q -> q^ threshold equals the oracle's sort, bit for bit, and
+    rds_solve_q labels the requested fraction (ties join RD)."""
+    cfg = wl.CONFIGS[name]
+    z, P = wl.make_image(cfg)
+    f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    s = rds.Solver(cfg.H, cfg.W)
+    s.set_image(z)
+    s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
+    N = cfg.H * cfg.W
+    for q in ((0.0, 1e-6, 0.1, 0.25, 0.5, 0.9, 1.0) if N < 10**7 else (0.0, 0.1, 0.5, 1.0)):
+        qh = s.band_for_fraction(q)
+        assert qh == orc.band_for_fraction(f, q), q
+        s.solve_q(cfg.lambdas[0], cfg.theta, cfg.tau, q, 0)
+        lab = s.labels()
+        assert np.array_equal(lab, orc.labels(f, qh))
+        assert (lab == 2).sum() >= np.ceil(q * N)
+    s.close()

@@ -436,3 +436,38 @@ def test_warm_start_respects_pinning(orc):
     assert np.array_equal(r["v"][rd], v.astype(np.float64)[rd])
     assert np.array_equal(r["v"][~rd], (f <= 0).astype(np.float64)[~rd])
     assert not r["p1"][~rd].any() and not r["p1"][-1].any() and not r["p2"][:, -1].any()
+
+
+# ------------------------------------------------------------------------------------------
+# q -> q^
+# ------------------------------------------------------------------------------------------
+
+def test_band_for_fraction_spec_example(orc):
+    """f = {-3..5} (3x3), q = 1/3 -> RD = {-1, 0, 1}, rd_fraction 3/9."""
+    f = np.arange(-3, 6, dtype=np.float32).reshape(3, 3)
+    qh = orc.band_for_fraction(f, 1.0 / 3.0)
+    lab = orc.labels(f, qh)
+    assert sorted(f[lab == 2].tolist()) == [-1.0, 0.0, 1.0]
+
+
+def test_band_for_fraction_definition(orc):
+    """Brute force against the definition: q^ is the smallest float32 with
+    #{|f| < q^} >= ceil(q N); q = 0 -> RD empty, q = 1 -> RD = Omega; RD grows with q."""
+    rng = np.random.default_rng(21)
+    for n in (1, 2, 7, 100, 1000):
+        f = rng.normal(size=n).astype(np.float32)
+        f[: n // 3] = np.round(f[: n // 3], 1)   # ties
+        prev = -1
+        for q in (0.0, 1e-9, 0.1, 1 / 3, 0.5, 0.9, 1.0):
+            qh = orc.band_for_fraction(f, q)
+            k = int(np.ceil(q * n))
+            cnt = int((np.abs(f) < qh).sum())
+            assert cnt >= k
+            below = np.nextafter(qh, np.float32(-np.inf), dtype=np.float32)
+            if k > 0:
+                assert int((np.abs(f) < below).sum()) < k       # minimality
+            else:
+                assert qh == 0.0 and cnt == 0
+            assert cnt >= prev
+            prev = cnt
+        assert int((np.abs(f) < orc.band_for_fraction(f, 1.0)).sum()) == n
