@@ -97,6 +97,8 @@ typedef struct {
                                 active tiles; 0 = process every cell (restriction without
                                 tile skipping) */
 #define RDS_OPT_GRAPH 5      /* 1 (default) = replay the K-loop as a CUDA graph */
+#define RDS_OPT_CTAS_PER_SM 6 /* cap on resident stencil CTAs per SM (0 = occupancy limit);
+                                 a tuning/diagnostic knob, results are identical */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */

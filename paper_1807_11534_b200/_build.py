@@ -42,7 +42,9 @@ def needs_build() -> bool:
 
 def _compile(src: str) -> tuple[str, str]:
     obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
-    cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+    # RDS_NVCC_DEFS: extra -D flags for tuning experiments (scripts/gpu_variants.sh)
+    extra = os.environ.get("RDS_NVCC_DEFS", "").split()
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

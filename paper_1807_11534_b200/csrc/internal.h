@@ -7,6 +7,13 @@
 // c = +inf) that the iteration reproduces exactly, so the stencil needs no bounds tests on
 // loads: only the two Neumann conditions (grad_1 = 0 on row H-1, grad_2 = 0 on column W-1)
 // are explicit.  pitch is a multiple of 32 elements (128 B rows for float planes).
+//
+// The stencil's state planes (rho1, rho2, v in both ping-pong buffers, and c) are
+// QUAD-SWIZZLED: within every aligned quad of columns 4g..4g+3 the memory order is
+// x0 x2 x1 x3 (swap of index bits 0 and 1), so one 16-byte load gives the packed f32x2
+// pairs (x0, x2), (x1, x3) the stencil computes on (k_stencil.cu).  PAD_C is a multiple of
+// 4, so the swizzle applies to the column index relative to the origin.  z, P, f, u, the
+// labels and the mask are natural-order planes.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -18,7 +25,10 @@ constexpr int PAD_R = 16;      // >= KF + 1 rows of halo above / below (KF <= 15
 constexpr int PAD_C = 32;      // left frame, keeps column 0 16-byte aligned
 constexpr int PAD_C_RIGHT = 128;  // a warp strip may read up to 127 columns past its start
 constexpr int TILE_H = 32, TILE_W = 32;
-constexpr int STENCIL_WARPS = 4;  // warps per CTA of the stencil kernel (one item per warp)
+constexpr int STENCIL_WARPS = 4;
+
+// element offset of column j inside a quad-swizzled row (valid for negative j as well)
+__host__ __device__ constexpr int swz(int j) { return (j & ~3) | ((j & 1) << 1) | ((j >> 1) & 1); }  // warps per CTA of the stencil kernel (one item per warp)
 
 // Column geometry of a stencil warp for KF fused iterations: the warp loads 128 columns
 // (float4 per lane); the valid output columns are [LH, LH + WV) of those.  The dependency
@@ -37,7 +47,7 @@ struct Item {
 
 struct StencilArgs {
     const float *p1_in, *p2_in, *v_in;   // plane origins (pixel (0,0))
-    const float *c;                      // theta*lambda*f on RD, -inf on Fg, +inf on Bg/frame
+    const float *c;                      // 2^-100 theta*lambda*f on RD, -inf Fg, +inf Bg/frame
     float *p1_out, *p2_out, *v_out;
     float *u_out;                        // only written when WRITE_U
     uint8_t *mask_out;                   // only written when WRITE_U
@@ -106,5 +116,9 @@ struct EnergyArgs {
 };
 constexpr int ENERGY_BLOCKS = 592;  // 4 x 148 SMs
 cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s);
+
+// out[i * out_pitch + j] = plane[i * pitch + swz(j)]: natural-order copy of a swizzled plane
+cudaError_t launch_unswizzle(const float *plane, int64_t pitch, int H, int W, float *out,
+                             int64_t out_pitch, cudaStream_t s);
 
 }  // namespace rds

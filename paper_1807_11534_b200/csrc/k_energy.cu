@@ -27,16 +27,18 @@ __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
     for (int64_t k = blockIdx.x * 256 + threadIdx.x; k < n; k += (int64_t)gridDim.x * 256) {
         const int i = (int)(k / a.W), j = (int)(k - (int64_t)i * a.W);
         const int64_t o = (int64_t)i * pitch + j;
+        const int64_t os = (int64_t)i * pitch + swz(j);  // v, rho are quad-swizzled
+        const int64_t osr = (int64_t)i * pitch + swz(j + 1), osl = (int64_t)i * pitch + swz(j - 1);
         const bool down = i < a.H - 1, right = j < a.W - 1;
-        const float v = a.v[o];
-        const float gv1 = down ? a.v[o + pitch] - v : 0.0f;
-        const float gv2 = right ? a.v[o + 1] - v : 0.0f;
+        const float v = a.v[os];
+        const float gv1 = down ? a.v[os + pitch] - v : 0.0f;
+        const float gv2 = right ? a.v[osr] - v : 0.0f;
         const float cu = clamp01(a.u[o]);
         const float gu1 = down ? clamp01(a.u[o + pitch]) - cu : 0.0f;
         const float gu2 = right ? clamp01(a.u[o + 1]) - cu : 0.0f;
         const float f = a.f[o];
         // rho1 on row H-1 and rho2 on column W-1 are identically 0; the frame holds 0
-        const float dv = a.p1[o] - a.p1[o - pitch] + a.p2[o] - a.p2[o - 1];
+        const float dv = a.p1[os] - a.p1[os - pitch] + a.p2[os] - a.p2[osl];
         const float t = a.lambda * f + dv;
         acc[0] += (double)sqrtf(gv1 * gv1 + gv2 * gv2);
         acc[1] += (double)f * (double)v;
@@ -76,6 +78,22 @@ __global__ void __launch_bounds__(256) k_energy_final(const double *partials, in
         for (int w = 0; w < 8; ++w) s += sh[w][threadIdx.x];
         out[threadIdx.x] = s;
     }
+}
+
+__global__ void k_unswizzle(const float *plane, int64_t pitch, int H, int W, float *out,
+                            int64_t out_pitch) {
+    const int64_t n = (int64_t)H * W;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(k / W), j = (int)(k - (int64_t)i * W);
+        out[(int64_t)i * out_pitch + j] = plane[(int64_t)i * pitch + swz(j)];
+    }
+}
+
+cudaError_t launch_unswizzle(const float *plane, int64_t pitch, int H, int W, float *out,
+                             int64_t out_pitch, cudaStream_t s) {
+    k_unswizzle<<<148 * 8, 256, 0, s>>>(plane, pitch, H, W, out, out_pitch);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s) {

@@ -114,8 +114,9 @@ cudaError_t launch_abs_hist(const float *z, const float *P, int64_t pitch, int H
 
 // ---------------------------------------------------------------------------------------
 // K1: one CTA per 32x32 tile, 256 threads, 4 consecutive pixels (one float4) per thread.
-// Writes f, the label byte, c (theta*lambda*f on RD, -inf on Fg, +inf on Bg), u = mask = u0,
-// and the initial state into BOTH ping-pong buffers (pinned pixels never change, and a
+// Writes f, the label byte, c' (2^-100 theta*lambda*f on RD, -inf on Fg, +inf on Bg), u = mask = u0,
+// and the initial state into BOTH ping-pong buffers (c', rho and v quad-swizzled, internal.h;
+// pinned pixels never change, and a
 // skipped work item must read as its initial value from either buffer).  Out-of-image
 // columns of the tile are written with the frame's pinned values (rho = 0, v = 0, c = +inf).
 // ---------------------------------------------------------------------------------------
@@ -155,8 +156,11 @@ __global__ void __launch_bounds__(256) k_setup(SetupArgs a) {
                 f[e] = fe;
                 lab[e] = rd ? 2 : (fg ? 1 : 0);
                 // RD: theta*lambda*f clamped to +-2^20 (the v-step saturates far earlier:
-                // |u| <= max|v| + 4 theta), so |c| * 2^-120 is negligible in the stencil
-                c[e] = rd ? fminf(fmaxf(__fmul_rn(a.theta_lambda, fe), -0x1p20f), 0x1p20f)
+                // |u| <= max|v| + 4 theta) and stored as c' = c * 2^-100, so |c'| <= 2^-80
+                // is negligible under the stencil's square root (k_stencil.cu, stage()).
+                c[e] = rd ? __fmul_rn(fminf(fmaxf(__fmul_rn(a.theta_lambda, fe), -0x1p20f),
+                                            0x1p20f),
+                                      0x1p-100f)
                           : (fg ? -INFINITY : INFINITY);
                 u[e] = u0;
                 msk[e] = fg ? 1 : 0;
@@ -177,11 +181,12 @@ __global__ void __launch_bounds__(256) k_setup(SetupArgs a) {
             }
         }
         *reinterpret_cast<float4 *>(a.f + o) = make_float4(f[0], f[1], f[2], f[3]);
-        *reinterpret_cast<float4 *>(a.c + o) = make_float4(c[0], c[1], c[2], c[3]);
         *reinterpret_cast<float4 *>(a.u + o) = make_float4(u[0], u[1], u[2], u[3]);
-        const float4 v4 = make_float4(v[0], v[1], v[2], v[3]);
-        const float4 p14 = make_float4(p1[0], p1[1], p1[2], p1[3]);
-        const float4 p24 = make_float4(p2[0], p2[1], p2[2], p2[3]);
+        // the stencil's state planes are quad-swizzled (internal.h): memory x0 x2 x1 x3
+        *reinterpret_cast<float4 *>(a.c + o) = make_float4(c[0], c[2], c[1], c[3]);
+        const float4 v4 = make_float4(v[0], v[2], v[1], v[3]);
+        const float4 p14 = make_float4(p1[0], p1[2], p1[1], p1[3]);
+        const float4 p24 = make_float4(p2[0], p2[2], p2[1], p2[3]);
         *reinterpret_cast<float4 *>(a.v0 + o) = v4;
         *reinterpret_cast<float4 *>(a.v1 + o) = v4;
         *reinterpret_cast<float4 *>(a.p10 + o) = p14;

@@ -22,7 +22,7 @@ namespace {
 
 thread_local std::string g_last_error;
 
-constexpr int kDefaultKF = 6;
+constexpr int kDefaultKF = 7;  // sweep: DESIGN.md §5
 
 }  // namespace
 
@@ -53,6 +53,7 @@ struct rds_handle {
     int *flag = nullptr;
     double *e_partials = nullptr, *e_out = nullptr;
     unsigned *hist = nullptr;        // radix-select histogram (rds_band_for_fraction)
+    float *scratch = nullptr;        // H*W natural-order staging for swizzled-plane getters
 
     cudaStream_t own_stream = nullptr, stream = nullptr;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -63,7 +64,7 @@ struct rds_handle {
     float lambda = 0, theta = 0;
     int cur = 0;  // ping-pong buffer holding the latest state
 
-    int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1;
+    int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1, opt_ctas = 0;
     rds_stats_t stats{};
 
     // cached CUDA graph of the K-loop
@@ -107,7 +108,7 @@ static void free_all(rds_t *h) {
         if (p) cudaFree(p);
     void *other[] = {h->lab,     h->mask,        h->tile_rd, h->tile_list, h->band_flag,
                      h->items,   h->queue,       h->counts,  h->n_rd_dev,  h->absmax_bits,
-                     h->flag,    h->e_partials,  h->e_out,   h->hist};
+                     h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch};
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -240,6 +241,15 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             return RDS_OK;
         case RDS_OPT_GRAPH:
             h->opt_graph = value != 0;
+            return RDS_OK;
+        case RDS_OPT_CTAS_PER_SM:
+            if (value < 0 || value > 64)
+                return fail(h, RDS_EINVAL, "rds_set_option: ctas_per_sm=%lld", (long long)value);
+            h->opt_ctas = (int)value;
+            if (h->graph) {
+                cudaGraphExecDestroy(h->graph);
+                h->graph = nullptr;
+            }
             return RDS_OK;
         default:
             return fail(h, RDS_EINVAL, "rds_set_option: unknown key %d", key);
@@ -387,7 +397,8 @@ static int blocks_per_sm(rds_t *h, int kf, int stages) {
     const bool aligned = (h->W & 3) == 0;
     int &slot = h->bps[kf][stages];
     if (slot <= 0) slot = stencil_blocks_per_sm(kf, stages, aligned);
-    return slot > 0 ? slot : 1;
+    const int b = slot > 0 ? slot : 1;
+    return (h->opt_ctas > 0 && h->opt_ctas < b) ? h->opt_ctas : b;
 }
 
 // Enqueue the K-loop: zero the per-launch work queues, then ceil(iters/kf) persistent
@@ -586,6 +597,23 @@ static int copy_out(rds_t *h, void *dst, const void *plane_origin, size_t elt, i
     return RDS_OK;
 }
 
+// Getter of a quad-swizzled state plane (rho1, rho2, v; internal.h): unswizzled by a
+// kernel, straight into a device destination or through a staging buffer for the host.
+static int copy_out_swizzled(rds_t *h, float *dst, const float *plane_origin, int on_device) {
+    if (on_device) {
+        CK(h, launch_unswizzle(plane_origin, h->pitch, (int)h->H, (int)h->W, dst, h->W,
+                               h->stream));
+        return RDS_OK;
+    }
+    if (!h->scratch) CK(h, cudaMalloc(&h->scratch, sizeof(float) * h->H * h->W));
+    CK(h, launch_unswizzle(plane_origin, h->pitch, (int)h->H, (int)h->W, h->scratch, h->W,
+                           h->stream));
+    CK(h, cudaMemcpyAsync(dst, h->scratch, sizeof(float) * h->H * h->W, cudaMemcpyDeviceToHost,
+                          h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    return RDS_OK;
+}
+
 #define NEED_SOLVED(name)                                                          \
     if (!h) return fail(nullptr, RDS_EINVAL, name ": NULL handle");                \
     if (!h->solved) return fail(h, RDS_ESTATE, name ": no solve has run yet");
@@ -605,15 +633,15 @@ int rds_get_mask(rds_t *h, uint8_t *out, int on_device) {
 int rds_get_v(rds_t *h, float *out, int on_device) {
     NEED_SOLVED("rds_get_v");
     if (!out) return fail(h, RDS_EINVAL, "rds_get_v: NULL out");
-    return copy_out(h, out, h->at(h->v[h->cur]), sizeof(float), on_device);
+    return copy_out_swizzled(h, out, h->at(h->v[h->cur]), on_device);
 }
 
 int rds_get_p(rds_t *h, float *rho1, float *rho2, int on_device) {
     NEED_SOLVED("rds_get_p");
     if (!rho1 || !rho2) return fail(h, RDS_EINVAL, "rds_get_p: NULL out");
-    int rc = copy_out(h, rho1, h->at(h->p1[h->cur]), sizeof(float), on_device);
+    int rc = copy_out_swizzled(h, rho1, h->at(h->p1[h->cur]), on_device);
     if (rc) return rc;
-    return copy_out(h, rho2, h->at(h->p2[h->cur]), sizeof(float), on_device);
+    return copy_out_swizzled(h, rho2, h->at(h->p2[h->cur]), on_device);
 }
 
 int rds_get_fitting(rds_t *h, float *out, int on_device) {

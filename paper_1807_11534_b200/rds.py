@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(_PKG, "librds.so")
 RDS_OK, RDS_EINVAL, RDS_ESTATE, RDS_ECUDA, RDS_ENOMEM = 0, -1, -2, -3, -4
 RDS_LABEL_BG, RDS_LABEL_FG, RDS_LABEL_RD = 0, 1, 2
 RDS_OPT_KFUSE, RDS_OPT_ITEM_ROWS, RDS_OPT_TIMING, RDS_OPT_SKIP, RDS_OPT_GRAPH = 1, 2, 3, 4, 5
+RDS_OPT_CTAS_PER_SM = 6
 
 EXPORTS = (
     "rds_create", "rds_destroy", "rds_set_stream", "rds_set_option", "rds_set_image",

@@ -21,6 +21,7 @@ ap.add_argument("--rows", default="64,128,256")
 ap.add_argument("--delta", type=float, default=math.inf)
 ap.add_argument("--iters", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--ctas", default="0", help="cap on stencil CTAs per SM (0 = occupancy)")
 args = ap.parse_args()
 
 cfg = wl.CONFIGS[args.config]
@@ -32,10 +33,12 @@ s.set_image(torch.from_numpy(z).cuda())
 s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, torch.from_numpy(P).cuda() if P is not None else None)
 am = s.absmax()
 delta = wl.band_delta(args.delta, am)
-for kf in [int(x) for x in args.kf.split(",")]:
-    for rows in [int(x) for x in args.rows.split(",")]:
+for kf, rows, ctas in [(int(a), int(b), int(c)) for a in args.kf.split(",")
+                       for b in args.rows.split(",") for c in args.ctas.split(",")]:
+    if True:
         s.set_option(rds.RDS_OPT_KFUSE, kf)
         s.set_option(rds.RDS_OPT_ITEM_ROWS, rows)
+        s.set_option(rds.RDS_OPT_CTAS_PER_SM, ctas)
         s.solve(cfg.lambdas[0], cfg.theta, cfg.tau, delta, K)  # warm (graph capture)
         s.stats()
         ts = []
@@ -45,7 +48,8 @@ for kf in [int(x) for x in args.kf.split(",")]:
         info = s.stats()
         lm = statistics.median(ts)
         px = info["n_active_tiles"] * 1024
-        print(json.dumps({"config": args.config, "kf": kf, "rows": rows, "loop_ms": lm,
+        print(json.dumps({"config": args.config, "kf": kf, "rows": rows, "ctas": ctas,
+                          "defs": os.environ.get("RDS_NVCC_DEFS", ""), "loop_ms": lm,
                           "gpix_iter_s": px * K / lm / 1e6, "items": info["n_active_items"],
                           "launches": info["launches"]}), flush=True)
 s.close()
