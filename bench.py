@@ -39,7 +39,13 @@ from paper_1807_11534_b200 import workloads as wl  # noqa: E402
 METRIC = "active Gpixel-iter/s at 4096^2 fp32 (restricted-domain dual iteration, C3 delta sweep)"
 UNIT = "Gpixel-iter/s"
 BYTES_PER_PX_ITER = 28  # read rho1, rho2, v, c (16 B) + write rho1, rho2, v (12 B)
-FLOPS_PER_PX_ITER = 24  # algorithmic FP32 operations of one iteration
+# Compute roofline of one pixel-iteration: 2 MUFU ops (sqrt, rcp) on the
+# 16-lane/clk/SM MUFU pipe and 15 FP32 ops on the 128-lane/clk/SM FMA pipe (both measured
+# in scripts/micro/); MUFU binds: 8 pixel-iterations per clock per SM.
+MUFU_PER_PX_ITER = 2
+FP32_PER_PX_ITER = 15
+MUFU_LANES_PER_SM = 16
+FP32_LANES_PER_SM = 128
 
 
 def parse():
@@ -324,7 +330,7 @@ def run_ours(args, dist):
     per_delta = []
     t_full = statistics.median(x["loop_ms"] for x in per[cfg.delta_rels[-1]]) \
         if math.isinf(cfg.delta_rels[-1]) else None
-    launch_ms_all, bytes_all, flops_all = [], [], []
+    launch_ms_all, bytes_all, pxit_all = [], [], []
     for dr, st, e in info:
         lm = statistics.median(x["loop_ms"] for x in per[dr])
         sm = statistics.median(x["setup_ms"] for x in per[dr])
@@ -334,7 +340,7 @@ def run_ours(args, dist):
         launch_ms_all.append(lm / launches)
         px = act_px[dr]
         bytes_all.append(BYTES_PER_PX_ITER * px * K / launches)
-        flops_all.append(FLOPS_PER_PX_ITER * px * K / launches)
+        pxit_all.append(px * K / launches)
         per_delta.append({
             "delta_rel": "inf" if math.isinf(dr) else dr,
             "loop_ms": lm, "setup_ms": sm,
@@ -352,8 +358,10 @@ def run_ours(args, dist):
     peaks = _peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     clock_mhz = ck.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    fp32_peak = 148 * 128 * 2 * clock_mhz * 1e6 / 1e12  # TFLOP/s at the observed SM clock
-    achieved_tf = statistics.mean(flops_all) / (launch_ms * 1e-3) / 1e12
+    n_sm = torch.cuda.get_device_properties(dist.local).multi_processor_count
+    px_per_clk_sm = min(MUFU_LANES_PER_SM / MUFU_PER_PX_ITER, FP32_LANES_PER_SM / FP32_PER_PX_ITER)
+    alu_peak = n_sm * px_per_clk_sm * clock_mhz * 1e6 / 1e9  # Gpx-iter/s at the observed clock
+    achieved_px = statistics.mean(pxit_all) / (launch_ms * 1e-3) / 1e9
     st0 = info[0][1]
     traffic = _traffic_from_profile(st0["k_fuse"])
     roofline = {
@@ -365,10 +373,13 @@ def run_ours(args, dist):
                   f"{st0['k_fuse']} fused iterations) per launch / mean launch time "
                   f"{launch_ms:.4f} ms; peak = MEASURED_PEAKS.json hbm_gbs (measured copy)"),
         "k_fuse": st0["k_fuse"],
-        "alu": {"achieved_tflops": achieved_tf, "peak_tflops": fp32_peak,
-                "frac": achieved_tf / fp32_peak,
-                "basis": f"{FLOPS_PER_PX_ITER} algorithmic FP32 ops per px-iter; peak = 148 SM x "
-                         f"128 FP32 lanes x 2 x {clock_mhz:.0f} MHz"},
+        "alu": {"bound": "alu", "achieved": achieved_px, "peak": alu_peak,
+                "unit": "Gpixel-iter/s", "frac": achieved_px / alu_peak,
+                "basis": (f"active pixel-iterations per launch / mean launch time; peak = {n_sm} SM"
+                          f" x {px_per_clk_sm:g} px-iter/clk (MUFU: {MUFU_PER_PX_ITER} ops per "
+                          f"px-iter at {MUFU_LANES_PER_SM}/clk/SM; FMA pipe: "
+                          f"{FP32_PER_PX_ITER} at {FP32_LANES_PER_SM}/clk/SM) x "
+                          f"{clock_mhz:.0f} MHz (observed)")},
     }
 
     launches_per_step = sum(st["launches"] + 4 + 2 for _, st, _ in info)
