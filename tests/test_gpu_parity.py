@@ -103,6 +103,72 @@ def test_setup_bitexact_c4(rds, orc):
     s.close()
 
 
+def _window_oracle(orc, f, delta, lam, cfg, K, r0, c0, h, w):
+    """Oracle u, v, rho on the block [r0, r0+h) x [c0, c0+w) of a full-size solve, computed
+    on a window with a 2K+2 margin.  One iteration's dependency cone is rows -2..+1 and
+    columns -2..+1, and a wrong (window) boundary propagates inward no faster,
+    so the block's values after K iterations equal the full-image iteration's exactly."""
+    H, W = f.shape
+    m = 2 * K + 2
+    R0, R1 = max(0, r0 - m), min(H, r0 + h + m)
+    C0, C1 = max(0, c0 - m), min(W, c0 + w + m)
+    o = orc.solve(np.ascontiguousarray(f[R0:R1, C0:C1]), delta, lam, np.float32(cfg.theta),
+                  cfg.tau, K)
+    sl = (slice(r0 - R0, r0 - R0 + h), slice(c0 - C0, c0 - C0 + w))
+    return {k: o[k][sl] for k in ("u", "v", "p1", "p2", "labels")}
+
+
+@pytest.mark.slow
+def test_c4_full_size(rds, orc):
+    """C4 (16384^2, 64 blocks of the selection-term generator) at full size in the bench's
+    launch configuration: (i) K = 100, sampled 48x48 blocks (corners, block seams, interior)
+    against the oracle on cone-sized windows; (ii) K = 1000 (the config's count), properties
+    that hold at any size."""
+    cfg = wl.CONFIGS["C4"]
+    z, P = wl.make_image(cfg)
+    f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    delta = wl.band_delta(0.2, orc.absmax(f))
+    lam = cfg.lambdas[0]
+    s = rds.Solver(cfg.H, cfg.W)
+    s.set_image(z)
+    s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
+    del z, P
+    K = 100
+    s.solve(lam, cfg.theta, cfg.tau, delta, K)
+    g = {"u": s.u(), "v": s.v()}
+    g["p1"], g["p2"] = s.p()
+    mask = s.mask()
+    H, W, b = cfg.H, cfg.W, 48
+    rng = np.random.default_rng(7)
+    blocks = [(0, 0), (0, W - b), (H - b, 0), (H - b, W - b), (2048 - b // 2, 2048 - b // 2),
+              (8192 - b // 2, 6144 - b // 2)] + \
+             [(int(rng.integers(0, H - b)), int(rng.integers(0, W - b))) for _ in range(3)]
+    for r0, c0 in blocks:
+        o = _window_oracle(orc, f, delta, lam, cfg, K, r0, c0, b, b)
+        gb = {k: g[k][r0:r0 + b, c0:c0 + b] for k in g}
+        gb["mask"] = mask[r0:r0 + b, c0:c0 + b]
+        compare(gb, o, ctx=f"C4 block ({r0},{c0}) K={K}")
+    del g, mask
+    s.solve(lam, cfg.theta, cfg.tau, delta, cfg.iters)
+    lab = s.labels()
+    assert np.array_equal(lab, orc.labels(f, delta))
+    v = s.v()
+    assert v.min() >= 0 and v.max() <= 1
+    off = lab != 2
+    u0 = (f <= 0).astype(np.float32)
+    assert np.array_equal(s.u()[off], u0[off]) and np.array_equal(v[off], u0[off])
+    del v, u0
+    p1, p2 = s.p()
+    assert not p1[off].any() and not p2[off].any()
+    assert not p1[-1].any() and not p2[:, -1].any()
+    pn = np.hypot(p1, p2)
+    assert pn.max() <= 1 + 1e-5
+    del p1, p2, pn
+    e = s.energy()
+    assert e["gap"] >= -1e-6 * abs(e["E_v"])
+    s.close()
+
+
 # ------------------------------------------------------------------------------------------
 # K3: the iteration on small and ragged shapes, every fusion depth, warm starts
 # ------------------------------------------------------------------------------------------

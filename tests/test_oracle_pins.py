@@ -471,3 +471,23 @@ def test_band_for_fraction_definition(orc):
             assert cnt >= prev
             prev = cnt
         assert int((np.abs(f) < orc.band_for_fraction(f, 1.0)).sum()) == n
+
+
+@pytest.mark.parametrize("delta_rel", [0.3, math.inf])
+def test_dependency_cone_window(orc, delta_rel):
+    """The premise of the full-size windowed parity tests (test_c4_full_size): after K
+    iterations a block's u, v, rho depend only on inputs within 2K+2 rows/columns, so the
+    oracle on a window with that margin reproduces the full-image iteration exactly -- and a
+    margin that is too small does not (the cone really reaches that far)."""
+    rng = np.random.default_rng(11)
+    H, W, K = 90, 84, 9
+    f = rng.uniform(-1, 1, (H, W)).astype(np.float32)
+    delta = wl.band_delta(delta_rel, orc.absmax(f))
+    full = orc.solve(f, delta, 4.0, np.float32(0.1), 0.125, K)
+    r0, c0, b = 40, 38, 8
+    for m, exact in ((2 * K + 2, True), (K // 2, False)):
+        win = orc.solve(np.ascontiguousarray(f[r0 - m:r0 + b + m, c0 - m:c0 + b + m]), delta,
+                        4.0, np.float32(0.1), 0.125, K)
+        same = all(np.array_equal(win[k][m:m + b, m:m + b], full[k][r0:r0 + b, c0:c0 + b])
+                   for k in ("u", "v", "p1", "p2"))
+        assert same == exact, (m, same)
