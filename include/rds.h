@@ -81,9 +81,11 @@ typedef struct {
     int32_t launches;        /* stencil launches in the K-loop */
     int32_t item_rows;       /* maximum output rows per work item (chosen per solve) */
     int32_t item_cols;       /* output columns per work item (strip width) */
-    int32_t pad_;
+    int32_t converged;       /* rds_solve_tol: 1 if the stopping rule fired before max_iters */
     float setup_ms;          /* fused fitting/band/init + compaction */
     float loop_ms;           /* the K-loop (all stencil launches) */
+    float residual;          /* rds_solve_tol: max(RMS du, RMS dv) at the last check; else -1 */
+    int32_t check_every;     /* rds_solve_tol: iterations between checks; 0 for rds_solve */
 } rds_stats_t;
 
 /* Options (rds_set_option). */
@@ -154,6 +156,21 @@ int rds_solve_q(rds_t *h, float lambda, float theta, float tau, double q, int32_
  * iters < 0, or any parameter non-finite (delta may be +inf); RDS_ESTATE if image or fitting
  * unset. */
 int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32_t iters);
+
+/* rds_solve with the paper's stopping rule (§4): "iterate until
+ *     max{ ||u^(l) - u^(l-1)||, ||v^(l) - v^(l-1)|| } <= delta_stop
+ * is met at the l-th iteration".  The norm is the RMS over all H x W pixels (DESIGN.md
+ * reading R-F2; pinned pixels contribute 0).  The rule is evaluated after iterations
+ * check_every, 2 check_every, ... and always at max_iters (check_every = 0 selects the
+ * library's k_fuse); the solve stops at the first check where it holds, else at max_iters.
+ * The check runs inside the fused stencil (the launch ending at a check also writes u and
+ * the mask) and a one-CTA reduction on the device; later launches exit immediately, so the
+ * call enqueues everything and returns without synchronising.  The outcome -- iterations
+ * done, converged flag, final residual -- is read by rds_get_stats (any getter resolves it).
+ * Errors: those of rds_solve, and RDS_EINVAL if tol < 0 or NaN, check_every < 0 or
+ * max_iters < 1. */
+int rds_solve_tol(rds_t *h, float lambda, float theta, float tau, float delta,
+                  int32_t max_iters, float tol, int32_t check_every);
 
 /* Getters: copy H x W results into `out` (host copies synchronise the handle's stream).
  * Errors: RDS_ESTATE before the first solve; RDS_EINVAL on NULL. */

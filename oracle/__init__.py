@@ -70,6 +70,9 @@ def _load():
         lib.orc_energy.argtypes = [P, i64, i64, d, P, P, P, P, P]
         lib.orc_solve.argtypes = [P, i64, i64, f, d, d, d, i, i, P, P, P, P, P, P, P, P, P]
         lib.orc_solve.restype = i
+        lib.orc_solve_tol.argtypes = [P, i64, i64, f, d, d, d, i, i, d, P, P, P, P, P,
+                                      ctypes.POINTER(i), ctypes.POINTER(d)]
+        lib.orc_solve_tol.restype = i
         lib.orc_solve_plain.argtypes = [P, i64, i64, d, d, d, i, P, P, P, P]
         lib.orc_solve_plain.restype = i
         lib.orc_inner.argtypes = [P, i64, i64, f, d, d, i, P, P, P, P]
@@ -216,6 +219,28 @@ def solve(f, delta, lam, theta, tau, iters, inner_steps=1, init=None, trace=Fals
     if trace:
         out["trace"] = tr[:iters]
     return out
+
+
+def solve_tol(f, delta, lam, theta, tau, max_iters, tol, check_every):
+    """The iteration with the paper's stopping rule (oracle.c orc_solve_tol):
+    checks after every check_every iterations and at max_iters, RMS norm.  Returns dict u, v,
+    p1, p2, labels, iters, residual."""
+    f = _f32(f)
+    H, W = f.shape
+    u = np.empty((H, W), dtype=np.float64)
+    v = np.empty_like(u)
+    p1 = np.empty_like(u)
+    p2 = np.empty_like(u)
+    lab = np.empty((H, W), dtype=np.uint8)
+    it = ctypes.c_int()
+    res = ctypes.c_double()
+    rc = _load().orc_solve_tol(_ptr(f), H, W, np.float32(delta), float(lam), float(theta),
+                               float(tau), int(max_iters), int(check_every), float(tol), _ptr(u),
+                               _ptr(v), _ptr(p1), _ptr(p2), _ptr(lab), ctypes.byref(it),
+                               ctypes.byref(res))
+    if rc != 0:
+        raise ValueError(f"orc_solve_tol rc={rc}")
+    return dict(u=u, v=v, p1=p1, p2=p2, labels=lab, iters=it.value, residual=res.value)
 
 
 def solve_plain(f, lam, theta, tau, iters):

@@ -261,10 +261,15 @@ void orc_energy(const float *f32, int64_t H, int64_t W, double lambda, const dou
 #define ORC_NTRACE 5
 int orc_ntrace(void) { return ORC_NTRACE; }
 
-int orc_solve(const float *f32, int64_t H, int64_t W, float delta, double lambda,
-              double theta, double tau, int iters, int inner_steps, const double *v_init,
-              const double *p1_init, const double *p2_init, double *u, double *v, double *p1,
-              double *p2, uint8_t *lab_out, double *trace) {
+/* The iteration; with check_every > 0 also the stopping rule of PAPER.md:234-238 (§4),     */
+/* "iterate until max{||u^l - u^(l-1)||, ||v^l - v^(l-1)||} <= delta is met at the l-th       */
+/* iteration", evaluated after iterations check_every, 2 check_every, ... and at iters, with */
+/* the RMS norm over all H*W pixels (reading R-F2).                                 */
+static int solve_core(const float *f32, int64_t H, int64_t W, float delta, double lambda,
+                      double theta, double tau, int iters, int inner_steps, const double *v_init,
+                      const double *p1_init, const double *p2_init, double *u, double *v,
+                      double *p1, double *p2, uint8_t *lab_out, double *trace, int check_every,
+                      double tol, int *iters_done, double *residual) {
     if (H < 1 || W < 1 || iters < 0 || inner_steps < 1) return -1;
     int64_t n = H * W;
     uint8_t *lab = (uint8_t *)malloc((size_t)n);
@@ -273,6 +278,7 @@ int orc_solve(const float *f32, int64_t H, int64_t W, float delta, double lambda
     double *w = (double *)malloc(sizeof(double) * (size_t)n);
     double *vprev = (double *)malloc(sizeof(double) * (size_t)n);
     double *rb = (double *)malloc(sizeof(double) * (size_t)H * 2);
+    double *uprev = check_every > 0 ? (double *)malloc(sizeof(double) * (size_t)n) : NULL;
 
     orc_labels(f32, n, delta, lab);
     for (int64_t k = 0; k < n; ++k) {
@@ -289,8 +295,11 @@ int orc_solve(const float *f32, int64_t H, int64_t W, float delta, double lambda
             u[k] = u0[k];
         }
 
+    if (iters_done) *iters_done = 0;
+    if (residual) *residual = -1.0;
     for (int it = 0; it < iters; ++it) {
         memcpy(vprev, v, sizeof(double) * (size_t)n);
+        if (uprev) memcpy(uprev, u, sizeof(double) * (size_t)n);
         for (int s = 0; s < inner_steps; ++s) {
             /* w = div rho - v/theta on the full grid */
 #pragma omp parallel for schedule(static)
@@ -372,6 +381,31 @@ int orc_solve(const float *f32, int64_t H, int64_t W, float delta, double lambda
             orc_energy(f32, H, W, lambda, u, v, p1, p2, e);
             tr[4] = e[3];
         }
+        if (iters_done) *iters_done = it + 1;
+        if (check_every > 0 && ((it + 1) % check_every == 0 || it + 1 == iters)) {
+            /* row sums in a fixed order: the result does not depend on the thread count */
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < H; ++i) {
+                double a = 0.0, b = 0.0;
+                for (int64_t j = 0; j < W; ++j) {
+                    int64_t k = IDX(i, j);
+                    double du = u[k] - uprev[k], dv = v[k] - vprev[k];
+                    a += du * du;
+                    b += dv * dv;
+                }
+                rb[2 * i] = a;
+                rb[2 * i + 1] = b;
+            }
+            double su = 0.0, sv = 0.0;
+            for (int64_t i = 0; i < H; ++i) {
+                su += rb[2 * i];
+                sv += rb[2 * i + 1];
+            }
+            double ru = sqrt(su / (double)n), rv = sqrt(sv / (double)n);
+            double r = ru > rv ? ru : rv;
+            if (residual) *residual = r;
+            if (r <= tol) break;
+        }
     }
     if (lab_out) memcpy(lab_out, lab, (size_t)n);
     free(lab);
@@ -380,7 +414,27 @@ int orc_solve(const float *f32, int64_t H, int64_t W, float delta, double lambda
     free(w);
     free(vprev);
     free(rb);
+    free(uprev);
     return 0;
+}
+
+int orc_solve(const float *f32, int64_t H, int64_t W, float delta, double lambda,
+              double theta, double tau, int iters, int inner_steps, const double *v_init,
+              const double *p1_init, const double *p2_init, double *u, double *v, double *p1,
+              double *p2, uint8_t *lab_out, double *trace) {
+    return solve_core(f32, H, W, delta, lambda, theta, tau, iters, inner_steps, v_init,
+                      p1_init, p2_init, u, v, p1, p2, lab_out, trace, 0, 0.0, NULL, NULL);
+}
+
+/* orc_solve with the stopping rule: stops at the first check with residual <= tol, else at  */
+/* max_iters.  Writes the iterations done and the residual of the last check.                */
+int orc_solve_tol(const float *f32, int64_t H, int64_t W, float delta, double lambda,
+                  double theta, double tau, int max_iters, int check_every, double tol,
+                  double *u, double *v, double *p1, double *p2, uint8_t *lab_out,
+                  int *iters_done, double *residual) {
+    if (check_every < 1 || max_iters < 1 || !(tol >= 0.0)) return -1;
+    return solve_core(f32, H, W, delta, lambda, theta, tau, max_iters, 1, NULL, NULL, NULL, u,
+                      v, p1, p2, lab_out, NULL, check_every, tol, iters_done, residual);
 }
 
 /* ---------------------------------------------------------------------------------------- */

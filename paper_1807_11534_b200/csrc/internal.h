@@ -45,6 +45,17 @@ struct Item {
     int32_t bands;  // b0 | (b1 << 16)
 };
 
+// Device record of a tolerance solve (rds_solve_tol): written by k_stop_check only.
+struct StopRecord {
+    int32_t flag;       // 1 once the rule fired (or the last check ran): later launches exit
+    int32_t iters;      // iterations completed when it fired
+    int32_t launches;   // stencil launches that ran (selects the ping-pong buffer)
+    int32_t converged;  // residual <= tol at that check
+    double residual;    // max(RMS du, RMS dv) at the last check
+    int32_t checks;     // checks evaluated
+    int32_t pad_;
+};
+
 struct StencilArgs {
     const float *p1_in, *p2_in, *v_in;   // plane origins (pixel (0,0))
     const float *c;                      // 2^-100 theta*lambda*f on RD, -inf Fg, +inf Bg/frame
@@ -54,6 +65,8 @@ struct StencilArgs {
     const Item *items;                   // active items (strip-major, runs split in chunks)
     const int32_t *n_items;              // device count
     int32_t *queue;                      // this launch's work counter (zeroed before the loop)
+    StopRecord *stop;                    // tolerance mode: skip the launch once stop->flag
+    double *chk;                         // CHECK launches: [item][2] sums of du^2, dv^2
     int64_t pitch;
     int H, W;
     float tau, theta, inv_theta;
@@ -100,8 +113,14 @@ cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_ban
                                int slots, int fixed_chunk, int warmup_rows, Item *items,
                                int32_t *counts, cudaStream_t s);
 
-cudaError_t launch_stencil(int kf, int stages, bool write_u, const StencilArgs &a,
+// mode: 0 iterate, 1 + write u and mask, 2 + stopping sums into a.chk (k_stencil.cu)
+cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a,
                            int grid, cudaStream_t s);
+// Stopping rule after a CHECK launch that ended at iteration it_end:
+// r = max(sqrt(sum du^2 / N), sqrt(sum dv^2 / N)); fire if r <= tol or is_last.
+cudaError_t launch_stop_check(const double *chk, const int32_t *n_items, double n_pixels,
+                              double tol, int it_end, int launch_idx, int is_last,
+                              StopRecord *rec, cudaStream_t s);
 int stencil_blocks_per_sm(int kf, int stages, bool aligned);
 bool kf_supported(int kf);
 int kf_list(int32_t *out, int cap);

@@ -105,3 +105,57 @@ cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s) {
 }
 
 }  // namespace rds
+
+namespace rds {
+
+// Stopping rule of PAPER.md:234-238, max{||u^l - u^(l-1)||, ||v^l - v^(l-1)||} <= tol, with
+// the RMS norm over all N pixels (reading R-F2): one CTA sums the CHECK launch's per-item
+// partials in a fixed order (thread-strided sums, then a fixed tree), so the decision is
+// deterministic.  Pinned pixels contribute 0 (u and v are constant there).
+__global__ void __launch_bounds__(256) k_stop_check(const double *chk, const int32_t *n_items_p,
+                                                    double n_pixels, double tol, int it_end,
+                                                    int launch_idx, int is_last,
+                                                    StopRecord *rec) {
+    if (*(volatile const int32_t *)&rec->flag != 0) return;  // uniform across the CTA
+    const int n_items = *n_items_p;
+    double su = 0.0, sv = 0.0;
+    for (int i = threadIdx.x; i < n_items; i += 256) {
+        su += chk[2 * i];
+        sv += chk[2 * i + 1];
+    }
+    __shared__ double sh[2][8];
+    su = warp_sum(su);
+    sv = warp_sum(sv);
+    if ((threadIdx.x & 31) == 0) {
+        sh[0][threadIdx.x >> 5] = su;
+        sh[1][threadIdx.x >> 5] = sv;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tu = 0.0, tv = 0.0;
+        for (int w = 0; w < 8; ++w) {
+            tu += sh[0][w];
+            tv += sh[1][w];
+        }
+        const double r = fmax(sqrt(tu / n_pixels), sqrt(tv / n_pixels));
+        rec->residual = r;
+        rec->checks += 1;
+        const bool conv = r <= tol;
+        if (conv || is_last) {
+            rec->iters = it_end;
+            rec->launches = launch_idx + 1;
+            rec->converged = conv ? 1 : 0;
+            rec->flag = 1;
+        }
+    }
+}
+
+cudaError_t launch_stop_check(const double *chk, const int32_t *n_items, double n_pixels,
+                              double tol, int it_end, int launch_idx, int is_last,
+                              StopRecord *rec, cudaStream_t s) {
+    k_stop_check<<<1, 256, 0, s>>>(chk, n_items, n_pixels, tol, it_end, launch_idx, is_last,
+                                   rec);
+    return cudaGetLastError();
+}
+
+}  // namespace rds

@@ -270,12 +270,26 @@ __device__ __forceinline__ void stage(const Q &ap1, const Q &ap2, const Q &av, c
     bw = f.w;
 }
 
+// Launch modes: PLAIN iterates; WRITE_U also writes u and the mask of the last level
+// (the last launch of a solve); CHECK additionally accumulates the paper's stopping
+// quantities sum (u^l - u^(l-1))^2 and sum (v^l - v^(l-1))^2 over the item's output pixels
+// (f2, rds_solve_tol).  u^(l-1) comes from stage S-2 one row step earlier,
+// or, for a single-stage launch, from the u plane written by the previous launch.
+enum { MODE_PLAIN = 0, MODE_WRITE_U = 1, MODE_CHECK = 2 };
+
+template <int S, int MODE>
+struct Extra {  // per-row-step state only the CHECK mode needs
+    Q uprev;    // u of level S-1 (stage S-2's u) at the last stage's row
+};
+
 // One row step: consume input row n from the ring, advance all S stages, store the level-S
 // row if it is an output row of this item, then refill the slot with row n+RING.
-template <int S, bool WRITE_U, bool ALIGNED, bool LAST>
-__device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B, int n,
-                                          const Ctx &x) {
+template <int S, int MODE, bool ALIGNED, bool LAST>
+__device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B,
+                                          const Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
+                                          const Ctx &x, float &acc_u, float &acc_v) {
     using SPL = Split<S>;
+    constexpr bool WRITE_U = MODE != MODE_PLAIN;
     cp_async_wait<RING - 1>();
     const float4 *slot = x.ring + (n & (RING - 1)) * 96;
     const float4 *crow = x.cring + ((n & (CR - 1)) + CR) * 32;  // row n; row n-L at -32 L
@@ -309,10 +323,25 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
         in2 = o2;
         inv = ov;
         ind = od;
+        if (MODE == MODE_CHECK && S >= 2 && t == S - 2) EB.uprev = uu;  // u^(l-1), row m
         if (t == S - 1) {
             B.q1 = o1;
             if (x.store_lane && m >= x.R0 && m < x.Rend) {
                 const int64_t o = (int64_t)m * x.pitch + x.col;
+                if (MODE == MODE_CHECK) {
+                    Q up;
+                    if (S >= 2) {
+                        up = EA.uprev;
+                    } else {  // single stage: u^(l-1) is in the u plane (natural order)
+                        const float4 q = *reinterpret_cast<const float4 *>(x.uo + o);
+                        up = Q{make_float2(q.x, q.z), make_float2(q.y, q.w)};
+                    }
+                    const float2 da = sub2(uu.a, up.a), db = sub2(uu.b, up.b);
+                    const Q &av = A.v[S - 1];  // v^(l-1) at row m
+                    const float2 ea = sub2(ov.a, av.a), eb = sub2(ov.b, av.b);
+                    acc_u += (da.x * da.x + da.y * da.y) + (db.x * db.x + db.y * db.y);
+                    acc_v += (ea.x * ea.x + ea.y * ea.y) + (eb.x * eb.x + eb.y * eb.y);
+                }
                 stq(x.p1o + o, o1);
                 stq(x.p2o + o, o2);
                 stq(x.vo + o, ov);
@@ -330,9 +359,10 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
     cp_async_commit();
 }
 
-template <int S, bool WRITE_U, bool ALIGNED, bool LAST>
-__device__ __forceinline__ void march(const Ctx &x, int n) {
+template <int S, int MODE, bool ALIGNED, bool LAST>
+__device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &acc_v) {
     PipeState<S> A, B;
+    Extra<S, MODE> EA, EB;
 #pragma unroll
     for (int t = 0; t < S; ++t) A.p1[t] = A.p2[t] = A.v[t] = A.w[t] = zeroq();
     A.q1 = zeroq();
@@ -340,9 +370,10 @@ __device__ __forceinline__ void march(const Ctx &x, int n) {
     for (int k = 0; k < PipeState<S>::ND; ++k) {
         A.d1[k] = A.d2[k] = A.dv[k] = A.dd[k] = zeroq();
     }
+    EA.uprev = zeroq();
     for (; n <= x.n_last; n += 2) {
-        pipe_step<S, WRITE_U, ALIGNED, LAST>(A, B, n, x);
-        pipe_step<S, WRITE_U, ALIGNED, LAST>(B, A, n + 1, x);
+        pipe_step<S, MODE, ALIGNED, LAST>(A, B, EA, EB, n, x, acc_u, acc_v);
+        pipe_step<S, MODE, ALIGNED, LAST>(B, A, EB, EA, n + 1, x, acc_u, acc_v);
     }
 }
 
@@ -352,13 +383,15 @@ struct MinBlocks {
     static constexpr int value = 2;
 };
 
-template <int KF, int S, bool WRITE_U, bool ALIGNED>
+template <int KF, int S, int MODE, bool ALIGNED>
 __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
     k_stencil(const StencilArgs a) {
     static_assert(S >= 1 && S <= KF && KF + 3 <= PAD_R, "stage count");
     static_assert(RING + KF + 3 <= CR, "c ring too short for the stage lags");
     constexpr int LH = lh_of(KF), WV = wv_of(KF);
     extern __shared__ float4 smem[];  // [warps][RING][3][32] then [warps][2 CR][32]
+    // tolerance mode: once the stopping rule has fired, the remaining launches are no-ops
+    if (a.stop != nullptr && *(volatile const int32_t *)&a.stop->flag != 0) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int n_items = *a.n_items;
     Ctx x;
@@ -404,34 +437,49 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
             if (n + r <= x.n_last) stage_row(x, n + r);
             cp_async_commit();
         }
+        float acc_u = 0.0f, acc_v = 0.0f;
         // the Neumann row H-1 matters whenever the march (cone included) reaches it
         if (x.n_last >= a.H - 1)
-            march<S, WRITE_U, ALIGNED, true>(x, n);
+            march<S, MODE, ALIGNED, true>(x, n, acc_u, acc_v);
         else
-            march<S, WRITE_U, ALIGNED, false>(x, n);
+            march<S, MODE, ALIGNED, false>(x, n, acc_u, acc_v);
+        if (MODE == MODE_CHECK) {  // per-item partial sums, fixed lane order (deterministic)
+            double su = acc_u, sv = acc_v;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                su += __shfl_xor_sync(0xffffffffu, su, off);
+                sv += __shfl_xor_sync(0xffffffffu, sv, off);
+            }
+            if (lane == 0) {
+                a.chk[2 * it] = su;
+                a.chk[2 * it + 1] = sv;
+            }
+        }
         cp_async_wait<0>();
         __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------------------------------
-// dispatch over (KF, S, WRITE_U, ALIGNED)
+// dispatch over (KF, S, MODE, ALIGNED)
 // ---------------------------------------------------------------------------------------
 typedef void (*StencilFn)(const StencilArgs);
 
 template <int KF, int S>
 struct Table {
-    static void fill(StencilFn (*t)[2][2]) {
-        t[S][0][0] = k_stencil<KF, S, false, false>;
-        t[S][1][0] = k_stencil<KF, S, true, false>;
-        t[S][0][1] = k_stencil<KF, S, false, true>;
-        t[S][1][1] = k_stencil<KF, S, true, true>;
+    static void fill(StencilFn (*t)[3][2]) {
+        t[S][0][0] = k_stencil<KF, S, MODE_PLAIN, false>;
+        t[S][1][0] = k_stencil<KF, S, MODE_WRITE_U, false>;
+        t[S][2][0] = k_stencil<KF, S, MODE_CHECK, false>;
+        t[S][0][1] = k_stencil<KF, S, MODE_PLAIN, true>;
+        t[S][1][1] = k_stencil<KF, S, MODE_WRITE_U, true>;
+        t[S][2][1] = k_stencil<KF, S, MODE_CHECK, true>;
         Table<KF, S - 1>::fill(t);
     }
 };
 template <int KF>
 struct Table<KF, 0> {
-    static void fill(StencilFn (*)[2][2]) {}
+    static void fill(StencilFn (*)[3][2]) {}
 };
 
 #ifndef RDS_KF_LIST
@@ -440,8 +488,8 @@ struct Table<KF, 0> {
 
 static const int kKfMax = 8;
 
-static StencilFn lookup(int kf, int stages, bool write_u, bool aligned) {
-    static StencilFn table[kKfMax + 1][kKfMax + 1][2][2];
+static StencilFn lookup(int kf, int stages, int mode, bool aligned) {
+    static StencilFn table[kKfMax + 1][kKfMax + 1][3][2];
     static bool init = false;
     if (!init) {
 #define RDS_FILL(K) Table<K, K>::fill(table[K]);
@@ -457,11 +505,12 @@ static StencilFn lookup(int kf, int stages, bool write_u, bool aligned) {
                                                  STENCIL_SMEM);
         init = true;
     }
-    if (kf < 1 || kf > kKfMax || stages < 1 || stages > kf) return nullptr;
-    return table[kf][stages][write_u ? 1 : 0][aligned ? 1 : 0];
+    if (kf < 1 || kf > kKfMax || stages < 1 || stages > kf || mode < 0 || mode > 2)
+        return nullptr;
+    return table[kf][stages][mode][aligned ? 1 : 0];
 }
 
-bool kf_supported(int kf) { return lookup(kf, 1, false, false) != nullptr; }
+bool kf_supported(int kf) { return lookup(kf, 1, MODE_PLAIN, false) != nullptr; }
 
 int kf_list(int32_t *out, int cap) {
     int n = 0;
@@ -474,7 +523,7 @@ int kf_list(int32_t *out, int cap) {
 }
 
 int stencil_blocks_per_sm(int kf, int stages, bool aligned) {
-    StencilFn fn = lookup(kf, stages, false, aligned);
+    StencilFn fn = lookup(kf, stages, MODE_PLAIN, aligned);
     if (!fn) return 0;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, STENCIL_WARPS * 32,
@@ -483,9 +532,9 @@ int stencil_blocks_per_sm(int kf, int stages, bool aligned) {
     return nb;
 }
 
-cudaError_t launch_stencil(int kf, int stages, bool write_u, const StencilArgs &a, int grid,
+cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a, int grid,
                            cudaStream_t s) {
-    StencilFn fn = lookup(kf, stages, write_u, (a.W & 3) == 0);
+    StencilFn fn = lookup(kf, stages, mode, (a.W & 3) == 0);
     if (!fn) return cudaErrorInvalidValue;
     if (grid <= 0) return cudaSuccess;
     fn<<<grid, STENCIL_WARPS * 32, STENCIL_SMEM, s>>>(a);

@@ -53,6 +53,11 @@ struct rds_handle {
     int *flag = nullptr;
     double *e_partials = nullptr, *e_out = nullptr;
     unsigned *hist = nullptr;        // radix-select histogram (rds_band_for_fraction)
+    StopRecord *stop = nullptr;      // tolerance solves (rds_solve_tol)
+    double *chk = nullptr;           // per-item stopping sums of a CHECK launch
+    size_t chk_bytes = 0;
+    bool tol_pending = false;        // a tolerance solve's outcome is still on the device
+    int cur0 = 0;                    // ping-pong buffer at the start of the last solve
     float *scratch = nullptr;        // H*W natural-order staging for swizzled-plane getters
 
     cudaStream_t own_stream = nullptr, stream = nullptr;
@@ -70,8 +75,8 @@ struct rds_handle {
     // cached CUDA graph of the K-loop
     cudaGraphExec_t graph = nullptr;
     struct Key {
-        int kf, iters, cur0, max_items;
-        float tau, theta;
+        int kf, iters, cur0, max_items, check_every;
+        float tau, theta, tol;
         bool operator==(const Key &o) const { return memcmp(this, &o, sizeof(Key)) == 0; }
     } gkey{};
 
@@ -108,7 +113,8 @@ static void free_all(rds_t *h) {
         if (p) cudaFree(p);
     void *other[] = {h->lab,     h->mask,        h->tile_rd, h->tile_list, h->band_flag,
                      h->items,   h->queue,       h->counts,  h->n_rd_dev,  h->absmax_bits,
-                     h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch};
+                     h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch,
+                     h->stop,    h->chk};
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -401,13 +407,61 @@ static int blocks_per_sm(rds_t *h, int kf, int stages) {
     return (h->opt_ctas > 0 && h->opt_ctas < b) ? h->opt_ctas : b;
 }
 
-// Enqueue the K-loop: zero the per-launch work queues, then ceil(iters/kf) persistent
-// stencil launches on ping-pong buffers (the last one also writes u and mask).
+// The K-loop as a list of stencil launches.  Fixed-K solves: ceil(K/kf) launches of kf
+// iterations (the last one shorter and writing u and the mask).  Tolerance solves
+// (check_every = m > 0): the stopping rule is evaluated after iterations m, 2m, ... and K;
+// each block between checks is cut into ceil(len/kf) near-equal launches (the longer ones
+// last), and the launch ending at a check runs in CHECK mode (u, mask and the stopping sums)
+// followed by k_stop_check.
+struct LaunchPlan {
+    int stages, mode, it_end;
+    bool check, last;
+};
+
+static int make_plan(int kf, int iters, int check_every, LaunchPlan *out, int cap) {
+    int n = 0;
+    if (check_every <= 0) {
+        int done = 0;
+        while (done < iters) {
+            const int st = (iters - done) >= kf ? kf : (iters - done);
+            done += st;
+            if (n < cap) out[n] = LaunchPlan{st, done == iters ? 1 : 0, done, false, done == iters};
+            ++n;
+        }
+        return n;
+    }
+    int prev = 0;
+    while (prev < iters) {
+        const int c = (iters - prev) > check_every ? prev + check_every : iters;
+        const int len = c - prev, nl = (len + kf - 1) / kf, base = len / nl, rem = len % nl;
+        int done = prev;
+        for (int k = 0; k < nl; ++k) {
+            const int st = base + (k >= nl - rem ? 1 : 0);
+            done += st;
+            const bool chk = k == nl - 1;
+            if (n < cap) out[n] = LaunchPlan{st, chk ? 2 : 0, done, chk, done == iters};
+            ++n;
+        }
+        // a single-stage CHECK launch reads u^(l-1) from the u plane: the launch before it
+        // (if any, and not itself a CHECK launch) must write u
+        if (n - 1 < cap && out[n - 1].stages == 1 && nl >= 2 && n - 2 < cap)
+            out[n - 2].mode = 1;
+        prev = c;
+    }
+    return n;
+}
+
+// Enqueue the K-loop: zero the per-launch work queues, then the planned persistent stencil
+// launches on ping-pong buffers (and the stopping checks of a tolerance solve).
 static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, float tau,
-                                float theta) {
-    const int launches = (iters + kf - 1) / kf;
+                                float theta, int check_every, float tol) {
+    const int launches = make_plan(kf, iters, check_every, nullptr, 0);
+    LaunchPlan *plan = new (std::nothrow) LaunchPlan[launches > 0 ? launches : 1];
+    if (!plan) return cudaErrorMemoryAllocation;
+    make_plan(kf, iters, check_every, plan, launches);
     cudaError_t e = cudaMemsetAsync(h->queue, 0, sizeof(int32_t) * launches, h->stream);
-    if (e != cudaSuccess) return e;
+    if (e == cudaSuccess && check_every > 0)
+        e = cudaMemsetAsync(h->stop, 0, sizeof(StopRecord), h->stream);
     StencilArgs a{};
     a.c = h->at(h->c);
     a.u_out = h->at(h->u);
@@ -420,10 +474,11 @@ static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, floa
     a.tau = tau;
     a.theta = theta;
     a.inv_theta = 1.0f / theta;
-    int done = 0, cur = h->cur, l = 0;
-    while (done < iters) {
-        const int stages = (iters - done) >= kf ? kf : (iters - done);
-        const bool last = done + stages == iters;
+    a.stop = check_every > 0 ? h->stop : nullptr;
+    a.chk = h->chk;
+    int cur = h->cur;
+    for (int l = 0; l < launches && e == cudaSuccess; ++l) {
+        const LaunchPlan &L = plan[l];
         a.p1_in = h->at(h->p1[cur]);
         a.p2_in = h->at(h->p2[cur]);
         a.v_in = h->at(h->v[cur]);
@@ -431,16 +486,17 @@ static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, floa
         a.p2_out = h->at(h->p2[cur ^ 1]);
         a.v_out = h->at(h->v[cur ^ 1]);
         a.queue = h->queue + l;
-        int grid = h->n_sm * blocks_per_sm(h, kf, stages);
+        int grid = h->n_sm * blocks_per_sm(h, kf, L.stages);
         const int need = (max_items + STENCIL_WARPS - 1) / STENCIL_WARPS;
         if (grid > need) grid = need;
-        e = launch_stencil(kf, stages, last, a, grid, h->stream);
-        if (e != cudaSuccess) return e;
+        e = launch_stencil(kf, L.stages, L.mode, a, grid, h->stream);
+        if (e == cudaSuccess && L.check)
+            e = launch_stop_check(h->chk, h->counts + 1, (double)h->H * (double)h->W, tol,
+                                  L.it_end, l, L.last ? 1 : 0, h->stop, h->stream);
         cur ^= 1;
-        done += stages;
-        ++l;
     }
-    return cudaSuccess;
+    delete[] plan;
+    return e;
 }
 
 static cudaError_t grow(void **p, size_t *cap, size_t bytes) {
@@ -453,8 +509,8 @@ static cudaError_t grow(void **p, size_t *cap, size_t bytes) {
     return e;
 }
 
-int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32_t iters) {
-    if (!h) return fail(nullptr, RDS_EINVAL, "rds_solve: NULL handle");
+static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delta, int32_t iters,
+                      int check_every, float tol) {
     if (!(lambda > 0.0f) || !isfinite(lambda))
         return fail(h, RDS_EINVAL, "rds_solve: lambda=%g must be finite and > 0", lambda);
     if (!(theta > 0.0f) || !isfinite(theta))
@@ -475,7 +531,7 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
     const int n_bands = (int)((h->H + TILE_H - 1) / TILE_H);
     const int max_items = n_strips * n_bands;
     const int fixed_chunk = h->opt_rows ? (h->opt_rows + TILE_H - 1) / TILE_H : 0;
-    const int launches = (iters + kf - 1) / kf;
+    const int launches = make_plan(kf, iters, check_every, nullptr, 0);
     {
         void *pf = h->band_flag, *pi = h->items, *pq = h->queue;
         const bool realloc_items = sizeof(Item) * (size_t)max_items > h->items_bytes;
@@ -486,6 +542,17 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
         h->band_flag = (int32_t *)pf;
         h->items = (Item *)pi;
         h->queue = (int32_t *)pq;
+        if (check_every > 0) {
+            void *pc = h->chk;
+            const bool realloc_chk = 2 * sizeof(double) * (size_t)max_items > h->chk_bytes;
+            CK(h, grow(&pc, &h->chk_bytes, 2 * sizeof(double) * (size_t)max_items));
+            h->chk = (double *)pc;
+            if (!h->stop) CK(h, cudaMalloc(&h->stop, sizeof(StopRecord)));
+            if (realloc_chk && h->graph) {
+                cudaGraphExecDestroy(h->graph);
+                h->graph = nullptr;
+            }
+        }
         if ((realloc_items || realloc_queue) && h->graph) {
             cudaGraphExecDestroy(h->graph);
             h->graph = nullptr;
@@ -532,11 +599,12 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
                                  2 * kf + 4, h->items, h->counts, h->stream));
     }
     h->warm_pending = false;
+    h->tol_pending = false;
     h->cur = 0;
     if (h->opt_timing) CK(h, cudaEventRecord(h->ev[1], h->stream));
 
     if (iters > 0) {
-        rds_handle::Key key{kf, iters, h->cur, max_items, tau, theta};
+        rds_handle::Key key{kf, iters, h->cur, max_items, check_every, tau, theta, tol};
         if (h->opt_graph && launches > 1) {
             if (!h->graph || !(h->gkey == key)) {
                 if (h->graph) {
@@ -550,7 +618,8 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
                 if (e == cudaSuccess) {
                     cudaStream_t keep = h->stream;
                     h->stream = cap;
-                    cudaError_t e2 = enqueue_loop(h, kf, iters, max_items, tau, theta);
+                    cudaError_t e2 =
+                        enqueue_loop(h, kf, iters, max_items, tau, theta, check_every, tol);
                     h->stream = keep;
                     e = cudaStreamEndCapture(cap, &g);
                     if (e == cudaSuccess) e = e2;
@@ -565,9 +634,13 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
             }
             CK(h, cudaGraphLaunch(h->graph, h->stream));
         } else {
-            CK(h, enqueue_loop(h, kf, iters, max_items, tau, theta));
+            CK(h, enqueue_loop(h, kf, iters, max_items, tau, theta, check_every, tol));
         }
-        if (launches & 1) h->cur ^= 1;
+        h->cur0 = h->cur;
+        if (check_every > 0)
+            h->tol_pending = true;  // the buffer holding the result is known on the device
+        else if (launches & 1)
+            h->cur ^= 1;
     }
     if (h->opt_timing) CK(h, cudaEventRecord(h->ev[2], h->stream));
 
@@ -582,10 +655,46 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
     st.n_items = max_items;
     st.iters = iters;
     st.k_fuse = kf;
-    st.launches = (iters + kf - 1) / kf;
+    st.launches = launches;
+    st.converged = 0;
+    st.residual = -1.0f;
+    st.check_every = check_every;
     st.item_rows = 0;  // filled by rds_get_stats (chosen on the device)
     st.item_cols = wv;
     st.setup_ms = st.loop_ms = -1.0f;
+    return RDS_OK;
+}
+
+int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32_t iters) {
+    if (!h) return fail(nullptr, RDS_EINVAL, "rds_solve: NULL handle");
+    return solve_impl(h, lambda, theta, tau, delta, iters, 0, 0.0f);
+}
+
+int rds_solve_tol(rds_t *h, float lambda, float theta, float tau, float delta, int32_t max_iters,
+                  float tol, int32_t check_every) {
+    if (!h) return fail(nullptr, RDS_EINVAL, "rds_solve_tol: NULL handle");
+    if (!(tol >= 0.0f)) return fail(h, RDS_EINVAL, "rds_solve_tol: tol=%g must be >= 0", tol);
+    if (check_every < 0)
+        return fail(h, RDS_EINVAL, "rds_solve_tol: check_every=%d must be >= 0", check_every);
+    if (max_iters < 1)
+        return fail(h, RDS_EINVAL, "rds_solve_tol: max_iters=%d must be >= 1", max_iters);
+    const int m = check_every > 0 ? check_every : (h->opt_kf ? h->opt_kf : kDefaultKF);
+    return solve_impl(h, lambda, theta, tau, delta, max_iters, m, tol);
+}
+
+// Bring the outcome of a tolerance solve to the host: which ping-pong buffer holds the
+// stopped state, the iteration count and the residual (synchronises the stream).
+static int resolve(rds_t *h) {
+    if (!h->tol_pending) return RDS_OK;
+    StopRecord r;
+    CK(h, cudaMemcpyAsync(&r, h->stop, sizeof r, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    h->cur = h->cur0 ^ (r.launches & 1);
+    h->stats.iters = r.iters;
+    h->stats.launches = r.launches;
+    h->stats.converged = r.converged;
+    h->stats.residual = (float)r.residual;
+    h->tol_pending = false;
     return RDS_OK;
 }
 
@@ -616,7 +725,11 @@ static int copy_out_swizzled(rds_t *h, float *dst, const float *plane_origin, in
 
 #define NEED_SOLVED(name)                                                          \
     if (!h) return fail(nullptr, RDS_EINVAL, name ": NULL handle");                \
-    if (!h->solved) return fail(h, RDS_ESTATE, name ": no solve has run yet");
+    if (!h->solved) return fail(h, RDS_ESTATE, name ": no solve has run yet");     \
+    {                                                                              \
+        const int rc_ = resolve(h);                                                \
+        if (rc_) return rc_;                                                       \
+    }
 
 int rds_get_u(rds_t *h, float *out, int on_device) {
     NEED_SOLVED("rds_get_u");

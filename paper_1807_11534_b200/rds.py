@@ -30,7 +30,7 @@ EXPORTS = (
     "rds_get_mask", "rds_get_v", "rds_get_p", "rds_get_fitting", "rds_get_labels",
     "rds_get_active_tiles", "rds_tile_shape", "rds_energy", "rds_get_stats",
     "rds_kfuse_supported", "rds_last_error", "rds_version", "rds_band_for_fraction",
-    "rds_solve_q",
+    "rds_solve_q", "rds_solve_tol",
 )
 
 
@@ -54,11 +54,12 @@ class rds_stats_t(ctypes.Structure):
                 ("n_active_cells", ctypes.c_int64),
                 ("iters", ctypes.c_int32), ("k_fuse", ctypes.c_int32),
                 ("launches", ctypes.c_int32), ("item_rows", ctypes.c_int32),
-                ("item_cols", ctypes.c_int32), ("pad_", ctypes.c_int32),
-                ("setup_ms", ctypes.c_float), ("loop_ms", ctypes.c_float)]
+                ("item_cols", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("setup_ms", ctypes.c_float), ("loop_ms", ctypes.c_float),
+                ("residual", ctypes.c_float), ("check_every", ctypes.c_int32)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 def _load():
@@ -92,6 +93,7 @@ def _load():
         "rds_version": [],
         "rds_band_for_fraction": [P, ctypes.c_double, ctypes.POINTER(f)],
         "rds_solve_q": [P, f, f, f, ctypes.c_double, i32],
+        "rds_solve_tol": [P, f, f, f, f, i32, f, i32],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -189,6 +191,11 @@ def rds_solve_q(h, lam, theta, tau, q, iters):
 
 def rds_solve(h, lam, theta, tau, delta, iters):
     _check(_lib.rds_solve(h, float(lam), float(theta), float(tau), float(delta), int(iters)), h)
+
+
+def rds_solve_tol(h, lam, theta, tau, delta, max_iters, tol, check_every=0):
+    _check(_lib.rds_solve_tol(h, float(lam), float(theta), float(tau), float(delta),
+                              int(max_iters), float(tol), int(check_every)), h)
 
 
 def _get(fn, h, out, dtype, shape):
@@ -333,6 +340,14 @@ class Solver:
 
     def solve(self, lam, theta, tau, delta, iters):
         rds_solve(self.h, lam, theta, tau, math.inf if delta is None else delta, iters)
+
+    def solve_tol(self, lam, theta, tau, delta, max_iters, tol, check_every=0):
+        """Stop at the first check (every check_every iterations, and at max_iters) where
+        max(RMS du, RMS dv) <= tol.  Returns the stats dict (iters,
+        converged, residual)."""
+        rds_solve_tol(self.h, lam, theta, tau, math.inf if delta is None else delta,
+                      max_iters, tol, check_every)
+        return self.stats()
 
     def _out(self, dtype, out):
         return np.empty(self.shape, dtype=dtype) if out is None else out

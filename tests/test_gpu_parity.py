@@ -438,3 +438,73 @@ def test_band_for_fraction_exact(rds, orc, name):
         assert np.array_equal(lab, orc.labels(f, qh))
         assert (lab == 2).sum() >= np.ceil(q * N)
     s.close()
+
+
+# ------------------------------------------------------------------------------------------
+# f2: tolerance solves -- stopping rule fused into the stencil
+# ------------------------------------------------------------------------------------------
+
+def _tol_case(rds, orc, z, P, cfg, lam, delta, max_iters, tol, m, ctx, **opt):
+    s = rds.Solver(*z.shape, **opt)
+    s.set_image(z)
+    s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
+    st = s.solve_tol(lam, cfg.theta, cfg.tau, delta, max_iters, tol, m)
+    me = st["check_every"]
+    assert me == (m or st["k_fuse"])
+    f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    o = orc.solve_tol(f, delta, lam, np.float32(cfg.theta), cfg.tau, max_iters, tol, me)
+    if st["iters"] != o["iters"]:
+        # only a check whose residual sits within rounding of tol may decide differently
+        lo = min(st["iters"], o["iters"])
+        r_lo = orc.solve_tol(f, delta, lam, np.float32(cfg.theta), cfg.tau, lo, np.inf,
+                             lo)["residual"]
+        assert abs(st["iters"] - o["iters"]) == me and abs(r_lo - tol) <= 2e-2 * tol, \
+            (ctx, st["iters"], o["iters"], r_lo)
+        o = orc.solve_tol(f, delta, lam, np.float32(cfg.theta), cfg.tau, st["iters"], np.inf,
+                          st["iters"])
+    assert st["converged"] == int(o["residual"] <= tol or st["iters"] < max_iters), ctx
+    assert abs(st["residual"] - o["residual"]) <= 2e-2 * max(o["residual"], 1e-6), \
+        (ctx, st["residual"], o["residual"])
+    p1, p2 = s.p()
+    g = dict(u=s.u(), v=s.v(), p1=p1, p2=p2, mask=s.mask())
+    compare(g, o, ctx=ctx)
+    return s, st
+
+
+@pytest.mark.parametrize("name,lam,dr,tol,m", [
+    ("C0", 5.0, 0.2, 1e-3, 0),          # empty band: fires at the first check, residual 0
+    ("C0", 5.0, math.inf, 1e-3, 0),
+    ("C1", 5.0, 0.2, 1e-3, 0),
+    ("C1", 2.0, math.inf, 2e-3, 10),    # blocks of 10 = two launches of 5 at k_fuse 7
+    ("C2", 5.0, 0.2, 5e-4, 8),
+])
+def test_solve_tol_configs(rds, orc, name, lam, dr, tol, m):
+    cfg = wl.CONFIGS[name]
+    z, P = wl.make_image(cfg)
+    delta = wl.band_delta(dr, orc.absmax(orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)))
+    s, st = _tol_case(rds, orc, z, P, cfg, lam, delta, cfg.iters, tol, m,
+                      f"{name} lam={lam} d={dr} tol={tol} m={m}")
+    if dr == 0.2 and name == "C0":
+        assert st["iters"] == st["check_every"] and st["residual"] == 0.0
+    s.close()
+
+
+@pytest.mark.parametrize("m,kf,max_iters,tol", [(1, 7, 23, 1e-3), (3, 2, 31, 0.0),
+                                               (9, 4, 50, 2e-3), (7, 7, 45, 0.0)])
+def test_solve_tol_schedules(rds, orc, m, kf, max_iters, tol):
+    """Single-stage CHECK launches (u^(l-1) from the u plane), blocks split across launches,
+    max_iters off the check grid, tol = 0 (runs to max_iters, converged = 0), ragged shape."""
+    cfg = wl.CONFIGS["C1"]
+    rng = np.random.default_rng(m * 100 + kf)
+    z = rng.uniform(0, 1, (75, 133)).astype(np.float32)
+    s, st = _tol_case(rds, orc, z, None, cfg, 5.0, np.float32(0.3), max_iters, tol, m,
+                      f"m={m} kf={kf} K={max_iters} tol={tol}", k_fuse=kf)
+    if tol == 0.0:
+        assert st["iters"] == max_iters and st["converged"] == 0
+    # graph replay and a fixed-K solve on the same handle afterwards
+    u1 = s.u().copy()
+    st2 = s.solve_tol(5.0, cfg.theta, cfg.tau, np.float32(0.3), max_iters, tol, m)
+    assert st2["iters"] == st["iters"] and np.array_equal(s.u(), u1)
+    s.solve(5.0, cfg.theta, cfg.tau, np.float32(0.3), st["iters"])
+    assert np.array_equal(s.u(), u1)
+    s.close()

@@ -491,3 +491,59 @@ def test_dependency_cone_window(orc, delta_rel):
         same = all(np.array_equal(win[k][m:m + b, m:m + b], full[k][r0:r0 + b, c0:c0 + b])
                    for k in ("u", "v", "p1", "p2"))
         assert same == exact, (m, same)
+
+
+# ------------------------------------------------------------------------------------------
+# f2: the stopping rule, RMS norm (reading R-F2)
+# ------------------------------------------------------------------------------------------
+
+def _rule_residual(orc, f, delta, lam, ell):
+    """max(RMS(u^l - u^(l-1)), RMS(v^l - v^(l-1))) from two plain fixed-K solves."""
+    a = orc.solve(f, delta, lam, np.float32(0.1), 0.125, ell)
+    b = orc.solve(f, delta, lam, np.float32(0.1), 0.125, ell - 1)
+    n = f.size
+    return max(math.sqrt(((a["u"] - b["u"]) ** 2).sum() / n),
+               math.sqrt(((a["v"] - b["v"]) ** 2).sum() / n))
+
+
+@pytest.mark.parametrize("m,tol,delta_rel", [(7, 3e-3, 0.4), (1, 1e-2, math.inf),
+                                             (5, 1e-3, math.inf), (4, 0.0, 0.3)])
+def test_stopping_rule_definition(orc, m, tol, delta_rel):
+    """orc_solve_tol stops at the FIRST check (multiples of m, and max_iters) whose residual,
+    recomputed here from two independent fixed-K solves, is <= tol; its state is the fixed-K
+    state at that iteration, bit for bit."""
+    rng = np.random.default_rng(5)
+    f = rng.uniform(-1, 1, (24, 30)).astype(np.float32)
+    delta = wl.band_delta(delta_rel, orc.absmax(f))
+    K = 40
+    o = orc.solve_tol(f, delta, 4.0, np.float32(0.1), 0.125, K, tol, m)
+    checks = list(range(m, K, m)) + [K]
+    want, r_want = None, None
+    for c in checks:
+        r = _rule_residual(orc, f, delta, 4.0, c)
+        if r <= tol or c == K:
+            want, r_want = c, r
+            break
+    assert o["iters"] == want
+    assert abs(o["residual"] - r_want) <= 1e-12 * max(1.0, r_want)
+    ref = orc.solve(f, delta, 4.0, np.float32(0.1), 0.125, want)
+    for k in ("u", "v", "p1", "p2"):
+        assert np.array_equal(o[k], ref[k])
+
+
+def test_stopping_rule_special_cases(orc):
+    rng = np.random.default_rng(6)
+    f = rng.uniform(-1, 1, (20, 20)).astype(np.float32)
+    # empty band: nothing moves, the first check fires with residual exactly 0
+    o = orc.solve_tol(f, np.float32(0.0), 4.0, np.float32(0.1), 0.125, 50, 0.0, 6)
+    assert o["iters"] == 6 and o["residual"] == 0.0
+    assert np.array_equal(o["u"], (f <= 0).astype(np.float64))
+    # tol = inf stops at the first check; max_iters shorter than check_every -> max_iters
+    o = orc.solve_tol(f, np.float32(np.inf), 4.0, np.float32(0.1), 0.125, 50, np.inf, 6)
+    assert o["iters"] == 6
+    o = orc.solve_tol(f, np.float32(np.inf), 4.0, np.float32(0.1), 0.125, 4, np.inf, 6)
+    assert o["iters"] == 4
+    # larger tolerances never stop later (the first index with r <= tol is monotone)
+    its = [orc.solve_tol(f, np.float32(np.inf), 4.0, np.float32(0.1), 0.125, 200, t, 3)["iters"]
+           for t in (1e-1, 1e-2, 1e-3, 1e-4)]
+    assert its == sorted(its)
