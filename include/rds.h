@@ -92,8 +92,8 @@ typedef struct {
 #define RDS_OPT_KFUSE 1      /* iterations per HBM round trip; 0 = library default; allowed
                                 values are listed by rds_kfuse_supported */
 #define RDS_OPT_ITEM_ROWS 2  /* maximum output rows per stencil work item (rounded up to a
-                                multiple of 32); 0 = automatic (about one item per resident
-                                warp, 64..512 rows) */
+                                multiple of 8); 0 = automatic (makespan model over resident
+                                warps, 8..512 rows) */
 #define RDS_OPT_TIMING 3     /* 1 = record setup/loop CUDA-event times in rds_stats_t */
 #define RDS_OPT_SKIP 4       /* 1 (default) = work only on strip x band cells overlapping
                                 active tiles; 0 = process every cell (restriction without

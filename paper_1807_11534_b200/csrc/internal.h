@@ -38,11 +38,11 @@ __host__ __device__ constexpr int lh_of(int kf) { return 4 * ((kf + 1 + 3) / 4);
 __host__ __device__ constexpr int rh_of(int kf) { return 4 * ((kf + 3) / 4); }
 __host__ __device__ constexpr int wv_of(int kf) { return 128 - lh_of(kf) - rh_of(kf); }
 
-// A stencil work item: output columns [strip*WV, (strip+1)*WV) and output rows
-// [b0*TILE_H, min(H, b1*TILE_H)) -- a piece of a vertical run of active 32-row bands.
+// A stencil work item: output columns [strip*WV, (strip+1)*WV) and output rows [r0, r1) --
+// a piece of a vertical run of active 32-row bands, cut at multiples of ITEM_Q rows.
+constexpr int ITEM_Q = 8;
 struct Item {
-    int32_t strip;
-    int32_t bands;  // b0 | (b1 << 16)
+    int32_t strip, r0, r1, pad_;
 };
 
 // Device record of a tolerance solve (rds_solve_tol): written by k_stop_check only.
@@ -106,10 +106,11 @@ cudaError_t launch_compact(const int32_t *flags, int n, int32_t *list, int32_t *
 cudaError_t launch_band_flags(const int32_t *tile_rd, int H, int W, int wv, int n_strips,
                               int skip, int32_t *band_flag, cudaStream_t s);
 // Work items from the band flags: maximal vertical runs of active bands per strip, each split
-// into near-equal pieces of <= chunk bands.  chunk = fixed_chunk if > 0, else the chunk in
-// [1, 16] minimising max(items, slots) * (32 chunk + warmup_rows) (makespan model).
-// out: items, counts[1] = number of items, counts[2] = chunk used, counts[3] = active cells.
-cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands,
+// into ceil(rows / chunk) near-equal pieces at ITEM_Q-row boundaries.  chunk = fixed_chunk
+// rounded up to ITEM_Q if > 0, else the candidate height minimising
+// ceil(items / slots) * (chunk + warmup_rows) (makespan model, k_setup.cu).
+// out: items, counts[1] = number of items, counts[2] = chunk rows, counts[3] = active cells.
+cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands, int H,
                                int slots, int fixed_chunk, int warmup_rows, Item *items,
                                int32_t *counts, cudaStream_t s);
 

@@ -299,8 +299,16 @@ cudaError_t launch_band_flags(const int32_t *tile_rd, int H, int W, int wv, int 
     return cudaGetLastError();
 }
 
-// Runs of active bands in strip s, split into pieces; emit == false only counts.
-__device__ int strip_items(const int32_t *flags, int n_bands, int chunk, int s, Item *out) {
+// Item rows are cut at multiples of ITEM_Q rows (finer than a 32-row band), so a sparse
+// active set, or a dense one that would overflow the resident warps by a few items, can be
+// spread over every warp.  Candidate item heights (rows) for the makespan model:
+__constant__ int kChunkRows[] = {8, 16, 24, 32, 40, 48, 64, 80, 96, 128, 160, 192, 256, 384, 512};
+constexpr int N_CHUNK = 15;
+
+// Runs of active bands in strip s (rows clipped to H), split into ceil(rows / chunk) pieces of
+// near-equal height at ITEM_Q-row boundaries; out == nullptr only counts.
+__device__ int strip_items(const int32_t *flags, int n_bands, int H, int chunk, int s,
+                           Item *out) {
     int n = 0, b = 0;
     while (b < n_bands) {
         if (!flags[b]) {
@@ -309,12 +317,14 @@ __device__ int strip_items(const int32_t *flags, int n_bands, int chunk, int s, 
         }
         int e = b;
         while (e < n_bands && flags[e]) ++e;
-        const int len = e - b, pieces = (len + chunk - 1) / chunk;
+        const int r0 = b * TILE_H, r1 = min(e * TILE_H, H);
+        const int q = (r1 - r0 + ITEM_Q - 1) / ITEM_Q;            // ITEM_Q-row slices
+        const int pieces = (r1 - r0 + chunk - 1) / chunk;
         for (int k = 0; k < pieces; ++k) {
             if (out) {
-                const int p0 = b + (int)((int64_t)k * len / pieces);
-                const int p1 = b + (int)((int64_t)(k + 1) * len / pieces);
-                out[n] = Item{s, p0 | (p1 << 16)};
+                const int p0 = r0 + ITEM_Q * (int)((int64_t)k * q / pieces);
+                const int p1 = min(r1, r0 + ITEM_Q * (int)((int64_t)(k + 1) * q / pieces));
+                out[n] = Item{s, p0, p1, 0};
             }
             ++n;
         }
@@ -323,38 +333,60 @@ __device__ int strip_items(const int32_t *flags, int n_bands, int chunk, int s, 
     return n;
 }
 
-// Single CTA: total active bands -> chunk; per-strip item counts -> block exclusive scan ->
-// items written in strip-major, ascending-row order (deterministic, no atomics).
+// Single CTA.  (1) For every candidate height c, the exact item count sum over runs of
+// ceil(rows / c); the makespan model picks the c minimising waves(c) * (c + warm-up rows),
+// waves = ceil(items / resident warps) (a launch costs whole rounds of items: one extra item
+// on a full wave doubles the launch), ties to the taller item (less warm-up work).
+// (2) Per-strip item counts -> block exclusive scan -> items written in strip-major,
+// ascending-row order (deterministic, no atomics).
 __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, int n_strips,
-                                                      int n_bands, int slots, int fixed_chunk,
-                                                      int warmup_rows, Item *items,
-                                                      int32_t *counts) {
-    __shared__ long long red[32];
+                                                      int n_bands, int H, int slots,
+                                                      int fixed_chunk, int warmup_rows,
+                                                      Item *items, int32_t *counts) {
+    __shared__ long long red[N_CHUNK + 1][32];
     __shared__ int off[32];
     __shared__ int chunk_s, base_s;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    long long tot = 0;
-    for (int i = tid; i < n_strips * n_bands; i += 1024) tot += band_flag[i] != 0;
-    for (int o = 16; o; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-    if (lane == 0) red[wid] = tot;
+    long long cnt_c[N_CHUNK + 1];
+#pragma unroll
+    for (int k = 0; k <= N_CHUNK; ++k) cnt_c[k] = 0;
+    for (int sidx = tid; sidx < n_strips; sidx += 1024) {
+        const int32_t *fl = band_flag + (int64_t)sidx * n_bands;
+        int b = 0;
+        while (b < n_bands) {
+            if (!fl[b]) {
+                ++b;
+                continue;
+            }
+            int e = b;
+            while (e < n_bands && fl[e]) ++e;
+            const int rows = min(e * TILE_H, H) - b * TILE_H;
+#pragma unroll
+            for (int k = 0; k < N_CHUNK; ++k) cnt_c[k] += (rows + kChunkRows[k] - 1) / kChunkRows[k];
+            cnt_c[N_CHUNK] += e - b;  // active cells
+            b = e;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k <= N_CHUNK; ++k) {
+        long long v = cnt_c[k];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[k][wid] = v;
+    }
     __syncthreads();
     if (tid == 0) {
-        long long t = 0;
-        for (int w = 0; w < 32; ++w) t += red[w];
-        int c = fixed_chunk;
+        int c = fixed_chunk > 0 ? (fixed_chunk + ITEM_Q - 1) / ITEM_Q * ITEM_Q : 0;
         if (c <= 0) {
-            // makespan model: items ~ t / c, each costing the chunk's rows plus the pipeline
-            // warm-up (2 KF + 4 rows)
             const long long sl = slots > 0 ? slots : 1;
             long long best = -1;
-            for (int cc = 1; cc <= 16; ++cc) {
-                // fractional rounds once over-subscribed (the queue is work-conserving), one
-                // latency-bound round below that
-                const long long items = (t + cc - 1) / cc;
-                const long long cost = (items > sl ? items : sl) * (cc * TILE_H + warmup_rows);
-                if (best < 0 || cost < best) {
+            for (int k = 0; k < N_CHUNK; ++k) {
+                long long items_k = 0;
+                for (int w = 0; w < 32; ++w) items_k += red[k][w];
+                const long long waves = (items_k + sl - 1) / sl;
+                const long long cost = (waves > 0 ? waves : 1) * (kChunkRows[k] + warmup_rows);
+                if (best < 0 || cost <= best) {
                     best = cost;
-                    c = cc;
+                    c = kChunkRows[k];
                 }
             }
         }
@@ -364,10 +396,10 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
     __syncthreads();
     const int chunk = chunk_s;
     for (int s0 = 0; s0 < n_strips; s0 += 1024) {
-        const int s = s0 + tid;
-        const int cnt = s < n_strips ? strip_items(band_flag + (int64_t)s * n_bands, n_bands,
-                                                   chunk, s, nullptr)
-                                     : 0;
+        const int sidx = s0 + tid;
+        const int cnt = sidx < n_strips ? strip_items(band_flag + (int64_t)sidx * n_bands, n_bands,
+                                                      H, chunk, sidx, nullptr)
+                                        : 0;
         // block exclusive scan of cnt
         int incl = cnt;
         for (int o = 1; o < 32; o <<= 1) {
@@ -387,8 +419,9 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
         }
         __syncthreads();
         const int start = base_s + off[wid] + incl - cnt;
-        if (s < n_strips)
-            strip_items(band_flag + (int64_t)s * n_bands, n_bands, chunk, s, items + start);
+        if (sidx < n_strips)
+            strip_items(band_flag + (int64_t)sidx * n_bands, n_bands, H, chunk, sidx,
+                        items + start);
         __syncthreads();
         if (tid == 1023) base_s = start + cnt;
         __syncthreads();
@@ -397,15 +430,15 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
         counts[1] = base_s;
         counts[2] = chunk;
         long long t = 0;
-        for (int w = 0; w < 32; ++w) t += red[w];
+        for (int w = 0; w < 32; ++w) t += red[N_CHUNK][w];
         counts[3] = (int32_t)t;
     }
 }
 
-cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands,
+cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands, int H,
                                int slots, int fixed_chunk, int warmup_rows, Item *items,
                                int32_t *counts, cudaStream_t s) {
-    k_build_items<<<1, 1024, 0, s>>>(band_flag, n_strips, n_bands, slots, fixed_chunk,
+    k_build_items<<<1, 1024, 0, s>>>(band_flag, n_strips, n_bands, H, slots, fixed_chunk,
                                      warmup_rows, items, counts);
     return cudaGetLastError();
 }

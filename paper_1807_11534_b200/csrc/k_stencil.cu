@@ -414,9 +414,8 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
         it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= n_items) break;  // warp-uniform
         const Item item = a.items[it];
-        const int b0 = item.bands & 0xffff, b1 = item.bands >> 16;
-        x.R0 = b0 * TILE_H;
-        x.Rend = min(b1 * TILE_H, a.H);
+        x.R0 = item.r0;
+        x.Rend = item.r1;
         x.col = item.strip * WV - LH + 4 * lane;
         x.store_lane = (4 * lane >= LH) && (4 * lane < LH + WV);
         x.right_edge = (x.col + 3 == a.W - 1);

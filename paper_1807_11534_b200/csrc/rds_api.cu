@@ -529,14 +529,15 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     const int wv = wv_of(kf);
     const int n_strips = (int)((h->W + wv - 1) / wv);
     const int n_bands = (int)((h->H + TILE_H - 1) / TILE_H);
-    const int max_items = n_strips * n_bands;
-    const int fixed_chunk = h->opt_rows ? (h->opt_rows + TILE_H - 1) / TILE_H : 0;
+    // items are cut at ITEM_Q-row boundaries: at most one per ITEM_Q rows of every strip
+    const int max_items = n_strips * (int)((h->H + ITEM_Q - 1) / ITEM_Q);
+    const int fixed_chunk = h->opt_rows;  // rows (rounded up to ITEM_Q on the device)
     const int launches = make_plan(kf, iters, check_every, nullptr, 0);
     {
         void *pf = h->band_flag, *pi = h->items, *pq = h->queue;
         const bool realloc_items = sizeof(Item) * (size_t)max_items > h->items_bytes;
         const bool realloc_queue = sizeof(int32_t) * (size_t)(launches + 1) > h->queue_bytes;
-        CK(h, grow(&pf, &h->band_bytes, sizeof(int32_t) * (size_t)max_items));
+        CK(h, grow(&pf, &h->band_bytes, sizeof(int32_t) * (size_t)n_strips * n_bands));
         CK(h, grow(&pi, &h->items_bytes, sizeof(Item) * (size_t)max_items));
         CK(h, grow(&pq, &h->queue_bytes, sizeof(int32_t) * (size_t)(launches + 1)));
         h->band_flag = (int32_t *)pf;
@@ -595,7 +596,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
                             h->band_flag, h->stream));
     {
         const int slots = h->n_sm * blocks_per_sm(h, kf, kf) * STENCIL_WARPS;
-        CK(h, launch_build_items(h->band_flag, n_strips, n_bands, slots, fixed_chunk,
+        CK(h, launch_build_items(h->band_flag, n_strips, n_bands, (int)h->H, slots, fixed_chunk,
                                  2 * kf + 4, h->items, h->counts, h->stream));
     }
     h->warm_pending = false;
@@ -652,7 +653,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     st.H = h->H;
     st.W = h->W;
     st.n_tiles = h->n_tiles;
-    st.n_items = max_items;
+    st.n_items = (int64_t)n_strips * n_bands;
     st.iters = iters;
     st.k_fuse = kf;
     st.launches = launches;
@@ -833,7 +834,7 @@ int rds_get_stats(rds_t *h, rds_stats_t *out) {
     CK(h, cudaStreamSynchronize(h->stream));
     h->stats.n_active_tiles = cnt[0];
     h->stats.n_active_items = cnt[1];
-    h->stats.item_rows = cnt[2] * TILE_H;
+    h->stats.item_rows = cnt[2];
     h->stats.n_active_cells = cnt[3];
     h->stats.n_rd = nrd;
     if (h->opt_timing) {
