@@ -101,6 +101,9 @@ typedef struct {
 #define RDS_OPT_GRAPH 5      /* 1 (default) = replay the K-loop as a CUDA graph */
 #define RDS_OPT_CTAS_PER_SM 6 /* cap on resident stencil CTAs per SM (0 = occupancy limit);
                                  a tuning/diagnostic knob, results are identical */
+#define RDS_OPT_STOP_NORM 7  /* norm of the stopping rule (rds_solve_tol, rds_solve_gt):
+                                0 (default) = Euclidean norm over pixels of unit area,
+                                sqrt(sum d^2); 1 = RMS, sqrt(sum d^2 / (H W)) */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */
@@ -159,18 +162,47 @@ int rds_solve(rds_t *h, float lambda, float theta, float tau, float delta, int32
 
 /* rds_solve with the paper's stopping rule (§4): "iterate until
  *     max{ ||u^(l) - u^(l-1)||, ||v^(l) - v^(l-1)|| } <= delta_stop
- * is met at the l-th iteration".  The norm is the RMS over all H x W pixels (DESIGN.md
- * reading R-F2; pinned pixels contribute 0).  The rule is evaluated after iterations
+ * is met at the l-th iteration".  The norm is the Euclidean norm over all H x W pixels of
+ * unit area, like the paper's E2 (reading R-F2; RDS_OPT_STOP_NORM = 1 selects the
+ * RMS); pinned pixels contribute 0.  The rule is evaluated after iterations
  * check_every, 2 check_every, ... and always at max_iters (check_every = 0 selects the
  * library's k_fuse); the solve stops at the first check where it holds, else at max_iters.
  * The check runs inside the fused stencil (the launch ending at a check also writes u and
- * the mask) and a one-CTA reduction on the device; later launches exit immediately, so the
- * call enqueues everything and returns without synchronising.  The outcome -- iterations
+ * the mask) and a one-CTA reduction on the device that also drives a CUDA-graph while loop
+ * over whole check blocks, so the call returns without synchronising and the GPU runs only
+ * the iterations up to the stop.  The outcome -- iterations
  * done, converged flag, final residual -- is read by rds_get_stats (any getter resolves it).
  * Errors: those of rds_solve, and RDS_EINVAL if tol < 0 or NaN, check_every < 0 or
  * max_iters < 1. */
 int rds_solve_tol(rds_t *h, float lambda, float theta, float tau, float delta,
                   int32_t max_iters, float tol, int32_t check_every);
+
+/* ---- float64 mode: the paper's evaluation protocol (§4) ---------------
+ * "For delta = 10^-10 we set u^GT(x) = u^(l) in the original dual formulation": a tolerance
+ * far below float32 resolution, so rds_solve_gt runs the same iteration (same band test,
+ * same stopping rule and RMS norm as rds_solve_tol) with every state array in float64,
+ * correctly rounded sqrt/division and no FMA contraction, into separate double planes (the
+ * float result of the last rds_solve / rds_solve_tol is untouched).  delta = INFINITY gives
+ * the unrestricted ("original") method.  Synchronous.  Errors: as rds_solve_tol, and
+ * RDS_EINVAL if check_every < 1. */
+typedef struct {
+    int32_t iters;      /* iterations done */
+    int32_t converged;  /* 1 if the stopping rule fired before max_iters */
+    double residual;    /* max(RMS du, RMS dv) at the last check */
+} rds_gt_t;
+int rds_solve_gt(rds_t *h, float lambda, float theta, float tau, float delta,
+                 int32_t max_iters, double tol, int32_t check_every, rds_gt_t *out);
+
+/* u of the last rds_solve_gt, H x W float64.  RDS_ESTATE if none ran. */
+int rds_get_u_gt(rds_t *h, double *out, int on_device);
+
+/* The paper's two error measures of the current float u (last rds_solve / rds_solve_tol)
+ * against u^GT (last rds_solve_gt), PAPER.md:247-251:
+ *   E1 = N(GT n Omega*) / N(GT u Omega*)   (Tanimoto; GT = [u^GT > eps], Omega* = [u > eps];
+ *                                           1 when both are empty, reading R-C15)
+ *   E2 = sum_x (u(x) - u^GT(x))^2          (unit pixel area, reading R-C15)
+ * eps = 0.5 is the paper's convention.  RDS_ESTATE unless both solves ran. */
+int rds_compare_gt(rds_t *h, float eps, double *e1, double *e2);
 
 /* Getters: copy H x W results into `out` (host copies synchronise the handle's stream).
  * Errors: RDS_ESTATE before the first solve; RDS_EINVAL on NULL. */

@@ -70,7 +70,7 @@ def _load():
         lib.orc_energy.argtypes = [P, i64, i64, d, P, P, P, P, P]
         lib.orc_solve.argtypes = [P, i64, i64, f, d, d, d, i, i, P, P, P, P, P, P, P, P, P]
         lib.orc_solve.restype = i
-        lib.orc_solve_tol.argtypes = [P, i64, i64, f, d, d, d, i, i, d, P, P, P, P, P,
+        lib.orc_solve_tol.argtypes = [P, i64, i64, f, d, d, d, i, i, d, i, P, P, P, P, P,
                                       ctypes.POINTER(i), ctypes.POINTER(d)]
         lib.orc_solve_tol.restype = i
         lib.orc_solve_plain.argtypes = [P, i64, i64, d, d, d, i, P, P, P, P]
@@ -221,10 +221,11 @@ def solve(f, delta, lam, theta, tau, iters, inner_steps=1, init=None, trace=Fals
     return out
 
 
-def solve_tol(f, delta, lam, theta, tau, max_iters, tol, check_every):
+def solve_tol(f, delta, lam, theta, tau, max_iters, tol, check_every, norm="l2"):
     """The iteration with the paper's stopping rule (oracle.c orc_solve_tol):
-    checks after every check_every iterations and at max_iters, RMS norm.  Returns dict u, v,
-    p1, p2, labels, iters, residual."""
+    checks after every check_every iterations and at max_iters; norm "l2" (Euclidean over
+    pixels of unit area, reading R-F2) or "rms".  Returns dict u, v, p1, p2, labels, iters,
+    residual."""
     f = _f32(f)
     H, W = f.shape
     u = np.empty((H, W), dtype=np.float64)
@@ -235,12 +236,29 @@ def solve_tol(f, delta, lam, theta, tau, max_iters, tol, check_every):
     it = ctypes.c_int()
     res = ctypes.c_double()
     rc = _load().orc_solve_tol(_ptr(f), H, W, np.float32(delta), float(lam), float(theta),
-                               float(tau), int(max_iters), int(check_every), float(tol), _ptr(u),
+                               float(tau), int(max_iters), int(check_every), float(tol),
+                               {"l2": 0, "rms": 1}[norm], _ptr(u),
                                _ptr(v), _ptr(p1), _ptr(p2), _ptr(lab), ctypes.byref(it),
                                ctypes.byref(res))
     if rc != 0:
         raise ValueError(f"orc_solve_tol rc={rc}")
     return dict(u=u, v=v, p1=p1, p2=p2, labels=lab, iters=it.value, residual=res.value)
+
+
+def tanimoto(a, b):
+    """E1 of PAPER.md:247 (Tanimoto coefficient of two thresholded results): N(a n b) /
+    N(a u b) over pixels ("number of nodes"); 1 when both sets are empty (reading R-C15)."""
+    a = np.asarray(a, bool)
+    b = np.asarray(b, bool)
+    union = int(np.count_nonzero(a | b))
+    return 1.0 if union == 0 else int(np.count_nonzero(a & b)) / union
+
+
+def l2_error(u, ugt):
+    """E2 of PAPER.md:247, the integral of (u* - u^GT)^2 over Omega with unit pixel area
+    (reading R-C15)."""
+    d = np.asarray(u, np.float64) - np.asarray(ugt, np.float64)
+    return float(np.sum(d * d))
 
 
 def solve_plain(f, lam, theta, tau, iters):

@@ -264,12 +264,13 @@ int orc_ntrace(void) { return ORC_NTRACE; }
 /* The iteration; with check_every > 0 also the stopping rule of PAPER.md:234-238 (§4),     */
 /* "iterate until max{||u^l - u^(l-1)||, ||v^l - v^(l-1)||} <= delta is met at the l-th       */
 /* iteration", evaluated after iterations check_every, 2 check_every, ... and at iters, with */
-/* the RMS norm over all H*W pixels (reading R-F2).                                 */
+/* the Euclidean norm over the H*W pixels of unit area (norm = 0) or the RMS (norm = 1)      */
+/* (reading R-F2).                                                                  */
 static int solve_core(const float *f32, int64_t H, int64_t W, float delta, double lambda,
                       double theta, double tau, int iters, int inner_steps, const double *v_init,
                       const double *p1_init, const double *p2_init, double *u, double *v,
                       double *p1, double *p2, uint8_t *lab_out, double *trace, int check_every,
-                      double tol, int *iters_done, double *residual) {
+                      double tol, int norm, int *iters_done, double *residual) {
     if (H < 1 || W < 1 || iters < 0 || inner_steps < 1) return -1;
     int64_t n = H * W;
     uint8_t *lab = (uint8_t *)malloc((size_t)n);
@@ -401,7 +402,8 @@ static int solve_core(const float *f32, int64_t H, int64_t W, float delta, doubl
                 su += rb[2 * i];
                 sv += rb[2 * i + 1];
             }
-            double ru = sqrt(su / (double)n), rv = sqrt(sv / (double)n);
+            double nd = norm ? (double)n : 1.0;
+            double ru = sqrt(su / nd), rv = sqrt(sv / nd);
             double r = ru > rv ? ru : rv;
             if (residual) *residual = r;
             if (r <= tol) break;
@@ -423,18 +425,18 @@ int orc_solve(const float *f32, int64_t H, int64_t W, float delta, double lambda
               const double *p1_init, const double *p2_init, double *u, double *v, double *p1,
               double *p2, uint8_t *lab_out, double *trace) {
     return solve_core(f32, H, W, delta, lambda, theta, tau, iters, inner_steps, v_init,
-                      p1_init, p2_init, u, v, p1, p2, lab_out, trace, 0, 0.0, NULL, NULL);
+                      p1_init, p2_init, u, v, p1, p2, lab_out, trace, 0, 0.0, 0, NULL, NULL);
 }
 
 /* orc_solve with the stopping rule: stops at the first check with residual <= tol, else at  */
 /* max_iters.  Writes the iterations done and the residual of the last check.                */
 int orc_solve_tol(const float *f32, int64_t H, int64_t W, float delta, double lambda,
                   double theta, double tau, int max_iters, int check_every, double tol,
-                  double *u, double *v, double *p1, double *p2, uint8_t *lab_out,
+                  int norm, double *u, double *v, double *p1, double *p2, uint8_t *lab_out,
                   int *iters_done, double *residual) {
     if (check_every < 1 || max_iters < 1 || !(tol >= 0.0)) return -1;
     return solve_core(f32, H, W, delta, lambda, theta, tau, max_iters, 1, NULL, NULL, NULL, u,
-                      v, p1, p2, lab_out, NULL, check_every, tol, iters_done, residual);
+                      v, p1, p2, lab_out, NULL, check_every, tol, norm, iters_done, residual);
 }
 
 /* ---------------------------------------------------------------------------------------- */

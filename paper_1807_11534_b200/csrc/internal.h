@@ -45,15 +45,32 @@ struct Item {
     int32_t strip, r0, r1, pad_;
 };
 
-// Device record of a tolerance solve (rds_solve_tol): written by k_stop_check only.
+// Device record of a tolerance solve (rds_solve_tol, rds_solve_gt): written by k_stop_check
+// only; zeroed before the solve.
 struct StopRecord {
     int32_t flag;       // 1 once the rule fired (or the last check ran): later launches exit
     int32_t iters;      // iterations completed when it fired
     int32_t launches;   // stencil launches that ran (selects the ping-pong buffer)
     int32_t converged;  // residual <= tol at that check
-    double residual;    // max(RMS du, RMS dv) at the last check
+    double residual;    // ||du||, ||dv|| max at the last check (norm: StopCheck::norm_div)
     int32_t checks;     // checks evaluated
-    int32_t pad_;
+    int32_t it;         // iterations done so far (advanced by every check)
+};
+
+// One evaluation of the stopping rule after a block of iterations.
+struct StopCheck {
+    const double *part;        // [n][2] partial sums of du^2, dv^2
+    const int32_t *n_part;     // device count n
+    double norm_div;           // 1 = Euclidean norm over pixels, H*W = RMS (reading R-F2)
+    double tol;
+    int block_iters;           // iterations of the block this check closes
+    int block_launches;        // stencil launches of that block (ping-pong parity)
+    int max_iters;             // the solve's K: the check at rec->it == K is the last
+    int set_cond;              // 1: also drive the enclosing CUDA-graph while loop
+    int body_iters;            // iterations per loop body, and the loop's last iteration:
+    int loop_end;              //   continue iff !fired && it + body_iters <= loop_end
+    cudaGraphConditionalHandle cond;
+    StopRecord *rec;
 };
 
 struct StencilArgs {
@@ -117,14 +134,11 @@ cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_ban
 // mode: 0 iterate, 1 + write u and mask, 2 + stopping sums into a.chk (k_stencil.cu)
 cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a,
                            int grid, cudaStream_t s);
-// Stopping rule after a CHECK launch that ended at iteration it_end:
-// r = max(sqrt(sum du^2 / N), sqrt(sum dv^2 / N)); fire if r <= tol or is_last.
-cudaError_t launch_stop_check(const double *chk, const int32_t *n_items, double n_pixels,
-                              double tol, int it_end, int launch_idx, int is_last,
-                              StopRecord *rec, cudaStream_t s);
 int stencil_blocks_per_sm(int kf, int stages, bool aligned);
 bool kf_supported(int kf);
 int kf_list(int32_t *out, int cap);
+// Stopping rule after a block of iterations (k_energy.cu).
+cudaError_t launch_stop_check(const StopCheck &c, cudaStream_t s);
 
 struct EnergyArgs {
     const float *f, *u, *v, *p1, *p2;
@@ -136,6 +150,28 @@ struct EnergyArgs {
 };
 constexpr int ENERGY_BLOCKS = 592;  // 4 x 148 SMs
 cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s);
+
+// float64 mode (k_fp64.cu): natural-order padded double planes, same pitch as the floats
+struct F64Args {
+    const float *z, *P;        // image and selection map (float planes; P may be null)
+    double *f, *u, *v;
+    double *p1[2], *p2[2];     // ping-pong rho
+    uint8_t *lab;
+    StopRecord *stop;          // early exit once the stopping rule fired (null: never)
+    int64_t pitch;
+    int H, W;
+    float c1, c2, gamma, delta;
+    double tau, theta, theta_lambda;
+};
+constexpr int F64_BLOCKS = 592;  // fixed grid of the double-precision kernels (4 x 148)
+int f64_grid(int64_t n);
+cudaError_t launch_f64_init(const F64Args &a, cudaStream_t s);
+// one iteration: rho from buffer b into b ^ 1, then u, v; part != null adds the stopping sums
+// (one [du^2, dv^2] pair per CTA of f64_grid)
+cudaError_t launch_f64_iter(const F64Args &a, int b, double *part, cudaStream_t s);
+// E1, E2 of the float u against a double u (out[0], out[1]); part holds 3 doubles per CTA
+cudaError_t launch_compare(const float *u, const double *ugt, int64_t pitch, int H, int W,
+                           float eps, double *part, double *out, cudaStream_t s);
 
 // out[i * out_pitch + j] = plane[i * pitch + swz(j)]: natural-order copy of a swizzled plane
 cudaError_t launch_unswizzle(const float *plane, int64_t pitch, int H, int W, float *out,

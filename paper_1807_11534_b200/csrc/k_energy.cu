@@ -108,20 +108,23 @@ cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s) {
 
 namespace rds {
 
-// Stopping rule of PAPER.md:234-238, max{||u^l - u^(l-1)||, ||v^l - v^(l-1)||} <= tol, with
-// the RMS norm over all N pixels (reading R-F2): one CTA sums the CHECK launch's per-item
-// partials in a fixed order (thread-strided sums, then a fixed tree), so the decision is
-// deterministic.  Pinned pixels contribute 0 (u and v are constant there).
-__global__ void __launch_bounds__(256) k_stop_check(const double *chk, const int32_t *n_items_p,
-                                                    double n_pixels, double tol, int it_end,
-                                                    int launch_idx, int is_last,
-                                                    StopRecord *rec) {
-    if (*(volatile const int32_t *)&rec->flag != 0) return;  // uniform across the CTA
-    const int n_items = *n_items_p;
+// Stopping rule of PAPER.md:234-238, max{||u^l - u^(l-1)||, ||v^l - v^(l-1)||} <= tol
+// (reading R-F2: Euclidean norm over pixels of unit area, or RMS): one CTA sums the block's
+// per-item (or per-CTA) partials in a fixed order (thread-strided sums, then a fixed tree),
+// so the decision is deterministic.  Pinned pixels contribute 0.  Every check advances the
+// record's iteration / launch counters; inside a CUDA-graph while loop the body's last check
+// also sets the loop condition.
+__global__ void __launch_bounds__(256) k_stop_check(const StopCheck c) {
+    StopRecord *rec = c.rec;
+    if (*(volatile const int32_t *)&rec->flag != 0) {  // uniform across the CTA
+        if (c.set_cond && threadIdx.x == 0) cudaGraphSetConditional(c.cond, 0);
+        return;
+    }
+    const int n = *c.n_part;
     double su = 0.0, sv = 0.0;
-    for (int i = threadIdx.x; i < n_items; i += 256) {
-        su += chk[2 * i];
-        sv += chk[2 * i + 1];
+    for (int i = threadIdx.x; i < n; i += 256) {
+        su += c.part[2 * i];
+        sv += c.part[2 * i + 1];
     }
     __shared__ double sh[2][8];
     su = warp_sum(su);
@@ -137,24 +140,26 @@ __global__ void __launch_bounds__(256) k_stop_check(const double *chk, const int
             tu += sh[0][w];
             tv += sh[1][w];
         }
-        const double r = fmax(sqrt(tu / n_pixels), sqrt(tv / n_pixels));
+        const double r = fmax(sqrt(tu / c.norm_div), sqrt(tv / c.norm_div));
+        const int it = rec->it + c.block_iters;
+        rec->it = it;
+        rec->launches += c.block_launches;
         rec->residual = r;
         rec->checks += 1;
-        const bool conv = r <= tol;
-        if (conv || is_last) {
-            rec->iters = it_end;
-            rec->launches = launch_idx + 1;
+        const bool conv = r <= c.tol;
+        const bool fire = conv || it >= c.max_iters;
+        if (fire) {
+            rec->iters = it;
             rec->converged = conv ? 1 : 0;
             rec->flag = 1;
         }
+        if (c.set_cond)
+            cudaGraphSetConditional(c.cond, (!fire && it + c.body_iters <= c.loop_end) ? 1 : 0);
     }
 }
 
-cudaError_t launch_stop_check(const double *chk, const int32_t *n_items, double n_pixels,
-                              double tol, int it_end, int launch_idx, int is_last,
-                              StopRecord *rec, cudaStream_t s) {
-    k_stop_check<<<1, 256, 0, s>>>(chk, n_items, n_pixels, tol, it_end, launch_idx, is_last,
-                                   rec);
+cudaError_t launch_stop_check(const StopCheck &c, cudaStream_t s) {
+    k_stop_check<<<1, 256, 0, s>>>(c);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,217 @@
+// k_fp64.cu -- the float64 mode of librds (sm_100a): the same restricted-domain iteration in
+// double precision, for the paper's ground-truth protocol (§4): "For
+// delta = 10^-10 we set u^GT(x) = u^(l) in the original dual formulation", then E1 (Tanimoto
+// of the thresholded results) and E2 (L2 difference) against a restricted solve.
+//
+// A tolerance of 1e-10 in the stopping rule is below float32 resolution, so this mode keeps
+// every state array in float64 and uses correctly rounded sqrt / division with no FMA
+// contraction (explicit _rn intrinsics), each formula evaluated left to right as written:
+//   w   = div rho - v / theta
+//   rho = (rho + tau grad w) / (1 + tau |grad w|) on RD, 0 on Fg u Bg   (Eq. 8)
+//   u   = v - theta div rho on RD, u0 elsewhere                 (Eq. 7)
+//   v   = min(max(u - (theta lambda) f, 0), 1) on RD, u0 elsewhere (Eq. 9)
+// with div rho = ((rho1 - rho1(i-1,j)) + rho2) - rho2(i,j-1) (reading R-C6).  Throughput is
+// not the point here (this is the reference-quality solver of the evaluation protocol, run on
+// the paper's 128 x 128 images), so it is a plain two-kernel-per-iteration scheme on natural-
+// order double planes (padded like the float planes; the frame holds zeros).
+#include <math.h>
+
+#include "internal.h"
+
+namespace rds {
+
+__device__ __forceinline__ float fit32(float z, float P, float c1, float c2, float gamma,
+                                       bool use_p) {
+    const float a = __fsub_rn(z, c1), b = __fsub_rn(z, c2);
+    float f = __fsub_rn(__fmul_rn(a, a), __fmul_rn(b, b));
+    if (use_p) f = __fadd_rn(f, __fmul_rn(gamma, P));
+    return f;
+}
+
+// div rho at (i, j) in the padded double planes (frame = 0; rho1 on row H-1 and rho2 on
+// column W-1 are identically 0, so no bounds tests are needed)
+__device__ __forceinline__ double div64(const double *p1, const double *p2, int64_t o,
+                                        int64_t pitch) {
+    double d = __dsub_rn(p1[o], p1[o - pitch]);
+    d = __dadd_rn(d, p2[o]);
+    return __dsub_rn(d, p2[o - 1]);
+}
+
+__global__ void k64_init(const F64Args a) {
+    const int64_t n = (int64_t)a.H * a.W;
+    const bool use_p = a.P != nullptr && a.gamma != 0.0f;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(k / a.W), j = (int)(k - (int64_t)i * a.W);
+        const int64_t o = (int64_t)i * a.pitch + j;
+        const float f = fit32(a.z[o], use_p ? a.P[o] : 0.0f, a.c1, a.c2, a.gamma, use_p);
+        const bool rd = fabsf(f) < a.delta;             // RD <=> |f| < delta (R-C7)
+        const double u0 = f <= 0.0f ? 1.0 : 0.0;        // H(-f), H(0) = 1
+        a.f[o] = (double)f;
+        a.lab[o] = rd ? 2 : (f <= 0.0f ? 1 : 0);
+        a.u[o] = u0;
+        a.v[o] = u0;
+        a.p1[0][o] = a.p1[1][o] = 0.0;
+        a.p2[0][o] = a.p2[1][o] = 0.0;
+    }
+}
+
+// rho-step: reads rho (buffer b) and v, writes rho (buffer b ^ 1)
+__global__ void k64_rho(const F64Args a, int b) {
+    if (a.stop != nullptr && *(volatile const int32_t *)&a.stop->flag != 0) return;
+    const int64_t n = (int64_t)a.H * a.W, P = a.pitch;
+    const double *p1 = a.p1[b], *p2 = a.p2[b];
+    double *q1 = a.p1[b ^ 1], *q2 = a.p2[b ^ 1];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(k / a.W), j = (int)(k - (int64_t)i * a.W);
+        const int64_t o = (int64_t)i * P + j;
+        if (a.lab[o] != 2) {
+            q1[o] = 0.0;
+            q2[o] = 0.0;
+            continue;
+        }
+        const double w = __dsub_rn(div64(p1, p2, o, P), __ddiv_rn(a.v[o], a.theta));
+        double g1 = 0.0, g2 = 0.0;
+        if (i < a.H - 1)
+            g1 = __dsub_rn(__dsub_rn(div64(p1, p2, o + P, P), __ddiv_rn(a.v[o + P], a.theta)), w);
+        if (j < a.W - 1)
+            g2 = __dsub_rn(__dsub_rn(div64(p1, p2, o + 1, P), __ddiv_rn(a.v[o + 1], a.theta)), w);
+        const double ng = __dsqrt_rn(__dadd_rn(__dmul_rn(g1, g1), __dmul_rn(g2, g2)));
+        const double den = __dadd_rn(1.0, __dmul_rn(a.tau, ng));
+        q1[o] = __ddiv_rn(__dadd_rn(p1[o], __dmul_rn(a.tau, g1)), den);
+        q2[o] = __ddiv_rn(__dadd_rn(p2[o], __dmul_rn(a.tau, g2)), den);
+    }
+}
+
+// u- and v-steps from rho (buffer b); with part != null also the stopping sums
+// sum (u - u_prev)^2, sum (v - v_prev)^2 of this iteration, one fixed-order partial per CTA
+__global__ void __launch_bounds__(256) k64_uv(const F64Args a, int b, double *part) {
+    if (a.stop != nullptr && *(volatile const int32_t *)&a.stop->flag != 0) return;
+    const int64_t n = (int64_t)a.H * a.W, P = a.pitch;
+    const double *p1 = a.p1[b], *p2 = a.p2[b];
+    double su = 0.0, sv = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(k / a.W), j = (int)(k - (int64_t)i * a.W);
+        const int64_t o = (int64_t)i * P + j;
+        if (a.lab[o] != 2) continue;                   // u = v = u0, unchanged
+        const double v = a.v[o];
+        const double u = __dsub_rn(v, __dmul_rn(a.theta, div64(p1, p2, o, P)));
+        const double t = __dsub_rn(u, __dmul_rn(a.theta_lambda, a.f[o]));
+        const double vn = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+        if (part) {
+            const double du = __dsub_rn(u, a.u[o]), dv = __dsub_rn(vn, v);
+            su = __fma_rn(du, du, su);
+            sv = __fma_rn(dv, dv, sv);
+        }
+        a.u[o] = u;
+        a.v[o] = vn;
+    }
+    if (part) {
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            su += __shfl_xor_sync(0xffffffffu, su, off);
+            sv += __shfl_xor_sync(0xffffffffu, sv, off);
+        }
+        __shared__ double sh[2][8];
+        if ((threadIdx.x & 31) == 0) {
+            sh[0][threadIdx.x >> 5] = su;
+            sh[1][threadIdx.x >> 5] = sv;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tu = 0.0, tv = 0.0;
+            for (int w = 0; w < 8; ++w) {
+                tu += sh[0][w];
+                tv += sh[1][w];
+            }
+            part[2 * blockIdx.x] = tu;
+            part[2 * blockIdx.x + 1] = tv;
+        }
+    }
+}
+
+int f64_grid(int64_t n) {
+    const int64_t g = (n + 255) / 256;
+    return (int)(g < F64_BLOCKS ? g : F64_BLOCKS);
+}
+
+cudaError_t launch_f64_init(const F64Args &a, cudaStream_t s) {
+    k64_init<<<f64_grid((int64_t)a.H * a.W), 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_f64_iter(const F64Args &a, int b, double *part, cudaStream_t s) {
+    const int g = f64_grid((int64_t)a.H * a.W);
+    k64_rho<<<g, 256, 0, s>>>(a, b);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k64_uv<<<g, 256, 0, s>>>(a, b ^ 1, part);
+    return cudaGetLastError();
+}
+
+// E1 = N(GT n Omega) / N(GT u Omega) with GT = [u_gt > eps], Omega = [u > eps] (1 when both
+// are empty, reading R-C15), E2 = sum (u - u_gt)^2 over pixels of unit area.
+// Integer counts and fixed-order double sums: deterministic.
+__global__ void __launch_bounds__(256) k_compare(const float *u, const double *ugt,
+                                                 int64_t pitch, int H, int W, float eps,
+                                                 double *part) {
+    const int64_t n = (int64_t)H * W;
+    long long in = 0, un = 0;
+    double e2 = 0.0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int i = (int)(k / W), j = (int)(k - (int64_t)i * W);
+        const int64_t o = (int64_t)i * pitch + j;
+        const double a = (double)u[o], g = ugt[o];
+        const bool om = u[o] > eps, gt = g > (double)eps;
+        in += om && gt;
+        un += om || gt;
+        const double d = __dsub_rn(a, g);
+        e2 = __fma_rn(d, d, e2);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        in += __shfl_xor_sync(0xffffffffu, in, off);
+        un += __shfl_xor_sync(0xffffffffu, un, off);
+        e2 += __shfl_xor_sync(0xffffffffu, e2, off);
+    }
+    __shared__ double sh[3][8];
+    if ((threadIdx.x & 31) == 0) {
+        sh[0][threadIdx.x >> 5] = (double)in;
+        sh[1][threadIdx.x >> 5] = (double)un;
+        sh[2][threadIdx.x >> 5] = e2;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += sh[threadIdx.x][w];
+        part[3 * blockIdx.x + threadIdx.x] = t;
+    }
+}
+
+__global__ void k_compare_final(const double *part, int nb, double *out) {
+    if (threadIdx.x == 0) {
+        double in = 0.0, un = 0.0, e2 = 0.0;
+        for (int b = 0; b < nb; ++b) {
+            in += part[3 * b];
+            un += part[3 * b + 1];
+            e2 += part[3 * b + 2];
+        }
+        out[0] = un > 0.0 ? in / un : 1.0;
+        out[1] = e2;
+    }
+}
+
+cudaError_t launch_compare(const float *u, const double *ugt, int64_t pitch, int H, int W,
+                           float eps, double *part, double *out, cudaStream_t s) {
+    const int g = f64_grid((int64_t)H * W);
+    k_compare<<<g, 256, 0, s>>>(u, ugt, pitch, H, W, eps, part);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    k_compare_final<<<1, 32, 0, s>>>(part, g, out);
+    return cudaGetLastError();
+}
+
+}  // namespace rds

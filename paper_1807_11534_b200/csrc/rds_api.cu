@@ -57,6 +57,12 @@ struct rds_handle {
     double *chk = nullptr;           // per-item stopping sums of a CHECK launch
     size_t chk_bytes = 0;
     bool tol_pending = false;        // a tolerance solve's outcome is still on the device
+    // float64 mode (rds_solve_gt): 7 double planes f, u, v, rho1 x2, rho2 x2 in one block
+    double *d64 = nullptr, *part64 = nullptr, *cmp_out = nullptr;
+    uint8_t *lab64 = nullptr;
+    StopRecord *stop64 = nullptr;
+    int32_t *n64 = nullptr;
+    bool have_gt = false;
     int cur0 = 0;                    // ping-pong buffer at the start of the last solve
     float *scratch = nullptr;        // H*W natural-order staging for swizzled-plane getters
 
@@ -70,12 +76,13 @@ struct rds_handle {
     int cur = 0;  // ping-pong buffer holding the latest state
 
     int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1, opt_ctas = 0;
+    int opt_norm = 0;  // stopping-rule norm: 0 Euclidean over pixels, 1 RMS (R-F2)
     rds_stats_t stats{};
 
     // cached CUDA graph of the K-loop
     cudaGraphExec_t graph = nullptr;
     struct Key {
-        int kf, iters, cur0, max_items, check_every;
+        int kf, iters, cur0, max_items, check_every, norm;
         float tau, theta, tol;
         bool operator==(const Key &o) const { return memcmp(this, &o, sizeof(Key)) == 0; }
     } gkey{};
@@ -114,7 +121,8 @@ static void free_all(rds_t *h) {
     void *other[] = {h->lab,     h->mask,        h->tile_rd, h->tile_list, h->band_flag,
                      h->items,   h->queue,       h->counts,  h->n_rd_dev,  h->absmax_bits,
                      h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch,
-                     h->stop,    h->chk};
+                     h->stop,    h->chk,         h->d64,     h->part64,    h->cmp_out,
+                     h->lab64,   h->stop64,      h->n64};
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -247,6 +255,11 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             return RDS_OK;
         case RDS_OPT_GRAPH:
             h->opt_graph = value != 0;
+            return RDS_OK;
+        case RDS_OPT_STOP_NORM:
+            if (value != 0 && value != 1)
+                return fail(h, RDS_EINVAL, "rds_set_option: stop_norm=%lld", (long long)value);
+            h->opt_norm = (int)value;
             return RDS_OK;
         case RDS_OPT_CTAS_PER_SM:
             if (value < 0 || value > 64)
@@ -415,7 +428,7 @@ static int blocks_per_sm(rds_t *h, int kf, int stages) {
 // followed by k_stop_check.
 struct LaunchPlan {
     int stages, mode, it_end;
-    bool check, last;
+    bool check;
 };
 
 static int make_plan(int kf, int iters, int check_every, LaunchPlan *out, int cap) {
@@ -425,7 +438,7 @@ static int make_plan(int kf, int iters, int check_every, LaunchPlan *out, int ca
         while (done < iters) {
             const int st = (iters - done) >= kf ? kf : (iters - done);
             done += st;
-            if (n < cap) out[n] = LaunchPlan{st, done == iters ? 1 : 0, done, false, done == iters};
+            if (n < cap) out[n] = LaunchPlan{st, done == iters ? 1 : 0, done, false};
             ++n;
         }
         return n;
@@ -439,7 +452,7 @@ static int make_plan(int kf, int iters, int check_every, LaunchPlan *out, int ca
             const int st = base + (k >= nl - rem ? 1 : 0);
             done += st;
             const bool chk = k == nl - 1;
-            if (n < cap) out[n] = LaunchPlan{st, chk ? 2 : 0, done, chk, done == iters};
+            if (n < cap) out[n] = LaunchPlan{st, chk ? 2 : 0, done, chk};
             ++n;
         }
         // a single-stage CHECK launch reads u^(l-1) from the u plane: the launch before it
@@ -451,17 +464,20 @@ static int make_plan(int kf, int iters, int check_every, LaunchPlan *out, int ca
     return n;
 }
 
-// Enqueue the K-loop: zero the per-launch work queues, then the planned persistent stencil
-// launches on ping-pong buffers (and the stopping checks of a tolerance solve).
-static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, float tau,
-                                float theta, int check_every, float tol) {
-    const int launches = make_plan(kf, iters, check_every, nullptr, 0);
-    LaunchPlan *plan = new (std::nothrow) LaunchPlan[launches > 0 ? launches : 1];
-    if (!plan) return cudaErrorMemoryAllocation;
-    make_plan(kf, iters, check_every, plan, launches);
-    cudaError_t e = cudaMemsetAsync(h->queue, 0, sizeof(int32_t) * launches, h->stream);
-    if (e == cudaSuccess && check_every > 0)
-        e = cudaMemsetAsync(h->stop, 0, sizeof(StopRecord), h->stream);
+struct TolParams {
+    int check_every = 0;   // 0: fixed-K solve
+    float tol = 0.0f;
+    int max_iters = 0;     // K
+    double norm_div = 1.0;
+};
+
+// Enqueue plan[0..n) on h->stream starting from ping-pong buffer `cur`, using work counters
+// queue[qbase ..].  Check launches are followed by k_stop_check; in a graph loop body the
+// last check also drives the loop (cond, body_iters, loop_end).
+static cudaError_t enqueue_plan(rds_t *h, const LaunchPlan *plan, int n, int kf, int max_items,
+                                float tau, float theta, const TolParams &tp, int qbase,
+                                int cur, bool drive_loop, cudaGraphConditionalHandle cond,
+                                int body_iters, int loop_end) {
     StencilArgs a{};
     a.c = h->at(h->c);
     a.u_out = h->at(h->u);
@@ -474,10 +490,11 @@ static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, floa
     a.tau = tau;
     a.theta = theta;
     a.inv_theta = 1.0f / theta;
-    a.stop = check_every > 0 ? h->stop : nullptr;
+    a.stop = tp.check_every > 0 ? h->stop : nullptr;
     a.chk = h->chk;
-    int cur = h->cur;
-    for (int l = 0; l < launches && e == cudaSuccess; ++l) {
+    int prev_it = n > 0 ? plan[0].it_end - plan[0].stages : 0, prev_l = 0;
+    cudaError_t e = cudaSuccess;
+    for (int l = 0; l < n && e == cudaSuccess; ++l) {
         const LaunchPlan &L = plan[l];
         a.p1_in = h->at(h->p1[cur]);
         a.p2_in = h->at(h->p2[cur]);
@@ -485,18 +502,148 @@ static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, floa
         a.p1_out = h->at(h->p1[cur ^ 1]);
         a.p2_out = h->at(h->p2[cur ^ 1]);
         a.v_out = h->at(h->v[cur ^ 1]);
-        a.queue = h->queue + l;
+        a.queue = h->queue + qbase + l;
         int grid = h->n_sm * blocks_per_sm(h, kf, L.stages);
         const int need = (max_items + STENCIL_WARPS - 1) / STENCIL_WARPS;
         if (grid > need) grid = need;
         e = launch_stencil(kf, L.stages, L.mode, a, grid, h->stream);
-        if (e == cudaSuccess && L.check)
-            e = launch_stop_check(h->chk, h->counts + 1, (double)h->H * (double)h->W, tol,
-                                  L.it_end, l, L.last ? 1 : 0, h->stop, h->stream);
+        if (e == cudaSuccess && L.check) {
+            StopCheck c{};
+            c.part = h->chk;
+            c.n_part = h->counts + 1;
+            c.norm_div = tp.norm_div;
+            c.tol = tp.tol;
+            c.block_iters = L.it_end - prev_it;
+            c.block_launches = l + 1 - prev_l;
+            c.max_iters = tp.max_iters;
+            c.set_cond = drive_loop && l == n - 1;
+            c.body_iters = body_iters;
+            c.loop_end = loop_end;
+            c.cond = cond;
+            c.rec = h->stop;
+            e = launch_stop_check(c, h->stream);
+            prev_it = L.it_end;
+            prev_l = l + 1;
+        }
         cur ^= 1;
     }
+    return e;
+}
+
+// Static K-loop: zero the work counters (and the stop record), then every planned launch.
+// A tolerance solve enqueued this way runs its remaining launches as immediate exits.
+static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, float tau,
+                                float theta, const TolParams &tp) {
+    const int launches = make_plan(kf, iters, tp.check_every, nullptr, 0);
+    LaunchPlan *plan = new (std::nothrow) LaunchPlan[launches > 0 ? launches : 1];
+    if (!plan) return cudaErrorMemoryAllocation;
+    make_plan(kf, iters, tp.check_every, plan, launches);
+    cudaError_t e = cudaMemsetAsync(h->queue, 0, sizeof(int32_t) * launches, h->stream);
+    if (e == cudaSuccess && tp.check_every > 0)
+        e = cudaMemsetAsync(h->stop, 0, sizeof(StopRecord), h->stream);
+    if (e == cudaSuccess)
+        e = enqueue_plan(h, plan, launches, kf, max_items, tau, theta, tp, 0, h->cur, false, 0,
+                         0, 0);
     delete[] plan;
     return e;
+}
+
+// Tolerance solve as one CUDA graph with device-side control flow: a while node repeats a
+// body of whole check blocks (two when a block has an odd number of launches, so the body
+// keeps the ping-pong parity) for as long as the body's last k_stop_check says so, then a
+// static tail covers the iterations past the last whole body.  Nothing runs after the rule
+// fires except the tail's immediate exits.  Queue counters: body [0, body_launches), tail
+// after that; the body zeroes its own at the start of every pass.
+static cudaError_t capture_tol_graph(rds_t *h, int kf, int iters, int max_items, float tau,
+                                     float theta, const TolParams &tp, cudaGraph_t *out) {
+    const int m = tp.check_every;
+    const int blk_n = make_plan(kf, m, m, nullptr, 0);
+    const int body_blocks = (blk_n & 1) ? 2 : 1;
+    const int body_iters = body_blocks * m;
+    const int loop_end = (iters / body_iters) * body_iters;
+    LaunchPlan *body = new (std::nothrow) LaunchPlan[body_blocks * blk_n];
+    const int tail_n = make_plan(kf, iters - loop_end, m, nullptr, 0);
+    LaunchPlan *tail = new (std::nothrow) LaunchPlan[tail_n > 0 ? tail_n : 1];
+    if (!body || !tail) {
+        delete[] body;
+        delete[] tail;
+        return cudaErrorMemoryAllocation;
+    }
+    make_plan(kf, body_iters, m, body, body_blocks * blk_n);
+    make_plan(kf, iters - loop_end, m, tail, tail_n);
+    for (int l = 0; l < tail_n; ++l) tail[l].it_end += loop_end;
+    const int body_n = body_blocks * blk_n;
+
+    cudaStream_t cap = nullptr;
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaGraphCreate(&g, 0);
+    cudaGraphConditionalHandle cond = 0;
+    if (e == cudaSuccess)
+        e = cudaGraphConditionalHandleCreate(&cond, g, loop_end > 0 ? 1 : 0,
+                                             cudaGraphCondAssignDefault);
+    cudaStream_t keep = h->stream;
+    h->stream = cap;
+    // prologue, the while node, the tail -- one capture sequence into g
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(cap, g, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) e = cudaMemsetAsync(h->stop, 0, sizeof(StopRecord), cap);
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(h->queue + body_n, 0, sizeof(int32_t) * (tail_n > 0 ? tail_n : 1),
+                            cap);
+    cudaGraph_t body_g = nullptr;
+    if (e == cudaSuccess) {
+        cudaStreamCaptureStatus st;
+        cudaGraph_t cg = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        e = cudaStreamGetCaptureInfo(cap, &st, nullptr, &cg, &deps, &nd);
+        cudaGraphNode_t wnode = nullptr;
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = cond;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        if (e == cudaSuccess) e = cudaGraphAddNode(&wnode, cg, deps, nd, &cp);
+        if (e == cudaSuccess) {
+            body_g = cp.conditional.phGraph_out[0];
+            e = cudaStreamUpdateCaptureDependencies(cap, &wnode, 1,
+                                                    cudaStreamSetCaptureDependencies);
+        }
+    }
+    // the tail, after the loop
+    if (e == cudaSuccess && tail_n > 0)
+        e = enqueue_plan(h, tail, tail_n, kf, max_items, tau, theta, tp, body_n, h->cur, false,
+                         0, 0, 0);
+    {
+        cudaGraph_t got = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(cap, &got);
+        if (e == cudaSuccess) e = e2;
+    }
+    // the loop body, captured into the while node's graph
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(cap, body_g, nullptr, nullptr, 0,
+                                          cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+        cudaError_t e1 = cudaMemsetAsync(h->queue, 0, sizeof(int32_t) * body_n, cap);
+        if (e1 == cudaSuccess)
+            e1 = enqueue_plan(h, body, body_n, kf, max_items, tau, theta, tp, 0, h->cur, true,
+                              cond, body_iters, loop_end);
+        cudaGraph_t got = nullptr;
+        const cudaError_t e2 = cudaStreamEndCapture(cap, &got);
+        e = e1 != cudaSuccess ? e1 : e2;
+    }
+    h->stream = keep;
+    if (cap) cudaStreamDestroy(cap);
+    delete[] body;
+    delete[] tail;
+    if (e != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return e;
+    }
+    *out = g;
+    return cudaSuccess;
 }
 
 static cudaError_t grow(void **p, size_t *cap, size_t bytes) {
@@ -605,37 +752,50 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     if (h->opt_timing) CK(h, cudaEventRecord(h->ev[1], h->stream));
 
     if (iters > 0) {
-        rds_handle::Key key{kf, iters, h->cur, max_items, check_every, tau, theta, tol};
-        if (h->opt_graph && launches > 1) {
+        TolParams tp;
+        tp.check_every = check_every;
+        tp.tol = tol;
+        tp.max_iters = iters;
+        tp.norm_div = h->opt_norm ? (double)h->H * (double)h->W : 1.0;
+        rds_handle::Key key{kf, iters, h->cur, max_items, check_every, h->opt_norm, tau, theta,
+                            tol};
+        if (h->opt_graph && (launches > 1 || check_every > 0)) {
             if (!h->graph || !(h->gkey == key)) {
                 if (h->graph) {
                     cudaGraphExecDestroy(h->graph);
                     h->graph = nullptr;
                 }
-                cudaStream_t cap;
-                CK(h, cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
                 cudaGraph_t g = nullptr;
-                cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
-                if (e == cudaSuccess) {
-                    cudaStream_t keep = h->stream;
-                    h->stream = cap;
-                    cudaError_t e2 =
-                        enqueue_loop(h, kf, iters, max_items, tau, theta, check_every, tol);
-                    h->stream = keep;
-                    e = cudaStreamEndCapture(cap, &g);
-                    if (e == cudaSuccess) e = e2;
+                cudaError_t e = cudaSuccess;
+                if (check_every > 0) {
+                    e = capture_tol_graph(h, kf, iters, max_items, tau, theta, tp, &g);
+                } else {
+                    cudaStream_t cap;
+                    CK(h, cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+                    e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+                    if (e == cudaSuccess) {
+                        cudaStream_t keep = h->stream;
+                        h->stream = cap;
+                        const cudaError_t e2 =
+                            enqueue_loop(h, kf, iters, max_items, tau, theta, tp);
+                        h->stream = keep;
+                        e = cudaStreamEndCapture(cap, &g);
+                        if (e == cudaSuccess) e = e2;
+                    }
+                    cudaStreamDestroy(cap);
                 }
                 if (e == cudaSuccess) e = cudaGraphInstantiate(&h->graph, g, 0);
                 if (g) cudaGraphDestroy(g);
-                cudaStreamDestroy(cap);
-                if (e != cudaSuccess)
+                if (e != cudaSuccess) {
+                    h->graph = nullptr;
                     return fail(h, RDS_ECUDA, "rds_solve: graph capture failed: %s",
                                 cudaGetErrorString(e));
+                }
                 h->gkey = key;
             }
             CK(h, cudaGraphLaunch(h->graph, h->stream));
         } else {
-            CK(h, enqueue_loop(h, kf, iters, max_items, tau, theta, check_every, tol));
+            CK(h, enqueue_loop(h, kf, iters, max_items, tau, theta, tp));
         }
         h->cur0 = h->cur;
         if (check_every > 0)
@@ -842,6 +1002,187 @@ int rds_get_stats(rds_t *h, rds_stats_t *out) {
         CK(h, cudaEventElapsedTime(&h->stats.loop_ms, h->ev[1], h->ev[2]));
     }
     *out = h->stats;
+    return RDS_OK;
+}
+
+int rds_solve_gt(rds_t *h, float lambda, float theta, float tau, float delta,
+                 int32_t max_iters, double tol, int32_t check_every, rds_gt_t *out) {
+    if (!h) return fail(nullptr, RDS_EINVAL, "rds_solve_gt: NULL handle");
+    if (!(lambda > 0.0f) || !isfinite(lambda) || !(theta > 0.0f) || !isfinite(theta))
+        return fail(h, RDS_EINVAL, "rds_solve_gt: need finite lambda, theta > 0");
+    if (!(tau > 0.0f) || !(tau <= 0.125f))
+        return fail(h, RDS_EINVAL, "rds_solve_gt: tau=%g must be in (0, 1/8]", tau);
+    if (isnan(delta) || delta < 0.0f)
+        return fail(h, RDS_EINVAL, "rds_solve_gt: delta=%g must be >= 0", delta);
+    if (max_iters < 1 || check_every < 1 || !(tol >= 0.0))
+        return fail(h, RDS_EINVAL, "rds_solve_gt: need max_iters >= 1, check_every >= 1, "
+                                   "tol >= 0");
+    if (!h->have_image || !h->have_fitting)
+        return fail(h, RDS_ESTATE, "rds_solve_gt: image and fitting must be set first");
+    if (!h->image_ok || !h->p_ok)
+        return fail(h, RDS_EINVAL, "rds_solve_gt: image or P has non-finite values");
+    const int nb = f64_grid(h->H * h->W);
+    if (!h->d64) {
+        CK(h, cudaMalloc(&h->d64, sizeof(double) * h->plane * 7));
+        CK(h, cudaMemsetAsync(h->d64, 0, sizeof(double) * h->plane * 7, h->stream));
+        CK(h, cudaMalloc(&h->lab64, h->plane));
+        CK(h, cudaMemsetAsync(h->lab64, 0, h->plane, h->stream));
+        CK(h, cudaMalloc(&h->part64, sizeof(double) * 3 * F64_BLOCKS));
+        CK(h, cudaMalloc(&h->cmp_out, sizeof(double) * 2));
+        CK(h, cudaMalloc(&h->stop64, sizeof(StopRecord)));
+        CK(h, cudaMalloc(&h->n64, sizeof(int32_t)));
+    }
+    CK(h, cudaMemcpyAsync(h->n64, &nb, sizeof nb, cudaMemcpyHostToDevice, h->stream));
+    CK(h, cudaMemsetAsync(h->stop64, 0, sizeof(StopRecord), h->stream));
+    F64Args a{};
+    a.z = h->at(h->z);
+    a.P = h->gamma != 0.0f ? h->at(h->P) : nullptr;
+    double *pl[7];
+    for (int k = 0; k < 7; ++k) pl[k] = h->d64 + h->plane * k + h->origin;
+    a.f = pl[0];
+    a.u = pl[1];
+    a.v = pl[2];
+    a.p1[0] = pl[3];
+    a.p1[1] = pl[4];
+    a.p2[0] = pl[5];
+    a.p2[1] = pl[6];
+    a.lab = h->lab64 + h->origin;
+    a.stop = h->stop64;
+    a.pitch = h->pitch;
+    a.H = (int)h->H;
+    a.W = (int)h->W;
+    a.c1 = h->c1;
+    a.c2 = h->c2;
+    a.gamma = h->gamma;
+    a.delta = delta;
+    a.tau = (double)tau;
+    a.theta = (double)theta;
+    a.theta_lambda = (double)theta * (double)lambda;
+    CK(h, launch_f64_init(a, h->stream));
+    StopCheck c{};
+    c.part = h->part64;
+    c.n_part = h->n64;
+    c.norm_div = h->opt_norm ? (double)h->H * (double)h->W : 1.0;
+    c.tol = tol;
+    c.max_iters = max_iters;
+    c.rec = h->stop64;
+    // One CUDA graph: a while node over whole bodies of checks (two checks when check_every
+    // is odd, so a body keeps the rho ping-pong parity), driven by the body's last
+    // k_stop_check, then a static tail up to max_iters.
+    const int body_checks = (check_every & 1) ? 2 : 1;
+    const int body_iters = body_checks * check_every;
+    const int loop_end = (max_iters / body_iters) * body_iters;
+    c.body_iters = body_iters;
+    c.loop_end = loop_end;
+    auto enqueue_iters = [&](int it0, int it1, bool drive) -> cudaError_t {
+        int last_check = it0;
+        cudaError_t e = cudaSuccess;
+        for (int it = it0; it < it1 && e == cudaSuccess; ++it) {
+            const bool check = ((it + 1) % check_every) == 0 || it + 1 == max_iters;
+            e = launch_f64_iter(a, it & 1, check ? h->part64 : nullptr, h->stream);
+            if (e == cudaSuccess && check) {
+                c.block_iters = it + 1 - last_check;
+                c.set_cond = drive && it + 1 == it1;
+                last_check = it + 1;
+                e = launch_stop_check(c, h->stream);
+            }
+        }
+        return e;
+    };
+    {
+        cudaStream_t cap = nullptr, keep = h->stream;
+        cudaGraph_t g = nullptr, body = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        cudaError_t e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaGraphCreate(&g, 0);
+        if (e == cudaSuccess)
+            e = cudaGraphConditionalHandleCreate(&c.cond, g, loop_end > 0 ? 1 : 0,
+                                                 cudaGraphCondAssignDefault);
+        h->stream = cap;
+        if (e == cudaSuccess)
+            e = cudaStreamBeginCaptureToGraph(cap, g, nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) e = cudaMemsetAsync(h->stop64, 0, sizeof(StopRecord), cap);
+        if (e == cudaSuccess) {
+            cudaStreamCaptureStatus st;
+            cudaGraph_t cg = nullptr;
+            const cudaGraphNode_t *deps = nullptr;
+            size_t nd = 0;
+            e = cudaStreamGetCaptureInfo(cap, &st, nullptr, &cg, &deps, &nd);
+            cudaGraphNode_t wnode = nullptr;
+            cudaGraphNodeParams cp = {};
+            cp.type = cudaGraphNodeTypeConditional;
+            cp.conditional.handle = c.cond;
+            cp.conditional.type = cudaGraphCondTypeWhile;
+            cp.conditional.size = 1;
+            if (e == cudaSuccess) e = cudaGraphAddNode(&wnode, cg, deps, nd, &cp);
+            if (e == cudaSuccess) {
+                body = cp.conditional.phGraph_out[0];
+                e = cudaStreamUpdateCaptureDependencies(cap, &wnode, 1,
+                                                        cudaStreamSetCaptureDependencies);
+            }
+        }
+        if (e == cudaSuccess) e = enqueue_iters(loop_end, max_iters, false);
+        {
+            cudaGraph_t got = nullptr;
+            const cudaError_t e2 = cudaStreamEndCapture(cap, &got);
+            if (e == cudaSuccess) e = e2;
+        }
+        if (e == cudaSuccess)
+            e = cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            const cudaError_t e1 = enqueue_iters(0, body_iters, true);
+            cudaGraph_t got = nullptr;
+            const cudaError_t e2 = cudaStreamEndCapture(cap, &got);
+            e = e1 != cudaSuccess ? e1 : e2;
+        }
+        h->stream = keep;
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
+        if (e == cudaSuccess) e = cudaGraphLaunch(ge, h->stream);
+        if (ge) cudaGraphExecDestroy(ge);
+        if (g) cudaGraphDestroy(g);
+        if (cap) cudaStreamDestroy(cap);
+        if (e != cudaSuccess)
+            return fail(h, RDS_ECUDA, "rds_solve_gt: %s", cudaGetErrorString(e));
+    }
+    StopRecord rec{};
+    CK(h, cudaMemcpyAsync(&rec, h->stop64, sizeof rec, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    h->have_gt = true;
+    if (out) {
+        out->iters = rec.iters;
+        out->converged = rec.converged;
+        out->residual = rec.residual;
+    }
+    return RDS_OK;
+}
+
+int rds_get_u_gt(rds_t *h, double *out, int on_device) {
+    if (!h) return fail(nullptr, RDS_EINVAL, "rds_get_u_gt: NULL handle");
+    if (!h->have_gt) return fail(h, RDS_ESTATE, "rds_get_u_gt: no rds_solve_gt has run yet");
+    if (!out) return fail(h, RDS_EINVAL, "rds_get_u_gt: NULL out");
+    const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    CK(h, cudaMemcpy2DAsync(out, sizeof(double) * h->W, h->d64 + h->plane + h->origin,
+                            sizeof(double) * h->pitch, sizeof(double) * h->W, h->H, kind,
+                            h->stream));
+    if (!on_device) CK(h, cudaStreamSynchronize(h->stream));
+    return RDS_OK;
+}
+
+int rds_compare_gt(rds_t *h, float eps, double *e1, double *e2) {
+    NEED_SOLVED("rds_compare_gt");
+    if (!h->have_gt) return fail(h, RDS_ESTATE, "rds_compare_gt: no rds_solve_gt has run yet");
+    if (!e1 || !e2) return fail(h, RDS_EINVAL, "rds_compare_gt: NULL out");
+    if (!(eps >= 0.0f && eps <= 1.0f))
+        return fail(h, RDS_EINVAL, "rds_compare_gt: eps=%g must be in [0, 1]", eps);
+    CK(h, launch_compare(h->at(h->u), h->d64 + h->plane + h->origin, h->pitch, (int)h->H,
+                         (int)h->W, eps, h->part64, h->cmp_out, h->stream));
+    double r[2];
+    CK(h, cudaMemcpyAsync(r, h->cmp_out, sizeof r, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    *e1 = r[0];
+    *e2 = r[1];
     return RDS_OK;
 }
 

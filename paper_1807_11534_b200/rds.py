@@ -23,6 +23,7 @@ RDS_OK, RDS_EINVAL, RDS_ESTATE, RDS_ECUDA, RDS_ENOMEM = 0, -1, -2, -3, -4
 RDS_LABEL_BG, RDS_LABEL_FG, RDS_LABEL_RD = 0, 1, 2
 RDS_OPT_KFUSE, RDS_OPT_ITEM_ROWS, RDS_OPT_TIMING, RDS_OPT_SKIP, RDS_OPT_GRAPH = 1, 2, 3, 4, 5
 RDS_OPT_CTAS_PER_SM = 6
+RDS_OPT_STOP_NORM = 7  # 0 Euclidean over pixels (default), 1 RMS
 
 EXPORTS = (
     "rds_create", "rds_destroy", "rds_set_stream", "rds_set_option", "rds_set_image",
@@ -30,7 +31,7 @@ EXPORTS = (
     "rds_get_mask", "rds_get_v", "rds_get_p", "rds_get_fitting", "rds_get_labels",
     "rds_get_active_tiles", "rds_tile_shape", "rds_energy", "rds_get_stats",
     "rds_kfuse_supported", "rds_last_error", "rds_version", "rds_band_for_fraction",
-    "rds_solve_q", "rds_solve_tol",
+    "rds_solve_q", "rds_solve_tol", "rds_solve_gt", "rds_get_u_gt", "rds_compare_gt",
 )
 
 
@@ -42,6 +43,14 @@ class RdsError(RuntimeError):
 
 class rds_energy_t(ctypes.Structure):
     _fields_ = [(k, ctypes.c_double) for k in ("E_v", "E_u", "D_p", "gap", "TV_v", "fit_v")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class rds_gt_t(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("residual", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -94,6 +103,9 @@ def _load():
         "rds_band_for_fraction": [P, ctypes.c_double, ctypes.POINTER(f)],
         "rds_solve_q": [P, f, f, f, ctypes.c_double, i32],
         "rds_solve_tol": [P, f, f, f, f, i32, f, i32],
+        "rds_solve_gt": [P, f, f, f, f, i32, ctypes.c_double, i32, ctypes.POINTER(rds_gt_t)],
+        "rds_get_u_gt": [P, P, i],
+        "rds_compare_gt": [P, f, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -118,7 +130,8 @@ def _buf(a, dtype, shape, writable=False):
     if hasattr(a, "data_ptr") and hasattr(a, "is_cuda"):  # torch tensor
         import torch
 
-        tdt = {np.float32: torch.float32, np.uint8: torch.uint8, np.int32: torch.int32}[dtype]
+        tdt = {np.float32: torch.float32, np.uint8: torch.uint8, np.int32: torch.int32,
+               np.float64: torch.float64}[dtype]
         if a.dtype != tdt or tuple(a.shape) != tuple(shape) or not a.is_contiguous():
             raise ValueError(f"expected contiguous {tdt} tensor of shape {shape}")
         return ctypes.c_void_p(a.data_ptr()), int(a.is_cuda), a
@@ -196,6 +209,19 @@ def rds_solve(h, lam, theta, tau, delta, iters):
 def rds_solve_tol(h, lam, theta, tau, delta, max_iters, tol, check_every=0):
     _check(_lib.rds_solve_tol(h, float(lam), float(theta), float(tau), float(delta),
                               int(max_iters), float(tol), int(check_every)), h)
+
+
+def rds_solve_gt(h, lam, theta, tau, delta, max_iters, tol, check_every):
+    r = rds_gt_t()
+    _check(_lib.rds_solve_gt(h, float(lam), float(theta), float(tau), float(delta),
+                             int(max_iters), float(tol), int(check_every), ctypes.byref(r)), h)
+    return r.as_dict()
+
+
+def rds_compare_gt(h, eps=0.5):
+    e1, e2 = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.rds_compare_gt(h, float(eps), ctypes.byref(e1), ctypes.byref(e2)), h)
+    return e1.value, e2.value
 
 
 def _get(fn, h, out, dtype, shape):
@@ -348,6 +374,20 @@ class Solver:
         rds_solve_tol(self.h, lam, theta, tau, math.inf if delta is None else delta,
                       max_iters, tol, check_every)
         return self.stats()
+
+    def solve_gt(self, lam, theta, tau, delta, max_iters, tol, check_every=10):
+        """float64 solve to tolerance (PAPER.md:234-238 ground truth; delta=inf = original
+        method).  Returns {iters, converged, residual}."""
+        return rds_solve_gt(self.h, lam, theta, tau, math.inf if delta is None else delta,
+                            max_iters, tol, check_every)
+
+    def u_gt(self, out=None):
+        out = np.empty(self.shape, np.float64) if out is None else out
+        return _get(_lib.rds_get_u_gt, self.h, out, np.float64, self.shape)
+
+    def compare_gt(self, eps=0.5):
+        """(E1, E2) of the current float u against u^GT."""
+        return rds_compare_gt(self.h, eps)
 
     def _out(self, dtype, out):
         return np.empty(self.shape, dtype=dtype) if out is None else out

@@ -444,24 +444,25 @@ def test_band_for_fraction_exact(rds, orc, name):
 # f2: tolerance solves -- stopping rule fused into the stencil
 # ------------------------------------------------------------------------------------------
 
-def _tol_case(rds, orc, z, P, cfg, lam, delta, max_iters, tol, m, ctx, **opt):
+def _tol_case(rds, orc, z, P, cfg, lam, delta, max_iters, tol, m, ctx, norm="l2", **opt):
     s = rds.Solver(*z.shape, **opt)
+    s.set_option(rds.RDS_OPT_STOP_NORM, {"l2": 0, "rms": 1}[norm])
     s.set_image(z)
     s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
     st = s.solve_tol(lam, cfg.theta, cfg.tau, delta, max_iters, tol, m)
     me = st["check_every"]
     assert me == (m or st["k_fuse"])
     f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
-    o = orc.solve_tol(f, delta, lam, np.float32(cfg.theta), cfg.tau, max_iters, tol, me)
+    o = orc.solve_tol(f, delta, lam, np.float32(cfg.theta), cfg.tau, max_iters, tol, me, norm)
     if st["iters"] != o["iters"]:
         # only a check whose residual sits within rounding of tol may decide differently
         lo = min(st["iters"], o["iters"])
         r_lo = orc.solve_tol(f, delta, lam, np.float32(cfg.theta), cfg.tau, lo, np.inf,
-                             lo)["residual"]
+                             lo, norm)["residual"]
         assert abs(st["iters"] - o["iters"]) == me and abs(r_lo - tol) <= 2e-2 * tol, \
             (ctx, st["iters"], o["iters"], r_lo)
         o = orc.solve_tol(f, delta, lam, np.float32(cfg.theta), cfg.tau, st["iters"], np.inf,
-                          st["iters"])
+                          st["iters"], norm)
     assert st["converged"] == int(o["residual"] <= tol or st["iters"] < max_iters), ctx
     assert abs(st["residual"] - o["residual"]) <= 2e-2 * max(o["residual"], 1e-6), \
         (ctx, st["residual"], o["residual"])
@@ -471,26 +472,28 @@ def _tol_case(rds, orc, z, P, cfg, lam, delta, max_iters, tol, m, ctx, **opt):
     return s, st
 
 
-@pytest.mark.parametrize("name,lam,dr,tol,m", [
-    ("C0", 5.0, 0.2, 1e-3, 0),          # empty band: fires at the first check, residual 0
-    ("C0", 5.0, math.inf, 1e-3, 0),
-    ("C1", 5.0, 0.2, 1e-3, 0),
-    ("C1", 2.0, math.inf, 2e-3, 10),    # blocks of 10 = two launches of 5 at k_fuse 7
-    ("C2", 5.0, 0.2, 5e-4, 8),
+@pytest.mark.parametrize("name,lam,dr,tol,m,norm", [
+    ("C0", 5.0, 0.2, 1e-2, 0, "l2"),      # empty band: fires at the first check, residual 0
+    ("C0", 5.0, math.inf, 1e-2, 0, "l2"),  # the paper's delta_stop on the paper's image size
+    ("C0", 5.0, math.inf, 1e-3, 0, "rms"),
+    ("C1", 5.0, 0.2, 0.5, 0, "l2"),
+    ("C1", 2.0, math.inf, 2e-3, 10, "rms"),  # blocks of 10 = two launches of 5 at k_fuse 7
+    ("C2", 5.0, 0.2, 1.0, 8, "l2"),
 ])
-def test_solve_tol_configs(rds, orc, name, lam, dr, tol, m):
+def test_solve_tol_configs(rds, orc, name, lam, dr, tol, m, norm):
     cfg = wl.CONFIGS[name]
     z, P = wl.make_image(cfg)
     delta = wl.band_delta(dr, orc.absmax(orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)))
     s, st = _tol_case(rds, orc, z, P, cfg, lam, delta, cfg.iters, tol, m,
-                      f"{name} lam={lam} d={dr} tol={tol} m={m}")
+                      f"{name} lam={lam} d={dr} tol={tol} m={m} {norm}", norm=norm)
     if dr == 0.2 and name == "C0":
         assert st["iters"] == st["check_every"] and st["residual"] == 0.0
     s.close()
 
 
-@pytest.mark.parametrize("m,kf,max_iters,tol", [(1, 7, 23, 1e-3), (3, 2, 31, 0.0),
-                                               (9, 4, 50, 2e-3), (7, 7, 45, 0.0)])
+@pytest.mark.parametrize("m,kf,max_iters,tol", [(1, 7, 23, 0.1), (3, 2, 31, 0.0),
+                                               (9, 4, 50, 0.2), (7, 7, 45, 0.0),
+                                               (7, 7, 3000, 0.05), (2, 5, 4001, 0.05)])
 def test_solve_tol_schedules(rds, orc, m, kf, max_iters, tol):
     """Single-stage CHECK launches (u^(l-1) from the u plane), blocks split across launches,
     max_iters off the check grid, tol = 0 (runs to max_iters, converged = 0), ragged shape."""
@@ -507,4 +510,58 @@ def test_solve_tol_schedules(rds, orc, m, kf, max_iters, tol):
     assert st2["iters"] == st["iters"] and np.array_equal(s.u(), u1)
     s.solve(5.0, cfg.theta, cfg.tau, np.float32(0.3), st["iters"])
     assert np.array_equal(s.u(), u1)
+    s.close()
+
+
+# ------------------------------------------------------------------------------------------
+# float64 mode: the paper's ground truth u^GT and E1 / E2
+# ------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["C0-original", "random-restricted"])
+def test_solve_gt_fp64(rds, orc, case):
+    """rds_solve_gt evaluates every formula in float64 in the order written, with correctly
+    rounded sqrt/division and no contraction -- like the fp64 oracle -- so the stopping
+    iteration agrees and the state is expected to be bit-identical."""
+    if case == "C0-original":
+        cfg = wl.CONFIGS["C0"]
+        z, P = wl.make_image(cfg)
+        delta, tol, m, K = math.inf, 1e-6, 10, 40000
+    else:
+        cfg = wl.CONFIGS["C1"]
+        z = np.random.default_rng(9).uniform(0, 1, (64, 70)).astype(np.float32)
+        P = None
+        delta, tol, m, K = np.float32(0.3), 1e-7, 7, 40000
+    f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    s = rds.Solver(*z.shape)
+    s.set_image(z)
+    s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
+    g = s.solve_gt(5.0, cfg.theta, cfg.tau, delta, K, tol, m)
+    o = orc.solve_tol(f, delta, 5.0, np.float32(cfg.theta), cfg.tau, K, tol, m)
+    assert g["converged"] == 1 and g["iters"] == o["iters"], (g, o["iters"])
+    assert abs(g["residual"] - o["residual"]) <= 1e-9 * o["residual"]
+    ug = s.u_gt()
+    assert np.abs(ug - o["u"]).max() <= 1e-12
+    assert np.array_equal(ug, o["u"]), "fp64 mode not bit-identical to the fp64 oracle"
+    s.close()
+
+
+def test_compare_gt_e1_e2(rds, orc):
+    """E1 / E2 on the GPU equal the oracle's definitions applied to the GPU's own arrays;
+    at q = 1 (delta = inf) the float solve to the paper's 1e-2 reproduces the thresholded
+    ground truth exactly (Table 1's q = 1 row: E1 = 1.000)."""
+    cfg = wl.CONFIGS["C0"]
+    z, P = wl.make_image(cfg)
+    s = rds.Solver(cfg.H, cfg.W)
+    s.set_image(z)
+    s.set_fitting(cfg.c1, cfg.c2)
+    s.solve_gt(5.0, cfg.theta, cfg.tau, math.inf, 100000, 1e-8, 10)
+    ug = s.u_gt()
+    for q in (1.0, 0.3, 0.0):
+        st = s.solve_tol(5.0, cfg.theta, cfg.tau, s.band_for_fraction(q), 20000, 1e-2)
+        u = s.u()
+        e1, e2 = s.compare_gt(0.5)
+        assert e1 == orc.tanimoto(u > 0.5, ug > 0.5), (q, e1)
+        assert abs(e2 - orc.l2_error(u, ug)) <= 1e-9 * max(1.0, e2), (q, e2)
+        if q == 1.0:
+            assert e1 == 1.0
     s.close()

@@ -497,18 +497,20 @@ def test_dependency_cone_window(orc, delta_rel):
 # f2: the stopping rule, RMS norm (reading R-F2)
 # ------------------------------------------------------------------------------------------
 
-def _rule_residual(orc, f, delta, lam, ell):
-    """max(RMS(u^l - u^(l-1)), RMS(v^l - v^(l-1))) from two plain fixed-K solves."""
+def _rule_residual(orc, f, delta, lam, ell, norm):
+    """max(||u^l - u^(l-1)||, ||v^l - v^(l-1)||) from two plain fixed-K solves, with the
+    Euclidean norm over pixels (norm="l2") or the RMS."""
     a = orc.solve(f, delta, lam, np.float32(0.1), 0.125, ell)
     b = orc.solve(f, delta, lam, np.float32(0.1), 0.125, ell - 1)
-    n = f.size
+    n = f.size if norm == "rms" else 1
     return max(math.sqrt(((a["u"] - b["u"]) ** 2).sum() / n),
                math.sqrt(((a["v"] - b["v"]) ** 2).sum() / n))
 
 
-@pytest.mark.parametrize("m,tol,delta_rel", [(7, 3e-3, 0.4), (1, 1e-2, math.inf),
-                                             (5, 1e-3, math.inf), (4, 0.0, 0.3)])
-def test_stopping_rule_definition(orc, m, tol, delta_rel):
+@pytest.mark.parametrize("m,tol,delta_rel,norm", [(7, 3e-3, 0.4, "rms"), (1, 1e-2, math.inf, "rms"),
+                                                  (5, 1e-3, math.inf, "rms"), (4, 0.0, 0.3, "rms"),
+                                                  (7, 3e-2, 0.4, "l2"), (3, 1e-2, math.inf, "l2")])
+def test_stopping_rule_definition(orc, m, tol, delta_rel, norm):
     """orc_solve_tol stops at the FIRST check (multiples of m, and max_iters) whose residual,
     recomputed here from two independent fixed-K solves, is <= tol; its state is the fixed-K
     state at that iteration, bit for bit."""
@@ -516,11 +518,11 @@ def test_stopping_rule_definition(orc, m, tol, delta_rel):
     f = rng.uniform(-1, 1, (24, 30)).astype(np.float32)
     delta = wl.band_delta(delta_rel, orc.absmax(f))
     K = 40
-    o = orc.solve_tol(f, delta, 4.0, np.float32(0.1), 0.125, K, tol, m)
+    o = orc.solve_tol(f, delta, 4.0, np.float32(0.1), 0.125, K, tol, m, norm)
     checks = list(range(m, K, m)) + [K]
     want, r_want = None, None
     for c in checks:
-        r = _rule_residual(orc, f, delta, 4.0, c)
+        r = _rule_residual(orc, f, delta, 4.0, c, norm)
         if r <= tol or c == K:
             want, r_want = c, r
             break
@@ -547,3 +549,23 @@ def test_stopping_rule_special_cases(orc):
     its = [orc.solve_tol(f, np.float32(np.inf), 4.0, np.float32(0.1), 0.125, 200, t, 3)["iters"]
            for t in (1e-1, 1e-2, 1e-3, 1e-4)]
     assert its == sorted(its)
+
+
+# ------------------------------------------------------------------------------------------
+# E1 / E2 of the paper's evaluation protocol
+# ------------------------------------------------------------------------------------------
+
+def test_tanimoto_and_l2(orc):
+    a = np.zeros((4, 5), bool)
+    b = np.zeros((4, 5), bool)
+    assert orc.tanimoto(a, b) == 1.0                       # empty/empty (R-C15)
+    a.flat[[0, 1, 2]] = True
+    b.flat[[1, 2, 3]] = True
+    assert orc.tanimoto(a, b) == 0.5                       # |{1,2}| / |{0,1,2,3}|
+    assert orc.tanimoto(a, a) == 1.0
+    assert orc.tanimoto(a, ~a) == 0.0
+    assert orc.tanimoto(a, b) == orc.tanimoto(b, a)
+    rng = np.random.default_rng(3)
+    u = rng.uniform(0, 1, (6, 7))
+    assert orc.l2_error(u, u) == 0.0
+    assert orc.l2_error(u + 0.25, u) == pytest.approx(42 * 0.0625, rel=1e-12)
