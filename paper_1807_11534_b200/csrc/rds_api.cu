@@ -22,7 +22,12 @@ namespace {
 
 thread_local std::string g_last_error;
 
-constexpr int kDefaultKF = 7;  // sweep: DESIGN.md §5
+// Default iterations per HBM round trip (DESIGN.md §5 sweeps): 7 where HBM traffic matters
+// (C2 and larger); 4 for images of <= 2^21 pixels, whose solves are bound by item latency
+// (shorter warm-up and marches: C1 1.55 vs 1.99 ms per 500 iterations).
+constexpr int kDefaultKF = 7, kSmallKF = 4;
+constexpr int64_t kSmallPixels = int64_t(1) << 21;
+static int default_kf(int64_t H, int64_t W) { return H * W <= kSmallPixels ? kSmallKF : kDefaultKF; }
 
 }  // namespace
 
@@ -672,7 +677,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     if (!h->image_ok || !h->p_ok)
         return fail(h, RDS_EINVAL, "rds_solve: image or P has non-finite values");
 
-    const int kf = h->opt_kf ? h->opt_kf : kDefaultKF;
+    const int kf = h->opt_kf ? h->opt_kf : default_kf(h->H, h->W);
     const int wv = wv_of(kf);
     const int n_strips = (int)((h->W + wv - 1) / wv);
     const int n_bands = (int)((h->H + TILE_H - 1) / TILE_H);
@@ -839,7 +844,7 @@ int rds_solve_tol(rds_t *h, float lambda, float theta, float tau, float delta, i
         return fail(h, RDS_EINVAL, "rds_solve_tol: check_every=%d must be >= 0", check_every);
     if (max_iters < 1)
         return fail(h, RDS_EINVAL, "rds_solve_tol: max_iters=%d must be >= 1", max_iters);
-    const int m = check_every > 0 ? check_every : (h->opt_kf ? h->opt_kf : kDefaultKF);
+    const int m = check_every > 0 ? check_every : (h->opt_kf ? h->opt_kf : default_kf(h->H, h->W));
     return solve_impl(h, lambda, theta, tau, delta, max_iters, m, tol);
 }
 
