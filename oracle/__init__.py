@@ -75,6 +75,12 @@ def _load():
         lib.orc_solve_tol.restype = i
         lib.orc_solve_plain.argtypes = [P, i64, i64, d, d, d, i, P, P, P, P]
         lib.orc_solve_plain.restype = i
+        lib.orc_grad3.argtypes = [P, i64, i64, i64, P, P, P]
+        lib.orc_div3.argtypes = [P, P, P, i64, i64, i64, P]
+        lib.orc_solve3.argtypes = [P, i64, i64, i64, f, d, d, d, i, P, P, P, P, P, P]
+        lib.orc_solve3.restype = i
+        lib.orc_solve3_plain.argtypes = [P, i64, i64, i64, d, d, d, i, P, P, P, P, P]
+        lib.orc_solve3_plain.restype = i
         lib.orc_inner.argtypes = [P, i64, i64, f, d, d, i, P, P, P, P]
         lib.orc_inner.restype = i
         lib.orc_band_for_fraction.argtypes = [P, i64, d]
@@ -243,6 +249,54 @@ def solve_tol(f, delta, lam, theta, tau, max_iters, tol, check_every, norm="l2")
     if rc != 0:
         raise ValueError(f"orc_solve_tol rc={rc}")
     return dict(u=u, v=v, p1=p1, p2=p2, labels=lab, iters=it.value, residual=res.value)
+
+
+# ------------------------------------------------------------------------------------------
+# f4: 3-D volumes (oracle.c orc_*3, reading R-F4).  Arrays are (D, H, W).
+# ------------------------------------------------------------------------------------------
+
+def grad3(u):
+    u = _f64(u)
+    D, H, W = u.shape
+    g = [np.empty_like(u) for _ in range(3)]
+    _load().orc_grad3(_ptr(u), D, H, W, _ptr(g[0]), _ptr(g[1]), _ptr(g[2]))
+    return tuple(g)
+
+
+def div3(p1, p2, p3):
+    p1, p2, p3 = _f64(p1), _f64(p2), _f64(p3)
+    D, H, W = p1.shape
+    d = np.empty_like(p1)
+    _load().orc_div3(_ptr(p1), _ptr(p2), _ptr(p3), D, H, W, _ptr(d))
+    return d
+
+
+def solve3(f, delta, lam, theta, tau, iters):
+    """Restricted-domain iteration on a volume f (D, H, W) float32: dict u, v, p1, p2, p3,
+    labels."""
+    f = _f32(f)
+    D, H, W = f.shape
+    out = {k: np.empty((D, H, W), np.float64) for k in ("u", "v", "p1", "p2", "p3")}
+    lab = np.empty((D, H, W), np.uint8)
+    rc = _load().orc_solve3(_ptr(f), D, H, W, np.float32(delta), float(lam), float(theta),
+                            float(tau), int(iters), _ptr(out["u"]), _ptr(out["v"]),
+                            _ptr(out["p1"]), _ptr(out["p2"]), _ptr(out["p3"]), _ptr(lab))
+    if rc != 0:
+        raise ValueError(f"orc_solve3 rc={rc}")
+    out["labels"] = lab
+    return out
+
+
+def solve3_plain(f, lam, theta, tau, iters):
+    f = _f32(f)
+    D, H, W = f.shape
+    out = {k: np.empty((D, H, W), np.float64) for k in ("u", "v", "p1", "p2", "p3")}
+    rc = _load().orc_solve3_plain(_ptr(f), D, H, W, float(lam), float(theta), float(tau),
+                                  int(iters), _ptr(out["u"]), _ptr(out["v"]), _ptr(out["p1"]),
+                                  _ptr(out["p2"]), _ptr(out["p3"]))
+    if rc != 0:
+        raise ValueError(f"orc_solve3_plain rc={rc}")
+    return out
 
 
 def tanimoto(a, b):

@@ -536,3 +536,166 @@ int orc_inner(const float *f32, int64_t H, int64_t W, float delta, double theta,
     free(w);
     return 0;
 }
+
+/* ---------------------------------------------------------------------------------------- */
+/* f4: the same method on 3-D volumes (§5: "extension to 3D").  A volume is    */
+/* D planes x H rows x W columns, plane-major.  The discrete operators extend reading R-C6   */
+/* axis by axis (reading R-F4): forward differences with a zero last plane / row / column,  */
+/* div = -grad^T, components rho1 (rows, i), rho2 (columns, j), rho3 (planes, k).           */
+/* Labels and the fitting term are per voxel (orc_fitting / orc_labels with n = D H W).     */
+/* ---------------------------------------------------------------------------------------- */
+#define IDX3(k, i, j) (((int64_t)(k) * H + (i)) * W + (j))
+
+void orc_grad3(const double *u, int64_t D, int64_t H, int64_t W, double *g1, double *g2,
+               double *g3) {
+    for (int64_t k = 0; k < D; ++k)
+        for (int64_t i = 0; i < H; ++i)
+            for (int64_t j = 0; j < W; ++j) {
+                int64_t x = IDX3(k, i, j);
+                g1[x] = (i < H - 1) ? u[IDX3(k, i + 1, j)] - u[x] : 0.0;
+                g2[x] = (j < W - 1) ? u[IDX3(k, i, j + 1)] - u[x] : 0.0;
+                g3[x] = (k < D - 1) ? u[IDX3(k + 1, i, j)] - u[x] : 0.0;
+            }
+}
+
+static inline double div3_at(const double *p1, const double *p2, const double *p3, int64_t D,
+                             int64_t H, int64_t W, int64_t k, int64_t i, int64_t j) {
+    double d = (i < H - 1) ? p1[IDX3(k, i, j)] : 0.0;
+    d = d - ((i > 0) ? p1[IDX3(k, i - 1, j)] : 0.0);
+    d = d + ((j < W - 1) ? p2[IDX3(k, i, j)] : 0.0);
+    d = d - ((j > 0) ? p2[IDX3(k, i, j - 1)] : 0.0);
+    d = d + ((k < D - 1) ? p3[IDX3(k, i, j)] : 0.0);
+    d = d - ((k > 0) ? p3[IDX3(k - 1, i, j)] : 0.0);
+    return d;
+}
+
+void orc_div3(const double *p1, const double *p2, const double *p3, int64_t D, int64_t H,
+              int64_t W, double *d) {
+    for (int64_t k = 0; k < D; ++k)
+        for (int64_t i = 0; i < H; ++i)
+            for (int64_t j = 0; j < W; ++j) d[IDX3(k, i, j)] = div3_at(p1, p2, p3, D, H, W, k, i, j);
+}
+
+/* The restricted-domain iteration of orc_solve (§2.1 + §3, Eq. 7-9) on a volume. */
+int orc_solve3(const float *f32, int64_t D, int64_t H, int64_t W, float delta, double lambda,
+               double theta, double tau, int iters, double *u, double *v, double *p1,
+               double *p2, double *p3, uint8_t *lab_out) {
+    if (D < 1 || H < 1 || W < 1 || iters < 0) return -1;
+    int64_t n = D * H * W;
+    uint8_t *lab = (uint8_t *)malloc((size_t)n);
+    double *u0 = (double *)malloc(sizeof(double) * (size_t)n);
+    double *w = (double *)malloc(sizeof(double) * (size_t)n);
+    orc_labels(f32, n, delta, lab);
+    for (int64_t x = 0; x < n; ++x) {
+        u0[x] = (f32[x] <= 0.0f) ? 1.0 : 0.0; /* H(-f), H(0) = 1 */
+        u[x] = v[x] = u0[x];
+        p1[x] = p2[x] = p3[x] = 0.0;
+    }
+    for (int it = 0; it < iters; ++it) {
+        /* w = div rho - v/theta on the full grid */
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < D; ++k)
+            for (int64_t i = 0; i < H; ++i)
+                for (int64_t j = 0; j < W; ++j)
+                    w[IDX3(k, i, j)] =
+                        div3_at(p1, p2, p3, D, H, W, k, i, j) - v[IDX3(k, i, j)] / theta;
+        /* rho-step on RD, 0 on Fg u Bg (Eq. 8) */
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < D; ++k)
+            for (int64_t i = 0; i < H; ++i)
+                for (int64_t j = 0; j < W; ++j) {
+                    int64_t x = IDX3(k, i, j);
+                    if (lab[x] != LAB_RD) {
+                        p1[x] = p2[x] = p3[x] = 0.0;
+                        continue;
+                    }
+                    double g1 = (i < H - 1) ? w[IDX3(k, i + 1, j)] - w[x] : 0.0;
+                    double g2 = (j < W - 1) ? w[IDX3(k, i, j + 1)] - w[x] : 0.0;
+                    double g3 = (k < D - 1) ? w[IDX3(k + 1, i, j)] - w[x] : 0.0;
+                    double den = 1.0 + tau * sqrt(g1 * g1 + g2 * g2 + g3 * g3);
+                    p1[x] = (p1[x] + tau * g1) / den;
+                    p2[x] = (p2[x] + tau * g2) / den;
+                    p3[x] = (p3[x] + tau * g3) / den;
+                }
+        /* u-step (Eq. 7), v-step (Eq. 9) */
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < D; ++k)
+            for (int64_t i = 0; i < H; ++i)
+                for (int64_t j = 0; j < W; ++j) {
+                    int64_t x = IDX3(k, i, j);
+                    if (lab[x] != LAB_RD) {
+                        u[x] = v[x] = u0[x];
+                        continue;
+                    }
+                    double ux = v[x] - theta * div3_at(p1, p2, p3, D, H, W, k, i, j);
+                    u[x] = ux;
+                    double t = ux - theta * lambda * (double)f32[x];
+                    v[x] = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+                }
+    }
+    if (lab_out) memcpy(lab_out, lab, (size_t)n);
+    free(lab);
+    free(u0);
+    free(w);
+    return 0;
+}
+
+/* The unrestricted 3-D iteration written out separately (no partition logic), the twin    */
+/* orc_solve3 must reproduce bit for bit at delta = +inf.                                    */
+int orc_solve3_plain(const float *f32, int64_t D, int64_t H, int64_t W, double lambda,
+                     double theta, double tau, int iters, double *u, double *v, double *p1,
+                     double *p2, double *p3) {
+    if (D < 1 || H < 1 || W < 1 || iters < 0) return -1;
+    int64_t n = D * H * W;
+    double *w = (double *)malloc(sizeof(double) * (size_t)n);
+    for (int64_t x = 0; x < n; ++x) {
+        v[x] = (f32[x] <= 0.0f) ? 1.0 : 0.0;
+        u[x] = v[x];
+        p1[x] = p2[x] = p3[x] = 0.0;
+    }
+    for (int it = 0; it < iters; ++it) {
+        for (int64_t k = 0; k < D; ++k)
+            for (int64_t i = 0; i < H; ++i)
+                for (int64_t j = 0; j < W; ++j) {
+                    double d = 0.0;
+                    if (i < H - 1) d += p1[IDX3(k, i, j)];
+                    if (i > 0) d -= p1[IDX3(k, i - 1, j)];
+                    if (j < W - 1) d += p2[IDX3(k, i, j)];
+                    if (j > 0) d -= p2[IDX3(k, i, j - 1)];
+                    if (k < D - 1) d += p3[IDX3(k, i, j)];
+                    if (k > 0) d -= p3[IDX3(k - 1, i, j)];
+                    w[IDX3(k, i, j)] = d - v[IDX3(k, i, j)] / theta;
+                }
+        for (int64_t k = 0; k < D; ++k)
+            for (int64_t i = 0; i < H; ++i)
+                for (int64_t j = 0; j < W; ++j) {
+                    int64_t x = IDX3(k, i, j);
+                    double g1 = 0.0, g2 = 0.0, g3 = 0.0;
+                    if (i < H - 1) g1 = w[IDX3(k, i + 1, j)] - w[x];
+                    if (j < W - 1) g2 = w[IDX3(k, i, j + 1)] - w[x];
+                    if (k < D - 1) g3 = w[IDX3(k + 1, i, j)] - w[x];
+                    double den = 1.0 + tau * sqrt(g1 * g1 + g2 * g2 + g3 * g3);
+                    p1[x] = (p1[x] + tau * g1) / den;
+                    p2[x] = (p2[x] + tau * g2) / den;
+                    p3[x] = (p3[x] + tau * g3) / den;
+                }
+        for (int64_t k = 0; k < D; ++k)
+            for (int64_t i = 0; i < H; ++i)
+                for (int64_t j = 0; j < W; ++j) {
+                    int64_t x = IDX3(k, i, j);
+                    double d = 0.0;
+                    if (i < H - 1) d += p1[x];
+                    if (i > 0) d -= p1[IDX3(k, i - 1, j)];
+                    if (j < W - 1) d += p2[x];
+                    if (j > 0) d -= p2[IDX3(k, i, j - 1)];
+                    if (k < D - 1) d += p3[x];
+                    if (k > 0) d -= p3[IDX3(k - 1, i, j)];
+                    double ux = v[x] - theta * d;
+                    u[x] = ux;
+                    double t = ux - theta * lambda * (double)f32[x];
+                    v[x] = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+                }
+    }
+    free(w);
+    return 0;
+}
