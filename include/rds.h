@@ -238,6 +238,30 @@ const char *rds_last_error(rds_t *h);
 /* Library version string. */
 const char *rds_version(void);
 
+/* ---- f4: 3-D volumes (§5 "extension to 3D") -------------------------------
+ * The same method on a D x H x W volume (plane-major, row-major planes): voxel labels and
+ * fitting term as above; grad = forward differences along rows, columns and planes with a
+ * zero last row / column / plane, div = -grad^T, rho = (rho1 rows, rho2 columns, rho3 planes)
+ * (reading R-F4).  tau must be in (0, 1/12] (||grad||^2 <= 12 in 3-D).  One fused
+ * pass per iteration (k_vol_step), the K-loop replayed from a CUDA graph.  Errors as for the
+ * 2-D calls; the buffers are D*H*W elements. */
+typedef struct rds3_handle rds3_t;
+int rds3_create(int64_t D, int64_t H, int64_t W, rds3_t **out);
+int rds3_destroy(rds3_t *h);
+int rds3_set_stream(rds3_t *h, void *stream);
+int rds3_set_image(rds3_t *h, const float *z, int on_device);
+int rds3_set_fitting(rds3_t *h, float c1, float c2, float gamma, const float *P, int on_device);
+int rds3_fitting_absmax(rds3_t *h, float *out);
+int rds3_solve(rds3_t *h, float lambda, float theta, float tau, float delta, int32_t iters);
+int rds3_get_u(rds3_t *h, float *out, int on_device);
+int rds3_get_v(rds3_t *h, float *out, int on_device);
+int rds3_get_p(rds3_t *h, float *rho1, float *rho2, float *rho3, int on_device);
+int rds3_get_mask(rds3_t *h, uint8_t *out, int on_device);
+int rds3_get_labels(rds3_t *h, uint8_t *out, int on_device);
+/* voxels in RD, K of the last solve, planes per CTA z-chunk, setup + K-loop time (ms) */
+int rds3_get_stats(rds3_t *h, int64_t *n_rd, int32_t *iters, int32_t *kz, float *ms);
+const char *rds3_last_error(rds3_t *h);
+
 #ifdef __cplusplus
 }
 #endif

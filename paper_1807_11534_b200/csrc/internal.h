@@ -173,6 +173,36 @@ cudaError_t launch_f64_iter(const F64Args &a, int b, double *part, cudaStream_t 
 cudaError_t launch_compare(const float *u, const double *ugt, int64_t pitch, int H, int W,
                            float eps, double *part, double *out, cudaStream_t s);
 
+// f4: 3-D volumes (k_vol.cu).  Padded volume: VOL_PZ frame planes before/after, VOL_PY_TOP
+// rows above and VOL_PY_BOT below each plane, VOL_PX_L columns left, >= VOL_PX_R right.
+constexpr int VOL_PZ = 2, VOL_PY_TOP = 2, VOL_PY_BOT = 16, VOL_PX_L = 4, VOL_PX_R = 32;
+struct VolArgs {
+    const float *p1_in, *p2_in, *p3_in, *v_in, *c;   // voxel (0,0,0) origins
+    float *p1_out, *p2_out, *p3_out, *v_out, *u_out;
+    uint8_t *mask_out;
+    int64_t plane, pitch;
+    int D, H, W, kz;                                 // kz = planes per CTA z-chunk
+    float tau, theta, inv_theta;
+};
+struct VolSetupArgs {
+    const float *z, *P;
+    float *f, *c, *u, *v0, *v1, *p10, *p11, *p20, *p21, *p30, *p31;
+    uint8_t *lab, *mask;
+    unsigned long long *n_rd;
+    int64_t plane, pitch;
+    int D, H, W;
+    float c1, c2, gamma, delta, theta_lambda;
+};
+cudaError_t launch_vol_step(const VolArgs &a, bool write_u, cudaStream_t s);
+cudaError_t launch_vol_setup(const VolSetupArgs &a, cudaStream_t s);
+cudaError_t launch_vol_absmax(const float *z, const float *P, int64_t plane, int64_t pitch,
+                              int D, int H, int W, float c1, float c2, float gamma,
+                              unsigned *out_bits, cudaStream_t s);
+cudaError_t launch_vol_copy_f32(float *dst, const float *src, int64_t plane, int64_t pitch,
+                                int D, int H, int W, int to_padded, cudaStream_t s);
+cudaError_t launch_vol_copy_u8(uint8_t *dst, const uint8_t *src, int64_t plane, int64_t pitch,
+                               int D, int H, int W, int to_padded, cudaStream_t s);
+
 // out[i * out_pitch + j] = plane[i * pitch + swz(j)]: natural-order copy of a swizzled plane
 cudaError_t launch_unswizzle(const float *plane, int64_t pitch, int H, int W, float *out,
                              int64_t out_pitch, cudaStream_t s);

@@ -1,0 +1,222 @@
+// k_vol.cu -- f4: the restricted-domain dual iteration on 3-D volumes (§5
+// "extension to 3D"), sm_100a.  Same method as the 2-D path, operators extended axis by axis
+// (reading R-F4): grad = forward differences along i (rows), j (columns), k (planes) with a
+// zero last row / column / plane, div = -grad^T, rho = (rho1, rho2, rho3).
+//
+// Layout: padded volume, voxel (k, i, j) at origin + k * plane + i * pitch + j with 2 frame
+// planes before and after, 2 frame rows above and 16 below, 4 frame columns left and >= 32
+// right (a CTA window reaches 2 before its tile and up to 16 / 32 past the last image
+// row / column); the frame holds pinned background (rho = 0, v = 0, c' = +inf), so no load
+// is bounds-checked.  c' = 2^-100 theta*lambda*f on RD, -inf on Fg, +inf on Bg (as in 2-D).
+//
+// k_vol_step: one iteration per launch, all of it in one pass over the volume (36 B per
+// voxel: read rho1..3, v, c'; write rho1..3, v).  A CTA of 32 x 16 threads owns one (i, j)
+// column each of a 16 x 32 window and marches along k through a z-chunk: per plane step n it
+// loads plane n, forms w(n) = div rho(n) - v(n)/theta, the rho update of plane n-1 (needs
+// w(n-1), w(n)), and the u- and v-steps of plane n-1 (need rho_new of plane n-1 at i-1, j-1
+// and of plane n-2).  Windows overlap by 3 columns / rows (the dependency cone of one
+// iteration), so each CTA writes a 13 x 29 tile; three __syncthreads per plane step.
+#include <math.h>
+
+#include "internal.h"
+
+namespace rds {
+
+constexpr int VT_X = 32, VT_Y = 16;          // threads per CTA (columns, rows)
+constexpr int VO_X = VT_X - 3, VO_Y = VT_Y - 3;  // output tile (29 x 13)
+
+__device__ __forceinline__ float vsqrt(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float vrcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+template <bool WRITE_U>
+__global__ void __launch_bounds__(VT_X * VT_Y) k_vol_step(const VolArgs a) {
+    __shared__ float s1[VT_Y][VT_X], s2[VT_Y][VT_X];   // rho1, rho2 of plane n
+    __shared__ float sw[2][VT_Y][VT_X];                // w of planes n-1, n (alternating)
+    __shared__ float q1s[VT_Y][VT_X], q2s[VT_Y][VT_X]; // rho1, rho2 new of plane n-1
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int j = blockIdx.x * VO_X - 2 + tx, i = blockIdx.y * VO_Y - 2 + ty;
+    const int k0 = blockIdx.z * a.kz, k1 = min(k0 + a.kz, a.D);
+    // every thread owns a column inside the padded frame (the frame is >= 2 wide)
+    const int64_t col = (int64_t)i * a.pitch + j;
+    const bool in_w = ty >= 1 && tx >= 1;                          // w needed here
+    const bool in_q = ty >= 1 && ty <= VT_Y - 2 && tx >= 1 && tx <= VT_X - 2;  // rho_new
+    const bool in_o = ty >= 2 && ty <= VT_Y - 2 && tx >= 2 && tx <= VT_X - 2 && i < a.H &&
+                      j < a.W;                                     // u, v output
+    const bool last_i = i == a.H - 1, last_j = j == a.W - 1;
+    const float tau = a.tau, theta = a.theta, inv_theta = a.inv_theta;
+    // pipeline registers: plane n-1 values of this column
+    // (the first step's plane n-1 = k0-2 only feeds w(k0-1) through rho3; its other values
+    // feed results that are discarded)
+    float pp1 = 0.f, pp2 = 0.f, pv = 0.f, pc = INFINITY;           // old rho, v, c' at n-1
+    float pp3 = a.p3_in[(int64_t)(k0 - 2) * a.plane + col];
+    float q3prev = 0.f;                                            // rho3 new at plane n-2
+    int cur = 0;
+    for (int n = k0 - 1; n <= k1; ++n) {
+        const int64_t o = (int64_t)n * a.plane + col;
+        const float p1n = a.p1_in[o], p2n = a.p2_in[o], p3n = a.p3_in[o];
+        const float vn = a.v_in[o], cn = a.c[o];
+        s1[ty][tx] = p1n;
+        s2[ty][tx] = p2n;
+        __syncthreads();
+        // w(n) = div rho(n) - v(n)/theta; the p3 of plane n-1 is pp3 (this column)
+        float wn = 0.f;
+        if (in_w) {
+            const float d = (p1n - s1[ty - 1][tx]) + (p2n - s2[ty][tx - 1]) + (p3n - pp3);
+            wn = fmaf(vn, -inv_theta, d);
+        }
+        sw[cur][ty][tx] = wn;
+        __syncthreads();
+        // rho-step at plane n-1 (Eq. 8): g from w(n-1) (sw[cur^1]) and w(n)
+        float q1 = 0.f, q2 = 0.f, q3 = 0.f;
+        if (in_q) {
+            const float w0 = sw[cur ^ 1][ty][tx];
+            const float g1 = last_i ? 0.f : sw[cur ^ 1][ty + 1][tx] - w0;
+            const float g2 = last_j ? 0.f : sw[cur ^ 1][ty][tx + 1] - w0;
+            const float g3 = (n - 1 == a.D - 1) ? 0.f : wn - w0;
+            const float s = fmaf(g1, g1, fmaf(g2, g2, fmaf(g3, g3, fabsf(pc))));
+            const float rr = vrcp(fmaf(tau, vsqrt(s), 1.0f));
+            q1 = fmaf(tau, g1, pp1) * rr;
+            q2 = fmaf(tau, g2, pp2) * rr;
+            q3 = fmaf(tau, g3, pp3) * rr;
+        }
+        q1s[ty][tx] = q1;
+        q2s[ty][tx] = q2;
+        __syncthreads();
+        // u- and v-steps at plane n-1 (Eq. 7, 9), output planes [k0, k1)
+        if (in_o && n - 1 >= k0) {
+            const float d = (q1 - q1s[ty - 1][tx]) + (q2 - q2s[ty][tx - 1]) + (q3 - q3prev);
+            const float u = fmaf(-theta, d, pv);
+            const float vnew = __saturatef(fmaf(pc, -0x1p100f, u));
+            const int64_t oo = (int64_t)(n - 1) * a.plane + col;
+            a.p1_out[oo] = q1;
+            a.p2_out[oo] = q2;
+            a.p3_out[oo] = q3;
+            a.v_out[oo] = vnew;
+            if (WRITE_U) {
+                const float uu = fabsf(pc) < INFINITY ? u : pv;  // pinned u0 off RD
+                a.u_out[oo] = uu;
+                a.mask_out[oo] = uu > 0.5f;
+            }
+        }
+        // rotate the pipeline
+        pp1 = p1n;
+        pp2 = p2n;
+        pp3 = p3n;
+        pv = vn;
+        pc = cn;
+        q3prev = q3;
+        cur ^= 1;
+    }
+}
+
+// K1 of the volume path: f (R-A1 order), label, c', u0 / mask, v0 and rho0 = 0 into both
+// buffers; frame voxels are never touched (they keep the allocation-time pinned values).
+__global__ void k_vol_setup(const VolSetupArgs a) {
+    const int64_t n = (int64_t)a.D * a.H * a.W;
+    const bool use_p = a.P != nullptr && a.gamma != 0.0f;
+    unsigned long long n_rd = 0;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = x / ((int64_t)a.H * a.W), r = x - k * a.H * a.W;
+        const int i = (int)(r / a.W), j = (int)(r - (int64_t)i * a.W);
+        const int64_t o = k * a.plane + (int64_t)i * a.pitch + j;
+        const float z = a.z[o];
+        const float aa = __fsub_rn(z, a.c1), bb = __fsub_rn(z, a.c2);
+        float f = __fsub_rn(__fmul_rn(aa, aa), __fmul_rn(bb, bb));
+        if (use_p) f = __fadd_rn(f, __fmul_rn(a.gamma, a.P[o]));
+        const bool rd = fabsf(f) < a.delta, fg = f <= 0.0f;
+        const float u0 = fg ? 1.0f : 0.0f;
+        a.f[o] = f;
+        a.lab[o] = rd ? 2 : (fg ? 1 : 0);
+        a.c[o] = rd ? __fmul_rn(fminf(fmaxf(__fmul_rn(a.theta_lambda, f), -0x1p20f), 0x1p20f),
+                                0x1p-100f)
+                    : (fg ? -INFINITY : INFINITY);
+        a.u[o] = u0;
+        a.mask[o] = fg ? 1 : 0;
+        a.v0[o] = a.v1[o] = u0;
+        a.p10[o] = a.p11[o] = a.p20[o] = a.p21[o] = a.p30[o] = a.p31[o] = 0.0f;
+        n_rd += rd;
+    }
+    if (n_rd) atomicAdd(a.n_rd, n_rd);  // integer count: order-independent
+}
+
+__global__ void k_vol_absmax(const float *z, const float *P, int64_t plane, int64_t pitch,
+                             int D, int H, int W, float c1, float c2, float gamma,
+                             unsigned *out_bits) {
+    const int64_t n = (int64_t)D * H * W;
+    const bool use_p = P != nullptr && gamma != 0.0f;
+    float m = 0.0f;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = x / ((int64_t)H * W), r = x - k * H * W;
+        const int i = (int)(r / W), j = (int)(r - (int64_t)i * W);
+        const int64_t o = k * plane + (int64_t)i * pitch + j;
+        const float aa = __fsub_rn(z[o], c1), bb = __fsub_rn(z[o], c2);
+        float f = __fsub_rn(__fmul_rn(aa, aa), __fmul_rn(bb, bb));
+        if (use_p) f = __fadd_rn(f, __fmul_rn(gamma, P[o]));
+        m = fmaxf(m, fabsf(f));
+    }
+    for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) atomicMax(out_bits, __float_as_uint(m));
+}
+
+// dense (D, H, W) <-> padded volume copies (one voxel per thread-iteration)
+template <typename T>
+__global__ void k_vol_copy(T *dst, const T *src, int64_t plane, int64_t pitch, int D, int H,
+                           int W, int to_padded) {
+    const int64_t n = (int64_t)D * H * W;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = x / ((int64_t)H * W), r = x - k * H * W;
+        const int i = (int)(r / W), j = (int)(r - (int64_t)i * W);
+        const int64_t o = k * plane + (int64_t)i * pitch + j;
+        if (to_padded)
+            dst[o] = src[x];
+        else
+            dst[x] = src[o];
+    }
+}
+
+cudaError_t launch_vol_step(const VolArgs &a, bool write_u, cudaStream_t s) {
+    dim3 block(VT_X, VT_Y);
+    dim3 grid((a.W + VO_X - 1) / VO_X, (a.H + VO_Y - 1) / VO_Y, (a.D + a.kz - 1) / a.kz);
+    if (write_u)
+        k_vol_step<true><<<grid, block, 0, s>>>(a);
+    else
+        k_vol_step<false><<<grid, block, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vol_setup(const VolSetupArgs &a, cudaStream_t s) {
+    k_vol_setup<<<148 * 8, 256, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vol_absmax(const float *z, const float *P, int64_t plane, int64_t pitch,
+                              int D, int H, int W, float c1, float c2, float gamma,
+                              unsigned *out_bits, cudaStream_t s) {
+    k_vol_absmax<<<148 * 4, 256, 0, s>>>(z, P, plane, pitch, D, H, W, c1, c2, gamma, out_bits);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vol_copy_f32(float *dst, const float *src, int64_t plane, int64_t pitch,
+                                int D, int H, int W, int to_padded, cudaStream_t s) {
+    k_vol_copy<float><<<148 * 8, 256, 0, s>>>(dst, src, plane, pitch, D, H, W, to_padded);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vol_copy_u8(uint8_t *dst, const uint8_t *src, int64_t plane, int64_t pitch,
+                               int D, int H, int W, int to_padded, cudaStream_t s) {
+    k_vol_copy<uint8_t><<<148 * 8, 256, 0, s>>>(dst, src, plane, pitch, D, H, W, to_padded);
+    return cudaGetLastError();
+}
+
+}  // namespace rds

@@ -32,6 +32,9 @@ EXPORTS = (
     "rds_get_active_tiles", "rds_tile_shape", "rds_energy", "rds_get_stats",
     "rds_kfuse_supported", "rds_last_error", "rds_version", "rds_band_for_fraction",
     "rds_solve_q", "rds_solve_tol", "rds_solve_gt", "rds_get_u_gt", "rds_compare_gt",
+    "rds3_create", "rds3_destroy", "rds3_set_stream", "rds3_set_image", "rds3_set_fitting",
+    "rds3_fitting_absmax", "rds3_solve", "rds3_get_u", "rds3_get_v", "rds3_get_p",
+    "rds3_get_mask", "rds3_get_labels", "rds3_get_stats", "rds3_last_error",
 )
 
 
@@ -106,12 +109,28 @@ def _load():
         "rds_solve_gt": [P, f, f, f, f, i32, ctypes.c_double, i32, ctypes.POINTER(rds_gt_t)],
         "rds_get_u_gt": [P, P, i],
         "rds_compare_gt": [P, f, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
+        "rds3_create": [i64, i64, i64, ctypes.POINTER(P)],
+        "rds3_destroy": [P],
+        "rds3_set_stream": [P, P],
+        "rds3_set_image": [P, P, i],
+        "rds3_set_fitting": [P, f, f, f, P, i],
+        "rds3_fitting_absmax": [P, ctypes.POINTER(f)],
+        "rds3_solve": [P, f, f, f, f, i32],
+        "rds3_get_u": [P, P, i],
+        "rds3_get_v": [P, P, i],
+        "rds3_get_p": [P, P, P, P, i],
+        "rds3_get_mask": [P, P, i],
+        "rds3_get_labels": [P, P, i],
+        "rds3_get_stats": [P, ctypes.POINTER(i64), ctypes.POINTER(i32), ctypes.POINTER(i32),
+                           ctypes.POINTER(f)],
+        "rds3_last_error": [P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int
     lib.rds_last_error.restype = ctypes.c_char_p
+    lib.rds3_last_error.restype = ctypes.c_char_p
     lib.rds_version.restype = ctypes.c_char_p
     return lib
 
@@ -419,3 +438,85 @@ class Solver:
 
     def stats(self):
         return rds_get_stats(self.h)
+
+
+# ------------------------------------------------------------------------------------------
+# f4: 3-D volumes (rds3_*)
+# ------------------------------------------------------------------------------------------
+
+def _check3(rc, h):
+    if rc != RDS_OK:
+        raise RdsError(rc, _lib.rds3_last_error(h).decode() if h else "")
+
+
+class Solver3:
+    """One rds3 handle for a D x H x W volume (host numpy or device torch buffers)."""
+
+    def __init__(self, D, H, W, stream=None):
+        self.shape = (int(D), int(H), int(W))
+        h = ctypes.c_void_p()
+        _check3(_lib.rds3_create(int(D), int(H), int(W), ctypes.byref(h)), None)
+        self.h = h
+        if stream is not None:
+            _check3(_lib.rds3_set_stream(self.h, ctypes.c_void_p(stream)), self.h)
+
+    def close(self):
+        if self.h is not None:
+            _lib.rds3_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_image(self, z):
+        p, dev, _k = _buf(z, np.float32, self.shape)
+        _check3(_lib.rds3_set_image(self.h, p, dev), self.h)
+
+    def set_fitting(self, c1, c2, gamma=0.0, P=None):
+        if P is None:
+            p, dev, _k = None, 0, None
+        else:
+            p, dev, _k = _buf(P, np.float32, self.shape)
+        _check3(_lib.rds3_set_fitting(self.h, float(c1), float(c2), float(gamma), p, dev), self.h)
+
+    def absmax(self):
+        out = ctypes.c_float()
+        _check3(_lib.rds3_fitting_absmax(self.h, ctypes.byref(out)), self.h)
+        return np.float32(out.value)
+
+    def solve(self, lam, theta, tau, delta, iters):
+        _check3(_lib.rds3_solve(self.h, float(lam), float(theta), float(tau),
+                                float(math.inf if delta is None else delta), int(iters)), self.h)
+
+    def _get(self, fn, dtype, out):
+        out = np.empty(self.shape, dtype) if out is None else out
+        p, dev, _k = _buf(out, dtype, self.shape, writable=True)
+        _check3(fn(self.h, p, dev), self.h)
+        return out
+
+    def u(self, out=None):
+        return self._get(_lib.rds3_get_u, np.float32, out)
+
+    def v(self, out=None):
+        return self._get(_lib.rds3_get_v, np.float32, out)
+
+    def mask(self, out=None):
+        return self._get(_lib.rds3_get_mask, np.uint8, out)
+
+    def labels(self, out=None):
+        return self._get(_lib.rds3_get_labels, np.uint8, out)
+
+    def p(self):
+        outs = [np.empty(self.shape, np.float32) for _ in range(3)]
+        ps = [_buf(o, np.float32, self.shape, writable=True) for o in outs]
+        _check3(_lib.rds3_get_p(self.h, ps[0][0], ps[1][0], ps[2][0], 0), self.h)
+        return tuple(outs)
+
+    def stats(self):
+        n_rd, it, kz, ms = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_float()
+        _check3(_lib.rds3_get_stats(self.h, ctypes.byref(n_rd), ctypes.byref(it),
+                                    ctypes.byref(kz), ctypes.byref(ms)), self.h)
+        return {"n_rd": n_rd.value, "iters": it.value, "kz": kz.value, "ms": ms.value}

@@ -15,6 +15,8 @@ The recipes follow SURVEY.md §8(d) (configs C0-C4 = BASELINE.json ``configs[0..
       -- distance-selective fitting (Eq. 3; P is not defined there, reading C13).
 * C3  4096^2 Voronoi of 200 sites, sigma=0.15          -- the "strong noise" case.
 * C4  16384^2 = 8x8 tiles of the C2 generator, seeds 100..163.
+* V1  256^3 volume, 12 random ellipsoids + ramp, sigma=0.1 -- the 3-D extension (f4,
+      PAPER.md:310; not a BASELINE config: the C1 recipe lifted to a volume).
 
 Everything is drawn in float64 with ``numpy.random.default_rng(seed)`` (PCG64) and cast to
 float32 last; z is not clipped (reading C14).  Pixel (i, j) has its centre at integer
@@ -229,6 +231,64 @@ def make_image(cfg: Config | str):
             P[bi * B:(bi + 1) * B, bj * B:(bj + 1) * B] = Pb
         return z, P
     raise KeyError(cfg.name)
+
+
+@dataclass(frozen=True)
+class VolConfig:
+    name: str
+    D: int
+    H: int
+    W: int
+    seed: int
+    c1: float
+    c2: float
+    lam: float
+    theta: float
+    tau: float
+    iters: int
+    delta_rels: tuple
+    desc: str = ""
+
+
+VOL_CONFIGS = {
+    "V1": VolConfig("V1", 256, 256, 256, 11, 0.75, 0.25, 5.0, 0.1, 1.0 / 12.0, 200,
+                    (0.2, INF), "256^3, 12 ellipsoids + ramp, sigma 0.1 (3-D extension, f4)"),
+}
+
+
+def gen_ellipsoids(D, H, W, seed, n_ell=12, bg=0.25, fg=0.75, ramp=0.05, sigma=0.1,
+                   amin=8.0, amax=60.0):
+    """Volume recipe (V1): per ellipsoid semi-axes (a, b, c) ~ U[amin, amax], centre ~
+    U[0,D) x U[0,H) x U[0,W), a random rotation (three angles ~ U[0, pi)), value fg
+    (overwrite) on bg; a ramp +-ramp along j; N(0, sigma^2) noise.  float32 (D, H, W)."""
+    rng = np.random.default_rng(seed)
+    z = np.full((D, H, W), bg, dtype=np.float64)
+    kk = np.arange(D, dtype=np.float64)[:, None, None]
+    ii = np.arange(H, dtype=np.float64)[None, :, None]
+    jj = np.arange(W, dtype=np.float64)[None, None, :]
+    for _ in range(n_ell):
+        a, b, c = rng.uniform(amin, amax, size=3)
+        ck, ci, cj = rng.uniform(0, D), rng.uniform(0, H), rng.uniform(0, W)
+        al, be, ga = rng.uniform(0.0, math.pi, size=3)
+        ca, sa, cb, sb, cg, sg = (math.cos(al), math.sin(al), math.cos(be), math.sin(be),
+                                  math.cos(ga), math.sin(ga))
+        R = np.array([[ca, -sa, 0], [sa, ca, 0], [0, 0, 1]]) @ \
+            np.array([[cb, 0, sb], [0, 1, 0], [-sb, 0, cb]]) @ \
+            np.array([[1, 0, 0], [0, cg, -sg], [0, sg, cg]])
+        dk, di, dj = kk - ck, ii - ci, jj - cj
+        x = R[0, 0] * dk + R[1, 0] * di + R[2, 0] * dj
+        y = R[0, 1] * dk + R[1, 1] * di + R[2, 1] * dj
+        w = R[0, 2] * dk + R[1, 2] * di + R[2, 2] * dj
+        z[(x / a) ** 2 + (y / b) ** 2 + (w / c) ** 2 <= 1.0] = fg
+    z = z + ramp * (2.0 * jj / max(W - 1, 1) - 1.0)
+    z = z + rng.normal(0.0, sigma, size=(D, H, W))
+    return z.astype(np.float32)
+
+
+def make_volume(cfg: VolConfig | str):
+    if isinstance(cfg, str):
+        cfg = VOL_CONFIGS[cfg]
+    return gen_ellipsoids(cfg.D, cfg.H, cfg.W, cfg.seed)
 
 
 def band_delta(delta_rel: float, absmax_f: float) -> np.float32:

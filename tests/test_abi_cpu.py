@@ -21,7 +21,7 @@ def lib():
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "rds.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(rds_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|const char \*)\s*(rds3?_\w+)\s*\(", src, re.M)))
 
 
 def test_header_symbols_exported(lib):
@@ -30,7 +30,7 @@ def test_header_symbols_exported(lib):
     assert len(names) >= 20
     out = subprocess.run(["nm", "-D", "--defined-only", path], capture_output=True, text=True,
                          check=True).stdout
-    exported = set(re.findall(r"\bT (rds_\w+)", out))
+    exported = set(re.findall(r"\bT (rds3?_\w+)", out))
     missing = [n for n in names if n not in exported]
     assert not missing, missing
     from paper_1807_11534_b200 import rds
