@@ -249,6 +249,8 @@ typedef struct rds3_handle rds3_t;
 int rds3_create(int64_t D, int64_t H, int64_t W, rds3_t **out);
 int rds3_destroy(rds3_t *h);
 int rds3_set_stream(rds3_t *h, void *stream);
+/* planes per CTA z-chunk of k_vol_step (0 = automatic); a tuning knob, results identical */
+int rds3_set_kz(rds3_t *h, int32_t kz);
 int rds3_set_image(rds3_t *h, const float *z, int on_device);
 int rds3_set_fitting(rds3_t *h, float c1, float c2, float gamma, const float *P, int on_device);
 int rds3_fitting_absmax(rds3_t *h, float *out);

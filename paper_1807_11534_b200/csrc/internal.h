@@ -175,7 +175,7 @@ cudaError_t launch_compare(const float *u, const double *ugt, int64_t pitch, int
 
 // f4: 3-D volumes (k_vol.cu).  Padded volume: VOL_PZ frame planes before/after, VOL_PY_TOP
 // rows above and VOL_PY_BOT below each plane, VOL_PX_L columns left, >= VOL_PX_R right.
-constexpr int VOL_PZ = 2, VOL_PY_TOP = 2, VOL_PY_BOT = 16, VOL_PX_L = 4, VOL_PX_R = 32;
+constexpr int VOL_PZ = 2, VOL_PY_TOP = 2, VOL_PY_BOT = 32, VOL_PX_L = 4, VOL_PX_R = 32;
 struct VolArgs {
     const float *p1_in, *p2_in, *p3_in, *v_in, *c;   // voxel (0,0,0) origins
     float *p1_out, *p2_out, *p3_out, *v_out, *u_out;
@@ -194,6 +194,7 @@ struct VolSetupArgs {
     float c1, c2, gamma, delta, theta_lambda;
 };
 cudaError_t launch_vol_step(const VolArgs &a, bool write_u, cudaStream_t s);
+int64_t vol_tiles(int64_t H, int64_t W);  // CTA (i, j) tiles of k_vol_step
 cudaError_t launch_vol_setup(const VolSetupArgs &a, cudaStream_t s);
 cudaError_t launch_vol_absmax(const float *z, const float *P, int64_t plane, int64_t pitch,
                               int D, int H, int W, float c1, float c2, float gamma,

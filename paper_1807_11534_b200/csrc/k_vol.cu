@@ -4,8 +4,8 @@
 // zero last row / column / plane, div = -grad^T, rho = (rho1, rho2, rho3).
 //
 // Layout: padded volume, voxel (k, i, j) at origin + k * plane + i * pitch + j with 2 frame
-// planes before and after, 2 frame rows above and 16 below, 4 frame columns left and >= 32
-// right (a CTA window reaches 2 before its tile and up to 16 / 32 past the last image
+// planes before and after, 2 frame rows above and 32 below, 4 frame columns left and >= 32
+// right (a CTA window reaches 2 before its tile and up to VT_Y / 32 past the last image
 // row / column); the frame holds pinned background (rho = 0, v = 0, c' = +inf), so no load
 // is bounds-checked.  c' = 2^-100 theta*lambda*f on RD, -inf on Fg, +inf on Bg (as in 2-D).
 //
@@ -22,7 +22,10 @@
 
 namespace rds {
 
-constexpr int VT_X = 32, VT_Y = 16;          // threads per CTA (columns, rows)
+#ifndef RDS_VOL_TY
+#define RDS_VOL_TY 16
+#endif
+constexpr int VT_X = 32, VT_Y = RDS_VOL_TY;  // threads per CTA (columns, rows)
 constexpr int VO_X = VT_X - 3, VO_Y = VT_Y - 3;  // output tile (29 x 13)
 
 __device__ __forceinline__ float vsqrt(float x) {
@@ -59,10 +62,20 @@ __global__ void __launch_bounds__(VT_X * VT_Y) k_vol_step(const VolArgs a) {
     float pp3 = a.p3_in[(int64_t)(k0 - 2) * a.plane + col];
     float q3prev = 0.f;                                            // rho3 new at plane n-2
     int cur = 0;
+    // plane n+1 is loaded one step ahead (registers), so HBM latency hides behind a step
+    int64_t o_next = (int64_t)(k0 - 1) * a.plane + col;
+    float x1 = a.p1_in[o_next], x2 = a.p2_in[o_next], x3 = a.p3_in[o_next];
+    float xv = a.v_in[o_next], xc = a.c[o_next];
     for (int n = k0 - 1; n <= k1; ++n) {
-        const int64_t o = (int64_t)n * a.plane + col;
-        const float p1n = a.p1_in[o], p2n = a.p2_in[o], p3n = a.p3_in[o];
-        const float vn = a.v_in[o], cn = a.c[o];
+        const float p1n = x1, p2n = x2, p3n = x3, vn = xv, cn = xc;
+        if (n < k1) {
+            o_next += a.plane;
+            x1 = a.p1_in[o_next];
+            x2 = a.p2_in[o_next];
+            x3 = a.p3_in[o_next];
+            xv = a.v_in[o_next];
+            xc = a.c[o_next];
+        }
         s1[ty][tx] = p1n;
         s2[ty][tx] = p2n;
         __syncthreads();
@@ -183,6 +196,10 @@ __global__ void k_vol_copy(T *dst, const T *src, int64_t plane, int64_t pitch, i
         else
             dst[x] = src[o];
     }
+}
+
+int64_t vol_tiles(int64_t H, int64_t W) {
+    return ((W + VO_X - 1) / VO_X) * ((H + VO_Y - 1) / VO_Y);
 }
 
 cudaError_t launch_vol_step(const VolArgs &a, bool write_u, cudaStream_t s) {

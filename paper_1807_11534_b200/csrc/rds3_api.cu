@@ -31,7 +31,7 @@ struct rds3_handle {
     float gkey_tau = 0, gkey_theta = 0;
     bool have_image = false, have_fitting = false, solved = false;
     float c1 = 0, c2 = 0, gamma = 0;
-    int cur = 0, kz = 0, iters = 0;
+    int cur = 0, kz = 0, iters = 0, opt_kz = 0;
     std::string err;
     float *at(float *b) const { return b + origin; }
     uint8_t *at(uint8_t *b) const { return b + origin; }
@@ -150,6 +150,12 @@ static int vol_in(rds3_t *h, float *vol, const float *src, int on_device) {
     return RDS_OK;
 }
 
+int rds3_set_kz(rds3_t *h, int32_t kz) {
+    if (!h || kz < 0) return RDS_EINVAL;
+    h->opt_kz = kz;
+    return RDS_OK;
+}
+
 int rds3_set_image(rds3_t *h, const float *z, int on_device) {
     if (!h || !z) return fail3(h, RDS_EINVAL, "rds3_set_image: NULL argument");
     const int rc = vol_in(h, h->z, z, on_device);
@@ -237,10 +243,10 @@ int rds3_solve(rds3_t *h, float lambda, float theta, float tau, float delta, int
         return fail3(h, RDS_ESTATE, "rds3_solve: image and fitting must be set first");
     // z-chunk per CTA: enough CTAs for ~4 waves of 4 resident CTAs per SM, >= 8 planes
     {
-        const int64_t tiles = ((h->W + 28) / 29) * ((h->H + 12) / 13);
+        const int64_t tiles = vol_tiles(h->H, h->W);
         int64_t chunks = (148 * 16 + tiles - 1) / tiles;
-        int kz = (int)((h->D + chunks - 1) / chunks);
-        if (kz < 8) kz = 8;
+        int kz = h->opt_kz > 0 ? h->opt_kz : (int)((h->D + chunks - 1) / chunks);
+        if (kz < 8 && h->opt_kz <= 0) kz = 8;
         if (kz > h->D) kz = (int)h->D;
         h->kz = kz;
     }

@@ -32,7 +32,8 @@ EXPORTS = (
     "rds_get_active_tiles", "rds_tile_shape", "rds_energy", "rds_get_stats",
     "rds_kfuse_supported", "rds_last_error", "rds_version", "rds_band_for_fraction",
     "rds_solve_q", "rds_solve_tol", "rds_solve_gt", "rds_get_u_gt", "rds_compare_gt",
-    "rds3_create", "rds3_destroy", "rds3_set_stream", "rds3_set_image", "rds3_set_fitting",
+    "rds3_create", "rds3_destroy", "rds3_set_stream", "rds3_set_kz", "rds3_set_image",
+    "rds3_set_fitting",
     "rds3_fitting_absmax", "rds3_solve", "rds3_get_u", "rds3_get_v", "rds3_get_p",
     "rds3_get_mask", "rds3_get_labels", "rds3_get_stats", "rds3_last_error",
 )
@@ -112,6 +113,7 @@ def _load():
         "rds3_create": [i64, i64, i64, ctypes.POINTER(P)],
         "rds3_destroy": [P],
         "rds3_set_stream": [P, P],
+        "rds3_set_kz": [P, i32],
         "rds3_set_image": [P, P, i],
         "rds3_set_fitting": [P, f, f, f, P, i],
         "rds3_fitting_absmax": [P, ctypes.POINTER(f)],
@@ -470,6 +472,9 @@ class Solver3:
             self.close()
         except Exception:
             pass
+
+    def set_kz(self, kz):
+        _check3(_lib.rds3_set_kz(self.h, int(kz)), self.h)
 
     def set_image(self, z):
         p, dev, _k = _buf(z, np.float32, self.shape)

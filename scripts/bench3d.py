@@ -18,6 +18,7 @@ from paper_1807_11534_b200 import workloads as wl  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="V1")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--kz", default="0", help="comma list of planes per z-chunk (0 = auto)")
 args = ap.parse_args()
 cfg = wl.VOL_CONFIGS[args.config]
 z = wl.make_volume(cfg)
@@ -29,7 +30,8 @@ am = s.absmax()
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
 n = cfg.D * cfg.H * cfg.W
-for dr in cfg.delta_rels:
+for kz, dr in [(int(k), dr) for k in args.kz.split(",") for dr in cfg.delta_rels]:
+    s.set_kz(kz)
     d = wl.band_delta(dr, am)
     s.solve(cfg.lam, cfg.theta, cfg.tau, d, cfg.iters)  # warm (graph capture)
     ts = []
