@@ -75,10 +75,13 @@ class Dist:
         self.local = int(os.environ.get("LOCAL_RANK", "0"))
         self.pg = None
         if self.world > 1:
+            import torch
             import torch.distributed as dist
 
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             backend = "nccl" if _cuda() else "gloo"
+            if _cuda():
+                torch.cuda.set_device(self.local)  # bind this rank's GPU before NCCL init
             dist.init_process_group(backend)
             self.pg = dist
 
