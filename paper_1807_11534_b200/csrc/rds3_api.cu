@@ -156,11 +156,32 @@ int rds3_set_kz(rds3_t *h, int32_t kz) {
     return RDS_OK;
 }
 
+// 1 if every value of a padded volume (frame included: zeros) is finite
+static int vol_finite(rds3_t *h, const float *vol, bool *ok) {
+    int *flag = nullptr;
+    CK3(h, cudaMalloc(&flag, sizeof(int)));
+    int bad = 0;
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), h->stream);
+    if (e == cudaSuccess)
+        e = launch_check_finite(vol, h->pitch, (int)(h->vol / h->pitch), (int)h->pitch, flag,
+                                h->stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFree(flag);
+    CK3(h, e);
+    *ok = bad == 0;
+    return RDS_OK;
+}
+
 int rds3_set_image(rds3_t *h, const float *z, int on_device) {
     if (!h || !z) return fail3(h, RDS_EINVAL, "rds3_set_image: NULL argument");
-    const int rc = vol_in(h, h->z, z, on_device);
+    int rc = vol_in(h, h->z, z, on_device);
     if (rc) return rc;
-    h->have_image = true;
+    bool ok = true;
+    if ((rc = vol_finite(h, h->z, &ok))) return rc;
+    h->have_image = ok;
+    if (!ok) return fail3(h, RDS_EINVAL, "rds3_set_image: non-finite values");
     return RDS_OK;
 }
 
@@ -174,8 +195,14 @@ int rds3_set_fitting(rds3_t *h, float c1, float c2, float gamma, const float *P,
             CK3(h, cudaMalloc(&h->P, sizeof(float) * h->vol));
             CK3(h, cudaMemsetAsync(h->P, 0, sizeof(float) * h->vol, h->stream));
         }
-        const int rc = vol_in(h, h->P, P, on_device);
+        int rc = vol_in(h, h->P, P, on_device);
         if (rc) return rc;
+        bool ok = true;
+        if ((rc = vol_finite(h, h->P, &ok))) return rc;
+        if (!ok) {
+            h->have_fitting = false;
+            return fail3(h, RDS_EINVAL, "rds3_set_fitting: P has non-finite values");
+        }
     }
     h->c1 = c1;
     h->c2 = c2;

@@ -114,3 +114,29 @@ def test_vol_v1_sampled(rds, orc):
     u0 = (f <= 0).astype(np.float32)
     assert np.array_equal(g["u"][off], u0[off]) and np.array_equal(g["v"][off], u0[off])
     assert not g["p3"][-1].any() and not g["p1"][:, -1].any() and not g["p2"][:, :, -1].any()
+
+
+def test_vol_errors(rds):
+    s = rds.Solver3(4, 5, 6)
+    z = np.zeros((4, 5, 6), np.float32)
+    with pytest.raises(rds.RdsError) as ei:
+        s.u()
+    assert ei.value.code == rds.RDS_ESTATE
+    with pytest.raises(rds.RdsError) as ei:
+        s.solve(1.0, 0.1, 0.125, 0.5, 10)  # no image yet
+    assert ei.value.code == rds.RDS_ESTATE
+    z[1, 2, 3] = np.nan
+    with pytest.raises(rds.RdsError) as ei:
+        s.set_image(z)
+    assert ei.value.code == rds.RDS_EINVAL
+    z[1, 2, 3] = 0.5
+    s.set_image(z)
+    s.set_fitting(0.75, 0.25)
+    with pytest.raises(rds.RdsError) as ei:
+        s.solve(1.0, 0.1, 0.125, 0.5, 10)  # tau > 1/12 in 3-D
+    assert ei.value.code == rds.RDS_EINVAL
+    with pytest.raises(rds.RdsError):
+        s.set_fitting(0.5, 0.5)
+    s.solve(1.0, 0.1, 1 / 12, 0.5, 10)
+    assert s.u().shape == (4, 5, 6)
+    s.close()
