@@ -493,7 +493,8 @@ def test_solve_tol_configs(rds, orc, name, lam, dr, tol, m, norm):
 
 @pytest.mark.parametrize("m,kf,max_iters,tol", [(1, 7, 23, 0.1), (3, 2, 31, 0.0),
                                                (9, 4, 50, 0.2), (7, 7, 45, 0.0),
-                                               (7, 7, 3000, 0.05), (2, 5, 4001, 0.05)])
+                                               (7, 7, 3000, 0.05), (2, 5, 4001, 0.05),
+                                               (10, 7, 7, 0.0)])
 def test_solve_tol_schedules(rds, orc, m, kf, max_iters, tol):
     """Single-stage CHECK launches (u^(l-1) from the u plane), blocks split across launches,
     max_iters off the check grid, tol = 0 (runs to max_iters, converged = 0), ragged shape."""
@@ -564,4 +565,23 @@ def test_compare_gt_e1_e2(rds, orc):
         assert abs(e2 - orc.l2_error(u, ug)) <= 1e-9 * max(1.0, e2), (q, e2)
         if q == 1.0:
             assert e1 == 1.0
+    s.close()
+
+
+def test_solve_tol_c3_full_size(rds, orc):
+    """The tolerance path (graph while loop, CHECK launches, per-item sums) at the headline
+    size in the bench's launch configuration: tol = 0 runs all 63 iterations (9 checks)."""
+    cfg = wl.CONFIGS["C3"]
+    z, P = wl.make_image(cfg)
+    f = orc.fitting(z, cfg.c1, cfg.c2)
+    delta = wl.band_delta(0.2, orc.absmax(f))
+    s = rds.Solver(cfg.H, cfg.W)
+    s.set_image(z)
+    s.set_fitting(cfg.c1, cfg.c2)
+    st = s.solve_tol(5.0, cfg.theta, cfg.tau, delta, 63, 0.0)
+    assert st["iters"] == 63 and st["converged"] == 0 and st["check_every"] == 7
+    o = orc.solve_tol(f, delta, 5.0, np.float32(cfg.theta), cfg.tau, 63, 0.0, 7)
+    assert abs(st["residual"] - o["residual"]) <= 2e-2 * o["residual"]
+    p1, p2 = s.p()
+    compare(dict(u=s.u(), v=s.v(), p1=p1, p2=p2, mask=s.mask()), o, ctx="C3 tol")
     s.close()
