@@ -685,13 +685,16 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     const int max_items = n_strips * (int)((h->H + ITEM_Q - 1) / ITEM_Q);
     const int fixed_chunk = h->opt_rows;  // rows (rounded up to ITEM_Q on the device)
     const int launches = make_plan(kf, iters, check_every, nullptr, 0);
+    // work counters: one per launch of the static plan; a tolerance graph also needs the
+    // counters of its loop body (up to two check blocks) besides those of its tail
+    const int n_queue = launches + 1 + (check_every > 0 ? 2 * ((check_every + kf - 1) / kf) : 0);
     {
         void *pf = h->band_flag, *pi = h->items, *pq = h->queue;
         const bool realloc_items = sizeof(Item) * (size_t)max_items > h->items_bytes;
-        const bool realloc_queue = sizeof(int32_t) * (size_t)(launches + 1) > h->queue_bytes;
+        const bool realloc_queue = sizeof(int32_t) * (size_t)n_queue > h->queue_bytes;
         CK(h, grow(&pf, &h->band_bytes, sizeof(int32_t) * (size_t)n_strips * n_bands));
         CK(h, grow(&pi, &h->items_bytes, sizeof(Item) * (size_t)max_items));
-        CK(h, grow(&pq, &h->queue_bytes, sizeof(int32_t) * (size_t)(launches + 1)));
+        CK(h, grow(&pq, &h->queue_bytes, sizeof(int32_t) * (size_t)n_queue));
         h->band_flag = (int32_t *)pf;
         h->items = (Item *)pi;
         h->queue = (int32_t *)pq;

@@ -123,7 +123,7 @@ def test_vol_errors(rds):
         s.u()
     assert ei.value.code == rds.RDS_ESTATE
     with pytest.raises(rds.RdsError) as ei:
-        s.solve(1.0, 0.1, 0.125, 0.5, 10)  # no image yet
+        s.solve(1.0, 0.1, 1 / 12, 0.5, 10)  # no image yet
     assert ei.value.code == rds.RDS_ESTATE
     z[1, 2, 3] = np.nan
     with pytest.raises(rds.RdsError) as ei:
