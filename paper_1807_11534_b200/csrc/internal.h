@@ -11,7 +11,7 @@
 // The stencil's state planes (rho1, rho2, v in both ping-pong buffers, and c) are
 // QUAD-SWIZZLED: within every aligned quad of columns 4g..4g+3 the memory order is
 // x0 x2 x1 x3 (swap of index bits 0 and 1), so one 16-byte load gives the packed f32x2
-// pairs (x0, x2), (x1, x3) the stencil computes on (k_stencil.cu).  PAD_C is a multiple of
+// pairs (x0, x2), (x1, x3) the stencil computes on (k_stencil_impl.cuh).  PAD_C is a multiple of
 // 4, so the swizzle applies to the column index relative to the origin.  z, P, f, u, the
 // labels and the mask are natural-order planes.
 #pragma once
@@ -131,7 +131,7 @@ cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_ban
                                int slots, int fixed_chunk, int warmup_rows, Item *items,
                                int32_t *counts, cudaStream_t s);
 
-// mode: 0 iterate, 1 + write u and mask, 2 + stopping sums into a.chk (k_stencil.cu)
+// mode: 0 iterate, 1 + write u and mask, 2 + stopping sums into a.chk (k_stencil_impl.cuh)
 cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a,
                            int grid, cudaStream_t s);
 int stencil_blocks_per_sm(int kf, int stages, bool aligned);

@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(256) k_setup(SetupArgs a) {
                 lab[e] = rd ? 2 : (fg ? 1 : 0);
                 // RD: theta*lambda*f clamped to +-2^20 (the v-step saturates far earlier:
                 // |u| <= max|v| + 4 theta) and stored as c' = c * 2^-100, so |c'| <= 2^-80
-                // is negligible under the stencil's square root (k_stencil.cu, stage()).
+                // is negligible under the stencil's square root (k_stencil_impl.cuh, stage()).
                 c[e] = rd ? __fmul_rn(fminf(fmaxf(__fmul_rn(a.theta_lambda, fe), -0x1p20f),
                                             0x1p20f),
                                       0x1p-100f)

@@ -1,0 +1,497 @@
+// k_stencil_impl.cuh -- K3, the hot loop of librds (included by k_stencil.cu, the dispatch,
+// and by the per-k_fuse instantiation units k_stencil_kf*.cu, which build in parallel):
+// S fused outer iterations of the restricted-
+// domain dual iteration per HBM round trip (temporal blocking), sm_100a.
+//
+// One outer iteration (PAPER.md:58-70 alternation, restricted forms Eq. 7-9):
+//   w   = div rho - v/theta                                   (reading R-C5)
+//   rho = (rho + tau grad w) / (1 + tau |grad w|) on RD, 0 on Fg u Bg
+//   u   = v - theta div rho on RD, u0 elsewhere
+//   v   = min(max(u - theta lambda f, 0), 1) on RD, u0 elsewhere
+// with grad = forward differences (zero on row H-1 / column W-1) and div = -grad^T
+// (reading R-C6).  The label and theta*lambda*f are folded into one float per pixel,
+// c' = 2^-100 theta*lambda*f on RD, -inf on Fg, +inf on Bg and on the frame, so
+// sat(u - c) = FFMA.SAT(c', -2^100, u) reproduces the pinned u0 exactly, and |c'| added
+// under the square root of |grad w| makes rho's update factor exactly 0 off RD.
+//
+// Execution model.  Each warp owns one work item: a strip of 128 columns
+// (4 per lane, float4 loads/stores, 512 B per row per array) of which WV = wv_of(KF) are
+// output columns, marching down the rows of a chunk.  The S iterations are a software
+// pipeline in registers: stage t consumes level t-1 at row m+1 and emits level t at row m,
+// so each input row is read once from HBM and each output row written once per S
+// iterations.  Horizontal neighbours come from warp shuffles (2 per stage per row); the
+// dependency cone (KF+1 columns/rows behind, KF ahead) is recomputed redundantly at the
+// strip and chunk edges instead of being exchanged.
+//
+// All per-pixel arithmetic is packed f32x2 (FFMA2 / FADD2 / FMUL2) on quad-swizzled data
+// (see "Packed-pair arithmetic" below); only the two MUFU ops and the saturating v-step are
+// scalar.
+//
+// Stage state per pixel (level t-1 at the stage's row m): rho1, rho2, v, w.  rho1 of
+// level t at row m-1 (needed by div) is the next stage's rho1 state, so it is not stored
+// twice.  The row loop is unrolled by two with two state sets (A -> B, B -> A) so the
+// per-row state shift is register renaming, not moves.
+#pragma once
+#include <math.h>
+
+#include "internal.h"
+
+namespace rds {
+
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------------------------------------------
+// Packed-pair arithmetic.  sm_100a issues FFMA2 / FADD2 / FMUL2 (PTX f32x2): one instruction
+// does the same fp32 operation, with the same round-to-nearest result, on two lanes of a
+// register pair.  The FMA pipe's lane throughput is unchanged (measured: FFMA2 issues at
+// half the FFMA rate, scripts/micro/ffma2_tput.cu), but every packed op frees an issue slot,
+// and this kernel is bound by instruction issue.
+//
+// A lane owns 4 consecutive columns x0..x3 of its strip.  The state planes rho1, rho2, v
+// and c are stored QUAD-SWIZZLED in HBM (memory order x0 x2 x1 x3 within every aligned
+// quad, internal.h), so one 16-byte load yields the pairs a = (x0, x2) and b = (x1, x3).
+// With that pairing every horizontal difference is a pair op: x(j+1) - x(j) is b - a for
+// the a pair and (x2, x4) - b for the b pair, where x2 = a.y and x4 comes from the next
+// lane; the left neighbours for div are (x(-1), x1) and a.
+// ---------------------------------------------------------------------------------------
+struct Q {
+    float2 a, b;  // a = (x0, x2), b = (x1, x3)
+};
+__device__ __forceinline__ float2 add2(float2 x, float2 y) { return __fadd2_rn(x, y); }
+__device__ __forceinline__ float2 sub2(float2 x, float2 y) {
+    return __fadd2_rn(x, make_float2(-y.x, -y.y));  // FADD2 with a negated operand
+}
+__device__ __forceinline__ float2 mul2(float2 x, float2 y) { return __fmul2_rn(x, y); }
+__device__ __forceinline__ float2 mul2(float2 x, float s) { return __fmul2_rn(x, make_float2(s, s)); }
+__device__ __forceinline__ float2 fma2(float2 x, float2 y, float2 z) { return __ffma2_rn(x, y, z); }
+__device__ __forceinline__ float2 fma2(float2 x, float s, float2 z) {
+    return __ffma2_rn(x, make_float2(s, s), z);
+}
+__device__ __forceinline__ float2 fma2(float2 x, float s, float t) {
+    return __ffma2_rn(x, make_float2(s, s), make_float2(t, t));
+}
+__device__ __forceinline__ float2 absq(float2 x) {  // folds into the FFMA2 operand as |R|
+    return make_float2(fabsf(x.x), fabsf(x.y));
+}
+__device__ __forceinline__ Q ldq(const float4 &m) {
+    return Q{make_float2(m.x, m.y), make_float2(m.z, m.w)};
+}
+__device__ __forceinline__ void stq(float *p, const Q &x) {  // swizzled store
+    *reinterpret_cast<float4 *>(p) = make_float4(x.a.x, x.a.y, x.b.x, x.b.y);
+}
+__device__ __forceinline__ Q zeroq() {
+    return Q{make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
+}
+
+// Input rows are staged in shared memory with cp.async (LDGSTS): a RING of slots per warp
+// for rho1, rho2, v (3 planes x 32 lanes x float4 = 1.5 KB per row) and a c ring that every
+// stage re-reads at its own (lagging) row instead of carrying c in registers.  The c ring
+// keeps each row twice (slots r mod CR and r mod CR + CR), so the row n-L of stage t is at a
+// compile-time offset -L from row n's upper copy: no index arithmetic per stage.  Every lane
+// copies and later reads only its own 16-byte pieces, so no cross-lane synchronisation is
+// needed (cp.async.wait_group is per-thread).
+constexpr int RING = 4;   // rows of rho1/rho2/v in flight (power of two)
+constexpr int CR = 16;    // rows of c kept (power of two; >= RING + KF + 3)
+constexpr int STENCIL_SMEM = STENCIL_WARPS * (RING * 96 + 2 * CR * 32) * (int)sizeof(float4);
+
+// Pipeline split: the S stages are cut into NS+1 chains ([0, sp(1)), [sp(1), sp(2)), ...)
+// joined through one-row delay buffers, so within one row step the chains are independent
+// dependency chains (instruction-level parallelism for 16 registers per extra chain).  Three
+// chains for S >= 6 measured best (RDS_CHAINS overrides for experiments).
+#ifndef RDS_CHAINS
+#define RDS_CHAINS 3
+#endif
+template <int S>
+struct Split {
+    static constexpr int NS = S >= 3 * RDS_CHAINS - 3 && RDS_CHAINS >= 3 ? RDS_CHAINS - 1
+                              : S >= 4                                 ? 1
+                                                                       : 0;
+    // k-th split point, k = 1..NS
+    __host__ __device__ static constexpr int sp(int k) { return (k * S) / (NS + 1); }
+    // number of split points <= t (the extra row lag of stage t)
+    __host__ __device__ static constexpr int lag(int t) {
+        int n = 0;
+        for (int k = 1; k <= NS; ++k) n += sp(k) <= t;
+        return n;
+    }
+    // k if t == sp(k), else 0
+    __host__ __device__ static constexpr int at(int t) {
+        for (int k = 1; k <= NS; ++k)
+            if (sp(k) == t) return k;
+        return 0;
+    }
+};
+
+template <int S>
+struct PipeState {
+    static constexpr int ND = Split<S>::NS > 0 ? Split<S>::NS : 1;
+    Q p1[S], p2[S], v[S], w[S];
+    Q q1;                                  // rho1 of the last level at the previous emitted row
+    Q d1[ND], d2[ND], dv[ND], dd[ND];      // delay buffers (chain-boundary outputs, one row back)
+};
+
+struct Ctx {
+    const float *p1i, *p2i, *vi, *ci;
+    float *p1o, *p2o, *vo, *uo;
+    uint8_t *mo;
+    float4 *ring;   // this lane's slot 0, plane 0; slot stride 96 float4, plane stride 32
+    float4 *cring;  // this lane's c slot 0; slot stride 32 float4, 2*CR slots
+    int64_t pitch;
+    int col, H, R0, Rend, n_last;
+    bool store_lane, right_edge;
+    Q kx;
+    float tau, theta, inv_theta;
+};
+
+__device__ __forceinline__ void stage_row(const Ctx &x, int r) {
+    const int rr = r & (RING - 1);  // two's complement: also right for r < 0
+    const int rc = r & (CR - 1);
+    float4 *slot = x.ring + rr * 96;
+    const int64_t off = (int64_t)r * x.pitch;
+    cp_async16(slot, x.p1i + off);
+    cp_async16(slot + 32, x.p2i + off);
+    cp_async16(slot + 64, x.vi + off);
+    cp_async16(x.cring + rc * 32, x.ci + off);
+    cp_async16(x.cring + (rc + CR) * 32, x.ci + off);
+}
+
+// rr = 1 / (1 + tau sqrt(s)) per element: two MUFU ops each, the FMA in between packed.
+__device__ __forceinline__ float2 rr_of(float2 s, float tau) {
+    const float2 den = fma2(make_float2(sqrt_approx(s.x), sqrt_approx(s.y)), tau, 1.0f);
+    return make_float2(rcp_approx(den.x), rcp_approx(den.y));
+}
+
+// div rho at the lane's quad from rho1 (this row and the row above) and rho2 (this row);
+// the left neighbour of x0 is the previous lane's x3.
+__device__ __forceinline__ Q div_q(const Q &p1, const Q &p1up, const Q &p2) {
+    const float l2 = __shfl_up_sync(0xffffffffu, p2.b.y, 1);
+    Q d;
+    d.a = add2(sub2(p1.a, p1up.a), sub2(p2.a, make_float2(l2, p2.b.x)));
+    d.b = add2(sub2(p1.b, p1up.b), sub2(p2.b, p2.a));
+    return d;
+}
+
+// Front half of a stage: w at row m+1 from the incoming row (inv, ind = div rho there), the
+// gradient at row m from the state w (aw), and rr = 1 / (1 + tau |grad w|).
+struct Front {
+    Q w, g1, g2, rr;
+};
+template <bool ALIGNED, bool LAST>
+__device__ __forceinline__ Front front(const Q &aw, const Q &inv, const Q &ind, const Q &c, int m,
+                                       const Ctx &x) {
+    constexpr unsigned FULL = 0xffffffffu;
+    Front f;
+    f.w.a = fma2(inv.a, -x.inv_theta, ind.a);
+    f.w.b = fma2(inv.b, -x.inv_theta, ind.b);
+    float wr = __shfl_down_sync(FULL, aw.a.x, 1);  // x4 of this lane = x0 of the next
+    if (ALIGNED && x.right_edge) wr = aw.b.y;      // grad_2 = 0 on column W-1
+    f.g1.a = sub2(f.w.a, aw.a);
+    f.g1.b = sub2(f.w.b, aw.b);
+    if (LAST && m == x.H - 1) f.g1 = zeroq();      // grad_1 = 0 on row H-1
+    f.g2.a = sub2(aw.b, aw.a);
+    f.g2.b = sub2(make_float2(aw.a.y, wr), aw.b);
+    if (!ALIGNED) {
+        f.g2.a = mul2(f.g2.a, x.kx.a);
+        f.g2.b = mul2(f.g2.b, x.kx.b);
+    }
+    // |grad w|^2 + |c'|: |c'| is +inf off RD (rr = 0) and <= 2^-80 on RD (see stage())
+    f.rr.a = rr_of(fma2(f.g1.a, f.g1.a, fma2(f.g2.a, f.g2.a, absq(c.a))), x.tau);
+    f.rr.b = rr_of(fma2(f.g1.b, f.g1.b, fma2(f.g2.b, f.g2.b, absq(c.b))), x.tau);
+    return f;
+}
+
+// Back half at row m: the rho update (Eq. 8 fixed point), then, with q1 = rho1 of the new
+// level at row m-1, div rho (od, exactly what the next stage's w needs), the u-step (Eq. 7)
+// and the v-step (Eq. 9).
+template <bool WRITE_U>
+__device__ __forceinline__ void back(const Q &g1, const Q &g2, const Q &rr, const Q &ap1,
+                                     const Q &ap2, const Q &av, const Q &q1, const Q &c,
+                                     const Ctx &x, Q &o1, Q &o2, Q &ov, Q &od, Q &ou) {
+    o1.a = mul2(fma2(g1.a, x.tau, ap1.a), rr.a);
+    o2.a = mul2(fma2(g2.a, x.tau, ap2.a), rr.a);
+    o1.b = mul2(fma2(g1.b, x.tau, ap1.b), rr.b);
+    o2.b = mul2(fma2(g2.b, x.tau, ap2.b), rr.b);
+    od = div_q(o1, q1, o2);
+    Q u;
+    u.a = fma2(od.a, -x.theta, av.a);
+    u.b = fma2(od.b, -x.theta, av.b);
+    ov.a = make_float2(__saturatef(fmaf(c.a.x, -0x1p100f, u.a.x)),
+                       __saturatef(fmaf(c.a.y, -0x1p100f, u.a.y)));
+    ov.b = make_float2(__saturatef(fmaf(c.b.x, -0x1p100f, u.b.x)),
+                       __saturatef(fmaf(c.b.y, -0x1p100f, u.b.y)));
+    if (WRITE_U) {
+        ou.a = make_float2(fabsf(c.a.x) < INFINITY ? u.a.x : av.a.x,
+                           fabsf(c.a.y) < INFINITY ? u.a.y : av.a.y);
+        ou.b = make_float2(fabsf(c.b.x) < INFINITY ? u.b.x : av.b.x,
+                           fabsf(c.b.y) < INFINITY ? u.b.y : av.b.y);
+    }
+}
+
+// One stage: consumes level t at row m+1 (in1, in2, inv and ind = div rho there, computed
+// once by the stage that emitted the row), uses the stage state (level t at row m) and q1
+// (rho1 of level t+1 at row m-1), emits level t+1 at row m (o1, o2, ov, od) and the new
+// state (level t at row m+1).
+//
+// c is stored as c' = c * 2^-100 (K1; exact for |c| >= 2^-26, within 2^-50 absolute below):
+// |c'| <= 2^-80 on RD (|c| <= 2^20) is far below the fp32 resolution of |grad w|^2 and +inf
+// off RD, where adding it under the square root makes the rho update factor exactly 0
+// (rho = 0 on Fg u Bg, Eq. 8) without predicates or extra instructions (|c'| is an FFMA2
+// operand modifier); u - c = fma(c', -2^100, u) exactly, and FFMA.SAT reproduces the pinned
+// 0 / 1 off RD (Eq. 9).
+template <bool WRITE_U, bool ALIGNED, bool LAST>
+__device__ __forceinline__ void stage(const Q &ap1, const Q &ap2, const Q &av, const Q &aw,
+                                      const Q &q1, const Q &in1, const Q &in2, const Q &inv,
+                                      const Q &ind, const float4 &c4, int m, const Ctx &x,
+                                      Q &bp1, Q &bp2, Q &bv, Q &bw, Q &o1, Q &o2, Q &ov, Q &od,
+                                      Q &ou) {
+    const Q c = ldq(c4);
+    const Front f = front<ALIGNED, LAST>(aw, inv, ind, c, m, x);
+    back<WRITE_U>(f.g1, f.g2, f.rr, ap1, ap2, av, q1, c, x, o1, o2, ov, od, ou);
+    bp1 = in1;
+    bp2 = in2;
+    bv = inv;
+    bw = f.w;
+}
+
+// Launch modes: PLAIN iterates; WRITE_U also writes u and the mask of the last level
+// (the last launch of a solve); CHECK additionally accumulates the paper's stopping
+// quantities sum (u^l - u^(l-1))^2 and sum (v^l - v^(l-1))^2 over the item's output pixels
+// (f2, rds_solve_tol).  u^(l-1) comes from stage S-2 one row step earlier,
+// or, for a single-stage launch, from the u plane written by the previous launch.
+enum { MODE_PLAIN = 0, MODE_WRITE_U = 1, MODE_CHECK = 2 };
+
+template <int S, int MODE>
+struct Extra {  // per-row-step state only the CHECK mode needs
+    Q uprev;    // u of level S-1 (stage S-2's u) at the last stage's row
+};
+
+// One row step: consume input row n from the ring, advance all S stages, store the level-S
+// row if it is an output row of this item, then refill the slot with row n+RING.
+template <int S, int MODE, bool ALIGNED, bool LAST>
+__device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B,
+                                          const Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
+                                          const Ctx &x, float &acc_u, float &acc_v) {
+    using SPL = Split<S>;
+    constexpr bool WRITE_U = MODE != MODE_PLAIN;
+    cp_async_wait<RING - 1>();
+    const float4 *slot = x.ring + (n & (RING - 1)) * 96;
+    const float4 *crow = x.cring + ((n & (CR - 1)) + CR) * 32;  // row n; row n-L at -32 L
+    Q in1 = ldq(slot[0]), in2 = ldq(slot[32]), inv = ldq(slot[64]);
+    // div rho of the incoming row (level 0): rho1 of row n-1 is stage 0's rho1 state
+    Q ind = div_q(in1, A.p1[0], in2);
+    Q uu;
+#pragma unroll
+    for (int t = 0; t < S; ++t) {
+        const int m = n - t - 1 - SPL::lag(t);  // row emitted (level t+1)
+        Q o1, o2, ov, od;
+        if (SPL::at(t)) {  // a new chain starts from its delay buffer
+            const int k = SPL::at(t) - 1;
+            B.d1[k] = in1;
+            B.d2[k] = in2;
+            B.dv[k] = inv;
+            B.dd[k] = ind;
+            in1 = A.d1[k];
+            in2 = A.d2[k];
+            inv = A.dv[k];
+            ind = A.dd[k];
+        }
+        const Q &q1 = (t == S - 1)          ? A.q1
+                      : SPL::at(t + 1)      ? A.d1[SPL::at(t + 1) > 0 ? SPL::at(t + 1) - 1 : 0]
+                                            : A.p1[(t + 1 < S) ? t + 1 : 0];
+        const float4 c4 = crow[-32 * (n - m)];  // n - m is a compile-time lag
+        stage<WRITE_U, ALIGNED, LAST>(A.p1[t], A.p2[t], A.v[t], A.w[t], q1, in1, in2, inv, ind,
+                                      c4, m, x, B.p1[t], B.p2[t], B.v[t], B.w[t], o1, o2, ov, od,
+                                      uu);
+        in1 = o1;
+        in2 = o2;
+        inv = ov;
+        ind = od;
+        if (MODE == MODE_CHECK && S >= 2 && t == S - 2) EB.uprev = uu;  // u^(l-1), row m
+        if (t == S - 1) {
+            B.q1 = o1;
+            if (x.store_lane && m >= x.R0 && m < x.Rend) {
+                const int64_t o = (int64_t)m * x.pitch + x.col;
+                if (MODE == MODE_CHECK) {
+                    Q up;
+                    if (S >= 2) {
+                        up = EA.uprev;
+                    } else {  // single stage: u^(l-1) is in the u plane (natural order)
+                        const float4 q = *reinterpret_cast<const float4 *>(x.uo + o);
+                        up = Q{make_float2(q.x, q.z), make_float2(q.y, q.w)};
+                    }
+                    const float2 da = sub2(uu.a, up.a), db = sub2(uu.b, up.b);
+                    const Q &av = A.v[S - 1];  // v^(l-1) at row m
+                    const float2 ea = sub2(ov.a, av.a), eb = sub2(ov.b, av.b);
+                    acc_u += (da.x * da.x + da.y * da.y) + (db.x * db.x + db.y * db.y);
+                    acc_v += (ea.x * ea.x + ea.y * ea.y) + (eb.x * eb.x + eb.y * eb.y);
+                }
+                stq(x.p1o + o, o1);
+                stq(x.p2o + o, o2);
+                stq(x.vo + o, ov);
+                if (WRITE_U) {  // u and the mask are natural-order planes
+                    *reinterpret_cast<float4 *>(x.uo + o) =
+                        make_float4(uu.a.x, uu.b.x, uu.a.y, uu.b.y);
+                    *reinterpret_cast<uchar4 *>(x.mo + o) =
+                        make_uchar4(uu.a.x > 0.5f, uu.b.x > 0.5f, uu.a.y > 0.5f, uu.b.y > 0.5f);
+                }
+            }
+        }
+    }
+    // refill the slot just consumed (its values are in registers and already used)
+    if (n + RING <= x.n_last) stage_row(x, n + RING);
+    cp_async_commit();
+}
+
+template <int S, int MODE, bool ALIGNED, bool LAST>
+__device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &acc_v) {
+    PipeState<S> A, B;
+    Extra<S, MODE> EA, EB;
+#pragma unroll
+    for (int t = 0; t < S; ++t) A.p1[t] = A.p2[t] = A.v[t] = A.w[t] = zeroq();
+    A.q1 = zeroq();
+#pragma unroll
+    for (int k = 0; k < PipeState<S>::ND; ++k) {
+        A.d1[k] = A.d2[k] = A.dv[k] = A.dd[k] = zeroq();
+    }
+    EA.uprev = zeroq();
+    for (; n <= x.n_last; n += 2) {
+        pipe_step<S, MODE, ALIGNED, LAST>(A, B, EA, EB, n, x, acc_u, acc_v);
+        pipe_step<S, MODE, ALIGNED, LAST>(B, A, EB, EA, n + 1, x, acc_u, acc_v);
+    }
+}
+
+// Two CTAs (8 warps) per SM: shared memory (88 KB per CTA) and registers both allow 2.
+template <int S>
+struct MinBlocks {
+    static constexpr int value = 2;
+};
+
+template <int KF, int S, int MODE, bool ALIGNED>
+__global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
+    k_stencil(const StencilArgs a) {
+    static_assert(S >= 1 && S <= KF && KF + 3 <= PAD_R, "stage count");
+    static_assert(RING + KF + 3 <= CR, "c ring too short for the stage lags");
+    constexpr int LH = lh_of(KF), WV = wv_of(KF);
+    extern __shared__ float4 smem[];  // [warps][RING][3][32] then [warps][2 CR][32]
+    // tolerance mode: once the stopping rule has fired, the remaining launches are no-ops
+    if (a.stop != nullptr && *(volatile const int32_t *)&a.stop->flag != 0) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int n_items = *a.n_items;
+    Ctx x;
+    x.pitch = a.pitch;
+    x.H = a.H;
+    x.tau = a.tau;
+    x.theta = a.theta;
+    x.inv_theta = a.inv_theta;
+    x.p1o = a.p1_out;
+    x.p2o = a.p2_out;
+    x.vo = a.v_out;
+    x.uo = a.u_out;
+    x.mo = a.mask_out;
+    x.ring = smem + warp * RING * 96 + lane;
+    x.cring = smem + STENCIL_WARPS * RING * 96 + warp * 2 * CR * 32 + lane;
+    // persistent warps: fetch items from this launch's queue until it is drained
+    for (;;) {
+        int it = 0;
+        if (lane == 0) it = atomicAdd(a.queue, 1);
+        it = __shfl_sync(0xffffffffu, it, 0);
+        if (it >= n_items) break;  // warp-uniform
+        const Item item = a.items[it];
+        x.R0 = item.r0;
+        x.Rend = item.r1;
+        x.col = item.strip * WV - LH + 4 * lane;
+        x.store_lane = (4 * lane >= LH) && (4 * lane < LH + WV);
+        x.right_edge = (x.col + 3 == a.W - 1);
+        x.kx.a = make_float2(x.col == a.W - 1 ? 0.0f : 1.0f, x.col + 2 == a.W - 1 ? 0.0f : 1.0f);
+        x.kx.b = make_float2(x.col + 1 == a.W - 1 ? 0.0f : 1.0f, x.col + 3 == a.W - 1 ? 0.0f : 1.0f);
+        x.p1i = a.p1_in + x.col;
+        x.p2i = a.p2_in + x.col;
+        x.vi = a.v_in + x.col;
+        x.ci = a.c + x.col;
+        // input rows [n, n_last]; the cone reaches S+1 rows up and S rows down, the delay
+        // buffer adds one row of latency.  The step count is made even (one extra warm-up
+        // row) for the two-state unrolled loop.
+        x.n_last = x.Rend - 1 + S + Split<S>::NS;
+        int n = x.R0 - (S + 1);
+        if (((x.n_last - n + 1) & 1) != 0) --n;
+#pragma unroll
+        for (int r = 0; r < RING; ++r) {
+            if (n + r <= x.n_last) stage_row(x, n + r);
+            cp_async_commit();
+        }
+        float acc_u = 0.0f, acc_v = 0.0f;
+        // the Neumann row H-1 matters whenever the march (cone included) reaches it
+        if (x.n_last >= a.H - 1)
+            march<S, MODE, ALIGNED, true>(x, n, acc_u, acc_v);
+        else
+            march<S, MODE, ALIGNED, false>(x, n, acc_u, acc_v);
+        if (MODE == MODE_CHECK) {  // per-item partial sums, fixed lane order (deterministic)
+            double su = acc_u, sv = acc_v;
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                su += __shfl_xor_sync(0xffffffffu, su, off);
+                sv += __shfl_xor_sync(0xffffffffu, sv, off);
+            }
+            if (lane == 0) {
+                a.chk[2 * it] = su;
+                a.chk[2 * it + 1] = sv;
+            }
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+    }
+}
+
+
+typedef void (*StencilFn)(const StencilArgs);
+
+// Fills t[S][mode][aligned] for S = 1..KF with the kernel instantiations of one k_fuse.
+template <int KF, int S>
+struct Table {
+    static void fill(StencilFn (*t)[3][2]) {
+        t[S][0][0] = k_stencil<KF, S, MODE_PLAIN, false>;
+        t[S][1][0] = k_stencil<KF, S, MODE_WRITE_U, false>;
+        t[S][2][0] = k_stencil<KF, S, MODE_CHECK, false>;
+        t[S][0][1] = k_stencil<KF, S, MODE_PLAIN, true>;
+        t[S][1][1] = k_stencil<KF, S, MODE_WRITE_U, true>;
+        t[S][2][1] = k_stencil<KF, S, MODE_CHECK, true>;
+        Table<KF, S - 1>::fill(t);
+    }
+};
+template <int KF>
+struct Table<KF, 0> {
+    static void fill(StencilFn (*)[3][2]) {}
+};
+
+constexpr int STENCIL_KF_MAX = 8;
+// defined in k_stencil_kf<K>.cu
+void stencil_fill_kf1(StencilFn (*t)[3][2]);
+void stencil_fill_kf2(StencilFn (*t)[3][2]);
+void stencil_fill_kf3(StencilFn (*t)[3][2]);
+void stencil_fill_kf4(StencilFn (*t)[3][2]);
+void stencil_fill_kf5(StencilFn (*t)[3][2]);
+void stencil_fill_kf6(StencilFn (*t)[3][2]);
+void stencil_fill_kf7(StencilFn (*t)[3][2]);
+void stencil_fill_kf8(StencilFn (*t)[3][2]);
+
+}  // namespace rds

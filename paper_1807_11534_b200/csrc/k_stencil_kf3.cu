@@ -1,0 +1,9 @@
+// k_stencil_kf3.cu -- the k_fuse = 3 instantiations of the K3 stencil (k_stencil_impl.cuh);
+// one translation unit per k_fuse so the build compiles them in parallel.
+#include "k_stencil_impl.cuh"
+
+namespace rds {
+
+void stencil_fill_kf3(StencilFn (*t)[3][2]) { Table<3, 3>::fill(t); }
+
+}  // namespace rds

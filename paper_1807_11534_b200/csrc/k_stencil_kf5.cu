@@ -1,0 +1,9 @@
+// k_stencil_kf5.cu -- the k_fuse = 5 instantiations of the K3 stencil (k_stencil_impl.cuh);
+// one translation unit per k_fuse so the build compiles them in parallel.
+#include "k_stencil_impl.cuh"
+
+namespace rds {
+
+void stencil_fill_kf5(StencilFn (*t)[3][2]) { Table<5, 5>::fill(t); }
+
+}  // namespace rds
