@@ -73,9 +73,9 @@ typedef struct {
     int64_t n_rd;            /* pixels in RD (label 2) */
     int64_t n_tiles;         /* 32x32 tiles covering the image */
     int64_t n_active_tiles;  /* tiles containing an RD pixel */
-    int64_t n_items;         /* strip x 32-row band cells covering the image */
+    int64_t n_items;         /* strip x 8-row band cells covering the image */
     int64_t n_active_items;  /* stencil work items launched (runs of active cells, split) */
-    int64_t n_active_cells;  /* strip x band cells overlapping an active tile */
+    int64_t n_active_cells;  /* strip x 8-row band cells holding an RD pixel */
     int32_t iters;           /* K of the last solve */
     int32_t k_fuse;          /* iterations fused per HBM round trip */
     int32_t launches;        /* stencil launches in the K-loop */
@@ -95,9 +95,9 @@ typedef struct {
                                 multiple of 8); 0 = automatic (makespan model over resident
                                 warps, 8..512 rows) */
 #define RDS_OPT_TIMING 3     /* 1 = record setup/loop CUDA-event times in rds_stats_t */
-#define RDS_OPT_SKIP 4       /* 1 (default) = work only on strip x band cells overlapping
-                                active tiles; 0 = process every cell (restriction without
-                                tile skipping) */
+#define RDS_OPT_SKIP 4       /* 1 (default) = work only on strip x 8-row band cells that
+                                hold an RD pixel; 0 = process every cell (restriction without
+                                skipping) */
 #define RDS_OPT_GRAPH 5      /* 1 (default) = replay the K-loop as a CUDA graph */
 #define RDS_OPT_CTAS_PER_SM 6 /* cap on resident stencil CTAs per SM (0 = occupancy limit);
                                  a tuning/diagnostic knob, results are identical */

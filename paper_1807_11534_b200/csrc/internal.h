@@ -25,6 +25,9 @@ constexpr int PAD_R = 16;      // >= KF + 1 rows of halo above / below (KF <= 15
 constexpr int PAD_C = 32;      // left frame, keeps column 0 16-byte aligned
 constexpr int PAD_C_RIGHT = 128;  // a warp strip may read up to 127 columns past its start
 constexpr int TILE_H = 32, TILE_W = 32;
+// work-item activity is decided per strip x BAND_H-row band, from RD counts per 32-column x
+// BAND_H-row sub-tile (SUBTILES per 32x32 tile)
+constexpr int BAND_H = 8, SUBTILES = TILE_H / BAND_H;
 constexpr int STENCIL_WARPS = 4;
 
 // element offset of column j inside a quad-swizzled row (valid for negative j as well)
@@ -108,6 +111,7 @@ struct SetupArgs {
     float *v0, *v1, *p10, *p11, *p20, *p21;
     uint8_t *lab, *mask;
     int32_t *tile_rd;                   // RD pixels per 32x32 tile
+    int32_t *sub_rd;                    // RD pixels per 32-column x BAND_H-row sub-tile
     int64_t pitch;
     int H, W;
     float c1, c2, gamma, delta, theta_lambda;
@@ -120,7 +124,7 @@ cudaError_t launch_compact(const int32_t *flags, int n, int32_t *list, int32_t *
                            long long *sum_out, cudaStream_t s);
 // band_flag[s * n_bands + b] = 1 iff strip s (output columns [s*wv, (s+1)*wv)) overlaps an
 // active 32x32 tile in tile row b (skip = 0 marks everything active).
-cudaError_t launch_band_flags(const int32_t *tile_rd, int H, int W, int wv, int n_strips,
+cudaError_t launch_band_flags(const int32_t *sub_rd, int H, int W, int wv, int n_strips,
                               int skip, int32_t *band_flag, cudaStream_t s);
 // Work items from the band flags: maximal vertical runs of active bands per strip, each split
 // into ceil(rows / chunk) near-equal pieces at ITEM_Q-row boundaries.  chunk = fixed_chunk

@@ -202,10 +202,14 @@ __global__ void __launch_bounds__(256) k_setup(SetupArgs a) {
     if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
+        const int tile = blockIdx.y * gridDim.x + blockIdx.x;
         int t = 0;
 #pragma unroll
         for (int w = 0; w < 8; ++w) t += warp_sum[w];
-        a.tile_rd[blockIdx.y * gridDim.x + blockIdx.x] = t;
+        a.tile_rd[tile] = t;
+        // warp w holds rows 4w..4w+3, so the 8-row sub-tile k is warps 2k, 2k+1
+#pragma unroll
+        for (int k = 0; k < SUBTILES; ++k) a.sub_rd[tile * SUBTILES + k] = warp_sum[2 * k] + warp_sum[2 * k + 1];
     }
 }
 
@@ -272,12 +276,13 @@ cudaError_t launch_compact(const int32_t *flags, int n, int32_t *list, int32_t *
     return cudaGetLastError();
 }
 
-// A strip's band b is active iff one of the 32x32 tiles its output columns overlap in tile
-// row b holds an RD pixel.  Processing a pinned pixel reproduces its value exactly, so any
-// superset of the needed work gives the same result; skip = 0 marks every band active.
-__global__ void k_band_flags(const int32_t *tile_rd, int H, int W, int wv, int n_strips,
+// A strip's band b (BAND_H = 8 rows) is active iff one of the 32-column x 8-row sub-tiles
+// its output columns overlap in that band holds an RD pixel.  Processing a pinned pixel
+// reproduces its value exactly, so any superset of the needed work gives the same result;
+// skip = 0 marks every band active.
+__global__ void k_band_flags(const int32_t *sub_rd, int H, int W, int wv, int n_strips,
                              int skip, int32_t *band_flag) {
-    const int n_bands = (H + TILE_H - 1) / TILE_H;
+    const int n_bands = (H + BAND_H - 1) / BAND_H;
     const int it = blockIdx.x * blockDim.x + threadIdx.x;
     if (it >= n_strips * n_bands) return;
     const int s = it / n_bands, b = it - s * n_bands;
@@ -286,16 +291,18 @@ __global__ void k_band_flags(const int32_t *tile_rd, int H, int W, int wv, int n
         return;
     }
     const int ntj = (W + TILE_W - 1) / TILE_W;
+    const int ti = b / SUBTILES, k = b - ti * SUBTILES;
     const int j0 = s * wv, j1 = min(W, (s + 1) * wv) - 1;
     int on = 0;
-    for (int tj = j0 / TILE_W; tj <= j1 / TILE_W; ++tj) on |= tile_rd[b * ntj + tj] != 0;
+    for (int tj = j0 / TILE_W; tj <= j1 / TILE_W; ++tj)
+        on |= sub_rd[(ti * ntj + tj) * SUBTILES + k] != 0;
     band_flag[it] = on;
 }
 
-cudaError_t launch_band_flags(const int32_t *tile_rd, int H, int W, int wv, int n_strips,
+cudaError_t launch_band_flags(const int32_t *sub_rd, int H, int W, int wv, int n_strips,
                               int skip, int32_t *band_flag, cudaStream_t s) {
-    const int n = n_strips * ((H + TILE_H - 1) / TILE_H);
-    k_band_flags<<<(n + 255) / 256, 256, 0, s>>>(tile_rd, H, W, wv, n_strips, skip, band_flag);
+    const int n = n_strips * ((H + BAND_H - 1) / BAND_H);
+    k_band_flags<<<(n + 255) / 256, 256, 0, s>>>(sub_rd, H, W, wv, n_strips, skip, band_flag);
     return cudaGetLastError();
 }
 
@@ -317,7 +324,7 @@ __device__ int strip_items(const int32_t *flags, int n_bands, int H, int chunk, 
         }
         int e = b;
         while (e < n_bands && flags[e]) ++e;
-        const int r0 = b * TILE_H, r1 = min(e * TILE_H, H);
+        const int r0 = b * BAND_H, r1 = min(e * BAND_H, H);
         const int q = (r1 - r0 + ITEM_Q - 1) / ITEM_Q;            // ITEM_Q-row slices
         const int pieces = (r1 - r0 + chunk - 1) / chunk;
         for (int k = 0; k < pieces; ++k) {
@@ -334,22 +341,24 @@ __device__ int strip_items(const int32_t *flags, int n_bands, int H, int chunk, 
 }
 
 // Single CTA.  (1) For every candidate height c, the exact item count sum over runs of
-// ceil(rows / c); the makespan model picks the c minimising waves(c) * (c + warm-up rows),
-// waves = ceil(items / resident warps) (a launch costs whole rounds of items: one extra item
-// on a full wave doubles the launch), ties to the taller item (less warm-up work).
+// ceil(rows / c); the makespan model picks the c minimising
+//     (waves - 1) * (hbar + w) + (c + w),   waves = ceil(items / resident warps),
+// hbar = active rows / items (the mean item height, below c when runs are short), w = the
+// pipeline warm-up rows: whole rounds of items (one extra item on a full wave doubles the
+// launch), the last round set by the tallest item; ties go to the taller item.
 // (2) Per-strip item counts -> block exclusive scan -> items written in strip-major,
 // ascending-row order (deterministic, no atomics).
 __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, int n_strips,
                                                       int n_bands, int H, int slots,
                                                       int fixed_chunk, int warmup_rows,
                                                       Item *items, int32_t *counts) {
-    __shared__ long long red[N_CHUNK + 1][32];
+    __shared__ long long red[N_CHUNK + 2][32];
     __shared__ int off[32];
     __shared__ int chunk_s, base_s;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    long long cnt_c[N_CHUNK + 1];
+    long long cnt_c[N_CHUNK + 2];  // items per candidate, active cells, active rows
 #pragma unroll
-    for (int k = 0; k <= N_CHUNK; ++k) cnt_c[k] = 0;
+    for (int k = 0; k <= N_CHUNK + 1; ++k) cnt_c[k] = 0;
     for (int sidx = tid; sidx < n_strips; sidx += 1024) {
         const int32_t *fl = band_flag + (int64_t)sidx * n_bands;
         int b = 0;
@@ -360,15 +369,16 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
             }
             int e = b;
             while (e < n_bands && fl[e]) ++e;
-            const int rows = min(e * TILE_H, H) - b * TILE_H;
+            const int rows = min(e * BAND_H, H) - b * BAND_H;
 #pragma unroll
             for (int k = 0; k < N_CHUNK; ++k) cnt_c[k] += (rows + kChunkRows[k] - 1) / kChunkRows[k];
             cnt_c[N_CHUNK] += e - b;  // active cells
+            cnt_c[N_CHUNK + 1] += rows;
             b = e;
         }
     }
 #pragma unroll
-    for (int k = 0; k <= N_CHUNK; ++k) {
+    for (int k = 0; k <= N_CHUNK + 1; ++k) {
         long long v = cnt_c[k];
         for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
         if (lane == 0) red[k][wid] = v;
@@ -378,13 +388,17 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
         int c = fixed_chunk > 0 ? (fixed_chunk + ITEM_Q - 1) / ITEM_Q * ITEM_Q : 0;
         if (c <= 0) {
             const long long sl = slots > 0 ? slots : 1;
-            long long best = -1;
+            long long rows_all = 0;
+            for (int w = 0; w < 32; ++w) rows_all += red[N_CHUNK + 1][w];
+            double best = -1.0;
             for (int k = 0; k < N_CHUNK; ++k) {
                 long long items_k = 0;
                 for (int w = 0; w < 32; ++w) items_k += red[k][w];
                 const long long waves = (items_k + sl - 1) / sl;
-                const long long cost = (waves > 0 ? waves : 1) * (kChunkRows[k] + warmup_rows);
-                if (best < 0 || cost <= best) {
+                const double hbar = items_k > 0 ? (double)rows_all / (double)items_k : 0.0;
+                const double cost = (double)(waves > 1 ? waves - 1 : 0) * (hbar + warmup_rows) +
+                                    (double)(kChunkRows[k] + warmup_rows);
+                if (best < 0.0 || cost <= best) {
                     best = cost;
                     c = kChunkRows[k];
                 }

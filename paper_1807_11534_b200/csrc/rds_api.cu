@@ -46,7 +46,7 @@ struct rds_handle {
     uint8_t *lab = nullptr, *mask = nullptr;
     // tiles / items
     int n_tiles = 0;
-    int32_t *tile_rd = nullptr, *tile_list = nullptr;
+    int32_t *tile_rd = nullptr, *tile_list = nullptr, *sub_rd = nullptr;
     int32_t *band_flag = nullptr;    // [strip][band] active flags
     Item *items = nullptr;           // stencil work items
     int32_t *queue = nullptr;        // per-launch work counters
@@ -124,6 +124,7 @@ static void free_all(rds_t *h) {
     for (float *p : fl)
         if (p) cudaFree(p);
     void *other[] = {h->lab,     h->mask,        h->tile_rd, h->tile_list, h->band_flag,
+                     h->sub_rd,
                      h->items,   h->queue,       h->counts,  h->n_rd_dev,  h->absmax_bits,
                      h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch,
                      h->stop,    h->chk,         h->d64,     h->part64,    h->cmp_out,
@@ -200,6 +201,7 @@ int rds_create(int64_t H, int64_t W, rds_t **out) {
     A(cudaMalloc(&h->mask, h->plane));
     A(cudaMemsetAsync(h->mask, 0, h->plane, h->stream));
     A(cudaMalloc(&h->tile_rd, sizeof(int32_t) * h->n_tiles));
+    A(cudaMalloc(&h->sub_rd, sizeof(int32_t) * h->n_tiles * SUBTILES));
     A(cudaMalloc(&h->tile_list, sizeof(int32_t) * h->n_tiles));
     A(cudaMalloc(&h->counts, sizeof(int32_t) * 4));
     A(cudaMemsetAsync(h->counts, 0, sizeof(int32_t) * 4, h->stream));
@@ -680,7 +682,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     const int kf = h->opt_kf ? h->opt_kf : default_kf(h->H, h->W);
     const int wv = wv_of(kf);
     const int n_strips = (int)((h->W + wv - 1) / wv);
-    const int n_bands = (int)((h->H + TILE_H - 1) / TILE_H);
+    const int n_bands = (int)((h->H + BAND_H - 1) / BAND_H);
     // items are cut at ITEM_Q-row boundaries: at most one per ITEM_Q rows of every strip
     const int max_items = n_strips * (int)((h->H + ITEM_Q - 1) / ITEM_Q);
     const int fixed_chunk = h->opt_rows;  // rows (rounded up to ITEM_Q on the device)
@@ -736,6 +738,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     s.lab = h->at(h->lab);
     s.mask = h->at(h->mask);
     s.tile_rd = h->tile_rd;
+    s.sub_rd = h->sub_rd;
     s.pitch = h->pitch;
     s.H = (int)h->H;
     s.W = (int)h->W;
@@ -747,7 +750,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     CK(h, launch_setup(s, h->stream));
     CK(h, launch_compact(h->tile_rd, h->n_tiles, h->tile_list, h->counts + 0, h->n_rd_dev,
                          h->stream));
-    CK(h, launch_band_flags(h->tile_rd, (int)h->H, (int)h->W, wv, n_strips, h->opt_skip,
+    CK(h, launch_band_flags(h->sub_rd, (int)h->H, (int)h->W, wv, n_strips, h->opt_skip,
                             h->band_flag, h->stream));
     {
         const int slots = h->n_sm * blocks_per_sm(h, kf, kf) * STENCIL_WARPS;
