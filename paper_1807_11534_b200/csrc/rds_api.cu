@@ -850,7 +850,10 @@ int rds_solve_tol(rds_t *h, float lambda, float theta, float tau, float delta, i
         return fail(h, RDS_EINVAL, "rds_solve_tol: check_every=%d must be >= 0", check_every);
     if (max_iters < 1)
         return fail(h, RDS_EINVAL, "rds_solve_tol: max_iters=%d must be >= 1", max_iters);
-    const int m = check_every > 0 ? check_every : (h->opt_kf ? h->opt_kf : default_kf(h->H, h->W));
+    // default: every 5th launch (C3: +4% over a fixed-K solve; every launch costs +19%,
+    // profiles/r01_tol_overhead.jsonl)
+    const int m = check_every > 0 ? check_every
+                                  : 5 * (h->opt_kf ? h->opt_kf : default_kf(h->H, h->W));
     return solve_impl(h, lambda, theta, tau, delta, max_iters, m, tol);
 }
 

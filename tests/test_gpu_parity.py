@@ -451,7 +451,7 @@ def _tol_case(rds, orc, z, P, cfg, lam, delta, max_iters, tol, m, ctx, norm="l2"
     s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
     st = s.solve_tol(lam, cfg.theta, cfg.tau, delta, max_iters, tol, m)
     me = st["check_every"]
-    assert me == (m or st["k_fuse"])
+    assert me == (m or 5 * st["k_fuse"])
     f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
     o = orc.solve_tol(f, delta, lam, np.float32(cfg.theta), cfg.tau, max_iters, tol, me, norm)
     if st["iters"] != o["iters"]:
@@ -578,7 +578,7 @@ def test_solve_tol_c3_full_size(rds, orc):
     s = rds.Solver(cfg.H, cfg.W)
     s.set_image(z)
     s.set_fitting(cfg.c1, cfg.c2)
-    st = s.solve_tol(5.0, cfg.theta, cfg.tau, delta, 63, 0.0)
+    st = s.solve_tol(5.0, cfg.theta, cfg.tau, delta, 63, 0.0, 7)
     assert st["iters"] == 63 and st["converged"] == 0 and st["check_every"] == 7
     o = orc.solve_tol(f, delta, 5.0, np.float32(cfg.theta), cfg.tau, 63, 0.0, 7)
     assert abs(st["residual"] - o["residual"]) <= 2e-2 * o["residual"]
