@@ -89,6 +89,7 @@ struct StencilArgs {
     double *chk;                         // CHECK launches: [item][2] sums of du^2, dv^2
     int64_t pitch;
     int H, W;
+    int img_h;                           // rows per image (H, or the image height of a batch)
     float tau, theta, inv_theta;
 };
 
@@ -113,7 +114,7 @@ struct SetupArgs {
     int32_t *tile_rd;                   // RD pixels per 32x32 tile
     int32_t *sub_rd;                    // RD pixels per 32-column x BAND_H-row sub-tile
     int64_t pitch;
-    int H, W;
+    int H, W, img_h;
     float c1, c2, gamma, delta, theta_lambda;
 };
 cudaError_t launch_setup(const SetupArgs &a, cudaStream_t s);
@@ -132,8 +133,8 @@ cudaError_t launch_band_flags(const int32_t *sub_rd, int H, int W, int wv, int n
 // ceil(items / slots) * (chunk + warmup_rows) (makespan model, k_setup.cu).
 // out: items, counts[1] = number of items, counts[2] = chunk rows, counts[3] = active cells.
 cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands, int H,
-                               int slots, int fixed_chunk, int warmup_rows, Item *items,
-                               int32_t *counts, cudaStream_t s);
+                               int slots, int fixed_chunk, int max_chunk, int warmup_rows,
+                               Item *items, int32_t *counts, cudaStream_t s);
 
 // mode: 0 iterate, 1 + write u and mask, 2 + stopping sums into a.chk (k_stencil_impl.cuh)
 cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a,
@@ -147,7 +148,7 @@ cudaError_t launch_stop_check(const StopCheck &c, cudaStream_t s);
 struct EnergyArgs {
     const float *f, *u, *v, *p1, *p2;
     int64_t pitch;
-    int H, W;
+    int H, W, img_h;
     double *partials;   // [n_blocks * 5]
     double *out;        // [5]: TV_v, sum f v, TV_cu, sum f cu, sum min(0, lambda f + div p)
     float lambda;
@@ -163,7 +164,7 @@ struct F64Args {
     uint8_t *lab;
     StopRecord *stop;          // early exit once the stopping rule fired (null: never)
     int64_t pitch;
-    int H, W;
+    int H, W, img_h;
     float c1, c2, gamma, delta;
     double tau, theta, theta_lambda;
 };

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
         const int64_t o = (int64_t)i * pitch + j;
         const int64_t os = (int64_t)i * pitch + swz(j);  // v, rho are quad-swizzled
         const int64_t osr = (int64_t)i * pitch + swz(j + 1), osl = (int64_t)i * pitch + swz(j - 1);
-        const bool down = i < a.H - 1, right = j < a.W - 1;
+        const bool down = i % a.img_h != a.img_h - 1, right = j < a.W - 1;
         const float v = a.v[os];
         const float gv1 = down ? a.v[os + pitch] - v : 0.0f;
         const float gv2 = right ? a.v[osr] - v : 0.0f;

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(256) k_setup(SetupArgs a) {
                 msk[e] = fg ? 1 : 0;
                 const bool warm = rd && a.wv != nullptr;
                 v[e] = warm ? WV[e] : u0;
-                p1[e] = (warm && i < a.H - 1) ? W1[e] : 0.0f;
+                p1[e] = (warm && i % a.img_h != a.img_h - 1) ? W1[e] : 0.0f;
                 p2[e] = (warm && jj < a.W - 1) ? W2[e] : 0.0f;
                 rd_count += rd;
             } else {
@@ -350,8 +350,9 @@ __device__ int strip_items(const int32_t *flags, int n_bands, int H, int chunk, 
 // ascending-row order (deterministic, no atomics).
 __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, int n_strips,
                                                       int n_bands, int H, int slots,
-                                                      int fixed_chunk, int warmup_rows,
-                                                      Item *items, int32_t *counts) {
+                                                      int fixed_chunk, int max_chunk,
+                                                      int warmup_rows, Item *items,
+                                                      int32_t *counts) {
     __shared__ long long red[N_CHUNK + 2][32];
     __shared__ int off[32];
     __shared__ int chunk_s, base_s;
@@ -386,12 +387,14 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
     __syncthreads();
     if (tid == 0) {
         int c = fixed_chunk > 0 ? (fixed_chunk + ITEM_Q - 1) / ITEM_Q * ITEM_Q : 0;
+        if (c > max_chunk) c = max_chunk;
         if (c <= 0) {
             const long long sl = slots > 0 ? slots : 1;
             long long rows_all = 0;
             for (int w = 0; w < 32; ++w) rows_all += red[N_CHUNK + 1][w];
             double best = -1.0;
             for (int k = 0; k < N_CHUNK; ++k) {
+                if (kChunkRows[k] > max_chunk && k > 0) continue;
                 long long items_k = 0;
                 for (int w = 0; w < 32; ++w) items_k += red[k][w];
                 const long long waves = (items_k + sl - 1) / sl;
@@ -450,10 +453,10 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
 }
 
 cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands, int H,
-                               int slots, int fixed_chunk, int warmup_rows, Item *items,
-                               int32_t *counts, cudaStream_t s) {
+                               int slots, int fixed_chunk, int max_chunk, int warmup_rows,
+                               Item *items, int32_t *counts, cudaStream_t s) {
     k_build_items<<<1, 1024, 0, s>>>(band_flag, n_strips, n_bands, H, slots, fixed_chunk,
-                                     warmup_rows, items, counts);
+                                     max_chunk, warmup_rows, items, counts);
     return cudaGetLastError();
 }
 

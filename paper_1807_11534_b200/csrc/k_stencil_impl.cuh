@@ -32,6 +32,7 @@
 // twice.  The row loop is unrolled by two with two state sets (A -> B, B -> A) so the
 // per-row state shift is register renaming, not moves.
 #pragma once
+#include <limits.h>
 #include <math.h>
 
 #include "internal.h"
@@ -158,6 +159,7 @@ struct Ctx {
     float4 *cring;  // this lane's c slot 0; slot stride 32 float4, 2*CR slots
     int64_t pitch;
     int col, H, R0, Rend, n_last;
+    int last0, last1;  // image-last rows (grad_1 = 0) inside this item's march window
     bool store_lane, right_edge;
     Q kx;
     float tau, theta, inv_theta;
@@ -207,7 +209,7 @@ __device__ __forceinline__ Front front(const Q &aw, const Q &inv, const Q &ind, 
     if (ALIGNED && x.right_edge) wr = aw.b.y;      // grad_2 = 0 on column W-1
     f.g1.a = sub2(f.w.a, aw.a);
     f.g1.b = sub2(f.w.b, aw.b);
-    if (LAST && m == x.H - 1) f.g1 = zeroq();      // grad_1 = 0 on row H-1
+    if (LAST && (m == x.last0 || m == x.last1)) f.g1 = zeroq();  // grad_1 = 0 on an image's last row
     f.g2.a = sub2(aw.b, aw.a);
     f.g2.b = sub2(make_float2(aw.a.y, wr), aw.b);
     if (!ALIGNED) {
@@ -441,7 +443,17 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
         }
         float acc_u = 0.0f, acc_v = 0.0f;
         // the Neumann row H-1 matters whenever the march (cone included) reaches it
-        if (x.n_last >= a.H - 1)
+        // image-last rows (the Neumann row of every image of a batch, img_h rows each; a single
+        // image has one, H - 1) inside the march window [n, n_last]; the item builder keeps the
+        // window shorter than two images, so there are at most two
+        {
+            const int ih = a.img_h;
+            int b0 = n < 0 ? ih - 1 : (n / ih) * ih + ih - 1;
+            if (b0 < n) b0 += ih;
+            x.last0 = b0 <= min(x.n_last, a.H - 1) ? b0 : INT_MIN;
+            x.last1 = b0 + ih <= min(x.n_last, a.H - 1) ? b0 + ih : INT_MIN;
+        }
+        if (x.last0 != INT_MIN)
             march<S, MODE, ALIGNED, true>(x, n, acc_u, acc_v);
         else
             march<S, MODE, ALIGNED, false>(x, n, acc_u, acc_v);

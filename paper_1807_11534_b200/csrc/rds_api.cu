@@ -33,6 +33,7 @@ static int default_kf(int64_t H, int64_t W) { return H * W <= kSmallPixels ? kSm
 
 struct rds_handle {
     int64_t H = 0, W = 0;
+    int64_t img_h = 0;     // rows per image: H, or the image height of a batch (rds_create_batch)
     int64_t pitch = 0;     // elements per padded row (multiple of 32)
     int64_t rows_alloc = 0;
     int64_t plane = 0;     // elements per plane
@@ -157,6 +158,7 @@ int rds_create(int64_t H, int64_t W, rds_t **out) {
     if (!h) return fail(nullptr, RDS_ENOMEM, "rds_create: host allocation failed");
     h->H = H;
     h->W = W;
+    h->img_h = H;
     h->pitch = ((PAD_C + W + PAD_C_RIGHT) + 31) / 32 * 32;
     h->rows_alloc = H + 2 * PAD_R;
     h->plane = h->pitch * h->rows_alloc;
@@ -214,6 +216,21 @@ int rds_create(int64_t H, int64_t W, rds_t **out) {
     A(cudaStreamSynchronize(h->stream));
 #undef A
     *out = h;
+    return RDS_OK;
+}
+
+int rds_create_batch(int64_t B, int64_t H, int64_t W, rds_t **out) {
+    if (!out) return fail(nullptr, RDS_EINVAL, "rds_create_batch: out is NULL");
+    *out = nullptr;
+    if (B < 1 || H < 32 || W < 1)
+        return fail(nullptr, RDS_EINVAL,
+                    "rds_create_batch: need B >= 1, H >= 32, W >= 1 (got %lld, %lld, %lld)",
+                    (long long)B, (long long)H, (long long)W);
+    if (B * H > (int64_t(1) << 30))
+        return fail(nullptr, RDS_EINVAL, "rds_create_batch: B*H too large");
+    const int rc = rds_create(B * H, W, out);
+    if (rc) return rc;
+    (*out)->img_h = H;
     return RDS_OK;
 }
 
@@ -494,6 +511,7 @@ static cudaError_t enqueue_plan(rds_t *h, const LaunchPlan *plan, int n, int kf,
     a.pitch = h->pitch;
     a.H = (int)h->H;
     a.W = (int)h->W;
+    a.img_h = (int)h->img_h;
     a.tau = tau;
     a.theta = theta;
     a.inv_theta = 1.0f / theta;
@@ -742,6 +760,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     s.pitch = h->pitch;
     s.H = (int)h->H;
     s.W = (int)h->W;
+    s.img_h = (int)h->img_h;
     s.c1 = h->c1;
     s.c2 = h->c2;
     s.gamma = h->gamma;
@@ -754,7 +773,15 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
                             h->band_flag, h->stream));
     {
         const int slots = h->n_sm * blocks_per_sm(h, kf, kf) * STENCIL_WARPS;
+        // a batch keeps every item's march window (rows + 2 kf + 4) within two images, so it
+        // meets at most two image-last rows (k_stencil_impl.cuh)
+        int max_chunk = 1 << 30;
+        if (h->img_h < h->H) {
+            max_chunk = (int)((2 * h->img_h - 2 * kf - 6) / ITEM_Q * ITEM_Q);
+            if (max_chunk < ITEM_Q) max_chunk = ITEM_Q;
+        }
         CK(h, launch_build_items(h->band_flag, n_strips, n_bands, (int)h->H, slots, fixed_chunk,
+                                 max_chunk,
                                  2 * kf + 4, h->items, h->counts, h->stream));
     }
     h->warm_pending = false;
@@ -981,6 +1008,7 @@ int rds_energy(rds_t *h, rds_energy_t *out) {
     a.pitch = h->pitch;
     a.H = (int)h->H;
     a.W = (int)h->W;
+    a.img_h = (int)h->img_h;
     a.partials = h->e_partials;
     a.out = h->e_out;
     a.lambda = h->lambda;
@@ -1065,6 +1093,7 @@ int rds_solve_gt(rds_t *h, float lambda, float theta, float tau, float delta,
     a.pitch = h->pitch;
     a.H = (int)h->H;
     a.W = (int)h->W;
+    a.img_h = (int)h->img_h;
     a.c1 = h->c1;
     a.c2 = h->c2;
     a.gamma = h->gamma;

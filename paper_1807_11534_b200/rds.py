@@ -26,7 +26,8 @@ RDS_OPT_CTAS_PER_SM = 6
 RDS_OPT_STOP_NORM = 7  # 0 Euclidean over pixels (default), 1 RMS
 
 EXPORTS = (
-    "rds_create", "rds_destroy", "rds_set_stream", "rds_set_option", "rds_set_image",
+    "rds_create", "rds_create_batch", "rds_destroy", "rds_set_stream", "rds_set_option",
+    "rds_set_image",
     "rds_set_fitting", "rds_set_state", "rds_fitting_absmax", "rds_solve", "rds_get_u",
     "rds_get_mask", "rds_get_v", "rds_get_p", "rds_get_fitting", "rds_get_labels",
     "rds_get_active_tiles", "rds_tile_shape", "rds_energy", "rds_get_stats",
@@ -83,6 +84,7 @@ def _load():
     P, i64, i32, f, i = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_float, ctypes.c_int
     sig = {
         "rds_create": [i64, i64, ctypes.POINTER(P)],
+        "rds_create_batch": [i64, i64, i64, ctypes.POINTER(P)],
         "rds_destroy": [P],
         "rds_set_stream": [P, P],
         "rds_set_option": [P, i, i64],
@@ -331,9 +333,14 @@ class Solver:
     """One librds handle for an H x W image.  Host (numpy) or device (torch) buffers."""
 
     def __init__(self, H, W, stream=None, k_fuse=0, item_rows=0, timing=False, skip=True,
-                 graph=True):
-        self.shape = (int(H), int(W))
-        self.h = rds_create(H, W)
+                 graph=True, batch=None):
+        self.shape = (int(H) * (int(batch) if batch else 1), int(W))
+        if batch is not None:
+            h = ctypes.c_void_p()
+            _check(_lib.rds_create_batch(int(batch), int(H), int(W), ctypes.byref(h)))
+            self.h = h
+        else:
+            self.h = rds_create(H, W)
         if stream is not None:
             rds_set_stream(self.h, stream)
         if k_fuse:
@@ -525,3 +532,40 @@ class Solver3:
         _check3(_lib.rds3_get_stats(self.h, ctypes.byref(n_rd), ctypes.byref(it),
                                     ctypes.byref(kz), ctypes.byref(ms)), self.h)
         return {"n_rd": n_rd.value, "iters": it.value, "kz": kz.value, "ms": ms.value}
+
+
+class BatchSolver(Solver):
+    """B independent H x W images solved together (rds_create_batch).  Inputs and outputs are
+    (B, H, W) arrays (the same memory as the stacked (B*H, W) problem)."""
+
+    def __init__(self, B, H, W, **kw):
+        super().__init__(H, W, batch=B, **kw)
+        self.bshape = (int(B), int(H), int(W))
+
+    def _flat(self, a):
+        return None if a is None else a.reshape(self.shape)
+
+    def set_image(self, z):
+        super().set_image(self._flat(z))
+
+    def set_fitting(self, c1, c2, gamma=0.0, P=None):
+        super().set_fitting(c1, c2, gamma, self._flat(P))
+
+    def u(self, out=None):
+        return super().u(self._flat(out)).reshape(self.bshape)
+
+    def v(self, out=None):
+        return super().v(self._flat(out)).reshape(self.bshape)
+
+    def mask(self, out=None):
+        return super().mask(self._flat(out)).reshape(self.bshape)
+
+    def labels(self, out=None):
+        return super().labels(self._flat(out)).reshape(self.bshape)
+
+    def fitting(self, out=None):
+        return super().fitting(self._flat(out)).reshape(self.bshape)
+
+    def p(self):
+        p1, p2 = super().p()
+        return p1.reshape(self.bshape), p2.reshape(self.bshape)
