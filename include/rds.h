@@ -110,11 +110,13 @@ typedef struct {
 int rds_create(int64_t H, int64_t W, rds_t **out);
 
 /* A batch of B independent H x W images solved together (serving many small images, e.g.
- * the paper's 128 x 128 ones, in one launch sequence): the images are stacked along rows into
- * one (B*H) x W problem whose every image keeps its own Neumann last row (grad_1 = 0 on
- * rows H-1, 2H-1, ...); rho never couples two images.  Every other call then takes and
- * returns (B*H) x W = B x H x W buffers; delta, q and the energies apply to the whole batch
- * (energies are sums over the images).  Errors: RDS_EINVAL if B < 1, H < 32, W < 1. */
+ * the paper's 128 x 128 ones, in one launch sequence).  Inside, image b occupies columns
+ * [b W, (b+1) W) of one H x (B W) problem -- narrow images share the stencil's 112-column
+ * strips -- and every image keeps its own Neumann last column (grad_2 = 0 on columns W-1,
+ * 2W-1, ...), so rho never couples two images.  Every other call takes and returns dense
+ * B x H x W buffers (the library transposes to and from its layout); delta, q and the
+ * energies apply to the whole batch (energies are sums over the images); active-tile
+ * indices refer to the internal H x (B W) layout.  Errors: RDS_EINVAL if B, H or W < 1. */
 int rds_create_batch(int64_t B, int64_t H, int64_t W, rds_t **out);
 
 /* Free everything; NULL is a no-op.  Synchronises the handle's stream first. */

@@ -89,7 +89,7 @@ struct StencilArgs {
     double *chk;                         // CHECK launches: [item][2] sums of du^2, dv^2
     int64_t pitch;
     int H, W;
-    int img_h;                           // rows per image (H, or the image height of a batch)
+    int img_w;                           // columns per image (W, or the image width of a batch)
     float tau, theta, inv_theta;
 };
 
@@ -114,7 +114,7 @@ struct SetupArgs {
     int32_t *tile_rd;                   // RD pixels per 32x32 tile
     int32_t *sub_rd;                    // RD pixels per 32-column x BAND_H-row sub-tile
     int64_t pitch;
-    int H, W, img_h;
+    int H, W, img_w;
     float c1, c2, gamma, delta, theta_lambda;
 };
 cudaError_t launch_setup(const SetupArgs &a, cudaStream_t s);
@@ -148,7 +148,7 @@ cudaError_t launch_stop_check(const StopCheck &c, cudaStream_t s);
 struct EnergyArgs {
     const float *f, *u, *v, *p1, *p2;
     int64_t pitch;
-    int H, W, img_h;
+    int H, W, img_w;
     double *partials;   // [n_blocks * 5]
     double *out;        // [5]: TV_v, sum f v, TV_cu, sum f cu, sum min(0, lambda f + div p)
     float lambda;
@@ -164,7 +164,7 @@ struct F64Args {
     uint8_t *lab;
     StopRecord *stop;          // early exit once the stopping rule fired (null: never)
     int64_t pitch;
-    int H, W, img_h;
+    int H, W, img_w;
     float c1, c2, gamma, delta;
     double tau, theta, theta_lambda;
 };
@@ -212,5 +212,10 @@ cudaError_t launch_vol_copy_u8(uint8_t *dst, const uint8_t *src, int64_t plane, 
 // out[i * out_pitch + j] = plane[i * pitch + swz(j)]: natural-order copy of a swizzled plane
 cudaError_t launch_unswizzle(const float *plane, int64_t pitch, int H, int W, float *out,
                              int64_t out_pitch, cudaStream_t s);
+// Batch layout (rds_create_batch): image b of B (H x img_w each) occupies columns
+// [b img_w, (b+1) img_w) of the H x (B img_w) planes.  Dense (B, H, img_w) <-> plane copies
+// (elt = 8, 4 or 1 bytes; swizzled = the plane is quad-swizzled, for rho and v).
+cudaError_t launch_batch_copy(void *dense, void *plane, int elt, int64_t pitch, int H,
+                              int img_w, int B, int to_plane, int swizzled, cudaStream_t s);
 
 }  // namespace rds

@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
         const int64_t o = (int64_t)i * pitch + j;
         const int64_t os = (int64_t)i * pitch + swz(j);  // v, rho are quad-swizzled
         const int64_t osr = (int64_t)i * pitch + swz(j + 1), osl = (int64_t)i * pitch + swz(j - 1);
-        const bool down = i % a.img_h != a.img_h - 1, right = j < a.W - 1;
+        const bool down = i < a.H - 1, right = j % a.img_w != a.img_w - 1;
         const float v = a.v[os];
         const float gv1 = down ? a.v[os + pitch] - v : 0.0f;
         const float gv2 = right ? a.v[osr] - v : 0.0f;
@@ -88,6 +88,38 @@ __global__ void k_unswizzle(const float *plane, int64_t pitch, int H, int W, flo
         const int i = (int)(k / W), j = (int)(k - (int64_t)i * W);
         out[(int64_t)i * out_pitch + j] = plane[(int64_t)i * pitch + swz(j)];
     }
+}
+
+template <typename T>
+__global__ void k_batch_copy(T *dense, T *plane, int64_t pitch, int H, int iw, int B,
+                             int to_plane, int swizzled) {
+    const int64_t n = (int64_t)B * H * iw;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t bh = k / iw;
+        const int j = (int)(k - bh * iw);
+        const int b = (int)(bh / H), i = (int)(bh - (int64_t)b * H);
+        const int col = b * iw + j;
+        const int64_t o = (int64_t)i * pitch + (swizzled ? swz(col) : col);
+        if (to_plane)
+            plane[o] = dense[k];
+        else
+            dense[k] = plane[o];
+    }
+}
+
+cudaError_t launch_batch_copy(void *dense, void *plane, int elt, int64_t pitch, int H,
+                              int img_w, int B, int to_plane, int swizzled, cudaStream_t s) {
+    if (elt == 8)
+        k_batch_copy<double><<<148 * 8, 256, 0, s>>>((double *)dense, (double *)plane, pitch, H,
+                                                      img_w, B, to_plane, swizzled);
+    else if (elt == 4)
+        k_batch_copy<float><<<148 * 8, 256, 0, s>>>((float *)dense, (float *)plane, pitch, H,
+                                                     img_w, B, to_plane, swizzled);
+    else
+        k_batch_copy<uint8_t><<<148 * 8, 256, 0, s>>>((uint8_t *)dense, (uint8_t *)plane, pitch,
+                                                       H, img_w, B, to_plane, swizzled);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_unswizzle(const float *plane, int64_t pitch, int H, int W, float *out,

@@ -73,9 +73,9 @@ __global__ void k64_rho(const F64Args a, int b) {
         }
         const double w = __dsub_rn(div64(p1, p2, o, P), __ddiv_rn(a.v[o], a.theta));
         double g1 = 0.0, g2 = 0.0;
-        if (i % a.img_h != a.img_h - 1)
+        if (i < a.H - 1)
             g1 = __dsub_rn(__dsub_rn(div64(p1, p2, o + P, P), __ddiv_rn(a.v[o + P], a.theta)), w);
-        if (j < a.W - 1)
+        if (j % a.img_w != a.img_w - 1)
             g2 = __dsub_rn(__dsub_rn(div64(p1, p2, o + 1, P), __ddiv_rn(a.v[o + 1], a.theta)), w);
         const double ng = __dsqrt_rn(__dadd_rn(__dmul_rn(g1, g1), __dmul_rn(g2, g2)));
         const double den = __dadd_rn(1.0, __dmul_rn(a.tau, ng));

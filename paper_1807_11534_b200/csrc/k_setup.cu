@@ -166,8 +166,8 @@ __global__ void __launch_bounds__(256) k_setup(SetupArgs a) {
                 msk[e] = fg ? 1 : 0;
                 const bool warm = rd && a.wv != nullptr;
                 v[e] = warm ? WV[e] : u0;
-                p1[e] = (warm && i % a.img_h != a.img_h - 1) ? W1[e] : 0.0f;
-                p2[e] = (warm && jj < a.W - 1) ? W2[e] : 0.0f;
+                p1[e] = (warm && i < a.H - 1) ? W1[e] : 0.0f;
+                p2[e] = (warm && jj % a.img_w != a.img_w - 1) ? W2[e] : 0.0f;
                 rd_count += rd;
             } else {
                 f[e] = 0.0f;

@@ -60,7 +60,8 @@ int stencil_blocks_per_sm(int kf, int stages, bool aligned) {
 
 cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a, int grid,
                            cudaStream_t s) {
-    StencilFn fn = lookup(kf, stages, mode, (a.W & 3) == 0);
+    // the packed path needs every image-last column at lane position 3 of a quad
+    StencilFn fn = lookup(kf, stages, mode, (a.img_w & 3) == 0);
     if (!fn) return cudaErrorInvalidValue;
     if (grid <= 0) return cudaSuccess;
     fn<<<grid, STENCIL_WARPS * 32, STENCIL_SMEM, s>>>(a);

@@ -32,7 +32,6 @@
 // twice.  The row loop is unrolled by two with two state sets (A -> B, B -> A) so the
 // per-row state shift is register renaming, not moves.
 #pragma once
-#include <limits.h>
 #include <math.h>
 
 #include "internal.h"
@@ -159,7 +158,6 @@ struct Ctx {
     float4 *cring;  // this lane's c slot 0; slot stride 32 float4, 2*CR slots
     int64_t pitch;
     int col, H, R0, Rend, n_last;
-    int last0, last1;  // image-last rows (grad_1 = 0) inside this item's march window
     bool store_lane, right_edge;
     Q kx;
     float tau, theta, inv_theta;
@@ -206,10 +204,10 @@ __device__ __forceinline__ Front front(const Q &aw, const Q &inv, const Q &ind, 
     f.w.a = fma2(inv.a, -x.inv_theta, ind.a);
     f.w.b = fma2(inv.b, -x.inv_theta, ind.b);
     float wr = __shfl_down_sync(FULL, aw.a.x, 1);  // x4 of this lane = x0 of the next
-    if (ALIGNED && x.right_edge) wr = aw.b.y;      // grad_2 = 0 on column W-1
+    if (ALIGNED && x.right_edge) wr = aw.b.y;      // grad_2 = 0 on an image's column W-1
     f.g1.a = sub2(f.w.a, aw.a);
     f.g1.b = sub2(f.w.b, aw.b);
-    if (LAST && (m == x.last0 || m == x.last1)) f.g1 = zeroq();  // grad_1 = 0 on an image's last row
+    if (LAST && m == x.H - 1) f.g1 = zeroq();      // grad_1 = 0 on row H-1
     f.g2.a = sub2(aw.b, aw.a);
     f.g2.b = sub2(make_float2(aw.a.y, wr), aw.b);
     if (!ALIGNED) {
@@ -423,9 +421,16 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
         x.Rend = item.r1;
         x.col = item.strip * WV - LH + 4 * lane;
         x.store_lane = (4 * lane >= LH) && (4 * lane < LH + WV);
-        x.right_edge = (x.col + 3 == a.W - 1);
-        x.kx.a = make_float2(x.col == a.W - 1 ? 0.0f : 1.0f, x.col + 2 == a.W - 1 ? 0.0f : 1.0f);
-        x.kx.b = make_float2(x.col + 1 == a.W - 1 ? 0.0f : 1.0f, x.col + 3 == a.W - 1 ? 0.0f : 1.0f);
+        // the Neumann column (grad_2 = 0) of every image: W - 1, or with a batch of images
+        // stacked along columns (rds_create_batch) every img_w-th column; the frame columns
+        // left of 0 give negative x.col + e, never an image-last column
+        {
+            const int iw = a.img_w;
+            auto last_col = [&](int c) { return c >= 0 && c < a.W && c % iw == iw - 1; };
+            x.right_edge = last_col(x.col + 3);
+            x.kx.a = make_float2(last_col(x.col) ? 0.0f : 1.0f, last_col(x.col + 2) ? 0.0f : 1.0f);
+            x.kx.b = make_float2(last_col(x.col + 1) ? 0.0f : 1.0f, last_col(x.col + 3) ? 0.0f : 1.0f);
+        }
         x.p1i = a.p1_in + x.col;
         x.p2i = a.p2_in + x.col;
         x.vi = a.v_in + x.col;
@@ -443,17 +448,7 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
         }
         float acc_u = 0.0f, acc_v = 0.0f;
         // the Neumann row H-1 matters whenever the march (cone included) reaches it
-        // image-last rows (the Neumann row of every image of a batch, img_h rows each; a single
-        // image has one, H - 1) inside the march window [n, n_last]; the item builder keeps the
-        // window shorter than two images, so there are at most two
-        {
-            const int ih = a.img_h;
-            int b0 = n < 0 ? ih - 1 : (n / ih) * ih + ih - 1;
-            if (b0 < n) b0 += ih;
-            x.last0 = b0 <= min(x.n_last, a.H - 1) ? b0 : INT_MIN;
-            x.last1 = b0 + ih <= min(x.n_last, a.H - 1) ? b0 + ih : INT_MIN;
-        }
-        if (x.last0 != INT_MIN)
+        if (x.n_last >= a.H - 1)
             march<S, MODE, ALIGNED, true>(x, n, acc_u, acc_v);
         else
             march<S, MODE, ALIGNED, false>(x, n, acc_u, acc_v);

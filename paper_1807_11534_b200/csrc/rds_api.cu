@@ -33,7 +33,8 @@ static int default_kf(int64_t H, int64_t W) { return H * W <= kSmallPixels ? kSm
 
 struct rds_handle {
     int64_t H = 0, W = 0;
-    int64_t img_h = 0;     // rows per image: H, or the image height of a batch (rds_create_batch)
+    int64_t img_w = 0;     // columns per image: W, or the image width of a batch
+    int64_t batch = 1;     // images stacked along columns (rds_create_batch)
     int64_t pitch = 0;     // elements per padded row (multiple of 32)
     int64_t rows_alloc = 0;
     int64_t plane = 0;     // elements per plane
@@ -158,7 +159,7 @@ int rds_create(int64_t H, int64_t W, rds_t **out) {
     if (!h) return fail(nullptr, RDS_ENOMEM, "rds_create: host allocation failed");
     h->H = H;
     h->W = W;
-    h->img_h = H;
+    h->img_w = W;
     h->pitch = ((PAD_C + W + PAD_C_RIGHT) + 31) / 32 * 32;
     h->rows_alloc = H + 2 * PAD_R;
     h->plane = h->pitch * h->rows_alloc;
@@ -222,15 +223,15 @@ int rds_create(int64_t H, int64_t W, rds_t **out) {
 int rds_create_batch(int64_t B, int64_t H, int64_t W, rds_t **out) {
     if (!out) return fail(nullptr, RDS_EINVAL, "rds_create_batch: out is NULL");
     *out = nullptr;
-    if (B < 1 || H < 32 || W < 1)
-        return fail(nullptr, RDS_EINVAL,
-                    "rds_create_batch: need B >= 1, H >= 32, W >= 1 (got %lld, %lld, %lld)",
+    if (B < 1 || H < 1 || W < 1)
+        return fail(nullptr, RDS_EINVAL, "rds_create_batch: need B, H, W >= 1 (got %lld, %lld, %lld)",
                     (long long)B, (long long)H, (long long)W);
-    if (B * H > (int64_t(1) << 30))
-        return fail(nullptr, RDS_EINVAL, "rds_create_batch: B*H too large");
-    const int rc = rds_create(B * H, W, out);
+    if (B * W > (int64_t(1) << 30))
+        return fail(nullptr, RDS_EINVAL, "rds_create_batch: B*W too large");
+    const int rc = rds_create(H, B * W, out);
     if (rc) return rc;
-    (*out)->img_h = H;
+    (*out)->img_w = W;
+    (*out)->batch = B;
     return RDS_OK;
 }
 
@@ -299,7 +300,27 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
     }
 }
 
+// H x W staging buffer (host transfers of batch layouts and swizzled planes)
+static int need_scratch(rds_t *h) {
+    if (!h->scratch) CK(h, cudaMalloc(&h->scratch, sizeof(double) * h->H * h->W));
+    return RDS_OK;
+}
+
 static int copy_in(rds_t *h, float *plane, const float *src, int on_device) {
+    if (h->batch > 1) {  // dense (B, H, img_w) -> image b at columns [b img_w, (b+1) img_w)
+        int rc = need_scratch(h);
+        if (rc) return rc;
+        const float *d = src;
+        if (!on_device) {
+            CK(h, cudaMemcpyAsync(h->scratch, src, sizeof(float) * h->H * h->W,
+                                  cudaMemcpyHostToDevice, h->stream));
+            d = h->scratch;
+        }
+        CK(h, launch_batch_copy(const_cast<float *>(d), h->at(plane), 4, h->pitch, (int)h->H,
+                                (int)h->img_w, (int)h->batch, 1, 0, h->stream));
+        if (!on_device) CK(h, cudaStreamSynchronize(h->stream));
+        return RDS_OK;
+    }
     cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     CK(h, cudaMemcpy2DAsync(h->at(plane), sizeof(float) * h->pitch, src, sizeof(float) * h->W,
                             sizeof(float) * h->W, h->H, kind, h->stream));
@@ -437,7 +458,7 @@ int rds_solve_q(rds_t *h, float lambda, float theta, float tau, double q, int32_
 
 // Resident stencil CTAs per SM for (kf, stages), cached (occupancy API).
 static int blocks_per_sm(rds_t *h, int kf, int stages) {
-    const bool aligned = (h->W & 3) == 0;
+    const bool aligned = (h->img_w & 3) == 0;
     int &slot = h->bps[kf][stages];
     if (slot <= 0) slot = stencil_blocks_per_sm(kf, stages, aligned);
     const int b = slot > 0 ? slot : 1;
@@ -511,7 +532,7 @@ static cudaError_t enqueue_plan(rds_t *h, const LaunchPlan *plan, int n, int kf,
     a.pitch = h->pitch;
     a.H = (int)h->H;
     a.W = (int)h->W;
-    a.img_h = (int)h->img_h;
+    a.img_w = (int)h->img_w;
     a.tau = tau;
     a.theta = theta;
     a.inv_theta = 1.0f / theta;
@@ -760,7 +781,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     s.pitch = h->pitch;
     s.H = (int)h->H;
     s.W = (int)h->W;
-    s.img_h = (int)h->img_h;
+    s.img_w = (int)h->img_w;
     s.c1 = h->c1;
     s.c2 = h->c2;
     s.gamma = h->gamma;
@@ -773,13 +794,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
                             h->band_flag, h->stream));
     {
         const int slots = h->n_sm * blocks_per_sm(h, kf, kf) * STENCIL_WARPS;
-        // a batch keeps every item's march window (rows + 2 kf + 4) within two images, so it
-        // meets at most two image-last rows (k_stencil_impl.cuh)
-        int max_chunk = 1 << 30;
-        if (h->img_h < h->H) {
-            max_chunk = (int)((2 * h->img_h - 2 * kf - 6) / ITEM_Q * ITEM_Q);
-            if (max_chunk < ITEM_Q) max_chunk = ITEM_Q;
-        }
+        const int max_chunk = 1 << 30;
         CK(h, launch_build_items(h->band_flag, n_strips, n_bands, (int)h->H, slots, fixed_chunk,
                                  max_chunk,
                                  2 * kf + 4, h->items, h->counts, h->stream));
@@ -900,7 +915,24 @@ static int resolve(rds_t *h) {
     return RDS_OK;
 }
 
+// batch layout -> dense (B, H, img_w); elt 4 (float, swizzled or not) or 1 (bytes)
+static int batch_out(rds_t *h, void *dst, const void *plane_origin, int elt, int swizzled,
+                     int on_device) {
+    int rc = need_scratch(h);
+    if (rc) return rc;
+    void *d = on_device ? dst : (void *)h->scratch;
+    CK(h, launch_batch_copy(d, const_cast<void *>(plane_origin), elt, h->pitch, (int)h->H,
+                            (int)h->img_w, (int)h->batch, 0, swizzled, h->stream));
+    if (!on_device) {
+        CK(h, cudaMemcpyAsync(dst, d, (size_t)elt * h->H * h->W, cudaMemcpyDeviceToHost,
+                              h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+    }
+    return RDS_OK;
+}
+
 static int copy_out(rds_t *h, void *dst, const void *plane_origin, size_t elt, int on_device) {
+    if (h->batch > 1) return batch_out(h, dst, plane_origin, (int)elt, 0, on_device);
     cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     CK(h, cudaMemcpy2DAsync(dst, elt * h->W, plane_origin, elt * h->pitch, elt * h->W, h->H,
                             kind, h->stream));
@@ -911,12 +943,16 @@ static int copy_out(rds_t *h, void *dst, const void *plane_origin, size_t elt, i
 // Getter of a quad-swizzled state plane (rho1, rho2, v; internal.h): unswizzled by a
 // kernel, straight into a device destination or through a staging buffer for the host.
 static int copy_out_swizzled(rds_t *h, float *dst, const float *plane_origin, int on_device) {
+    if (h->batch > 1) return batch_out(h, dst, plane_origin, 4, 1, on_device);
     if (on_device) {
         CK(h, launch_unswizzle(plane_origin, h->pitch, (int)h->H, (int)h->W, dst, h->W,
                                h->stream));
         return RDS_OK;
     }
-    if (!h->scratch) CK(h, cudaMalloc(&h->scratch, sizeof(float) * h->H * h->W));
+    {
+        const int rc = need_scratch(h);
+        if (rc) return rc;
+    }
     CK(h, launch_unswizzle(plane_origin, h->pitch, (int)h->H, (int)h->W, h->scratch, h->W,
                            h->stream));
     CK(h, cudaMemcpyAsync(dst, h->scratch, sizeof(float) * h->H * h->W, cudaMemcpyDeviceToHost,
@@ -1008,7 +1044,7 @@ int rds_energy(rds_t *h, rds_energy_t *out) {
     a.pitch = h->pitch;
     a.H = (int)h->H;
     a.W = (int)h->W;
-    a.img_h = (int)h->img_h;
+    a.img_w = (int)h->img_w;
     a.partials = h->e_partials;
     a.out = h->e_out;
     a.lambda = h->lambda;
@@ -1093,7 +1129,7 @@ int rds_solve_gt(rds_t *h, float lambda, float theta, float tau, float delta,
     a.pitch = h->pitch;
     a.H = (int)h->H;
     a.W = (int)h->W;
-    a.img_h = (int)h->img_h;
+    a.img_w = (int)h->img_w;
     a.c1 = h->c1;
     a.c2 = h->c2;
     a.gamma = h->gamma;
@@ -1205,6 +1241,7 @@ int rds_get_u_gt(rds_t *h, double *out, int on_device) {
     if (!h) return fail(nullptr, RDS_EINVAL, "rds_get_u_gt: NULL handle");
     if (!h->have_gt) return fail(h, RDS_ESTATE, "rds_get_u_gt: no rds_solve_gt has run yet");
     if (!out) return fail(h, RDS_EINVAL, "rds_get_u_gt: NULL out");
+    if (h->batch > 1) return batch_out(h, out, h->d64 + h->plane + h->origin, 8, 0, on_device);
     const cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     CK(h, cudaMemcpy2DAsync(out, sizeof(double) * h->W, h->d64 + h->plane + h->origin,
                             sizeof(double) * h->pitch, sizeof(double) * h->W, h->H, kind,

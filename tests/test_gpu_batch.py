@@ -33,7 +33,8 @@ def _check(g, o, ctx):
 
 
 @pytest.mark.parametrize("B,H,W,delta_rel,kf", [(5, 40, 70, 0.3, 0), (3, 33, 129, math.inf, 0),
-                                               (7, 45, 64, 0.4, 7), (2, 96, 50, 0.2, 3)])
+                                               (7, 45, 64, 0.4, 7), (2, 96, 50, 0.2, 3),
+                                               (9, 17, 13, 0.3, 0), (4, 1, 30, math.inf, 5)])
 def test_batch_equals_independent_solves(rds, orc, B, H, W, delta_rel, kf):
     rng = np.random.default_rng(B * 1000 + H)
     z = rng.uniform(0, 1, (B, H, W)).astype(np.float32)
@@ -49,7 +50,7 @@ def test_batch_equals_independent_solves(rds, orc, B, H, W, delta_rel, kf):
     for b in range(B):
         o = orc.solve(f[b], delta, 4.0, np.float32(0.1), 0.125, 60)
         _check({k: x[b] for k, x in g.items()}, o, f"image {b}")
-        assert not g["p1"][b][-1].any()          # each image's own Neumann row
+        assert not g["p1"][b][-1].any() and not g["p2"][b][:, -1].any()  # own Neumann rows/cols
         e = orc.energy(f[b], 4.0, g["u"][b], g["v"][b], g["p1"][b], g["p2"][b])
         for k in e_tot:
             e_tot[k] += e[k]
@@ -77,6 +78,6 @@ def test_batch_of_paper_size_images(rds, orc):
 
 def test_batch_errors(rds):
     with pytest.raises(rds.RdsError):
-        rds.BatchSolver(4, 16, 16)   # images shorter than 32 rows are not supported
-    with pytest.raises(rds.RdsError):
         rds.BatchSolver(0, 64, 16)
+    with pytest.raises(rds.RdsError):
+        rds.BatchSolver(3, 64, 0)
