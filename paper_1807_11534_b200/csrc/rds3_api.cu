@@ -8,6 +8,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <string>
 
 #include "internal.h"
@@ -268,6 +270,10 @@ int rds3_solve(rds3_t *h, float lambda, float theta, float tau, float delta, int
         return fail3(h, RDS_EINVAL, "rds3_solve: need delta >= 0, iters >= 0");
     if (!h->have_image || !h->have_fitting)
         return fail3(h, RDS_ESTATE, "rds3_solve: image and fitting must be set first");
+    nvtxRangePushA("rds3_solve");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
     // z-chunk per CTA: enough CTAs for ~4 waves of 4 resident CTAs per SM, >= 8 planes
     {
         const int64_t tiles = vol_tiles(h->H, h->W);

@@ -11,6 +11,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <string>
 
 #include "internal.h"
@@ -21,6 +23,12 @@ using namespace rds;
 namespace {
 
 thread_local std::string g_last_error;
+
+// NVTX range for profilers (nsys / ncu --nvtx): one per host phase of a solve
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // Default iterations per HBM round trip (DESIGN.md §5 sweeps): 7 where HBM traffic matters
 // (C2 and larger); 4 for images of <= 2^21 pixels, whose solves are bound by item latency
@@ -756,6 +764,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
         }
     }
 
+    NvtxRange nvtx_solve(check_every > 0 ? "rds_solve_tol" : "rds_solve");
     if (h->opt_timing) CK(h, cudaEventRecord(h->ev[0], h->stream));
     SetupArgs s{};
     s.z = h->at(h->z);
@@ -1034,6 +1043,7 @@ int rds_tile_shape(int *th, int *tw) {
 
 int rds_energy(rds_t *h, rds_energy_t *out) {
     NEED_SOLVED("rds_energy");
+    NvtxRange nvtx_energy("rds_energy");
     if (!out) return fail(h, RDS_EINVAL, "rds_energy: NULL out");
     EnergyArgs a{};
     a.f = h->at(h->f);
@@ -1099,6 +1109,7 @@ int rds_solve_gt(rds_t *h, float lambda, float theta, float tau, float delta,
         return fail(h, RDS_ESTATE, "rds_solve_gt: image and fitting must be set first");
     if (!h->image_ok || !h->p_ok)
         return fail(h, RDS_EINVAL, "rds_solve_gt: image or P has non-finite values");
+    NvtxRange nvtx_gt("rds_solve_gt");
     const int nb = f64_grid(h->H * h->W);
     if (!h->d64) {
         CK(h, cudaMalloc(&h->d64, sizeof(double) * h->plane * 7));
