@@ -239,6 +239,12 @@ int rds_energy(rds_t *h, rds_energy_t *out);
 /* Statistics of the last solve (synchronises the stream). */
 int rds_get_stats(rds_t *h, rds_stats_t *out);
 
+/* Diagnostic (memory safety without a sanitizer): the number of elements in the padded frame
+ * around the image, over every device plane, that no longer hold the pinned value they were
+ * allocated with (rho = v = u = f = z = 0, c' = +inf, labels = mask = 0).  Any nonzero count
+ * means a kernel wrote outside the image.  Synchronous. */
+int rds_check_frame(rds_t *h, int64_t *bad_count);
+
 /* Supported RDS_OPT_KFUSE values: writes up to cap values into out, returns how many exist. */
 int rds_kfuse_supported(int32_t *out, int cap);
 

@@ -212,6 +212,11 @@ cudaError_t launch_vol_copy_u8(uint8_t *dst, const uint8_t *src, int64_t plane, 
 // out[i * out_pitch + j] = plane[i * pitch + swz(j)]: natural-order copy of a swizzled plane
 cudaError_t launch_unswizzle(const float *plane, int64_t pitch, int H, int W, float *out,
                              int64_t out_pitch, cudaStream_t s);
+// Count frame elements of a padded plane that no longer hold their pinned value.
+cudaError_t launch_frame_check(const void *base, int elt, int64_t pitch, int64_t rows,
+                               int64_t origin_row, int64_t origin_col, int H, int W,
+                               int swizzled, double expect, unsigned long long *bad,
+                               cudaStream_t s);
 // Batch layout (rds_create_batch): image b of B (H x img_w each) occupies columns
 // [b img_w, (b+1) img_w) of the H x (B img_w) planes.  Dense (B, H, img_w) <-> plane copies
 // (elt = 8, 4 or 1 bytes; swizzled = the plane is quad-swizzled, for rho and v).

@@ -122,6 +122,45 @@ cudaError_t launch_batch_copy(void *dense, void *plane, int elt, int64_t pitch, 
     return cudaGetLastError();
 }
 
+// Frame integrity (a memory-safety check that needs no sanitizer): every element of a padded
+// plane outside the H x W image must still hold the pinned frame value it was allocated with.
+// Counts the elements that differ (natural-order column index mapped through the swizzle for
+// swizzled planes).
+template <typename T>
+__global__ void k_frame_check(const T *base, int64_t pitch, int64_t rows, int64_t origin_row,
+                              int64_t origin_col, int H, int W, int swizzled, T expect,
+                              unsigned long long *bad) {
+    const int64_t n = rows * pitch;
+    unsigned long long cnt = 0;
+    // k enumerates LOGICAL positions (row r, column c of the padded plane); a frame position
+    // (outside the image) is looked up where it is stored: column c itself, or its swizzled
+    // column for quad-swizzled planes (the swizzle stays inside an aligned quad)
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = k / pitch, c = k - r * pitch;
+        const int64_t i = r - origin_row, j = c - origin_col;
+        if (i >= 0 && i < H && j >= 0 && j < W) continue;  // image element
+        const int64_t cc = (swizzled ? (int64_t)swz((int)j) : j) + origin_col;
+        if (!(base[r * pitch + cc] == expect)) ++cnt;
+    }
+    if (cnt) atomicAdd(bad, cnt);
+}
+
+cudaError_t launch_frame_check(const void *base, int elt, int64_t pitch, int64_t rows,
+                               int64_t origin_row, int64_t origin_col, int H, int W,
+                               int swizzled, double expect, unsigned long long *bad,
+                               cudaStream_t s) {
+    if (elt == 4)
+        k_frame_check<float><<<148 * 4, 256, 0, s>>>((const float *)base, pitch, rows,
+                                                      origin_row, origin_col, H, W, swizzled,
+                                                      (float)expect, bad);
+    else
+        k_frame_check<uint8_t><<<148 * 4, 256, 0, s>>>((const uint8_t *)base, pitch, rows,
+                                                        origin_row, origin_col, H, W, swizzled,
+                                                        (uint8_t)expect, bad);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_unswizzle(const float *plane, int64_t pitch, int H, int W, float *out,
                              int64_t out_pitch, cudaStream_t s) {
     k_unswizzle<<<148 * 8, 256, 0, s>>>(plane, pitch, H, W, out, out_pitch);

@@ -1277,6 +1277,38 @@ int rds_compare_gt(rds_t *h, float eps, double *e1, double *e2) {
     return RDS_OK;
 }
 
+int rds_check_frame(rds_t *h, int64_t *bad_count) {
+    if (!h || !bad_count) return fail(h, RDS_EINVAL, "rds_check_frame: NULL argument");
+    {
+        const int rc = resolve(h);
+        if (rc) return rc;
+    }
+    unsigned long long *bad = nullptr;
+    CK(h, cudaMalloc(&bad, sizeof *bad));
+    cudaError_t e = cudaMemsetAsync(bad, 0, sizeof *bad, h->stream);
+    struct P {
+        const void *base;
+        int elt, swz;
+        double expect;
+    };
+    const P planes[] = {{h->p1[0], 4, 1, 0.0}, {h->p1[1], 4, 1, 0.0}, {h->p2[0], 4, 1, 0.0},
+                        {h->p2[1], 4, 1, 0.0}, {h->v[0], 4, 1, 0.0},  {h->v[1], 4, 1, 0.0},
+                        {h->c, 4, 1, INFINITY},  {h->u, 4, 0, 0.0},    {h->f, 4, 0, 0.0},
+                        {h->z, 4, 0, 0.0},       {h->mask, 1, 0, 0.0}, {h->lab, 1, 0, 0.0}};
+    for (const P &q : planes)
+        if (e == cudaSuccess)
+            e = launch_frame_check(q.base, q.elt, h->pitch, h->rows_alloc, PAD_R, PAD_C,
+                                   (int)h->H, (int)h->W, q.swz, q.expect, bad, h->stream);
+    unsigned long long n = 0;
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(&n, bad, sizeof n, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    cudaFree(bad);
+    CK(h, e);
+    *bad_count = (int64_t)n;
+    return RDS_OK;
+}
+
 int rds_kfuse_supported(int32_t *out, int cap) { return kf_list(out, cap); }
 
 const char *rds_last_error(rds_t *h) {

@@ -33,6 +33,7 @@ EXPORTS = (
     "rds_get_active_tiles", "rds_tile_shape", "rds_energy", "rds_get_stats",
     "rds_kfuse_supported", "rds_last_error", "rds_version", "rds_band_for_fraction",
     "rds_solve_q", "rds_solve_tol", "rds_solve_gt", "rds_get_u_gt", "rds_compare_gt",
+    "rds_check_frame",
     "rds3_create", "rds3_destroy", "rds3_set_stream", "rds3_set_kz", "rds3_set_image",
     "rds3_set_fitting",
     "rds3_fitting_absmax", "rds3_solve", "rds3_get_u", "rds3_get_v", "rds3_get_p",
@@ -112,6 +113,7 @@ def _load():
         "rds_solve_gt": [P, f, f, f, f, i32, ctypes.c_double, i32, ctypes.POINTER(rds_gt_t)],
         "rds_get_u_gt": [P, P, i],
         "rds_compare_gt": [P, f, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
+        "rds_check_frame": [P, ctypes.POINTER(i64)],
         "rds3_create": [i64, i64, i64, ctypes.POINTER(P)],
         "rds3_destroy": [P],
         "rds3_set_stream": [P, P],
@@ -447,6 +449,12 @@ class Solver:
 
     def stats(self):
         return rds_get_stats(self.h)
+
+    def check_frame(self):
+        """Frame elements outside the image that kernels overwrote (must be 0)."""
+        n = ctypes.c_int64()
+        _check(_lib.rds_check_frame(self.h, ctypes.byref(n)), self.h)
+        return n.value
 
 
 # ------------------------------------------------------------------------------------------

@@ -585,3 +585,27 @@ def test_solve_tol_c3_full_size(rds, orc):
     p1, p2 = s.p()
     compare(dict(u=s.u(), v=s.v(), p1=p1, p2=p2, mask=s.mask()), o, ctx="C3 tol")
     s.close()
+
+
+@pytest.mark.parametrize("shape,kf", [((37, 61), 0), ((64, 128), 7), ((5, 3), 2),
+                                      ((130, 250), 5), ((33, 129), 8)])
+def test_frame_untouched(rds, shape, kf):
+    """Memory safety without a sanitizer (compute-sanitizer is closed on this pool): after
+    solves in every launch mode, warm starts, tolerance and fp64 solves, no element of the
+    padded frame around the image has changed (rds_check_frame)."""
+    H, W = shape
+    z = np.random.default_rng(H * W).uniform(0, 1, shape).astype(np.float32)
+    s = rds.Solver(H, W, k_fuse=kf)
+    s.set_image(z)
+    s.set_fitting(0.75, 0.25, 1.5, np.random.default_rng(1).uniform(0, 1, shape).astype(np.float32))
+    d = 0.3 * s.absmax()
+    s.solve(4.0, 0.1, 0.125, d, 23)
+    assert s.check_frame() == 0
+    s.solve_tol(4.0, 0.1, 0.125, d, 40, 1e-3, 3)
+    assert s.check_frame() == 0
+    s.set_state(s.v(), *s.p())
+    s.solve(4.0, 0.1, 0.125, math.inf, 9)
+    s.solve_gt(4.0, 0.1, 0.125, math.inf, 30, 1e-6, 7)
+    s.energy()
+    assert s.check_frame() == 0
+    s.close()
