@@ -4,8 +4,9 @@
 //   fit(w) = sum f w
 //   D(rho) = sum min(0, lambda f + div rho)   (Lagrangian dual of Eq. 4 over u in [0,1])
 // for w = v and w = clamp(u, 0, 1).  Per-pixel terms in float32, per-thread/warp/block sums
-// in float64; the grid has a fixed size and a fixed pixel -> thread assignment and the two
-// passes combine partials in a fixed order, so the result is bit-reproducible.
+// in float64; the grid has a fixed size and a fixed pixel -> thread assignment (rows to CTAs,
+// columns to threads) and the two passes combine partials in a fixed order, so the result is
+// bit-reproducible.
 #include "internal.h"
 
 namespace rds {
@@ -21,30 +22,36 @@ __device__ __forceinline__ double warp_sum(double x) {
 __device__ __forceinline__ float clamp01(float x) { return fminf(fmaxf(x, 0.0f), 1.0f); }
 
 __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
-    const int64_t n = (int64_t)a.H * a.W;
     const int64_t pitch = a.pitch;
     double acc[NE] = {0, 0, 0, 0, 0};
-    for (int64_t k = blockIdx.x * 256 + threadIdx.x; k < n; k += (int64_t)gridDim.x * 256) {
-        const int i = (int)(k / a.W), j = (int)(k - (int64_t)i * a.W);
-        const int64_t o = (int64_t)i * pitch + j;
-        const int64_t os = (int64_t)i * pitch + swz(j);  // v, rho are quad-swizzled
-        const int64_t osr = (int64_t)i * pitch + swz(j + 1), osl = (int64_t)i * pitch + swz(j - 1);
-        const bool down = i < a.H - 1, right = j % a.img_w != a.img_w - 1;
-        const float v = a.v[os];
-        const float gv1 = down ? a.v[os + pitch] - v : 0.0f;
-        const float gv2 = right ? a.v[osr] - v : 0.0f;
-        const float cu = clamp01(a.u[o]);
-        const float gu1 = down ? clamp01(a.u[o + pitch]) - cu : 0.0f;
-        const float gu2 = right ? clamp01(a.u[o + 1]) - cu : 0.0f;
-        const float f = a.f[o];
-        // rho1 on row H-1 and rho2 on column W-1 are identically 0; the frame holds 0
-        const float dv = a.p1[os] - a.p1[os - pitch] + a.p2[os] - a.p2[osl];
-        const float t = a.lambda * f + dv;
-        acc[0] += (double)sqrtf(gv1 * gv1 + gv2 * gv2);
-        acc[1] += (double)f * (double)v;
-        acc[2] += (double)sqrtf(gu1 * gu1 + gu2 * gu2);
-        acc[3] += (double)f * (double)cu;
-        acc[4] += (double)fminf(t, 0.0f);
+    // fixed pixel -> thread map: CTA b takes rows b, b + G, ...; thread t columns t, t + 256, ...
+    for (int i = blockIdx.x; i < a.H; i += gridDim.x) {
+        const int64_t row = (int64_t)i * pitch;
+        const bool down = i < a.H - 1;
+        int jm = threadIdx.x % a.img_w;  // column within its image (batches)
+        for (int j = threadIdx.x; j < a.W; j += 256) {
+            const int64_t o = row + j;
+            const int64_t os = row + swz(j);  // v, rho are quad-swizzled
+            const bool right = jm != a.img_w - 1;
+            const float v = a.v[os];
+            const float gv1 = down ? a.v[os + pitch] - v : 0.0f;
+            const float gv2 = right ? a.v[row + swz(j + 1)] - v : 0.0f;
+            const float cu = clamp01(a.u[o]);
+            const float gu1 = down ? clamp01(a.u[o + pitch]) - cu : 0.0f;
+            const float gu2 = right ? clamp01(a.u[o + 1]) - cu : 0.0f;
+            const float f = a.f[o];
+            // rho1 on row H-1 and rho2 on an image's last column are identically 0; the frame
+            // holds 0
+            const float dv = a.p1[os] - a.p1[os - pitch] + a.p2[os] - a.p2[row + swz(j - 1)];
+            const float t = a.lambda * f + dv;
+            acc[0] += (double)sqrtf(gv1 * gv1 + gv2 * gv2);
+            acc[1] += (double)f * (double)v;
+            acc[2] += (double)sqrtf(gu1 * gu1 + gu2 * gu2);
+            acc[3] += (double)f * (double)cu;
+            acc[4] += (double)fminf(t, 0.0f);
+            jm += 256;
+            while (jm >= a.img_w) jm -= a.img_w;
+        }
     }
     __shared__ double sh[8][NE];
 #pragma unroll
