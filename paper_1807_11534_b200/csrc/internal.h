@@ -123,16 +123,16 @@ cudaError_t launch_setup(const SetupArgs &a, cudaStream_t s);
 // counts[0] = number of nonzero flags; if sum_out != null also the int64 sum of the values.
 cudaError_t launch_compact(const int32_t *flags, int n, int32_t *list, int32_t *count,
                            long long *sum_out, cudaStream_t s);
-// band_flag[s * n_bands + b] = 1 iff strip s (output columns [s*wv, (s+1)*wv)) overlaps an
-// active 32x32 tile in tile row b (skip = 0 marks everything active).
+// band_bits[s * ceil(n_bands/32) + b/32] bit b%32 = 1 iff strip s (output columns
+// [s*wv, (s+1)*wv)) overlaps an 8-row band b holding an RD pixel (skip = 0: every band).
 cudaError_t launch_band_flags(const int32_t *sub_rd, int H, int W, int wv, int n_strips,
-                              int skip, int32_t *band_flag, cudaStream_t s);
+                              int skip, uint32_t *band_bits, cudaStream_t s);
 // Work items from the band flags: maximal vertical runs of active bands per strip, each split
 // into ceil(rows / chunk) near-equal pieces at ITEM_Q-row boundaries.  chunk = fixed_chunk
 // rounded up to ITEM_Q if > 0, else the candidate height minimising
 // ceil(items / slots) * (chunk + warmup_rows) (makespan model, k_setup.cu).
 // out: items, counts[1] = number of items, counts[2] = chunk rows, counts[3] = active cells.
-cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands, int H,
+cudaError_t launch_build_items(const uint32_t *band_bits, int n_strips, int n_bands, int H,
                                int slots, int fixed_chunk, int max_chunk, int warmup_rows,
                                Item *items, int32_t *counts, cudaStream_t s);
 

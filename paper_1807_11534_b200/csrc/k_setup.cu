@@ -281,29 +281,60 @@ cudaError_t launch_compact(const int32_t *flags, int n, int32_t *list, int32_t *
 // reproduces its value exactly, so any superset of the needed work gives the same result;
 // skip = 0 marks every band active.
 __global__ void k_band_flags(const int32_t *sub_rd, int H, int W, int wv, int n_strips,
-                             int skip, int32_t *band_flag) {
-    const int n_bands = (H + BAND_H - 1) / BAND_H;
-    const int it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (it >= n_strips * n_bands) return;
-    const int s = it / n_bands, b = it - s * n_bands;
-    if (!skip) {
-        band_flag[it] = 1;
-        return;
-    }
-    const int ntj = (W + TILE_W - 1) / TILE_W;
-    const int ti = b / SUBTILES, k = b - ti * SUBTILES;
-    const int j0 = s * wv, j1 = min(W, (s + 1) * wv) - 1;
+                             int skip, uint32_t *band_bits) {
+    const int n_bands = (H + BAND_H - 1) / BAND_H, nbw = (n_bands + 31) / 32;
+    const int it = blockIdx.x * blockDim.x + threadIdx.x;  // s * nbw * 32 + b: a warp = one word
+    if (it >= n_strips * nbw * 32) return;                  // whole warps only (see launch)
+    const int s = it / (nbw * 32), b = it - s * nbw * 32;
     int on = 0;
-    for (int tj = j0 / TILE_W; tj <= j1 / TILE_W; ++tj)
-        on |= sub_rd[(ti * ntj + tj) * SUBTILES + k] != 0;
-    band_flag[it] = on;
+    if (b < n_bands) {
+        if (!skip) {
+            on = 1;
+        } else {
+            const int ntj = (W + TILE_W - 1) / TILE_W;
+            const int ti = b / SUBTILES, k = b - ti * SUBTILES;
+            const int j0 = s * wv, j1 = min(W, (s + 1) * wv) - 1;
+            for (int tj = j0 / TILE_W; tj <= j1 / TILE_W; ++tj)
+                on |= sub_rd[(ti * ntj + tj) * SUBTILES + k] != 0;
+        }
+    }
+    const uint32_t word = __ballot_sync(0xffffffffu, on);
+    if ((threadIdx.x & 31) == 0) band_bits[it >> 5] = word;
 }
 
 cudaError_t launch_band_flags(const int32_t *sub_rd, int H, int W, int wv, int n_strips,
-                              int skip, int32_t *band_flag, cudaStream_t s) {
-    const int n = n_strips * ((H + BAND_H - 1) / BAND_H);
-    k_band_flags<<<(n + 255) / 256, 256, 0, s>>>(sub_rd, H, W, wv, n_strips, skip, band_flag);
+                              int skip, uint32_t *band_bits, cudaStream_t s) {
+    const int nbw = ((H + BAND_H - 1) / BAND_H + 31) / 32;
+    const int n = n_strips * nbw * 32;  // a multiple of 32: every warp is complete
+    k_band_flags<<<(n + 255) / 256, 256, 0, s>>>(sub_rd, H, W, wv, n_strips, skip, band_bits);
     return cudaGetLastError();
+}
+
+// The next run [b, e) of set bits at or after position *pos in a strip's band bitmask
+// (nbw words); false when there is none.  *pos is left at e.
+__device__ bool next_run(const uint32_t *bits, int nbw, int *pos, int *b, int *e) {
+    int p = *pos, w = p >> 5;
+    if (w >= nbw) return false;
+    uint32_t x = bits[w] & (0xffffffffu << (p & 31));
+    while (x == 0) {
+        if (++w >= nbw) return false;
+        x = bits[w];
+    }
+    *b = (w << 5) + __ffs(x) - 1;
+    // run end: first clear bit after b
+    p = *b;
+    uint32_t y = ~bits[w] & (0xffffffffu << (p & 31));
+    while (y == 0) {
+        if (++w >= nbw) {
+            *e = nbw << 5;
+            *pos = *e;
+            return true;
+        }
+        y = ~bits[w];
+    }
+    *e = (w << 5) + __ffs(y) - 1;
+    *pos = *e;
+    return true;
 }
 
 // Item rows are cut at multiples of ITEM_Q rows (finer than a 32-row band), so a sparse
@@ -314,16 +345,9 @@ constexpr int N_CHUNK = 15;
 
 // Runs of active bands in strip s (rows clipped to H), split into ceil(rows / chunk) pieces of
 // near-equal height at ITEM_Q-row boundaries; out == nullptr only counts.
-__device__ int strip_items(const int32_t *flags, int n_bands, int H, int chunk, int s,
-                           Item *out) {
-    int n = 0, b = 0;
-    while (b < n_bands) {
-        if (!flags[b]) {
-            ++b;
-            continue;
-        }
-        int e = b;
-        while (e < n_bands && flags[e]) ++e;
+__device__ int strip_items(const uint32_t *bits, int nbw, int H, int chunk, int s, Item *out) {
+    int n = 0, pos = 0, b, e;
+    while (next_run(bits, nbw, &pos, &b, &e)) {
         const int r0 = b * BAND_H, r1 = min(e * BAND_H, H);
         const int q = (r1 - r0 + ITEM_Q - 1) / ITEM_Q;            // ITEM_Q-row slices
         const int pieces = (r1 - r0 + chunk - 1) / chunk;
@@ -335,7 +359,6 @@ __device__ int strip_items(const int32_t *flags, int n_bands, int H, int chunk, 
             }
             ++n;
         }
-        b = e;
     }
     return n;
 }
@@ -348,7 +371,7 @@ __device__ int strip_items(const int32_t *flags, int n_bands, int H, int chunk, 
 // launch), the last round set by the tallest item; ties go to the taller item.
 // (2) Per-strip item counts -> block exclusive scan -> items written in strip-major,
 // ascending-row order (deterministic, no atomics).
-__global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, int n_strips,
+__global__ void __launch_bounds__(1024) k_build_items(const uint32_t *band_bits, int n_strips,
                                                       int n_bands, int H, int slots,
                                                       int fixed_chunk, int max_chunk,
                                                       int warmup_rows, Item *items,
@@ -360,22 +383,16 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
     long long cnt_c[N_CHUNK + 2];  // items per candidate, active cells, active rows
 #pragma unroll
     for (int k = 0; k <= N_CHUNK + 1; ++k) cnt_c[k] = 0;
+    const int nbw = (n_bands + 31) / 32;
     for (int sidx = tid; sidx < n_strips; sidx += 1024) {
-        const int32_t *fl = band_flag + (int64_t)sidx * n_bands;
-        int b = 0;
-        while (b < n_bands) {
-            if (!fl[b]) {
-                ++b;
-                continue;
-            }
-            int e = b;
-            while (e < n_bands && fl[e]) ++e;
+        const uint32_t *bits = band_bits + (int64_t)sidx * nbw;
+        int pos = 0, b, e;
+        while (next_run(bits, nbw, &pos, &b, &e)) {
             const int rows = min(e * BAND_H, H) - b * BAND_H;
 #pragma unroll
             for (int k = 0; k < N_CHUNK; ++k) cnt_c[k] += (rows + kChunkRows[k] - 1) / kChunkRows[k];
             cnt_c[N_CHUNK] += e - b;  // active cells
             cnt_c[N_CHUNK + 1] += rows;
-            b = e;
         }
     }
 #pragma unroll
@@ -414,8 +431,8 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
     const int chunk = chunk_s;
     for (int s0 = 0; s0 < n_strips; s0 += 1024) {
         const int sidx = s0 + tid;
-        const int cnt = sidx < n_strips ? strip_items(band_flag + (int64_t)sidx * n_bands, n_bands,
-                                                      H, chunk, sidx, nullptr)
+        const int cnt = sidx < n_strips ? strip_items(band_bits + (int64_t)sidx * nbw, nbw, H,
+                                                      chunk, sidx, nullptr)
                                         : 0;
         // block exclusive scan of cnt
         int incl = cnt;
@@ -437,8 +454,7 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
         __syncthreads();
         const int start = base_s + off[wid] + incl - cnt;
         if (sidx < n_strips)
-            strip_items(band_flag + (int64_t)sidx * n_bands, n_bands, H, chunk, sidx,
-                        items + start);
+            strip_items(band_bits + (int64_t)sidx * nbw, nbw, H, chunk, sidx, items + start);
         __syncthreads();
         if (tid == 1023) base_s = start + cnt;
         __syncthreads();
@@ -452,10 +468,10 @@ __global__ void __launch_bounds__(1024) k_build_items(const int32_t *band_flag, 
     }
 }
 
-cudaError_t launch_build_items(const int32_t *band_flag, int n_strips, int n_bands, int H,
+cudaError_t launch_build_items(const uint32_t *band_bits, int n_strips, int n_bands, int H,
                                int slots, int fixed_chunk, int max_chunk, int warmup_rows,
                                Item *items, int32_t *counts, cudaStream_t s) {
-    k_build_items<<<1, 1024, 0, s>>>(band_flag, n_strips, n_bands, H, slots, fixed_chunk,
+    k_build_items<<<1, 1024, 0, s>>>(band_bits, n_strips, n_bands, H, slots, fixed_chunk,
                                      max_chunk, warmup_rows, items, counts);
     return cudaGetLastError();
 }

@@ -57,7 +57,7 @@ struct rds_handle {
     // tiles / items
     int n_tiles = 0;
     int32_t *tile_rd = nullptr, *tile_list = nullptr, *sub_rd = nullptr;
-    int32_t *band_flag = nullptr;    // [strip][band] active flags
+    uint32_t *band_flag = nullptr;   // [strip][band word] active-band bitmasks
     Item *items = nullptr;           // stencil work items
     int32_t *queue = nullptr;        // per-launch work counters
     size_t band_bytes = 0, items_bytes = 0, queue_bytes = 0;
@@ -741,10 +741,10 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
         void *pf = h->band_flag, *pi = h->items, *pq = h->queue;
         const bool realloc_items = sizeof(Item) * (size_t)max_items > h->items_bytes;
         const bool realloc_queue = sizeof(int32_t) * (size_t)n_queue > h->queue_bytes;
-        CK(h, grow(&pf, &h->band_bytes, sizeof(int32_t) * (size_t)n_strips * n_bands));
+        CK(h, grow(&pf, &h->band_bytes, sizeof(uint32_t) * (size_t)n_strips * ((n_bands + 31) / 32)));
         CK(h, grow(&pi, &h->items_bytes, sizeof(Item) * (size_t)max_items));
         CK(h, grow(&pq, &h->queue_bytes, sizeof(int32_t) * (size_t)n_queue));
-        h->band_flag = (int32_t *)pf;
+        h->band_flag = (uint32_t *)pf;
         h->items = (Item *)pi;
         h->queue = (int32_t *)pq;
         if (check_every > 0) {
