@@ -1,6 +1,8 @@
 // k_stencil.cu -- dispatch of K3 (the stencil kernel template lives in k_stencil_impl.cuh,
 // its instantiations in k_stencil_kf<K>.cu): kernel lookup by (k_fuse, stages, mode,
 // alignment), occupancy, launch.
+#include <stdlib.h>
+
 #include "k_stencil_impl.cuh"
 
 namespace rds {
@@ -64,7 +66,23 @@ cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a, i
     StencilFn fn = lookup(kf, stages, mode, (a.img_w & 3) == 0);
     if (!fn) return cudaErrorInvalidValue;
     if (grid <= 0) return cudaSuccess;
-    fn<<<grid, STENCIL_WARPS * 32, STENCIL_SMEM, s>>>(a);
+    // Programmatic dependent launch: the next stencil launch of the K loop is set up while the
+    // previous one drains its last items (its CTAs take SM slots as the previous CTAs exit and
+    // wait in griddepcontrol.wait until that grid has completed and its writes are visible).
+    // In a captured graph this becomes a programmatic edge.  RDS_NO_PDL=1 disables it (A/B).
+    static const bool pdl = getenv("RDS_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(STENCIL_WARPS * 32);
+    cfg.dynamicSmemBytes = STENCIL_SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    void *args[] = {const_cast<StencilArgs *>(&a)};
+    cudaLaunchKernelExC(&cfg, (const void *)fn, args);
     return cudaGetLastError();
 }
 

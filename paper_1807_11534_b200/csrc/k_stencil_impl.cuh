@@ -393,6 +393,9 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
     static_assert(RING + KF + 3 <= CR, "c ring too short for the stage lags");
     constexpr int LH = lh_of(KF), WV = wv_of(KF);
     extern __shared__ float4 smem[];  // [warps][RING][3][32] then [warps][2 CR][32]
+    // launched as a programmatic dependent of the previous stencil launch: nothing below may
+    // run before that grid has completed (its planes, the stop flag)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     // tolerance mode: once the stopping rule has fired, the remaining launches are no-ops
     if (a.stop != nullptr && *(volatile const int32_t *)&a.stop->flag != 0) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
