@@ -236,6 +236,39 @@ int rds_tile_shape(int *th, int *tw);
  * Deterministic two-pass reduction; synchronous.  Errors: RDS_ESTATE before a solve. */
 int rds_energy(rds_t *h, rds_energy_t *out);
 
+/* ---- row strips: one image split across ranks ("extension") ----
+ * The iteration's dependency cone (rows -2..+1 per iteration, §8(a) S4-S6) lets a handle that
+ * holds a row strip of the image plus halo rows reproduce the whole-image iterates exactly on
+ * its owned rows: with s iterations between halo refreshes, the rows next to a strip's cut go
+ * wrong by at most 2s rows below a top cut and s rows above a bottom cut, so a top halo of
+ * >= 2s rows and a bottom halo of >= s + 1 rows keep every owned row (and the row just past
+ * it) bit-identical to a whole-image solve, per pixel the same float operations.  The host
+ * protocol (paper_1807_11534_b200/strips.py): rds_solve(s) on every strip, then repeatedly
+ * exchange halo rows (rds_get_state_rows -> neighbour's rds_set_state_rows) and
+ * rds_solve_continue(s).  delta must be the same absolute value on every strip. */
+
+/* Run `iters` more iterations from the current state with the parameters, labels and work
+ * items of the last rds_solve / rds_solve_tol / rds_solve_q (no setup; fixed K; writes u and
+ * the mask at the end).  A tolerance solve's outcome is resolved first (synchronises).
+ * iters = 0 is a no-op.  Errors: RDS_ESTATE before a solve; RDS_EINVAL if iters < 0. */
+int rds_solve_continue(rds_t *h, int32_t iters);
+
+/* Copy rows [row0, row0 + nrows) of the current state out of / into the handle.  Buffer
+ * layout: three planes v, rho1, rho2, each nrows x W float32 row-major (natural column
+ * order), i.e. 3 * nrows * W floats.  Host buffers (on_device = 0) are synchronous; device
+ * buffers are stream-ordered.  Setting rows replaces the state the next rds_solve_continue
+ * starts from (labels and c' are not touched).  Errors: RDS_ESTATE before a solve;
+ * RDS_EINVAL if the rows leave [0, H), nrows < 0, buffer NULL with nrows > 0, or a batch
+ * handle. */
+int rds_get_state_rows(rds_t *h, int64_t row0, int64_t nrows, float *out, int on_device);
+int rds_set_state_rows(rds_t *h, int64_t row0, int64_t nrows, const float *in, int on_device);
+
+/* Rows summed by rds_energy: [row0, row1) (row1 < 0 means H; default all rows).  A strip
+ * sums only its owned rows; the terms at the last owned row read the row below it (the
+ * halo).  Summing the strips' TV_v, fit_v, E_u and D_p then gives the whole image's.
+ * Errors: RDS_EINVAL unless 0 <= row0 <= row1 <= H. */
+int rds_set_energy_rows(rds_t *h, int64_t row0, int64_t row1);
+
 /* Statistics of the last solve (synchronises the stream). */
 int rds_get_stats(rds_t *h, rds_stats_t *out);
 

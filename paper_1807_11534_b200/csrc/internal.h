@@ -149,6 +149,7 @@ struct EnergyArgs {
     const float *f, *u, *v, *p1, *p2;
     int64_t pitch;
     int H, W, img_w;
+    int row0, row1;     // rows summed: [row0, row1) (rds_set_energy_rows; default [0, H))
     double *partials;   // [n_blocks * 5]
     double *out;        // [5]: TV_v, sum f v, TV_cu, sum f cu, sum min(0, lambda f + div p)
     float lambda;

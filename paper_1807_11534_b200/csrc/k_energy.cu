@@ -24,8 +24,8 @@ __device__ __forceinline__ float clamp01(float x) { return fminf(fmaxf(x, 0.0f),
 __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
     const int64_t pitch = a.pitch;
     double acc[NE] = {0, 0, 0, 0, 0};
-    // fixed pixel -> thread map: CTA b takes rows b, b + G, ...; thread t columns t, t + 256, ...
-    for (int i = blockIdx.x; i < a.H; i += gridDim.x) {
+    // fixed pixel -> thread map: CTA b takes rows row0 + b, row0 + b + G, ...; thread t columns t, t + 256, ...
+    for (int i = a.row0 + blockIdx.x; i < a.row1; i += gridDim.x) {
         const int64_t row = (int64_t)i * pitch;
         const bool down = i < a.H - 1;
         int jm = threadIdx.x % a.img_w;  // column within its image (batches)

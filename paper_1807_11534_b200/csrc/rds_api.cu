@@ -89,6 +89,12 @@ struct rds_handle {
     float c1 = 0, c2 = 0, gamma = 0;
     float lambda = 0, theta = 0;
     int cur = 0;  // ping-pong buffer holding the latest state
+    // what rds_solve_continue needs from the last solve (labels, c' and items stay in place)
+    int last_kf = 0, last_max_items = 0;
+    float last_tau = 0;
+    int64_t e_row0 = 0, e_row1 = -1;  // rows summed by rds_energy (-1: H)
+    float *rows_buf = nullptr;        // staging of rds_get/set_state_rows with host buffers
+    size_t rows_bytes = 0;
 
     int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1, opt_ctas = 0;
     int opt_norm = 0;  // stopping-rule norm: 0 Euclidean over pixels, 1 RMS (R-F2)
@@ -138,7 +144,7 @@ static void free_all(rds_t *h) {
                      h->items,   h->queue,       h->counts,  h->n_rd_dev,  h->absmax_bits,
                      h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch,
                      h->stop,    h->chk,         h->d64,     h->part64,    h->cmp_out,
-                     h->lab64,   h->stop64,      h->n64};
+                     h->lab64,   h->stop64,      h->n64,       h->rows_buf};
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -869,6 +875,9 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
 
     h->lambda = lambda;
     h->theta = theta;
+    h->last_kf = kf;
+    h->last_max_items = max_items;
+    h->last_tau = tau;
     h->solved = true;
     rds_stats_t &st = h->stats;
     memset(&st, 0, sizeof st);
@@ -978,6 +987,93 @@ static int copy_out_swizzled(rds_t *h, float *dst, const float *plane_origin, in
         if (rc_) return rc_;                                                       \
     }
 
+// ---- row strips (multi-GPU decomposition) -------------------------------------
+
+int rds_solve_continue(rds_t *h, int32_t iters) {
+    NEED_SOLVED("rds_solve_continue");
+    if (iters < 0) return fail(h, RDS_EINVAL, "rds_solve_continue: iters=%d must be >= 0", iters);
+    if (iters == 0) return RDS_OK;
+    const int kf = h->last_kf;
+    const int launches = make_plan(kf, iters, 0, nullptr, 0);
+    {
+        void *pq = h->queue;
+        const bool realloc_queue = sizeof(int32_t) * (size_t)launches > h->queue_bytes;
+        CK(h, grow(&pq, &h->queue_bytes, sizeof(int32_t) * (size_t)launches));
+        h->queue = (int32_t *)pq;
+        if (realloc_queue && h->graph) {  // the cached K-loop graph points at the old counters
+            cudaGraphExecDestroy(h->graph);
+            h->graph = nullptr;
+        }
+    }
+    NvtxRange nvtx("rds_solve_continue");
+    if (h->opt_timing) {
+        CK(h, cudaEventRecord(h->ev[0], h->stream));
+        CK(h, cudaEventRecord(h->ev[1], h->stream));
+    }
+    TolParams tp;
+    tp.max_iters = iters;
+    CK(h, enqueue_loop(h, kf, iters, h->last_max_items, h->last_tau, h->theta, tp));
+    if (launches & 1) h->cur ^= 1;
+    if (h->opt_timing) CK(h, cudaEventRecord(h->ev[2], h->stream));
+    h->stats.iters += iters;
+    h->stats.launches += launches;
+    h->stats.converged = 0;
+    h->stats.residual = -1.0f;
+    h->stats.check_every = 0;
+    return RDS_OK;
+}
+
+static int state_rows(rds_t *h, int64_t row0, int64_t nrows, float *buf, int on_device,
+                      int put, const char *name) {
+    if (h->batch > 1) return fail(h, RDS_EINVAL, "%s: not available on a batch handle", name);
+    if (row0 < 0 || nrows < 0 || row0 + nrows > h->H)
+        return fail(h, RDS_EINVAL, "%s: rows [%lld, %lld) outside [0, %lld)", name,
+                    (long long)row0, (long long)(row0 + nrows), (long long)h->H);
+    if (nrows == 0) return RDS_OK;
+    if (!buf) return fail(h, RDS_EINVAL, "%s: NULL buffer", name);
+    const int64_t n = nrows * h->W;  // elements per plane
+    const size_t bytes = sizeof(float) * 3 * (size_t)n;
+    float *d = buf;
+    if (!on_device) {
+        void *pb = h->rows_buf;
+        CK(h, grow(&pb, &h->rows_bytes, bytes));
+        h->rows_buf = (float *)pb;
+        d = h->rows_buf;
+        if (put) CK(h, cudaMemcpyAsync(d, buf, bytes, cudaMemcpyHostToDevice, h->stream));
+    }
+    float *planes[3] = {h->v[h->cur], h->p1[h->cur], h->p2[h->cur]};
+    for (int q = 0; q < 3; ++q)
+        CK(h, launch_batch_copy(d + q * n, h->at(planes[q]) + row0 * h->pitch, 4, h->pitch,
+                                (int)nrows, (int)h->W, 1, put, 1, h->stream));
+    if (!on_device) {
+        if (!put) CK(h, cudaMemcpyAsync(buf, d, bytes, cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+    }
+    return RDS_OK;
+}
+
+int rds_get_state_rows(rds_t *h, int64_t row0, int64_t nrows, float *out, int on_device) {
+    NEED_SOLVED("rds_get_state_rows");
+    return state_rows(h, row0, nrows, out, on_device, 0, "rds_get_state_rows");
+}
+
+int rds_set_state_rows(rds_t *h, int64_t row0, int64_t nrows, const float *in, int on_device) {
+    NEED_SOLVED("rds_set_state_rows");
+    return state_rows(h, row0, nrows, const_cast<float *>(in), on_device, 1,
+                      "rds_set_state_rows");
+}
+
+int rds_set_energy_rows(rds_t *h, int64_t row0, int64_t row1) {
+    if (!h) return fail(nullptr, RDS_EINVAL, "rds_set_energy_rows: NULL handle");
+    if (row1 < 0) row1 = h->H;
+    if (row0 < 0 || row0 > row1 || row1 > h->H)
+        return fail(h, RDS_EINVAL, "rds_set_energy_rows: rows [%lld, %lld) outside [0, %lld)",
+                    (long long)row0, (long long)row1, (long long)h->H);
+    h->e_row0 = row0;
+    h->e_row1 = row1;
+    return RDS_OK;
+}
+
 int rds_get_u(rds_t *h, float *out, int on_device) {
     NEED_SOLVED("rds_get_u");
     if (!out) return fail(h, RDS_EINVAL, "rds_get_u: NULL out");
@@ -1055,6 +1151,8 @@ int rds_energy(rds_t *h, rds_energy_t *out) {
     a.H = (int)h->H;
     a.W = (int)h->W;
     a.img_w = (int)h->img_w;
+    a.row0 = (int)h->e_row0;
+    a.row1 = (int)(h->e_row1 < 0 ? h->H : h->e_row1);
     a.partials = h->e_partials;
     a.out = h->e_out;
     a.lambda = h->lambda;

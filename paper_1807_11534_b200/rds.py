@@ -33,7 +33,8 @@ EXPORTS = (
     "rds_get_active_tiles", "rds_tile_shape", "rds_energy", "rds_get_stats",
     "rds_kfuse_supported", "rds_last_error", "rds_version", "rds_band_for_fraction",
     "rds_solve_q", "rds_solve_tol", "rds_solve_gt", "rds_get_u_gt", "rds_compare_gt",
-    "rds_check_frame",
+    "rds_check_frame", "rds_solve_continue", "rds_get_state_rows", "rds_set_state_rows",
+    "rds_set_energy_rows",
     "rds3_create", "rds3_destroy", "rds3_set_stream", "rds3_set_kz", "rds3_set_image",
     "rds3_set_fitting",
     "rds3_fitting_absmax", "rds3_solve", "rds3_get_u", "rds3_get_v", "rds3_get_p",
@@ -114,6 +115,10 @@ def _load():
         "rds_get_u_gt": [P, P, i],
         "rds_compare_gt": [P, f, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)],
         "rds_check_frame": [P, ctypes.POINTER(i64)],
+        "rds_solve_continue": [P, i32],
+        "rds_get_state_rows": [P, i64, i64, P, i],
+        "rds_set_state_rows": [P, i64, i64, P, i],
+        "rds_set_energy_rows": [P, i64, i64],
         "rds3_create": [i64, i64, i64, ctypes.POINTER(P)],
         "rds3_destroy": [P],
         "rds3_set_stream": [P, P],
@@ -247,6 +252,27 @@ def rds_compare_gt(h, eps=0.5):
     e1, e2 = ctypes.c_double(), ctypes.c_double()
     _check(_lib.rds_compare_gt(h, float(eps), ctypes.byref(e1), ctypes.byref(e2)), h)
     return e1.value, e2.value
+
+
+def rds_solve_continue(h, iters):
+    _check(_lib.rds_solve_continue(h, int(iters)), h)
+
+
+def rds_get_state_rows(h, row0, nrows, out, W):
+    """rows [row0, row0 + nrows) of (v, rho1, rho2) into out (3, nrows, W) float32."""
+    p, dev, _keep = _buf(out, np.float32, (3, nrows, W), writable=True)
+    _check(_lib.rds_get_state_rows(h, int(row0), int(nrows), p, dev), h)
+    return out
+
+
+def rds_set_state_rows(h, row0, buf, W):
+    nrows = int(buf.shape[1])
+    p, dev, _keep = _buf(buf, np.float32, (3, nrows, W))
+    _check(_lib.rds_set_state_rows(h, int(row0), nrows, p, dev), h)
+
+
+def rds_set_energy_rows(h, row0, row1):
+    _check(_lib.rds_set_energy_rows(h, int(row0), int(row1)), h)
 
 
 def _get(fn, h, out, dtype, shape):
@@ -396,6 +422,22 @@ class Solver:
 
     def solve(self, lam, theta, tau, delta, iters):
         rds_solve(self.h, lam, theta, tau, math.inf if delta is None else delta, iters)
+
+    def solve_continue(self, iters):
+        """`iters` more iterations from the current state (parameters of the last solve)."""
+        rds_solve_continue(self.h, iters)
+
+    def state_rows(self, row0, nrows, out=None):
+        """(3, nrows, W) float32: v, rho1, rho2 on rows [row0, row0 + nrows)."""
+        W = self.shape[1]
+        out = np.empty((3, nrows, W), np.float32) if out is None else out
+        return rds_get_state_rows(self.h, row0, nrows, out, W)
+
+    def set_state_rows(self, row0, buf):
+        rds_set_state_rows(self.h, row0, buf, self.shape[1])
+
+    def set_energy_rows(self, row0, row1=-1):
+        rds_set_energy_rows(self.h, row0, row1)
 
     def solve_tol(self, lam, theta, tau, delta, max_iters, tol, check_every=0):
         """Stop at the first check (every check_every iterations, and at max_iters) where

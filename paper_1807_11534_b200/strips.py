@@ -1,0 +1,228 @@
+"""Row strips: one image split across ranks (§5, names larger
+problems as the method's extension).
+
+Every iteration of Eq. 7-9 reads, for the new state at row i, the old
+state at rows i-2 .. i+1 (SURVEY §8(a) S4-S6 footprint).  A handle that holds a strip of rows
+plus halo rows therefore computes its owned rows exactly as a whole-image solve would, as
+long as the rows it got wrong at its cuts (the strip's first row lacks the row above it, its
+last row the row below) have not reached them: after s iterations the damage reaches 2s rows
+down from a top cut and s rows up from a bottom cut.  With a top halo of 2s rows and a bottom
+halo of s + 1 rows, refreshed from the neighbours every s iterations, the owned rows and the
+row just below them stay bit-identical to the whole-image iterates (same float operations per
+pixel), which is what `tests/test_gpu_strips.py` checks on one GPU and
+`tests/test_dist_cpu.py` checks for the torch.distributed exchange with the CPU oracle.
+
+The exchange is the path's one real communication step: per refresh each cut moves
+(2s + s + 1) rows x W x (v, rho1, rho2) float32, e.g. 22 rows x 16384 x 12 B = 4.3 MB at
+C4 with s = 7, against 7 iterations of ~34 M pixels per GPU at G = 8.  It uses
+torch.distributed point-to-point (NCCL on GPUs; gloo on CPU for the tests) on the handle's
+stream (torch's current stream).  Everything else a strip needs is rank-local; delta must be
+the same absolute value everywhere (`absmax` all-reduces max |f|) and energies are summed
+over ranks (`energy`).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def halo_rows(seg_iters: int) -> tuple[int, int]:
+    """(top, bottom) halo rows for `seg_iters` iterations between refreshes."""
+    if seg_iters < 1:
+        raise ValueError("seg_iters must be >= 1")
+    return 2 * seg_iters, seg_iters + 1
+
+
+@dataclass(frozen=True)
+class Strip:
+    rank: int
+    lo: int     # owned global rows [lo, hi)
+    hi: int
+    top: int    # halo rows held above lo / below hi
+    bot: int
+
+    @property
+    def r0(self) -> int:  # first global row held
+        return self.lo - self.top
+
+    @property
+    def rows(self) -> int:  # rows held
+        return self.hi - self.lo + self.top + self.bot
+
+    @property
+    def owned(self) -> slice:  # owned rows in local coordinates
+        return slice(self.top, self.top + self.hi - self.lo)
+
+
+def partition(H: int, G: int, seg_iters: int) -> list[Strip]:
+    """G near-equal row strips of an H-row image (the first H % G one row taller), each with
+    the halos of `halo_rows(seg_iters)` (none at the image's own top and bottom)."""
+    if G < 1 or H < G:
+        raise ValueError(f"cannot split {H} rows into {G} strips")
+    top, bot = halo_rows(seg_iters)
+    base, extra = divmod(H, G)
+    out, lo = [], 0
+    for k in range(G):
+        hi = lo + base + (1 if k < extra else 0)
+        out.append(Strip(k, lo, hi, top if k > 0 else 0, bot if k < G - 1 else 0))
+        lo = hi
+    for s in out:
+        if s.hi - s.lo < top and G > 1:
+            raise ValueError(f"strip {s.rank} owns {s.hi - s.lo} rows, fewer than the {top}-row "
+                             f"halo its neighbour needs: use fewer ranks or a shorter segment")
+    return out
+
+
+def segments(iters: int, seg_iters: int) -> list[int]:
+    """Iterations per segment: `seg_iters` each, the last one shorter."""
+    full, rem = divmod(iters, seg_iters)
+    return [seg_iters] * full + ([rem] if rem else [])
+
+
+def exchange_plan(plan: list[Strip]) -> list[tuple[int, int, int, int, int]]:
+    """Halo refresh as (src_rank, src_row, dst_rank, dst_row, nrows) copies in local row
+    coordinates: every halo row comes from the rank that owns that global row."""
+    out = []
+    for k in range(len(plan) - 1):
+        a, b = plan[k], plan[k + 1]  # a above b; a.hi == b.lo
+        # b's top halo = a's last b.top owned rows
+        out.append((a.rank, a.owned.stop - b.top, b.rank, 0, b.top))
+        # a's bottom halo = b's first a.bot owned rows
+        out.append((b.rank, b.top, a.rank, a.rows - a.bot, a.bot))
+    return out
+
+
+def solve_local(engines, plan, lam, theta, tau, delta, iters, seg_iters):
+    """All strips in one process (one GPU, handles run one after another): the exchange
+    through host-side copies of the device state rows.  Used to test the decomposition on a
+    single device; `StripSolver` is the one-rank-per-GPU form."""
+    xplan = exchange_plan(plan)
+    for n, it in enumerate(segments(iters, seg_iters) or [0]):
+        if n == 0:
+            for e in engines:
+                e.solve(lam, theta, tau, delta, it)
+            continue
+        bufs = [(d, dr, engines[s].state_rows(sr, m)) for s, sr, d, dr, m in xplan]
+        for d, dr, buf in bufs:
+            engines[d].set_state_rows(dr, buf)
+        for e in engines:
+            e.solve_continue(it)
+
+
+class StripSolver:
+    """This rank's strip of an H x W image, one process per GPU (torch.distributed
+    initialised by the caller).  `engine` defaults to an `rds.Solver` on torch's current
+    stream; tests pass a stand-in with the same methods."""
+
+    def __init__(self, H, W, seg_iters, engine=None, group=None, **solver_kw):
+        import torch
+        import torch.distributed as dist
+
+        self.dist, self.torch, self.group = dist, torch, group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.H, self.W, self.seg_iters = int(H), int(W), int(seg_iters)
+        self.plan = partition(self.H, self.world, self.seg_iters)
+        self.me = self.plan[self.rank]
+        self.xplan = exchange_plan(self.plan)
+        nccl = dist.get_backend(group) == "nccl"
+        self.device = torch.device("cuda", torch.cuda.current_device()) if nccl else \
+            torch.device("cpu")
+        if engine is None:
+            from . import rds
+
+            engine = rds.Solver(self.me.rows, self.W,
+                                stream=torch.cuda.current_stream().cuda_stream, **solver_kw)
+        self.engine = engine
+        # exchange buffers in the engine's state precision (float32 for librds)
+        self.dtype = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}[
+            np.dtype(getattr(engine, "state_dtype", np.float32))]
+
+    # -- inputs: the full image or this strip's held rows ---------------------------------
+    def _rows(self, a):
+        if a is None:
+            return None
+        if a.shape[0] == self.H:
+            a = a[self.me.r0: self.me.r0 + self.me.rows]
+        if tuple(a.shape) != (self.me.rows, self.W):
+            raise ValueError(f"expected ({self.H} or {self.me.rows}, {self.W}), got {a.shape}")
+        return np.ascontiguousarray(a) if isinstance(a, np.ndarray) else a.contiguous()
+
+    def set_image(self, z):
+        self.engine.set_image(self._rows(z))
+
+    def set_fitting(self, c1, c2, gamma=0.0, P=None):
+        self.engine.set_fitting(c1, c2, gamma, self._rows(P))
+
+    def absmax(self):
+        """Global max |f| (all-reduce max of the strips' exact float32 maxima)."""
+        t = self.torch.tensor([float(self.engine.absmax())], dtype=self.torch.float64,
+                              device=self.device)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return np.float32(t.item())
+
+    # -- the iteration ----------------------------------------------------------------------
+    def _exchange(self):
+        torch, dist = self.torch, self.dist
+        ops, recvs = [], []
+        for s, sr, d, dr, m in self.xplan:
+            if s == self.rank:
+                buf = torch.empty((3, m, self.W), dtype=self.dtype, device=self.device)
+                self._get_rows(sr, m, buf)
+                ops.append(dist.P2POp(dist.isend, buf, d, self.group))
+            if d == self.rank:
+                buf = torch.empty((3, m, self.W), dtype=self.dtype, device=self.device)
+                ops.append(dist.P2POp(dist.irecv, buf, s, self.group))
+                recvs.append((dr, buf))
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+        for dr, buf in recvs:
+            self.engine.set_state_rows(dr, buf if buf.is_cuda else buf.numpy())
+
+    def _get_rows(self, r0, m, buf):
+        if buf.is_cuda:
+            self.engine.state_rows(r0, m, out=buf)
+        else:
+            buf.copy_(self.torch.from_numpy(self.engine.state_rows(r0, m)))
+
+    def solve(self, lam, theta, tau, delta, iters):
+        for n, it in enumerate(segments(int(iters), self.seg_iters) or [0]):
+            if n == 0:
+                self.engine.solve(lam, theta, tau, delta, it)
+            else:
+                self._exchange()
+                self.engine.solve_continue(it)
+
+    # -- outputs: owned rows ----------------------------------------------------------------
+    def u(self):
+        return self.engine.u()[self.me.owned]
+
+    def mask(self):
+        return self.engine.mask()[self.me.owned]
+
+    def energy(self):
+        """Whole-image energies: the strips' owned-row sums of TV(v), lambda<f, v>, E(u) and
+        D(rho), all-reduced (the gap and E(v) recomputed from the sums)."""
+        self.engine.set_energy_rows(self.me.owned.start, self.me.owned.stop)
+        e = self.engine.energy()
+        t = self.torch.tensor([e["TV_v"], e["fit_v"], e["E_u"], e["D_p"]],
+                              dtype=self.torch.float64, device=self.device)
+        self.dist.all_reduce(t, group=self.group)
+        tv, fit, eu, dp = t.tolist()
+        return dict(E_v=tv + fit, E_u=eu, D_p=dp, gap=tv + fit - dp, TV_v=tv, fit_v=fit)
+
+    def gather_u(self, dst=0):
+        """The whole u on rank `dst` (None elsewhere); strips padded to the tallest."""
+        torch, dist = self.torch, self.dist
+        sizes = [s.hi - s.lo for s in self.plan]
+        u = np.asarray(self.u())
+        mine = torch.zeros((max(sizes), self.W), dtype=torch.float64, device=self.device)
+        mine[: u.shape[0]] = torch.from_numpy(u.astype(np.float64)).to(self.device)
+        if self.rank == dst:
+            parts = [torch.empty_like(mine) for _ in sizes]
+            dist.gather(mine, parts, dst=dst, group=self.group)
+            return np.concatenate([p[:n].cpu().numpy() for p, n in zip(parts, sizes)])
+        dist.gather(mine, None, dst=dst, group=self.group)
+        return None

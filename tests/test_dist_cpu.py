@@ -48,3 +48,64 @@ def test_replicas_gloo_world2():
     for rank, t, w, v in out:
         assert t == 20.0 and w == 3e9
         assert v == pytest.approx(3e9 / 0.020 / 1e9)
+
+
+def _strip_worker(rank, world, port, q):
+    """One rank of a row-strip solve over gloo: torch.distributed point-to-point halo
+    exchange, all-reduced max |f|, gathered u (the oracle is every strip's engine)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "tests"))
+    import numpy as np
+    import torch.distributed as dist
+
+    from _orc_engine import OracleEngine
+    from paper_1807_11534_b200 import strips
+    from paper_1807_11534_b200 import workloads as wl
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        H, W, s, K = 70, 29, 3, 17
+        z = wl.gen_voronoi(N=70, seed=5, n_sites=10)[:H, :W].copy()
+        plan = strips.partition(H, world, s)
+        me = plan[rank]
+        ss = strips.StripSolver(H, W, s, engine=OracleEngine(me.rows, W))
+        ss.set_image(z)                       # full image in, the strip's rows used
+        ss.set_fitting(0.8, 0.2)
+        amax = ss.absmax()
+        delta = wl.band_delta(0.3, amax)
+        ss.solve(5.0, 0.1, 0.125, delta, K)
+        u = ss.gather_u()
+        q.put((rank, float(amax), float(delta), None if u is None else u.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_strips_gloo(orc, world):
+    import numpy as np
+    import torch.multiprocessing as mp
+
+    from paper_1807_11534_b200 import workloads as wl
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_strip_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=180) for _ in procs), key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    z = wl.gen_voronoi(N=70, seed=5, n_sites=10)[:70, :29].copy()
+    f = orc.fitting(z, 0.8, 0.2)
+    amax = orc.absmax(f)
+    delta = wl.band_delta(0.3, amax)
+    ref = orc.solve(f, delta, 5.0, 0.1, 0.125, 17)
+    assert all(o[1] == float(amax) and o[2] == float(delta) for o in out)
+    assert np.array_equal(np.array(out[0][3]), ref["u"])

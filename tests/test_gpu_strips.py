@@ -1,0 +1,143 @@
+"""GPU checks of the row-strip entry points (rds_solve_continue, rds_get/set_state_rows,
+rds_set_energy_rows) and of the strip decomposition on one device: G strip handles with
+halos, refreshed every s iterations, reproduce the whole-image librds solve bit for bit on
+their owned rows (same float operations per pixel; paper_1807_11534_b200/strips.py)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1807_11534_b200 import strips
+from paper_1807_11534_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+PAR = (5.0, 0.1, 0.125)
+
+
+@pytest.fixture(scope="module")
+def rds():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1807_11534_b200 import _build
+
+    _build.build()
+    from paper_1807_11534_b200 import rds as _rds
+
+    return _rds
+
+
+def _image(H, W, seed):
+    return wl.gen_voronoi(N=max(H, W), seed=seed, n_sites=25)[:H, :W].copy()
+
+
+def _state(s):
+    p1, p2 = s.p()
+    return dict(u=s.u(), v=s.v(), p1=p1, p2=p2, mask=s.mask())
+
+
+@pytest.mark.parametrize("K1,K2,kf", [(10, 11, 4), (7, 7, 7), (1, 20, 0), (13, 0, 3)])
+def test_continue_equals_one_solve(rds, K1, K2, kf):
+    z = _image(150, 133, 1)
+    a, b = rds.Solver(150, 133, k_fuse=kf), rds.Solver(150, 133, k_fuse=kf)
+    for s in (a, b):
+        s.set_image(z)
+        s.set_fitting(0.8, 0.2)
+    delta = wl.band_delta(0.3, a.absmax())
+    a.solve(*PAR, delta, K1 + K2)
+    b.solve(*PAR, delta, K1)
+    b.solve_continue(K2)
+    sa, sb = _state(a), _state(b)
+    for k in sa:
+        assert np.array_equal(sa[k], sb[k]), k
+    assert b.stats()["iters"] == K1 + K2
+    assert b.check_frame() == 0
+
+
+def test_continue_after_tolerance_solve(rds):
+    z = _image(96, 96, 2)
+    a, b = rds.Solver(96, 96), rds.Solver(96, 96)
+    for s in (a, b):
+        s.set_image(z)
+        s.set_fitting(0.8, 0.2)
+    st = a.solve_tol(*PAR, math.inf, 200, 1e-3, 10)
+    n = st["iters"]
+    assert 0 < n <= 200
+    a.solve_continue(9)
+    b.solve(*PAR, math.inf, n + 9)
+    sa, sb = _state(a), _state(b)
+    for k in sa:
+        assert np.array_equal(sa[k], sb[k]), k
+
+
+def test_state_rows_roundtrip(rds):
+    import torch
+
+    H, W = 70, 45
+    s = rds.Solver(H, W)
+    s.set_image(_image(H, W, 3))
+    s.set_fitting(0.8, 0.2)
+    s.solve(*PAR, math.inf, 12)
+    p1, p2 = s.p()
+    rows = s.state_rows(10, 7)
+    assert rows.shape == (3, 7, W)
+    assert np.array_equal(rows[0], s.v()[10:17])
+    assert np.array_equal(rows[1], p1[10:17]) and np.array_equal(rows[2], p2[10:17])
+    dev = torch.empty((3, 7, W), dtype=torch.float32, device="cuda")
+    s.state_rows(10, 7, out=dev)
+    assert np.array_equal(dev.cpu().numpy(), rows)
+    new = np.random.default_rng(0).uniform(-0.5, 0.5, (3, 4, W)).astype(np.float32)
+    s.set_state_rows(H - 4, new)
+    assert np.array_equal(s.state_rows(H - 4, 4), new)
+    s.set_state_rows(0, torch.from_numpy(new).cuda())
+    assert np.array_equal(s.state_rows(0, 4), new)
+    assert s.check_frame() == 0
+    for bad in ((-1, 3), (H - 2, 3)):
+        with pytest.raises(rds.RdsError):
+            s.state_rows(*bad)
+    with pytest.raises(rds.RdsError):
+        s.set_energy_rows(5, H + 1)
+    fresh = rds.Solver(H, W)
+    with pytest.raises(rds.RdsError):
+        fresh.solve_continue(3)
+    with pytest.raises(rds.RdsError):
+        fresh.state_rows(0, 1)
+
+
+@pytest.mark.parametrize("H,W,G,s,K,delta_rel,kf", [(257, 190, 2, 7, 40, 0.3, 7),
+                                                    (300, 129, 3, 5, 33, math.inf, 4),
+                                                    (200, 96, 4, 4, 21, 0.2, 0),
+                                                    (181, 77, 3, 3, 10, 0.4, 3)])
+def test_strips_bitwise_whole_image(rds, H, W, G, s, K, delta_rel, kf):
+    z = _image(H, W, G * 100 + s)
+    ref = rds.Solver(H, W, k_fuse=kf)
+    ref.set_image(z)
+    ref.set_fitting(0.8, 0.2)
+    delta = wl.band_delta(delta_rel, ref.absmax())
+    ref.solve(*PAR, delta, K)
+    want = _state(ref)
+    e_ref = ref.energy()
+    plan = strips.partition(H, G, s)
+    engines = []
+    for st in plan:
+        e = rds.Solver(st.rows, W, k_fuse=kf)
+        e.set_image(z[st.r0:st.r0 + st.rows])
+        e.set_fitting(0.8, 0.2)
+        engines.append(e)
+    strips.solve_local(engines, plan, *PAR, delta, K, s)
+    tot = dict.fromkeys(("TV_v", "fit_v", "E_u", "D_p"), 0.0)
+    for st, e in zip(plan, engines):
+        got = _state(e)
+        stop = st.owned.stop + (1 if st.bot else 0)   # the row below the owned ones too
+        for k in got:
+            assert np.array_equal(got[k][st.owned.start:stop],
+                                  want[k][st.lo:st.lo + stop - st.owned.start]), (st.rank, k)
+        e.set_energy_rows(st.owned.start, st.owned.stop)
+        en = e.energy()
+        for k in tot:
+            tot[k] += en[k]
+        assert e.check_frame() == 0
+    for k in tot:
+        assert tot[k] == pytest.approx(e_ref[k], rel=1e-9, abs=1e-9), k

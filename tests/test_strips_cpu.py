@@ -1,0 +1,95 @@
+"""Row-strip decomposition on CPU: the partition and halo-exchange plan, and
+the protocol run with the oracle as every strip's engine, which must reproduce the
+whole-image oracle iterates bit for bit on the owned rows (the dependency-cone argument in
+paper_1807_11534_b200/strips.py)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1807_11534_b200 import strips
+from paper_1807_11534_b200 import workloads as wl
+from _orc_engine import OracleEngine
+
+
+@pytest.mark.parametrize("H,G,s", [(100, 1, 3), (100, 2, 3), (101, 3, 5), (64, 4, 2),
+                                   (300, 7, 7)])
+def test_partition_and_exchange_plan(H, G, s):
+    plan = strips.partition(H, G, s)
+    owner = np.full(H, -1)
+    for st in plan:
+        owner[st.lo:st.hi] = st.rank
+        assert st.top == (0 if st.rank == 0 else 2 * s)
+        assert st.bot == (0 if st.rank == G - 1 else s + 1)
+    assert (owner >= 0).all() and (np.diff(owner) >= 0).all()
+    sizes = [st.hi - st.lo for st in plan]
+    assert max(sizes) - min(sizes) <= 1
+    filled = {st.rank: np.zeros(st.rows, bool) for st in plan}
+    for src, sr, dst, dr, m in strips.exchange_plan(plan):
+        a, b = plan[src], plan[dst]
+        for k in range(m):
+            g_src, g_dst = a.r0 + sr + k, b.r0 + dr + k
+            assert g_src == g_dst                      # the same global row
+            assert owner[g_src] == src                 # taken from its owner
+            assert not (b.lo <= g_dst < b.hi)          # written into a halo only
+            filled[dst][dr + k] = True
+    for st in plan:                                    # every halo row refreshed
+        halo = np.ones(st.rows, bool)
+        halo[st.owned] = False
+        assert np.array_equal(filled[st.rank], halo)
+
+
+def test_partition_rejects_thin_strips():
+    with pytest.raises(ValueError):
+        strips.partition(30, 4, 5)  # 7-8 rows per strip < the 10-row top halo
+    with pytest.raises(ValueError):
+        strips.partition(3, 4, 1)
+    assert strips.segments(23, 7) == [7, 7, 7, 2]
+    assert strips.segments(21, 7) == [7, 7, 7]
+    assert strips.segments(0, 7) == []
+
+
+def _image(H, W, seed):
+    return wl.gen_voronoi(N=max(H, W), seed=seed, n_sites=12)[:H, :W].copy()
+
+
+def _strip_solve(z, plan, c, delta, K, s, par):
+    engines = []
+    for st in plan:
+        e = OracleEngine(st.rows, z.shape[1])
+        e.set_image(z[st.r0:st.r0 + st.rows])
+        e.set_fitting(*c)
+        engines.append(e)
+    strips.solve_local(engines, plan, *par, delta, K, s)
+    return engines
+
+
+@pytest.mark.parametrize("H,W,G,s,K,delta_rel", [(60, 37, 2, 3, 14, 0.3),
+                                                 (75, 20, 3, 5, 23, math.inf),
+                                                 (48, 33, 4, 2, 9, 0.25),
+                                                 (40, 16, 2, 1, 6, 0.4)])
+def test_strips_reproduce_whole_image_oracle(orc, H, W, G, s, K, delta_rel):
+    z = _image(H, W, G * 10 + s)
+    c, par = (0.8, 0.2), (5.0, 0.1, 0.125)
+    f = orc.fitting(z, *c)
+    delta = wl.band_delta(delta_rel, orc.absmax(f))
+    ref = orc.solve(f, delta, 5.0, 0.1, 0.125, K)
+    plan = strips.partition(H, G, s)
+    for st, e in zip(plan, _strip_solve(z, plan, c, delta, K, s, par)):
+        for k in ("u", "v", "p1", "p2"):
+            got = e.st[k][st.owned]
+            assert np.array_equal(got, ref[k][st.lo:st.hi]), (st.rank, k)
+
+
+def test_strips_need_the_halo(orc):
+    """With a top halo one segment shorter than 2s the owned rows differ: the halo is not
+    a formality (unrestricted band, so every pixel iterates)."""
+    H, W, G, s, K = 60, 24, 2, 4, 16
+    z = _image(H, W, 7)
+    f = orc.fitting(z, 0.8, 0.2)
+    ref = orc.solve(f, np.float32(np.inf), 5.0, 0.1, 0.125, K)
+    plan = strips.partition(H, G, s)
+    short = [strips.Strip(p.rank, p.lo, p.hi, max(0, p.top - s), p.bot) for p in plan]
+    engines = _strip_solve(z, short, (0.8, 0.2), np.float32(np.inf), K, s, (5.0, 0.1, 0.125))
+    st, e = short[1], engines[1]
+    assert not np.array_equal(e.st["u"][st.owned], ref["u"][st.lo:st.hi])
