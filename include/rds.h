@@ -123,7 +123,9 @@ int rds_create_batch(int64_t B, int64_t H, int64_t W, rds_t **out);
 int rds_destroy(rds_t *h);
 
 /* All later work is ordered on `stream` (a cudaStream_t, e.g.
- * torch.cuda.current_stream().cuda_stream).  NULL selects the handle's private stream. */
+ * torch.cuda.current_stream().cuda_stream).  NULL selects the handle's private stream; the
+ * legacy default stream is cudaStreamLegacy ((cudaStream_t)0x1) -- the Python binding maps
+ * torch's default stream (cuda_stream == 0) to it. */
 int rds_set_stream(rds_t *h, void *stream);
 
 /* Set an option (RDS_OPT_*). RDS_EINVAL on unknown key or unsupported value. */

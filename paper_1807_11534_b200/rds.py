@@ -186,8 +186,20 @@ def rds_destroy(h):
     _check(_lib.rds_destroy(h))
 
 
+CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: what torch's default stream (cuda_stream 0) is
+
+
+def _stream_arg(stream_ptr):
+    """None -> NULL (the handle's private stream); 0 (torch's default stream) ->
+    cudaStreamLegacy, so that `torch.cuda.current_stream().cuda_stream` always means the
+    stream torch is using; anything else is a cudaStream_t."""
+    if stream_ptr is None:
+        return ctypes.c_void_p(None)
+    return ctypes.c_void_p(int(stream_ptr) or CUDA_STREAM_LEGACY)
+
+
 def rds_set_stream(h, stream_ptr):
-    _check(_lib.rds_set_stream(h, ctypes.c_void_p(stream_ptr or None)), h)
+    _check(_lib.rds_set_stream(h, _stream_arg(stream_ptr)), h)
 
 
 def rds_set_option(h, key, value):
@@ -517,7 +529,7 @@ class Solver3:
         _check3(_lib.rds3_create(int(D), int(H), int(W), ctypes.byref(h)), None)
         self.h = h
         if stream is not None:
-            _check3(_lib.rds3_set_stream(self.h, ctypes.c_void_p(stream)), self.h)
+            _check3(_lib.rds3_set_stream(self.h, _stream_arg(stream)), self.h)
 
     def close(self):
         if self.h is not None:

@@ -93,9 +93,11 @@ def exchange_plan(plan: list[Strip]) -> list[tuple[int, int, int, int, int]]:
     return out
 
 
-def solve_local(engines, plan, lam, theta, tau, delta, iters, seg_iters):
+def solve_local(engines, plan, lam, theta, tau, delta, iters, seg_iters, device=None):
     """All strips in one process (one GPU, handles run one after another): the exchange
-    through host-side copies of the device state rows.  Used to test the decomposition on a
+    copies the state rows through host buffers, or through torch tensors on `device`
+    (stream-ordered, no synchronisation: the engines must then run on torch's current
+    stream, so the caching allocator sees every use of a buffer).  Used to test and time the decomposition on a
     single device; `StripSolver` is the one-rank-per-GPU form."""
     xplan = exchange_plan(plan)
     for n, it in enumerate(segments(iters, seg_iters) or [0]):
@@ -103,7 +105,16 @@ def solve_local(engines, plan, lam, theta, tau, delta, iters, seg_iters):
             for e in engines:
                 e.solve(lam, theta, tau, delta, it)
             continue
-        bufs = [(d, dr, engines[s].state_rows(sr, m)) for s, sr, d, dr, m in xplan]
+        if device is None:
+            bufs = [(d, dr, engines[s].state_rows(sr, m)) for s, sr, d, dr, m in xplan]
+        else:
+            import torch
+
+            bufs = []
+            for s, sr, d, dr, m in xplan:
+                W = engines[s].shape[1]
+                buf = torch.empty((3, m, W), dtype=torch.float32, device=device)
+                bufs.append((d, dr, engines[s].state_rows(sr, m, out=buf)))
         for d, dr, buf in bufs:
             engines[d].set_state_rows(dr, buf)
         for e in engines:

@@ -141,3 +141,28 @@ def test_strips_bitwise_whole_image(rds, H, W, G, s, K, delta_rel, kf):
         assert e.check_frame() == 0
     for k in tot:
         assert tot[k] == pytest.approx(e_ref[k], rel=1e-9, abs=1e-9), k
+
+
+def test_torch_default_stream(rds):
+    """stream=0 (torch's default stream) is the legacy default stream, not the private one:
+    work is ordered with torch's (temporary device inputs are safe) and CUDA events on it
+    time the solve."""
+    import torch
+
+    H, W = 512, 512
+    z = _image(H, W, 9)
+    ref = rds.Solver(H, W)
+    ref.set_image(z)
+    ref.set_fitting(0.8, 0.2)
+    ref.solve(*PAR, math.inf, 200)
+    s = rds.Solver(H, W, stream=torch.cuda.default_stream().cuda_stream)
+    with torch.cuda.stream(torch.cuda.default_stream()):
+        s.set_image(torch.from_numpy(z).cuda() * 1.0)   # a temporary freed right after
+        s.set_fitting(0.8, 0.2)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        s.solve(*PAR, math.inf, 200)
+        b.record()
+        torch.cuda.synchronize()
+    assert a.elapsed_time(b) > 0.05
+    assert np.array_equal(s.u(), ref.u())
