@@ -1,5 +1,5 @@
-"""GPU parity of batched solves (rds_create_batch): B independent images stacked along rows,
-each with its own Neumann last row, must reproduce B independent oracle solves."""
+"""GPU parity of batched solves (rds_create_batch): B independent images stacked along
+columns, each with its own Neumann last column, must reproduce B independent oracle solves."""
 import math
 
 import numpy as np
