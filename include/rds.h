@@ -86,6 +86,7 @@ typedef struct {
     float loop_ms;           /* the K-loop (all stencil launches) */
     float residual;          /* rds_solve_tol: max(RMS du, RMS dv) at the last check; else -1 */
     int32_t check_every;     /* rds_solve_tol: iterations between checks; 0 for rds_solve */
+    int32_t compact;         /* 1 if the last solve ran the compacted RD iteration (RDS_OPT_COMPACT) */
 } rds_stats_t;
 
 /* Options (rds_set_option). */
@@ -104,6 +105,16 @@ typedef struct {
 #define RDS_OPT_STOP_NORM 7  /* norm of the stopping rule (rds_solve_tol, rds_solve_gt):
                                 0 (default) = Euclidean norm over pixels of unit area,
                                 sqrt(sum d^2); 1 = RMS, sqrt(sum d^2 / (H W)) */
+
+#define RDS_OPT_COMPACT 8    /* f3: iterate on the RD pixels alone, stored compactly
+                                in row-major RD order with their stencil neighbours' indices, in
+                                one persistent cooperative kernel (k_rdc.cu) instead of the dense
+                                temporally blocked stencil.  0 (default) = dense; 1 = compact for
+                                every fixed-K rds_solve / rds_solve_q; 2 = compact when RD holds
+                                <= 8% of the pixels.  Same float operations per pixel as the dense
+                                path (results agree value for value); the solve synchronises once
+                                to size the compact arrays; tolerance solves stay dense.  Images
+                                of more than 2^30 pixels always take the dense path. */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */

@@ -157,6 +157,38 @@ struct EnergyArgs {
 constexpr int ENERGY_BLOCKS = 592;  // 4 x 148 SMs
 cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s);
 
+// f3: compacted restricted-domain iteration (k_rdc.cu).  Neighbour codes: >= 0 compact index
+// of an RD pixel; RDC_BG / RDC_FG a pinned pixel (rho = 0, v = u0 = 0 / 1) or the frame;
+// RDC_EDGE the missing forward neighbour on row H-1 / an image's last column (grad = 0).
+constexpr int RDC_BG = -1, RDC_FG = -2, RDC_EDGE = -3;
+constexpr int RDC_THREADS = 512;
+struct RdcSetup {
+    int n, H, W, img_w;
+    int64_t pitch;
+    const int32_t *list, *idxmap;
+    int32_t *nbr;                 // [6][n]: x-e1, x+e1, x-e2, x+e2, x+e1-e2, x-e1+e2
+    float *c, *p1, *p2, *v, *u;   // compact arrays (gather: buffer 0; scatter: final buffers)
+    const float *cplane;          // dense plane origins
+    float *p1plane, *p2plane, *vplane, *uplane;
+    uint8_t *mask;
+};
+struct RdcIter {
+    int n, K;
+    const int32_t *nbr;
+    const float *c;
+    float *p1[2], *p2[2], *v[2], *u;
+    float tau, theta, inv_theta;
+    unsigned long long *bar;
+};
+cudaError_t launch_rdc_count(const uint8_t *lab, int64_t pitch, int H, int W, int32_t *rowcnt,
+                             int32_t *rowoff, int32_t *total, cudaStream_t s);
+cudaError_t launch_rdc_fill(const uint8_t *lab, int64_t pitch, int H, int W,
+                            const int32_t *rowoff, int32_t *idxmap, int32_t *list,
+                            cudaStream_t s);
+cudaError_t launch_rdc_gather(const RdcSetup &a, cudaStream_t s);
+cudaError_t launch_rdc_scatter(const RdcSetup &a, cudaStream_t s);
+cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s);
+
 // float64 mode (k_fp64.cu): natural-order padded double planes, same pitch as the floats
 struct F64Args {
     const float *z, *P;        // image and selection map (float planes; P may be null)

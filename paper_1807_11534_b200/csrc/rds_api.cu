@@ -98,6 +98,12 @@ struct rds_handle {
 
     int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1, opt_ctas = 0;
     int opt_norm = 0;  // stopping-rule norm: 0 Euclidean over pixels, 1 RMS (R-F2)
+    int opt_compact = 0;  // f3: 0 dense stencil, 1 compacted RD iteration, 2 auto (RDS_OPT_COMPACT)
+    // compacted RD iteration (k_rdc.cu): index map, row counts/offsets, total, compact arrays
+    int32_t *rdc_idx = nullptr, *rdc_row = nullptr, *rdc_tot = nullptr;
+    void *rdc_buf = nullptr;
+    size_t rdc_bytes = 0;
+    unsigned long long *rdc_bar = nullptr;
     rds_stats_t stats{};
 
     // cached CUDA graph of the K-loop
@@ -144,13 +150,15 @@ static void free_all(rds_t *h) {
                      h->items,   h->queue,       h->counts,  h->n_rd_dev,  h->absmax_bits,
                      h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch,
                      h->stop,    h->chk,         h->d64,     h->part64,    h->cmp_out,
-                     h->lab64,   h->stop64,      h->n64,       h->rows_buf};
+                     h->lab64,   h->stop64,      h->n64,       h->rows_buf,
+                     h->rdc_idx, h->rdc_row,     h->rdc_buf,   h->rdc_bar};  // rdc_tot points into rdc_row
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
     for (auto &e : h->ev)
         if (e) cudaEventDestroy(e);
     if (h->own_stream) cudaStreamDestroy(h->own_stream);
+    (void)cudaGetLastError();  // a failed free must not surface in an unrelated later call
 }
 
 static cudaError_t alloc_plane(rds_t *h, float **p, float frame_value) {
@@ -294,6 +302,11 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             return RDS_OK;
         case RDS_OPT_GRAPH:
             h->opt_graph = value != 0;
+            return RDS_OK;
+        case RDS_OPT_COMPACT:
+            if (value < 0 || value > 2)
+                return fail(h, RDS_EINVAL, "rds_set_option: compact=%lld", (long long)value);
+            h->opt_compact = (int)value;
             return RDS_OK;
         case RDS_OPT_STOP_NORM:
             if (value != 0 && value != 1)
@@ -716,6 +729,99 @@ static cudaError_t grow(void **p, size_t *cap, size_t bytes) {
     return e;
 }
 
+// f3: build the compacted RD state (index map in row-major RD order, neighbour codes, c',
+// the starting rho / v gathered from dense buffer 0).  Synchronises once to size the arrays.
+// With RDS_OPT_COMPACT = 2 the compact path is taken only when the band holds at most
+// kCompactAutoFrac of the pixels (above that its working set leaves L2 and the dense
+// temporally blocked stencil is faster).
+constexpr double kCompactAutoFrac = 0.08;
+struct CompactPlan {
+    bool use = false;
+    RdcSetup su{};
+    RdcIter it{};
+};
+static int compact_prepare(rds_t *h, float tau, float theta, CompactPlan *cp) {
+    cp->use = false;
+    const int64_t npx = h->H * h->W;
+    if (npx > INT32_MAX / 2) return RDS_OK;  // compact indices are int32: keep the dense path
+    if (!h->rdc_idx) {
+        CK(h, cudaMalloc(&h->rdc_idx, sizeof(int32_t) * npx));
+        CK(h, cudaMalloc(&h->rdc_row, sizeof(int32_t) * (2 * h->H + 1)));
+        CK(h, cudaMalloc(&h->rdc_bar, sizeof(unsigned long long)));
+    }
+    h->rdc_tot = h->rdc_row + 2 * h->H;
+    CK(h, launch_rdc_count(h->at(h->lab), h->pitch, (int)h->H, (int)h->W, h->rdc_row,
+                           h->rdc_row + h->H, h->rdc_tot, h->stream));
+    int32_t n = 0;
+    CK(h, cudaMemcpyAsync(&n, h->rdc_tot, sizeof n, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (h->opt_compact == 2 && (double)n > kCompactAutoFrac * (double)npx) return RDS_OK;
+    // list, nbr[6], c, p1 x2, p2 x2, v x2, u: 15 words per RD pixel
+    const size_t words = 15 * (size_t)(n > 0 ? n : 1);
+    void *pb = h->rdc_buf;
+    CK(h, grow(&pb, &h->rdc_bytes, sizeof(int32_t) * words));
+    h->rdc_buf = pb;
+    int32_t *list = (int32_t *)pb, *nbr = list + n;
+    float *f = (float *)(nbr + 6 * (size_t)n);
+    float *c = f, *p1a = f + n, *p1b = f + 2 * (size_t)n, *p2a = f + 3 * (size_t)n,
+          *p2b = f + 4 * (size_t)n, *va = f + 5 * (size_t)n, *vb = f + 6 * (size_t)n,
+          *u = f + 7 * (size_t)n;
+    CK(h, launch_rdc_fill(h->at(h->lab), h->pitch, (int)h->H, (int)h->W, h->rdc_row + h->H,
+                          h->rdc_idx, list, h->stream));
+    RdcSetup &su = cp->su;
+    su = RdcSetup{};
+    su.n = n;
+    su.H = (int)h->H;
+    su.W = (int)h->W;
+    su.img_w = (int)h->img_w;
+    su.pitch = h->pitch;
+    su.list = list;
+    su.idxmap = h->rdc_idx;
+    su.nbr = nbr;
+    su.c = c;
+    su.p1 = p1a;
+    su.p2 = p2a;
+    su.v = va;
+    su.u = u;
+    su.cplane = h->at(h->c);
+    su.p1plane = h->at(h->p1[0]);
+    su.p2plane = h->at(h->p2[0]);
+    su.vplane = h->at(h->v[0]);
+    su.uplane = h->at(h->u);
+    su.mask = h->at(h->mask);
+    CK(h, launch_rdc_gather(su, h->stream));
+    RdcIter &it = cp->it;
+    it = RdcIter{};
+    it.n = n;
+    it.nbr = nbr;
+    it.c = c;
+    it.p1[0] = p1a;
+    it.p1[1] = p1b;
+    it.p2[0] = p2a;
+    it.p2[1] = p2b;
+    it.v[0] = va;
+    it.v[1] = vb;
+    it.u = u;
+    it.tau = tau;
+    it.theta = theta;
+    it.inv_theta = 1.0f / theta;
+    it.bar = h->rdc_bar;
+    cp->use = true;
+    return RDS_OK;
+}
+
+// run the compact iteration and put the final state into dense buffer 0
+static int compact_run(rds_t *h, CompactPlan *cp, int iters) {
+    cp->it.K = iters;
+    CK(h, launch_rdc_iter(cp->it, h->n_sm, h->stream));
+    RdcSetup su = cp->su;
+    su.p1 = cp->it.p1[iters & 1];
+    su.p2 = cp->it.p2[iters & 1];
+    su.v = cp->it.v[iters & 1];
+    CK(h, launch_rdc_scatter(su, h->stream));
+    return RDS_OK;
+}
+
 static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delta, int32_t iters,
                       int check_every, float tol) {
     if (!(lambda > 0.0f) || !isfinite(lambda))
@@ -814,12 +920,22 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
                                  max_chunk,
                                  2 * kf + 4, h->items, h->counts, h->stream));
     }
+    CompactPlan cplan;
+    if (iters > 0 && check_every == 0 && h->opt_compact) {
+        const int rc = compact_prepare(h, tau, theta, &cplan);
+        if (rc) return rc;
+    }
     h->warm_pending = false;
     h->tol_pending = false;
     h->cur = 0;
     if (h->opt_timing) CK(h, cudaEventRecord(h->ev[1], h->stream));
 
-    if (iters > 0) {
+    if (iters > 0 && cplan.use) {
+        NvtxRange nvtx_rdc("rds_solve (compact RD)");
+        const int rc = compact_run(h, &cplan, iters);
+        if (rc) return rc;
+        h->cur0 = 0;
+    } else if (iters > 0) {
         TolParams tp;
         tp.check_every = check_every;
         tp.tol = tol;
@@ -887,7 +1003,8 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     st.n_items = (int64_t)n_strips * n_bands;
     st.iters = iters;
     st.k_fuse = kf;
-    st.launches = launches;
+    st.launches = cplan.use ? 1 : launches;
+    st.compact = cplan.use ? 1 : 0;
     st.converged = 0;
     st.residual = -1.0f;
     st.check_every = check_every;

@@ -24,6 +24,7 @@ RDS_LABEL_BG, RDS_LABEL_FG, RDS_LABEL_RD = 0, 1, 2
 RDS_OPT_KFUSE, RDS_OPT_ITEM_ROWS, RDS_OPT_TIMING, RDS_OPT_SKIP, RDS_OPT_GRAPH = 1, 2, 3, 4, 5
 RDS_OPT_CTAS_PER_SM = 6
 RDS_OPT_STOP_NORM = 7  # 0 Euclidean over pixels (default), 1 RMS
+RDS_OPT_COMPACT = 8    # f3: 0 dense stencil (default), 1 compacted RD iteration, 2 auto
 
 EXPORTS = (
     "rds_create", "rds_create_batch", "rds_destroy", "rds_set_stream", "rds_set_option",
@@ -72,7 +73,8 @@ class rds_stats_t(ctypes.Structure):
                 ("launches", ctypes.c_int32), ("item_rows", ctypes.c_int32),
                 ("item_cols", ctypes.c_int32), ("converged", ctypes.c_int32),
                 ("setup_ms", ctypes.c_float), ("loop_ms", ctypes.c_float),
-                ("residual", ctypes.c_float), ("check_every", ctypes.c_int32)]
+                ("residual", ctypes.c_float), ("check_every", ctypes.c_int32),
+                ("compact", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -373,7 +375,7 @@ class Solver:
     """One librds handle for an H x W image.  Host (numpy) or device (torch) buffers."""
 
     def __init__(self, H, W, stream=None, k_fuse=0, item_rows=0, timing=False, skip=True,
-                 graph=True, batch=None):
+                 graph=True, batch=None, compact=0):
         self.shape = (int(H) * (int(batch) if batch else 1), int(W))
         if batch is not None:
             h = ctypes.c_void_p()
@@ -390,6 +392,8 @@ class Solver:
         rds_set_option(self.h, RDS_OPT_TIMING, int(timing))
         rds_set_option(self.h, RDS_OPT_SKIP, int(skip))
         rds_set_option(self.h, RDS_OPT_GRAPH, int(graph))
+        if compact:
+            rds_set_option(self.h, RDS_OPT_COMPACT, int(compact))
 
     def close(self):
         if self.h is not None:

@@ -1,0 +1,130 @@
+"""f3: the compacted RD iteration (RDS_OPT_COMPACT) runs the same float
+operations per pixel as the dense stencil, so both paths must give the same u, v, rho and
+mask value for value (signed zeros aside) on every shape, band and iteration count; the
+dense path itself is pinned to the oracle by tests/test_gpu_parity.py, and one case here
+checks the compact path against the oracle directly."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1807_11534_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+PAR = (5.0, 0.1, 0.125)
+
+
+@pytest.fixture(scope="module")
+def rds():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1807_11534_b200 import _build
+
+    _build.build()
+    from paper_1807_11534_b200 import rds as _rds
+
+    return _rds
+
+
+def _run(rds, z, delta, K, compact, batch=None, kf=0, lam=5.0, warm=None, P=None, gamma=0.0):
+    H, W = z.shape[-2:] if batch else z.shape
+    s = rds.BatchSolver(batch, H, W, compact=compact, k_fuse=kf) if batch else \
+        rds.Solver(H, W, compact=compact, k_fuse=kf)
+    s.set_image(z)
+    s.set_fitting(0.8, 0.2, gamma, P)
+    if warm is not None:
+        s.set_state(*warm)
+    s.solve(lam, 0.1, 0.125, delta, K)
+    p1, p2 = s.p()
+    out = dict(u=s.u(), v=s.v(), p1=p1, p2=p2, mask=s.mask(), labels=s.labels())
+    return s, out
+
+
+def _same(a, b):
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k   # == on floats: -0.0 equals +0.0
+
+
+@pytest.mark.parametrize("H,W,delta_rel,K", [(1, 1, 0.5, 3), (7, 5, math.inf, 9),
+                                             (64, 64, 0.2, 1), (64, 64, 0.2, 2),
+                                             (130, 97, 0.1, 50), (257, 300, 0.3, 37),
+                                             (200, 131, math.inf, 20), (96, 128, 0.0, 10),
+                                             (333, 45, 0.05, 64)])
+def test_compact_equals_dense(rds, orc, H, W, delta_rel, K):
+    z = wl.gen_voronoi(N=max(H, W), seed=H + W, n_sites=9)[:H, :W].copy()
+    f = orc.fitting(z, 0.8, 0.2)
+    delta = wl.band_delta(delta_rel, orc.absmax(f)) if delta_rel else np.float32(0.0)
+    s_d, d = _run(rds, z, delta, K, 0)
+    s_c, c = _run(rds, z, delta, K, 1)
+    assert s_c.stats()["compact"] == 1 and s_d.stats()["compact"] == 0
+    _same(d, c)
+    assert s_c.energy() == s_d.energy()
+    assert s_c.check_frame() == 0
+
+
+def test_compact_oracle(rds, orc):
+    z, _ = wl.make_image("C1")
+    z = z[:300, :260].copy()
+    f = orc.fitting(z, 0.8, 0.2)
+    delta = wl.band_delta(0.1, orc.absmax(f))
+    s, g = _run(rds, z, delta, 120, 1)
+    o = orc.solve(f, delta, *PAR, 120)
+    for k in ("u", "v", "p1", "p2"):
+        assert np.abs(g[k].astype(np.float64) - o[k]).max() <= 5e-4, k
+    assert np.mean(g["mask"] != (o["u"] > 0.5)) <= 5e-4
+    assert np.array_equal(g["labels"], o["labels"])
+
+
+def test_compact_variants(rds):
+    """Batch handles (per-image Neumann columns, widths not multiples of 4), the selection
+    term, warm starts, every k_fuse of the dense twin, and the auto switch."""
+    rng = np.random.default_rng(4)
+    zb = rng.uniform(0, 1, (3, 40, 30)).astype(np.float32)
+    _, d = _run(rds, zb, np.float32(0.3), 25, 0, batch=3)
+    _, c = _run(rds, zb, np.float32(0.3), 25, 1, batch=3)
+    _same(d, c)
+    z = wl.gen_voronoi(N=150, seed=8, n_sites=12)[:150, :150].copy()
+    P = rng.uniform(0, 1, z.shape).astype(np.float32)
+    for kf in (1, 4, 7):
+        _, d = _run(rds, z, np.float32(0.25), 30, 0, kf=kf, P=P, gamma=1.5)
+        _, c = _run(rds, z, np.float32(0.25), 30, 1, kf=kf, P=P, gamma=1.5)
+        _same(d, c)
+    warm = wl.random_state(150, 150, 3)
+    _, d = _run(rds, z, np.float32(0.2), 15, 0, warm=warm)
+    _, c = _run(rds, z, np.float32(0.2), 15, 1, warm=warm)
+    _same(d, c)
+    s, _ = _run(rds, z, np.float32(math.inf), 5, 2)     # RD = everything: dense
+    assert s.stats()["compact"] == 0
+    s, _ = _run(rds, z, np.float32(0.01), 5, 2)        # a thin band: compact
+    assert s.stats()["compact"] == 1 and s.stats()["n_rd"] <= 0.08 * z.size
+
+
+def test_compact_then_continue(rds):
+    z = wl.gen_voronoi(N=120, seed=2, n_sites=10)[:120, :120].copy()
+    s1, _ = _run(rds, z, np.float32(0.3), 20, 1)
+    s1.solve_continue(13)
+    s2, _ = _run(rds, z, np.float32(0.3), 33, 0)
+    p1a, p2a = s1.p()
+    p1b, p2b = s2.p()
+    for a, b in ((s1.u(), s2.u()), (s1.v(), s2.v()), (p1a, p1b), (p2a, p2b)):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("delta_rel", [0.05, 0.1])
+def test_compact_c3_full(rds, delta_rel):
+    """Full C3 (4096^2, K = 1000) at the low-band deltas where the compact path pays."""
+    z, _ = wl.make_image("C3")
+    s_d = rds.Solver(*z.shape)
+    s_d.set_image(z)
+    s_d.set_fitting(0.8, 0.2)
+    delta = wl.band_delta(delta_rel, s_d.absmax())
+    s_d.solve(*PAR, delta, 1000)
+    s_c = rds.Solver(*z.shape, compact=1)
+    s_c.set_image(z)
+    s_c.set_fitting(0.8, 0.2)
+    s_c.solve(*PAR, delta, 1000)
+    assert np.array_equal(s_c.u(), s_d.u())
+    assert np.array_equal(s_c.v(), s_d.v())
