@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--rows", type=int, default=0, help="rows per work item (0=lib default)")
     ap.add_argument("--iters", type=int, default=0, help="override K (diagnostics only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-compact", action="store_true",
+                    help="skip the f3 compacted-RD section (restricted_compact)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     return ap.parse_args()
@@ -417,6 +419,8 @@ def run_ours(args, dist):
     if not args.no_e2e:
         line["e2e"] = e2e(args, s, cfg, z, P, deltas, K, lam, dist, work_step)
     s.close()
+    if not args.no_compact:
+        line["restricted_compact"] = compact_section(cfg, zt, Pt, am, K, lam, sp, per_delta)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         r, cores, sample, _ = oracle_rate(cfg, z, P, cfg.delta_rels, args.cpu_seconds)
         line["cpu_baseline"] = {"value": r / 1e9, "unit": UNIT, "cores": cores,
@@ -457,6 +461,43 @@ def e2e(args, s, cfg, z, P, deltas, K, lam, dist, work_step):
             "ms_per_step": 1e3 * dt / args.steps,
             "path": "rds_set_image/rds_set_fitting (pinned host) -> rds_solve -> rds_get_mask "
                     "(host) + rds_energy per delta"}
+
+
+def compact_section(cfg, zt, Pt, am, K, lam, sp, per_delta):
+    """f3 beside the headline (untimed for `value`): the same sweep, plus two thinner bands,
+    solved with RDS_OPT_COMPACT = 2 (the library takes the compacted RD iteration where its
+    cost model predicts a win, else the dense stencil).  Whole-solve times (setup + K-loop,
+    CUDA events, median of 3) against the dense delta = inf solve: the paper's restricted vs
+    full speedup once the work scales with the RD pixels rather than the tiles they touch."""
+    import statistics
+
+    from paper_1807_11534_b200 import rds
+
+    full = [p for p in per_delta if p["delta_rel"] == "inf"]
+    if not full:
+        return None
+    t_full = full[0]["loop_ms"] + full[0]["setup_ms"]
+    s = rds.Solver(cfg.H, cfg.W, stream=sp, timing=True, compact=2)
+    s.set_image(zt)
+    s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, Pt)
+    out = []
+    for dr in sorted(set(cfg.delta_rels) | {0.02, 0.05}):
+        d = wl.band_delta(dr, am)
+        s.solve(lam, cfg.theta, cfg.tau, d, K)
+        ts, st = [], None
+        for _ in range(3):
+            s.solve(lam, cfg.theta, cfg.tau, d, K)
+            st = s.stats()
+            ts.append(st["loop_ms"] + st["setup_ms"])
+        t = statistics.median(ts)
+        out.append({"delta_rel": "inf" if math.isinf(dr) else dr,
+                    "path": "compact" if st["compact"] else "dense",
+                    "rd_frac": st["n_rd"] / (cfg.H * cfg.W), "solve_ms": t,
+                    "speedup_vs_full": t_full / t,
+                    "rd_gpix_iter_s": st["n_rd"] * K / (t * 1e-3) / 1e9})
+    s.close()
+    return {"per_delta": out, "full_dense_solve_ms": t_full,
+            "basis": "RDS_OPT_COMPACT=2 solve (setup + K-loop) vs the dense delta=inf solve"}
 
 
 def _overhead(per_delta):

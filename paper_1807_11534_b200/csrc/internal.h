@@ -161,24 +161,35 @@ cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s);
 // of an RD pixel; RDC_BG / RDC_FG a pinned pixel (rho = 0, v = u0 = 0 / 1) or the frame;
 // RDC_EDGE the missing forward neighbour on row H-1 / an image's last column (grad = 0).
 constexpr int RDC_BG = -1, RDC_FG = -2, RDC_EDGE = -3;
+// Packed neighbour codes, two words per RD pixel: word A = the RD index of (i-1, j), else of
+// (i-1, j+1) | classes of up, up-right, left << RDC_IDX_BITS; word B = the RD index of
+// (i+1, j), else of (i+1, j-1) | classes of down, down-left, right.  2-bit classes:
+constexpr unsigned RDC_C_RD = 0, RDC_C_BG = 1, RDC_C_FG = 2, RDC_C_EDGE = 3;
+constexpr int RDC_IDX_BITS = 26;  // compact path only for n_rd < 2^26
+constexpr unsigned RDC_IDX_MASK = (1u << RDC_IDX_BITS) - 1u;
+__host__ __device__ inline unsigned rdc_cls(int code) {
+    return code >= 0 ? RDC_C_RD : (code == RDC_FG ? RDC_C_FG : (code == RDC_EDGE ? RDC_C_EDGE : RDC_C_BG));
+}
+constexpr int RDC_BAR_BYTES = 128;  // grid barrier counter (one 128-byte line)
 constexpr int RDC_THREADS = 512;
 struct RdcSetup {
     int n, H, W, img_w;
     int64_t pitch;
     const int32_t *list, *idxmap;
-    int32_t *nbr;                 // [6][n]: x-e1, x+e1, x-e2, x+e2, x+e1-e2, x-e1+e2
-    float *c, *p1, *p2, *v, *u;   // compact arrays (gather: buffer 0; scatter: final buffers)
+    uint2 *code;                  // packed neighbour codes
+    float4 *rec;                  // (rho1, rho2, v, c') per RD pixel (gather: start; scatter: final)
+    float *u;
     const float *cplane;          // dense plane origins
     float *p1plane, *p2plane, *vplane, *uplane;
     uint8_t *mask;
 };
 struct RdcIter {
     int n, K;
-    const int32_t *nbr;
-    const float *c;
-    float *p1[2], *p2[2], *v[2], *u;
+    const uint2 *code;
+    float4 *rec[2];               // pass k reads rec[k & 1], writes rec[(k + 1) & 1]
+    float *u;
     float tau, theta, inv_theta;
-    unsigned long long *bar;
+    unsigned *bar;                // RDC_BAR_BYTES, zeroed per launch
 };
 cudaError_t launch_rdc_count(const uint8_t *lab, int64_t pitch, int H, int W, int32_t *rowcnt,
                              int32_t *rowoff, int32_t *total, cudaStream_t s);

@@ -21,6 +21,7 @@
 // is scattered back into the dense planes, after which every getter, rds_energy and
 // rds_solve_continue work unchanged.
 #include <math.h>
+#include <stdlib.h>
 
 #include "internal.h"
 
@@ -116,25 +117,28 @@ __global__ void k_rdc_fill(const uint8_t *lab, int64_t pitch, int H, int W, cons
     }
 }
 
-// per RD pixel: neighbour codes, c' and the starting state from the dense planes
+// per RD pixel: neighbour codes and the record (rho1, rho2, v, c') from the dense planes
 __global__ void k_rdc_gather(const RdcSetup a) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.n; r += gridDim.x * blockDim.x) {
         const int64_t pix = a.list[r];
         const int i = (int)(pix / a.W), j = (int)(pix - (int64_t)i * a.W);
         const bool top = i == 0, bottom = i == a.H - 1, left = j == 0;
         const bool right = j % a.img_w == a.img_w - 1;  // grad_2 = 0 (per image of a batch)
-        const int64_t n = a.n;
-        a.nbr[0 * n + r] = top ? RDC_BG : a.idxmap[pix - a.W];                 // x - e1
-        a.nbr[1 * n + r] = bottom ? RDC_EDGE : a.idxmap[pix + a.W];            // x + e1
-        a.nbr[2 * n + r] = left ? RDC_BG : a.idxmap[pix - 1];                  // x - e2
-        a.nbr[3 * n + r] = right ? RDC_EDGE : a.idxmap[pix + 1];               // x + e2
-        a.nbr[4 * n + r] = (bottom || left) ? RDC_BG : a.idxmap[pix + a.W - 1];  // x + e1 - e2
-        a.nbr[5 * n + r] = (top || j == a.W - 1) ? RDC_BG : a.idxmap[pix - a.W + 1];  // x - e1 + e2
+        // index-map codes of the six neighbours (frame: pinned 0 / Neumann edge)
+        const int up = top ? RDC_BG : a.idxmap[pix - a.W];
+        const int dn = bottom ? RDC_EDGE : a.idxmap[pix + a.W];
+        const int lf = left ? RDC_BG : a.idxmap[pix - 1];
+        const int rt = right ? RDC_EDGE : a.idxmap[pix + 1];
+        const int dl = (bottom || left) ? RDC_BG : a.idxmap[pix + a.W - 1];
+        const int ur = (top || j == a.W - 1) ? RDC_BG : a.idxmap[pix - a.W + 1];
+        // packed (see RdcCode): anchors = the RD index of up (else ur) and of down (else dl)
+        const unsigned ia = up >= 0 ? up : (ur >= 0 ? ur : 0);
+        const unsigned ib = dn >= 0 ? dn : (dl >= 0 ? dl : 0);
+        const unsigned fa = rdc_cls(up) | (rdc_cls(ur) << 2) | (rdc_cls(lf) << 4);
+        const unsigned fb = rdc_cls(dn) | (rdc_cls(dl) << 2) | (rdc_cls(rt) << 4);
+        a.code[r] = make_uint2(ia | (fa << RDC_IDX_BITS), ib | (fb << RDC_IDX_BITS));
         const int64_t o = (int64_t)i * a.pitch + swz(j);
-        a.c[r] = a.cplane[o];
-        a.p1[r] = a.p1plane[o];
-        a.p2[r] = a.p2plane[o];
-        a.v[r] = a.vplane[o];
+        a.rec[r] = make_float4(a.p1plane[o], a.p2plane[o], a.vplane[o], a.cplane[o]);
     }
 }
 
@@ -144,34 +148,36 @@ __global__ void k_rdc_scatter(const RdcSetup a) {
         const int64_t pix = a.list[r];
         const int i = (int)(pix / a.W), j = (int)(pix - (int64_t)i * a.W);
         const int64_t o = (int64_t)i * a.pitch + swz(j), on = (int64_t)i * a.pitch + j;
-        a.p1plane[o] = a.p1[r];
-        a.p2plane[o] = a.p2[r];
-        a.vplane[o] = a.v[r];
+        const float4 x = a.rec[r];
+        a.p1plane[o] = x.x;
+        a.p2plane[o] = x.y;
+        a.vplane[o] = x.z;
         const float u = a.u[r];
         a.uplane[on] = u;
         a.mask[on] = u > 0.5f;
     }
 }
 
-struct Nb {
-    float p1, p2;
-};
-// rho^k at a neighbour code (0 off RD: rho = 0 on Fg u Bg, Eq. 8); L2 loads, the arrays are
-// rewritten by other CTAs between passes
-__device__ __forceinline__ Nb rho_at(const float *P1, const float *P2, int code) {
-    if (code < 0) return Nb{0.0f, 0.0f};
-    return Nb{__ldcg(P1 + code), __ldcg(P2 + code)};
+// the record of a neighbour code: an RD pixel's (rho1, rho2, v, c') from this pass's buffer
+// (L2 loads: other CTAs rewrote it before the last barrier), or a pinned pixel's
+// (0, 0, u0, -): rho = 0 on Fg u Bg (Eq. 8), v = u0
+__device__ __forceinline__ float4 rec_at(const float4 *B, int code) {
+    if (code >= 0) return __ldcg(B + code);
+    return make_float4(0.0f, 0.0f, code == RDC_FG ? 1.0f : 0.0f, 0.0f);
 }
 
-// grid-wide barrier k (monotone counter; every CTA adds 1 per barrier)
-__device__ __forceinline__ void grid_barrier(unsigned long long *ctr, unsigned long long target) {
+// Grid-wide barrier number k (1, 2, ...): one release-add per CTA on a monotone counter,
+// then an acquire spin until all gridDim.x CTAs have arrived k times.  (A two-level version
+// with group counters measured slower: its serial fence/atomic chain outweighs the
+// contention of ~300 arrivals on one address.)
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned k) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(ctr, 1ull);
-        unsigned long long v;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        const unsigned target = k * gridDim.x;
+        unsigned v;
         do {
-            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
         } while (v < target);
     }
     __syncthreads();
@@ -179,115 +185,106 @@ __device__ __forceinline__ void grid_barrier(unsigned long long *ctr, unsigned l
 
 }  // namespace
 
-// What a pixel's pass needs besides the state: its neighbour codes and the c' of the pixel
-// and of its two forward neighbours (constant over the solve).
+// A pixel's neighbour codes (constant over the solve), decoded from its packed pair.
 struct PixConst {
     int r, up, dn, lf, rt, dl, ur;
-    float cx, cd, cr;
 };
 
-__device__ __forceinline__ PixConst pix_const(const RdcIter &a, int r) {
-    const int64_t n = a.n;
+__device__ __forceinline__ int cls_code(unsigned c) {  // pinned class -> neighbour code
+    return c == RDC_C_FG ? RDC_FG : (c == RDC_C_EDGE ? RDC_EDGE : RDC_BG);
+}
+
+__device__ __forceinline__ PixConst decode(uint2 w, int r) {
+    const int ia = (int)(w.x & RDC_IDX_MASK), ib = (int)(w.y & RDC_IDX_MASK);
+    const unsigned fa = w.x >> RDC_IDX_BITS, fb = w.y >> RDC_IDX_BITS;
+    const unsigned cu = fa & 3, cur = (fa >> 2) & 3, cl = fa >> 4;
+    const unsigned cd = fb & 3, cdl = (fb >> 2) & 3, cr = fb >> 4;
     PixConst q;
     q.r = r;
-    q.up = __ldg(a.nbr + r);
-    q.dn = __ldg(a.nbr + n + r);
-    q.lf = __ldg(a.nbr + 2 * n + r);
-    q.rt = __ldg(a.nbr + 3 * n + r);
-    q.dl = __ldg(a.nbr + 4 * n + r);
-    q.ur = __ldg(a.nbr + 5 * n + r);
-    q.cx = __ldg(a.c + r);
-    q.cd = q.dn >= 0 ? __ldg(a.c + q.dn) : 0.0f;
-    q.cr = q.rt >= 0 ? __ldg(a.c + q.rt) : 0.0f;
+    // row-major RD order: (i, j +- 1) are r +- 1; (i-1, j+1) follows (i-1, j), (i+1, j-1)
+    // precedes (i+1, j) when both are RD
+    q.up = cu == RDC_C_RD ? ia : cls_code(cu);
+    q.ur = cur == RDC_C_RD ? (cu == RDC_C_RD ? ia + 1 : ia) : cls_code(cur);
+    q.dn = cd == RDC_C_RD ? ib : cls_code(cd);
+    q.dl = cdl == RDC_C_RD ? (cd == RDC_C_RD ? ib - 1 : ib) : cls_code(cdl);
+    q.lf = cl == RDC_C_RD ? r - 1 : cls_code(cl);
+    q.rt = cr == RDC_C_RD ? r + 1 : cls_code(cr);
     return q;
 }
 
-// v^k at y (code, c' of y) from v^{k-1}: Eq. 7 and 9, the pinned u0 off RD; pass 0: v^0
-__device__ __forceinline__ float v_of(const float *Vp, int code, float cy, float dy, int k,
-                                      float theta) {
-    if (code < 0) return code == RDC_FG ? 1.0f : 0.0f;
-    const float vp = __ldcg(Vp + code);
-    if (k == 0) return vp;
-    return __saturatef(__fmaf_rn(cy, -0x1p100f, __fmaf_rn(dy, -theta, vp)));
+// v^k of a neighbour y (code, record, div p^k there) from v^{k-1}: Eq. 7 and 9; pass 0: v^0
+__device__ __forceinline__ float v_of(int code, const float4 &y, float dy, int k, float theta) {
+    if (code < 0 || k == 0) return y.z;  // pinned u0 / v^0
+    return __saturatef(__fmaf_rn(y.w, -0x1p100f, __fmaf_rn(dy, -theta, y.z)));
 }
 
-struct PassBufs {
-    const float *P1, *P2, *Vp;
-    float *Q1, *Q2, *Vo, *U;
-};
-
-// pass k at one RD pixel (see the header comment); the same float operations as K3
-__device__ __forceinline__ void pix_pass(const PixConst &q, const PassBufs &b, int k, int K,
-                                         float tau, float theta, float inv_theta) {
-    const Nb px = rho_at(b.P1, b.P2, q.r);
-    const Nb pu = rho_at(b.P1, b.P2, q.up), pl = rho_at(b.P1, b.P2, q.lf);
+// Pass k at one RD pixel (see the header comment), reading records (rho^k, v^{k-1}, c') from
+// B and writing (rho^{k+1}, v^k, c') to O -- the same float operations as K3.
+__device__ __forceinline__ void pix_pass(const PixConst &q, const float4 *B, float4 *O,
+                                         float *U, int k, int K, float tau, float theta,
+                                         float inv_theta) {
+    const float4 X = __ldcg(B + q.r);
+    const float4 Up = rec_at(B, q.up), Lf = rec_at(B, q.lf);
     // div p^k = (p1 - p1(x - e1)) + (p2 - p2(x - e2))
-    const float dx = __fadd_rn(__fsub_rn(px.p1, pu.p1), __fsub_rn(px.p2, pl.p2));
-    const float vpx = __ldcg(b.Vp + q.r);
-    const float ux = __fmaf_rn(dx, -theta, vpx);
-    const float vx = k == 0 ? vpx : __saturatef(__fmaf_rn(q.cx, -0x1p100f, ux));
+    const float dx = __fadd_rn(__fsub_rn(X.x, Up.x), __fsub_rn(X.y, Lf.y));
+    const float ux = __fmaf_rn(dx, -theta, X.z);
+    const float vx = k == 0 ? X.z : __saturatef(__fmaf_rn(X.w, -0x1p100f, ux));
     if (k == K) {  // last pass: u^K and v^K only
-        b.Vo[q.r] = vx;
-        b.U[q.r] = ux;  // an RD pixel reports u itself (u0 only off RD)
+        O[q.r] = make_float4(X.x, X.y, vx, X.w);
+        U[q.r] = ux;  // an RD pixel reports u itself (u0 only off RD)
         return;
     }
     const float wx = __fmaf_rn(vx, -inv_theta, dx);
     float g1 = 0.0f, g2 = 0.0f;
     if (q.dn != RDC_EDGE) {  // grad_1 = 0 on row H-1
-        const Nb pd = rho_at(b.P1, b.P2, q.dn), pdl = rho_at(b.P1, b.P2, q.dl);
-        const float dd = __fadd_rn(__fsub_rn(pd.p1, px.p1), __fsub_rn(pd.p2, pdl.p2));
-        g1 = __fsub_rn(__fmaf_rn(v_of(b.Vp, q.dn, q.cd, dd, k, theta), -inv_theta, dd), wx);
+        const float4 D = rec_at(B, q.dn), DL = rec_at(B, q.dl);
+        const float dd = __fadd_rn(__fsub_rn(D.x, X.x), __fsub_rn(D.y, DL.y));
+        g1 = __fsub_rn(__fmaf_rn(v_of(q.dn, D, dd, k, theta), -inv_theta, dd), wx);
     }
     if (q.rt != RDC_EDGE) {  // grad_2 = 0 on an image's last column
-        const Nb pr = rho_at(b.P1, b.P2, q.rt), pur = rho_at(b.P1, b.P2, q.ur);
-        const float dr = __fadd_rn(__fsub_rn(pr.p1, pur.p1), __fsub_rn(pr.p2, px.p2));
-        g2 = __fsub_rn(__fmaf_rn(v_of(b.Vp, q.rt, q.cr, dr, k, theta), -inv_theta, dr), wx);
+        const float4 R = rec_at(B, q.rt), UR = rec_at(B, q.ur);
+        const float dr = __fadd_rn(__fsub_rn(R.x, UR.x), __fsub_rn(R.y, X.y));
+        g2 = __fsub_rn(__fmaf_rn(v_of(q.rt, R, dr, k, theta), -inv_theta, dr), wx);
     }
-    const float s = __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, fabsf(q.cx)));
+    const float s = __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, fabsf(X.w)));
     const float rr = rcp_ax(__fmaf_rn(sqrt_ax(s), tau, 1.0f));
-    b.Q1[q.r] = __fmul_rn(__fmaf_rn(g1, tau, px.p1), rr);
-    b.Q2[q.r] = __fmul_rn(__fmaf_rn(g2, tau, px.p2), rr);
-    if (k > 0) b.Vo[q.r] = vx;
+    O[q.r] = make_float4(__fmul_rn(__fmaf_rn(g1, tau, X.x), rr),
+                         __fmul_rn(__fmaf_rn(g2, tau, X.y), rr), vx, X.w);
 }
 
-__device__ __forceinline__ PassBufs pass_bufs(const RdcIter &a, int k) {
-    // selects, not indexing: a runtime index into the parameter arrays costs a stack copy
-    const bool odd = k & 1;
-    PassBufs b;
-    b.P1 = odd ? a.p1[1] : a.p1[0];
-    b.P2 = odd ? a.p2[1] : a.p2[0];
-    b.Q1 = odd ? a.p1[0] : a.p1[1];
-    b.Q2 = odd ? a.p2[0] : a.p2[1];
-    b.Vp = (k == 0 || odd) ? a.v[0] : a.v[1];  // v^{k-1} in buffer (k-1)&1; pass 0: v^0
-    b.Vo = odd ? a.v[1] : a.v[0];
-    b.U = a.u;
-    return b;
-}
-
-// NPT > 0: every thread owns the fixed pixels t0 + q * stride (q < NPT), whose constants stay
-// in registers for the whole solve; NPT = 0: any n, constants reloaded every pass.
+// Each CTA owns a contiguous range of RD pixels (neighbours in the row above / below are
+// nearby records: L1 reuse).  NPT > 0: every thread owns the fixed pixels
+// start + t + q * blockDim (q < NPT) and keeps their codes in registers for the whole solve;
+// NPT = 0: any n, codes reloaded every pass.
 template <int NPT>
 __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
-    const int stride = gridDim.x * blockDim.x;
-    const int t0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const int chunk = (a.n + gridDim.x - 1) / gridDim.x;
+    const int start = blockIdx.x * chunk;
+    const int stop = min(a.n, start + chunk);
     const float tau = a.tau, theta = a.theta, inv_theta = a.inv_theta;
-    PixConst pc[NPT > 0 ? NPT : 1];
+    uint2 cw[NPT > 0 ? NPT : 1];  // packed codes of the owned pixels (2 registers each)
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
-        const int r = t0 + q * stride;
-        pc[q] = r < a.n ? pix_const(a, r) : PixConst{-1};
+        const int r = start + threadIdx.x + q * blockDim.x;
+        cw[q] = r < stop ? __ldg(a.code + r) : make_uint2(0u, 0u);
     }
     for (int k = 0; k <= a.K; ++k) {
-        const PassBufs b = pass_bufs(a, k);
+        const bool odd = k & 1;  // selects: a runtime index into a.rec would cost a stack copy
+        const float4 *B = odd ? a.rec[1] : a.rec[0];
+        float4 *O = odd ? a.rec[0] : a.rec[1];
         if (NPT > 0) {
 #pragma unroll
-            for (int q = 0; q < NPT; ++q)
-                if (pc[q].r >= 0) pix_pass(pc[q], b, k, a.K, tau, theta, inv_theta);
+            for (int q = 0; q < NPT; ++q) {
+                const int r = start + threadIdx.x + q * blockDim.x;
+                if (r < stop)
+                    pix_pass(decode(cw[q], r), B, O, a.u, k, a.K, tau, theta, inv_theta);
+            }
         } else {
-            for (int r = t0; r < a.n; r += stride)
-                pix_pass(pix_const(a, r), b, k, a.K, tau, theta, inv_theta);
+            for (int r = start + threadIdx.x; r < stop; r += blockDim.x)
+                pix_pass(decode(__ldg(a.code + r), r), B, O, a.u, k, a.K, tau, theta,
+                         inv_theta);
         }
-        if (k < a.K) grid_barrier(a.bar, (unsigned long long)gridDim.x * (unsigned long long)(k + 1));
+        if (k < a.K) grid_barrier(a.bar, (unsigned)(k + 1));
     }
 }
 
@@ -303,7 +300,8 @@ static int grid_of(int n_sm) {
             (void)cudaGetLastError();
             b = 1;
         }
-        if (b > 2) b = 2;  // fewer CTAs: a cheaper grid barrier (one atomic per CTA)
+        static const int cap = getenv("RDS_RDC_MAXB") ? atoi(getenv("RDS_RDC_MAXB")) : 3;
+        if (b > cap) b = cap;  // fewer CTAs: a cheaper grid barrier (one atomic per CTA)
     }
     return b * n_sm;
 }
@@ -345,18 +343,22 @@ cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s) {
     RdcFn fn = nullptr;
     int g = 0;
     const int64_t n = a.n;
+    static const int max_npt = getenv("RDS_RDC_MAXNPT") ? atoi(getenv("RDS_RDC_MAXNPT")) : 2;
     if (n <= (int64_t)grid_of<1>(n_sm) * RDC_THREADS) {
         fn = k_rdc_iter<1>;
         g = grid_of<1>(n_sm);
-    } else if (n <= (int64_t)grid_of<2>(n_sm) * RDC_THREADS * 2) {
+    } else if (max_npt >= 2 && n <= (int64_t)grid_of<2>(n_sm) * RDC_THREADS * 2) {
         fn = k_rdc_iter<2>;
         g = grid_of<2>(n_sm);
-    } else if (n <= (int64_t)grid_of<4>(n_sm) * RDC_THREADS * 4) {
+    } else if (max_npt >= 4 && n <= (int64_t)grid_of<4>(n_sm) * RDC_THREADS * 4) {
         fn = k_rdc_iter<4>;
         g = grid_of<4>(n_sm);
-    } else if (n <= (int64_t)grid_of<8>(n_sm) * RDC_THREADS * 8) {
+    } else if (max_npt >= 8 && n <= (int64_t)grid_of<8>(n_sm) * RDC_THREADS * 8) {
         fn = k_rdc_iter<8>;
         g = grid_of<8>(n_sm);
+    } else if (max_npt >= 16 && n <= (int64_t)grid_of<16>(n_sm) * RDC_THREADS * 16) {
+        fn = k_rdc_iter<16>;
+        g = grid_of<16>(n_sm);
     } else {
         fn = k_rdc_iter<0>;
         g = grid_of<0>(n_sm);
@@ -364,7 +366,7 @@ cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s) {
     const int64_t need = (n + RDC_THREADS - 1) / RDC_THREADS;
     if (g > need) g = (int)need;
     void *args[] = {const_cast<RdcIter *>(&a)};
-    cudaError_t e = cudaMemsetAsync(a.bar, 0, sizeof(unsigned long long), s);
+    cudaError_t e = cudaMemsetAsync(a.bar, 0, RDC_BAR_BYTES, s);
     if (e != cudaSuccess) return e;
     return cudaLaunchCooperativeKernel((const void *)fn, dim3(g), dim3(RDC_THREADS), args, 0, s);
 }

@@ -103,7 +103,7 @@ struct rds_handle {
     int32_t *rdc_idx = nullptr, *rdc_row = nullptr, *rdc_tot = nullptr;
     void *rdc_buf = nullptr;
     size_t rdc_bytes = 0;
-    unsigned long long *rdc_bar = nullptr;
+    unsigned *rdc_bar = nullptr;
     rds_stats_t stats{};
 
     // cached CUDA graph of the K-loop
@@ -729,43 +729,60 @@ static cudaError_t grow(void **p, size_t *cap, size_t bytes) {
     return e;
 }
 
-// f3: build the compacted RD state (index map in row-major RD order, neighbour codes, c',
-// the starting rho / v gathered from dense buffer 0).  Synchronises once to size the arrays.
-// With RDS_OPT_COMPACT = 2 the compact path is taken only when the band holds at most
-// kCompactAutoFrac of the pixels (above that its working set leaves L2 and the dense
-// temporally blocked stencil is faster).
-constexpr double kCompactAutoFrac = 0.08;
+// f3: build the compacted RD state (index map in row-major RD order, packed neighbour codes,
+// records (rho1, rho2, v, c') gathered from dense buffer 0).  Synchronises once to size the
+// arrays.  RDS_OPT_COMPACT = 2 takes the compact path when its cost model beats the dense
+// one by 10% (constants measured on B200, profiles/r01_compact_*.jsonl):
+//   dense   per iteration ~ max(3 us, active-tile pixels / 1.0e12 /s)  (launch floor | K3 rate)
+//   compact per iteration ~ 2 us (grid barrier) + n_rd / R, R = 1.5e11 /s while the compact
+//           working set (~44 B per RD pixel) fits in L2, 1.0e11 /s beyond
+// i.e. thin scattered bands (C3 up to delta ~ 0.1 max|f|: 1.26-4.8x; C4 at 0.02: 2x) and
+// small images, whose dense solve is launch bound (C1: 1.3-1.45x); wider bands stay dense.
+static bool compact_pays(int64_t n_rd, int64_t act_tile_px, size_t l2_bytes) {
+    const double dense = fmax(3.0e-6, (double)act_tile_px / 1.0e12);
+    const double rate = (double)n_rd * 44.0 < 0.8 * (double)l2_bytes ? 1.5e11 : 1.0e11;
+    const double compact = 2.0e-6 + (double)n_rd / rate;
+    return compact < 0.9 * dense;
+}
+
 struct CompactPlan {
     bool use = false;
     RdcSetup su{};
     RdcIter it{};
 };
-static int compact_prepare(rds_t *h, float tau, float theta, CompactPlan *cp) {
+static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactPlan *cp) {
     cp->use = false;
     const int64_t npx = h->H * h->W;
     if (npx > INT32_MAX / 2) return RDS_OK;  // compact indices are int32: keep the dense path
+    if (iters > 4000000) return RDS_OK;      // the grid-barrier counter is 32-bit
     if (!h->rdc_idx) {
         CK(h, cudaMalloc(&h->rdc_idx, sizeof(int32_t) * npx));
         CK(h, cudaMalloc(&h->rdc_row, sizeof(int32_t) * (2 * h->H + 1)));
-        CK(h, cudaMalloc(&h->rdc_bar, sizeof(unsigned long long)));
+        CK(h, cudaMalloc(&h->rdc_bar, RDC_BAR_BYTES));
     }
     h->rdc_tot = h->rdc_row + 2 * h->H;
     CK(h, launch_rdc_count(h->at(h->lab), h->pitch, (int)h->H, (int)h->W, h->rdc_row,
                            h->rdc_row + h->H, h->rdc_tot, h->stream));
-    int32_t n = 0;
+    int32_t n = 0, act = 0;
     CK(h, cudaMemcpyAsync(&n, h->rdc_tot, sizeof n, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaMemcpyAsync(&act, h->counts + 0, sizeof act, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
-    if (h->opt_compact == 2 && (double)n > kCompactAutoFrac * (double)npx) return RDS_OK;
-    // list, nbr[6], c, p1 x2, p2 x2, v x2, u: 15 words per RD pixel
-    const size_t words = 15 * (size_t)(n > 0 ? n : 1);
+    if (n >= (int32_t)RDC_IDX_MASK) return RDS_OK;  // packed codes hold 26-bit indices
+    if (h->opt_compact == 2) {
+        int dev = 0, l2 = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+        if (!compact_pays(n, (int64_t)act * TILE_H * TILE_W, (size_t)l2)) return RDS_OK;
+    }
+    // records x2 (float4), packed codes (uint2), list, u
+    const size_t nn = (size_t)(n > 0 ? n : 1);
     void *pb = h->rdc_buf;
-    CK(h, grow(&pb, &h->rdc_bytes, sizeof(int32_t) * words));
+    CK(h, grow(&pb, &h->rdc_bytes, nn * (16 * 2 + 8 + 4 + 4)));
     h->rdc_buf = pb;
-    int32_t *list = (int32_t *)pb, *nbr = list + n;
-    float *f = (float *)(nbr + 6 * (size_t)n);
-    float *c = f, *p1a = f + n, *p1b = f + 2 * (size_t)n, *p2a = f + 3 * (size_t)n,
-          *p2b = f + 4 * (size_t)n, *va = f + 5 * (size_t)n, *vb = f + 6 * (size_t)n,
-          *u = f + 7 * (size_t)n;
+    float4 *rec0 = (float4 *)pb, *rec1 = rec0 + nn;
+    uint2 *code = (uint2 *)(rec1 + nn);
+    int32_t *list = (int32_t *)(code + nn);
+    float *u = (float *)(list + nn);
     CK(h, launch_rdc_fill(h->at(h->lab), h->pitch, (int)h->H, (int)h->W, h->rdc_row + h->H,
                           h->rdc_idx, list, h->stream));
     RdcSetup &su = cp->su;
@@ -777,11 +794,8 @@ static int compact_prepare(rds_t *h, float tau, float theta, CompactPlan *cp) {
     su.pitch = h->pitch;
     su.list = list;
     su.idxmap = h->rdc_idx;
-    su.nbr = nbr;
-    su.c = c;
-    su.p1 = p1a;
-    su.p2 = p2a;
-    su.v = va;
+    su.code = code;
+    su.rec = rec0;
     su.u = u;
     su.cplane = h->at(h->c);
     su.p1plane = h->at(h->p1[0]);
@@ -793,14 +807,9 @@ static int compact_prepare(rds_t *h, float tau, float theta, CompactPlan *cp) {
     RdcIter &it = cp->it;
     it = RdcIter{};
     it.n = n;
-    it.nbr = nbr;
-    it.c = c;
-    it.p1[0] = p1a;
-    it.p1[1] = p1b;
-    it.p2[0] = p2a;
-    it.p2[1] = p2b;
-    it.v[0] = va;
-    it.v[1] = vb;
+    it.code = code;
+    it.rec[0] = rec0;
+    it.rec[1] = rec1;
     it.u = u;
     it.tau = tau;
     it.theta = theta;
@@ -815,9 +824,7 @@ static int compact_run(rds_t *h, CompactPlan *cp, int iters) {
     cp->it.K = iters;
     CK(h, launch_rdc_iter(cp->it, h->n_sm, h->stream));
     RdcSetup su = cp->su;
-    su.p1 = cp->it.p1[iters & 1];
-    su.p2 = cp->it.p2[iters & 1];
-    su.v = cp->it.v[iters & 1];
+    su.rec = cp->it.rec[(iters + 1) & 1];  // pass K wrote (rho^K, v^K) there
     CK(h, launch_rdc_scatter(su, h->stream));
     return RDS_OK;
 }
@@ -922,7 +929,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     }
     CompactPlan cplan;
     if (iters > 0 && check_every == 0 && h->opt_compact) {
-        const int rc = compact_prepare(h, tau, theta, &cplan);
+        const int rc = compact_prepare(h, tau, theta, iters, &cplan);
         if (rc) return rc;
     }
     h->warm_pending = false;

@@ -95,10 +95,18 @@ def test_compact_variants(rds):
     _, d = _run(rds, z, np.float32(0.2), 15, 0, warm=warm)
     _, c = _run(rds, z, np.float32(0.2), 15, 1, warm=warm)
     _same(d, c)
-    s, _ = _run(rds, z, np.float32(math.inf), 5, 2)     # RD = everything: dense
-    assert s.stats()["compact"] == 0
-    s, _ = _run(rds, z, np.float32(0.01), 5, 2)        # a thin band: compact
-    assert s.stats()["compact"] == 1 and s.stats()["n_rd"] <= 0.08 * z.size
+    for d in (np.float32(math.inf), np.float32(0.01)):  # small image: dense is launch bound
+        s, _ = _run(rds, z, d, 5, 2)
+        assert s.stats()["compact"] == 1
+    z3, _ = wl.make_image("C3")                        # thin scattered band on 4096^2: compact
+    s3 = rds.Solver(*z3.shape, compact=2)
+    s3.set_image(z3)
+    s3.set_fitting(0.8, 0.2)
+    am = s3.absmax()
+    s3.solve(*PAR, wl.band_delta(0.02, am), 5)
+    assert s3.stats()["compact"] == 1
+    s3.solve(*PAR, wl.band_delta(0.2, am), 5)
+    assert s3.stats()["compact"] == 0
 
 
 def test_compact_then_continue(rds):
