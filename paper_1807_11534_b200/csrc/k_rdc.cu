@@ -158,11 +158,25 @@ __global__ void k_rdc_scatter(const RdcSetup a) {
     }
 }
 
+// Record loads: RDC_L1 = 1 caches them in L1 (each record is read by up to 7 pixels of a pass;
+// the acquire load that ends every grid barrier invalidates the SM's L1, so no line from an
+// earlier pass survives), 0 reads through L2 only (ld.global.cg).
+#ifndef RDC_L1
+#define RDC_L1 1
+#endif
+__device__ __forceinline__ float4 ld_rec(const float4 *p) {
+#if RDC_L1
+    return *p;
+#else
+    return __ldcg(p);
+#endif
+}
+
 // the record of a neighbour code: an RD pixel's (rho1, rho2, v, c') from this pass's buffer
-// (L2 loads: other CTAs rewrote it before the last barrier), or a pinned pixel's
-// (0, 0, u0, -): rho = 0 on Fg u Bg (Eq. 8), v = u0
+// (rewritten by other CTAs before the last barrier), or a pinned pixel's (0, 0, u0, -):
+// rho = 0 on Fg u Bg (Eq. 8), v = u0
 __device__ __forceinline__ float4 rec_at(const float4 *B, int code) {
-    if (code >= 0) return __ldcg(B + code);
+    if (code >= 0) return ld_rec(B + code);
     return make_float4(0.0f, 0.0f, code == RDC_FG ? 1.0f : 0.0f, 0.0f);
 }
 
@@ -223,7 +237,7 @@ __device__ __forceinline__ float v_of(int code, const float4 &y, float dy, int k
 __device__ __forceinline__ void pix_pass(const PixConst &q, const float4 *B, float4 *O,
                                          float *U, int k, int K, float tau, float theta,
                                          float inv_theta) {
-    const float4 X = __ldcg(B + q.r);
+    const float4 X = ld_rec(B + q.r);
     const float4 Up = rec_at(B, q.up), Lf = rec_at(B, q.lf);
     // div p^k = (p1 - p1(x - e1)) + (p2 - p2(x - e2))
     const float dx = __fadd_rn(__fsub_rn(X.x, Up.x), __fsub_rn(X.y, Lf.y));
