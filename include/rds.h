@@ -110,13 +110,14 @@ typedef struct {
                                 in row-major RD order with their stencil neighbours' indices, in
                                 one persistent cooperative kernel (k_rdc.cu) instead of the dense
                                 temporally blocked stencil.  0 (default) = dense; 1 = compact for
-                                every fixed-K rds_solve / rds_solve_q; 2 = compact where a cost
-                                model predicts it faster (thin scattered bands on large images,
-                                e.g. C3 below delta ~ 0.08 max|f|).  Same float operations per
+                                every rds_solve / rds_solve_q / rds_solve_tol; 2 = compact where
+                                a cost model predicts it faster (thin scattered bands, e.g. C3
+                                up to delta ~ 0.1 max|f|, and small images).  Same float operations per
                                 pixel as the dense path (results agree value for value); the
                                 solve synchronises once to size the compact arrays; tolerance
-                                solves stay dense, and so do images of more than 2^30 pixels,
-                                bands of 2^26 or more pixels and K > 4e6. */
+                                solves (rds_solve_tol) evaluate the stopping rule inside the
+                                same persistent kernel; images of more than 2^30 pixels, bands
+                                of 2^26 or more pixels and K > 4e6 stay dense. */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */

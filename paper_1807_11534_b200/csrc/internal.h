@@ -172,6 +172,7 @@ __host__ __device__ inline unsigned rdc_cls(int code) {
 }
 constexpr int RDC_BAR_BYTES = 128;  // grid barrier counter (one 128-byte line)
 constexpr int RDC_THREADS = 512;
+constexpr int RDC_MAX_GRID = 4 * 148 * 4;  // bound on k_rdc_iter CTAs (the stopping-sum buffer)
 struct RdcSetup {
     int n, H, W, img_w;
     int64_t pitch;
@@ -190,6 +191,12 @@ struct RdcIter {
     float *u;
     float tau, theta, inv_theta;
     unsigned *bar;                // RDC_BAR_BYTES, zeroed per launch
+    // tolerance solves (check_every > 0): per-CTA partial sums, the outcome (StopRecord
+    // fields iters, converged, residual, checks, flag; launches = 0)
+    int check_every;
+    double tol, norm_div;
+    double *part;                 // [2 * grid]
+    StopRecord *rec_out;
 };
 cudaError_t launch_rdc_count(const uint8_t *lab, int64_t pitch, int H, int W, int32_t *rowcnt,
                              int32_t *rowoff, int32_t *total, cudaStream_t s);
@@ -197,7 +204,7 @@ cudaError_t launch_rdc_fill(const uint8_t *lab, int64_t pitch, int H, int W,
                             const int32_t *rowoff, int32_t *idxmap, int32_t *list,
                             cudaStream_t s);
 cudaError_t launch_rdc_gather(const RdcSetup &a, cudaStream_t s);
-cudaError_t launch_rdc_scatter(const RdcSetup &a, cudaStream_t s);
+cudaError_t launch_rdc_scatter(const RdcSetup &a, const RdcIter &it, cudaStream_t s);
 cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s);
 
 // float64 mode (k_fp64.cu): natural-order padded double planes, same pitch as the floats

@@ -139,19 +139,24 @@ __global__ void k_rdc_gather(const RdcSetup a) {
         a.code[r] = make_uint2(ia | (fa << RDC_IDX_BITS), ib | (fb << RDC_IDX_BITS));
         const int64_t o = (int64_t)i * a.pitch + swz(j);
         a.rec[r] = make_float4(a.p1plane[o], a.p2plane[o], a.vplane[o], a.cplane[o]);
+        a.u[r] = a.uplane[(int64_t)i * a.pitch + j];  // u^0 = u0 (a check after iteration 1)
     }
 }
 
-// final state back into the dense planes (rho, v swizzled; u, mask natural order)
-__global__ void k_rdc_scatter(const RdcSetup a) {
+// final state back into the dense planes (rho, v swizzled; u, mask natural order).  After l
+// iterations rho^l is in the buffer pass l read (rec[l & 1]) and v^l in the one it wrote.
+__global__ void k_rdc_scatter(const RdcSetup a, const float4 *rec0, const float4 *rec1, int K,
+                              const StopRecord *stop) {
+    const int l = stop ? stop->iters : K;
+    const float4 *Pb = (l & 1) ? rec1 : rec0, *Vb = (l & 1) ? rec0 : rec1;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.n; r += gridDim.x * blockDim.x) {
         const int64_t pix = a.list[r];
         const int i = (int)(pix / a.W), j = (int)(pix - (int64_t)i * a.W);
         const int64_t o = (int64_t)i * a.pitch + swz(j), on = (int64_t)i * a.pitch + j;
-        const float4 x = a.rec[r];
+        const float4 x = Pb[r];
         a.p1plane[o] = x.x;
         a.p2plane[o] = x.y;
-        a.vplane[o] = x.z;
+        a.vplane[o] = Vb[r].z;
         const float u = a.u[r];
         a.uplane[on] = u;
         a.mask[on] = u > 0.5f;
@@ -236,16 +241,22 @@ __device__ __forceinline__ float v_of(int code, const float4 &y, float dy, int k
 // B and writing (rho^{k+1}, v^k, c') to O -- the same float operations as K3.
 __device__ __forceinline__ void pix_pass(const PixConst &q, const float4 *B, float4 *O,
                                          float *U, int k, int K, float tau, float theta,
-                                         float inv_theta) {
+                                         float inv_theta, bool chk, bool wr_u, float &su,
+                                         float &sv) {
     const float4 X = ld_rec(B + q.r);
     const float4 Up = rec_at(B, q.up), Lf = rec_at(B, q.lf);
     // div p^k = (p1 - p1(x - e1)) + (p2 - p2(x - e2))
     const float dx = __fadd_rn(__fsub_rn(X.x, Up.x), __fsub_rn(X.y, Lf.y));
     const float ux = __fmaf_rn(dx, -theta, X.z);
     const float vx = k == 0 ? X.z : __saturatef(__fmaf_rn(X.w, -0x1p100f, ux));
-    if (k == K) {  // last pass: u^K and v^K only
+    if (chk) {  // the stopping sums of iteration k: u^k - u^{k-1}, v^k - v^{k-1}
+        const float du = ux - U[q.r], dv = vx - X.z;
+        su += du * du;
+        sv += dv * dv;
+    }
+    if (wr_u) U[q.r] = ux;  // an RD pixel reports u itself (u0 only off RD)
+    if (k == K) {           // last pass: u^K and v^K only
         O[q.r] = make_float4(X.x, X.y, vx, X.w);
-        U[q.r] = ux;  // an RD pixel reports u itself (u0 only off RD)
         return;
     }
     const float wx = __fmaf_rn(vx, -inv_theta, dx);
@@ -266,6 +277,33 @@ __device__ __forceinline__ void pix_pass(const PixConst &q, const float4 *B, flo
                          __fmul_rn(__fmaf_rn(g2, tau, X.y), rr), vx, X.w);
 }
 
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// CTA sum of two doubles in a fixed order (xor-shuffle tree, then the warps in order); the
+// result is valid in thread 0
+__device__ __forceinline__ void cta_sum2(double &a, double &b, double (*sh)[RDC_THREADS / 32]) {
+    a = warp_sum_d(a);
+    b = warp_sum_d(b);
+    const int w = threadIdx.x >> 5;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        sh[0][w] = a;
+        sh[1][w] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a = b = 0.0;
+        for (int i = 0; i < RDC_THREADS / 32; ++i) {
+            a += sh[0][i];
+            b += sh[1][i];
+        }
+    }
+}
+
 // Each CTA owns a contiguous range of RD pixels (neighbours in the row above / below are
 // nearby records: L1 reuse).  NPT > 0: every thread owns the fixed pixels
 // start + t + q * blockDim (q < NPT) and keeps their codes in registers for the whole solve;
@@ -282,23 +320,66 @@ __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
         const int r = start + threadIdx.x + q * blockDim.x;
         cw[q] = r < stop ? __ldg(a.code + r) : make_uint2(0u, 0u);
     }
+    __shared__ double sh[2][RDC_THREADS / 32];
+    __shared__ int stop_s;
+    const int m = a.check_every;  // tolerance solves: check after iterations m, 2m, ..., K
     for (int k = 0; k <= a.K; ++k) {
         const bool odd = k & 1;  // selects: a runtime index into a.rec would cost a stack copy
         const float4 *B = odd ? a.rec[1] : a.rec[0];
         float4 *O = odd ? a.rec[0] : a.rec[1];
+        const bool chk = m > 0 && k >= 1 && (k % m == 0 || k == a.K);
+        const bool chk_next = m > 0 && k + 1 <= a.K && ((k + 1) % m == 0 || k + 1 == a.K);
+        const bool wr_u = k >= 1 && (k == a.K || chk || chk_next);
+        float su = 0.0f, sv = 0.0f;
         if (NPT > 0) {
 #pragma unroll
             for (int q = 0; q < NPT; ++q) {
                 const int r = start + threadIdx.x + q * blockDim.x;
                 if (r < stop)
-                    pix_pass(decode(cw[q], r), B, O, a.u, k, a.K, tau, theta, inv_theta);
+                    pix_pass(decode(cw[q], r), B, O, a.u, k, a.K, tau, theta, inv_theta, chk,
+                             wr_u, su, sv);
             }
         } else {
             for (int r = start + threadIdx.x; r < stop; r += blockDim.x)
                 pix_pass(decode(__ldg(a.code + r), r), B, O, a.u, k, a.K, tau, theta,
-                         inv_theta);
+                         inv_theta, chk, wr_u, su, sv);
         }
-        if (k < a.K) grid_barrier(a.bar, (unsigned)(k + 1));
+        if (chk) {  // this CTA's partial sums, published by the barrier below
+            double du = su, dv = sv;
+            cta_sum2(du, dv, sh);
+            if (threadIdx.x == 0) {
+                a.part[2 * blockIdx.x] = du;
+                a.part[2 * blockIdx.x + 1] = dv;
+            }
+        }
+        if (k < a.K || m > 0) grid_barrier(a.bar, (unsigned)(k + 1));
+        if (chk) {  // every CTA forms the same total in the same order: one common decision
+            double tu = 0.0, tv = 0.0;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+                tu += __ldcg(a.part + 2 * b);
+                tv += __ldcg(a.part + 2 * b + 1);
+            }
+            cta_sum2(tu, tv, sh);
+            if (threadIdx.x == 0) {
+                const double r = fmax(sqrt(tu / a.norm_div), sqrt(tv / a.norm_div));
+                const bool conv = r <= a.tol, fire = conv || k == a.K;
+                stop_s = fire;
+                if (blockIdx.x == 0) {
+                    StopRecord *rec = a.rec_out;
+                    rec->residual = r;
+                    rec->checks += 1;
+                    rec->it = k;
+                    if (fire) {
+                        rec->iters = k;
+                        rec->converged = conv ? 1 : 0;
+                        rec->launches = 0;
+                        rec->flag = 1;
+                    }
+                }
+            }
+            __syncthreads();
+            if (stop_s) break;
+        }
     }
 }
 
@@ -343,11 +424,12 @@ cudaError_t launch_rdc_gather(const RdcSetup &a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_rdc_scatter(const RdcSetup &a, cudaStream_t s) {
+cudaError_t launch_rdc_scatter(const RdcSetup &a, const RdcIter &it, cudaStream_t s) {
     if (a.n <= 0) return cudaSuccess;
     int g = (a.n + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    k_rdc_scatter<<<g, 256, 0, s>>>(a);
+    k_rdc_scatter<<<g, 256, 0, s>>>(a, it.rec[0], it.rec[1], it.K,
+                                    it.check_every > 0 ? it.rec_out : nullptr);
     return cudaGetLastError();
 }
 
@@ -379,6 +461,7 @@ cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s) {
     }
     const int64_t need = (n + RDC_THREADS - 1) / RDC_THREADS;
     if (g > need) g = (int)need;
+    if (g > RDC_MAX_GRID) g = RDC_MAX_GRID;
     void *args[] = {const_cast<RdcIter *>(&a)};
     cudaError_t e = cudaMemsetAsync(a.bar, 0, RDC_BAR_BYTES, s);
     if (e != cudaSuccess) return e;

@@ -104,6 +104,7 @@ struct rds_handle {
     void *rdc_buf = nullptr;
     size_t rdc_bytes = 0;
     unsigned *rdc_bar = nullptr;
+    double *rdc_part = nullptr;       // per-CTA stopping sums of a compact tolerance solve
     rds_stats_t stats{};
 
     // cached CUDA graph of the K-loop
@@ -151,7 +152,7 @@ static void free_all(rds_t *h) {
                      h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch,
                      h->stop,    h->chk,         h->d64,     h->part64,    h->cmp_out,
                      h->lab64,   h->stop64,      h->n64,       h->rows_buf,
-                     h->rdc_idx, h->rdc_row,     h->rdc_buf,   h->rdc_bar};  // rdc_tot points into rdc_row
+                     h->rdc_idx, h->rdc_row,     h->rdc_buf,   h->rdc_bar, h->rdc_part};  // rdc_tot points into rdc_row
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -759,6 +760,7 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactP
         CK(h, cudaMalloc(&h->rdc_idx, sizeof(int32_t) * npx));
         CK(h, cudaMalloc(&h->rdc_row, sizeof(int32_t) * (2 * h->H + 1)));
         CK(h, cudaMalloc(&h->rdc_bar, RDC_BAR_BYTES));
+        CK(h, cudaMalloc(&h->rdc_part, sizeof(double) * 2 * RDC_MAX_GRID));
     }
     h->rdc_tot = h->rdc_row + 2 * h->H;
     CK(h, launch_rdc_count(h->at(h->lab), h->pitch, (int)h->H, (int)h->W, h->rdc_row,
@@ -819,13 +821,20 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactP
     return RDS_OK;
 }
 
-// run the compact iteration and put the final state into dense buffer 0
-static int compact_run(rds_t *h, CompactPlan *cp, int iters) {
-    cp->it.K = iters;
-    CK(h, launch_rdc_iter(cp->it, h->n_sm, h->stream));
-    RdcSetup su = cp->su;
-    su.rec = cp->it.rec[(iters + 1) & 1];  // pass K wrote (rho^K, v^K) there
-    CK(h, launch_rdc_scatter(su, h->stream));
+// run the compact iteration and put the final state into dense buffer 0; a tolerance solve
+// (check_every > 0) leaves its outcome in h->stop like the dense one (launches = 0: the state
+// is in buffer 0 either way)
+static int compact_run(rds_t *h, CompactPlan *cp, int iters, const TolParams &tp) {
+    RdcIter &it = cp->it;
+    it.K = iters;
+    it.check_every = tp.check_every;
+    it.tol = tp.tol;
+    it.norm_div = tp.norm_div;
+    it.part = h->rdc_part;
+    it.rec_out = tp.check_every > 0 ? h->stop : nullptr;
+    if (tp.check_every > 0) CK(h, cudaMemsetAsync(h->stop, 0, sizeof(StopRecord), h->stream));
+    CK(h, launch_rdc_iter(it, h->n_sm, h->stream));
+    CK(h, launch_rdc_scatter(cp->su, it, h->stream));
     return RDS_OK;
 }
 
@@ -928,7 +937,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
                                  2 * kf + 4, h->items, h->counts, h->stream));
     }
     CompactPlan cplan;
-    if (iters > 0 && check_every == 0 && h->opt_compact) {
+    if (iters > 0 && h->opt_compact) {
         const int rc = compact_prepare(h, tau, theta, iters, &cplan);
         if (rc) return rc;
     }
@@ -939,9 +948,15 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
 
     if (iters > 0 && cplan.use) {
         NvtxRange nvtx_rdc("rds_solve (compact RD)");
-        const int rc = compact_run(h, &cplan, iters);
+        TolParams tp;
+        tp.check_every = check_every;
+        tp.tol = tol;
+        tp.max_iters = iters;
+        tp.norm_div = h->opt_norm ? (double)h->H * (double)h->W : 1.0;
+        const int rc = compact_run(h, &cplan, iters, tp);
         if (rc) return rc;
         h->cur0 = 0;
+        if (check_every > 0) h->tol_pending = true;
     } else if (iters > 0) {
         TolParams tp;
         tp.check_every = check_every;
@@ -1048,9 +1063,9 @@ static int resolve(rds_t *h) {
     StopRecord r;
     CK(h, cudaMemcpyAsync(&r, h->stop, sizeof r, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
-    h->cur = h->cur0 ^ (r.launches & 1);
+    h->cur = h->cur0 ^ (r.launches & 1);  // compact path: launches = 0, state in buffer 0
     h->stats.iters = r.iters;
-    h->stats.launches = r.launches;
+    if (!h->stats.compact) h->stats.launches = r.launches;
     h->stats.converged = r.converged;
     h->stats.residual = (float)r.residual;
     h->tol_pending = false;

@@ -136,3 +136,51 @@ def test_compact_c3_full(rds, delta_rel):
     s_c.solve(*PAR, delta, 1000)
     assert np.array_equal(s_c.u(), s_d.u())
     assert np.array_equal(s_c.v(), s_d.v())
+
+
+def _resid(a, b):
+    return max(float(np.sqrt(np.sum((a[0].astype(np.float64) - b[0]) ** 2))),
+               float(np.sqrt(np.sum((a[1].astype(np.float64) - b[1]) ** 2))))
+
+
+@pytest.mark.parametrize("img,delta_rel,tol,m", [("C0", math.inf, 1e-2, 10),
+                                                 ("C3crop", 0.1, 5e-2, 7),
+                                                 ("C3crop", 0.05, 2e-2, 1)])
+def test_compact_tolerance(rds, img, delta_rel, tol, m):
+    """The stopping rule inside the persistent kernel: it stops at the first check l with
+    max(||u^l - u^(l-1)||, ||v^l - v^(l-1)||) <= tol (reading R-F2), leaving
+    exactly the fixed-K state of l iterations, at the same l as the dense tolerance solve."""
+    if img == "C0":
+        z, _ = wl.make_image("C0")
+    else:
+        z = wl.make_image("C3")[0][:384, :448].copy()
+    H, W = z.shape
+
+    def solver(compact):
+        s = rds.Solver(H, W, compact=compact)
+        s.set_image(z)
+        s.set_fitting(0.8, 0.2)
+        return s
+
+    s = solver(1)
+    d = wl.band_delta(delta_rel, s.absmax())
+    st = s.solve_tol(*PAR, d, 2000, tol, m)
+    assert st["compact"] == 1
+    l = st["iters"]
+    assert st["converged"] == 1 and 0 < l < 2000 and (l % m == 0)
+    f = solver(1)
+    f.solve(*PAR, d, l)
+    p1a, p2a = s.p()
+    p1b, p2b = f.p()
+    for a, b in ((s.u(), f.u()), (s.v(), f.v()), (p1a, p1b), (p2a, p2b), (s.mask(), f.mask())):
+        assert np.array_equal(a, b)
+    uv = {}
+    for k in sorted({l, l - 1, l - m, l - m - 1} - {0, -1} if l > m else {l, l - 1}):
+        f.solve(*PAR, d, k)
+        uv[k] = (f.u(), f.v())
+    r_l = _resid(uv[l], uv[l - 1])
+    assert r_l <= tol and abs(r_l - st["residual"]) <= 1e-4 * max(r_l, 1e-12) + 1e-7
+    if l > m:
+        assert _resid(uv[l - m], uv[l - m - 1]) > tol
+    sd = solver(0).solve_tol(*PAR, d, 2000, tol, m)     # the dense twin stops at the same l
+    assert sd["compact"] == 0 and sd["iters"] == l
