@@ -463,6 +463,10 @@ def e2e(args, s, cfg, z, P, deltas, K, lam, dist, work_step):
                     "(host) + rds_energy per delta"}
 
 
+RDC_BYTES_PER_RD_ITER = 40  # k_rdc_iter: record (16 B) in + out, packed codes (8 B)
+L2_READ_GBS = 17900.0       # measured L2-resident read bandwidth, profiles/micro_l2_bw.txt
+
+
 def compact_section(cfg, zt, Pt, am, K, lam, sp, per_delta):
     """f3 beside the headline (untimed for `value`): the same sweep, plus two thinner bands,
     solved with RDS_OPT_COMPACT = 2 (the library takes the compacted RD iteration where its
@@ -490,11 +494,20 @@ def compact_section(cfg, zt, Pt, am, K, lam, sp, per_delta):
             st = s.stats()
             ts.append(st["loop_ms"] + st["setup_ms"])
         t = statistics.median(ts)
-        out.append({"delta_rel": "inf" if math.isinf(dr) else dr,
-                    "path": "compact" if st["compact"] else "dense",
-                    "rd_frac": st["n_rd"] / (cfg.H * cfg.W), "solve_ms": t,
-                    "speedup_vs_full": t_full / t,
-                    "rd_gpix_iter_s": st["n_rd"] * K / (t * 1e-3) / 1e9})
+        row = {"delta_rel": "inf" if math.isinf(dr) else dr,
+               "path": "compact" if st["compact"] else "dense",
+               "rd_frac": st["n_rd"] / (cfg.H * cfg.W), "solve_ms": t,
+               "speedup_vs_full": t_full / t,
+               "rd_gpix_iter_s": st["n_rd"] * K / (t * 1e-3) / 1e9}
+        if st["compact"]:
+            # k_rdc_iter moves 40 algorithmic bytes per RD pixel-iteration (own record in and
+            # out, packed codes) against the measured L2 read bandwidth; it is latency / grid
+            # barrier bound, so this fraction stays well below 1
+            lm = statistics.median(ts) - st["setup_ms"]
+            gbs = RDC_BYTES_PER_RD_ITER * st["n_rd"] * K / (lm * 1e-3) / 1e9
+            row["roofline"] = {"bound": "l2", "achieved": gbs, "peak": L2_READ_GBS,
+                               "unit": "GB/s", "frac": gbs / L2_READ_GBS}
+        out.append(row)
     s.close()
     return {"per_delta": out, "full_dense_solve_ms": t_full,
             "basis": "RDS_OPT_COMPACT=2 solve (setup + K-loop) vs the dense delta=inf solve"}
