@@ -184,3 +184,22 @@ def test_compact_tolerance(rds, img, delta_rel, tol, m):
         assert _resid(uv[l - m], uv[l - m - 1]) > tol
     sd = solver(0).solve_tol(*PAR, d, 2000, tol, m)     # the dense twin stops at the same l
     assert sd["compact"] == 0 and sd["iters"] == l
+
+
+def test_compact_tolerance_batch(rds):
+    """A batch handle on the compact path with the stopping rule: same stop and state as the
+    dense twin (per-image Neumann columns, widths not multiples of 4)."""
+    rng = np.random.default_rng(11)
+    zb = np.clip(rng.normal(0.5, 0.3, (4, 36, 22)), 0, 1).astype(np.float32)
+    out = []
+    for compact in (0, 1):
+        s = rds.BatchSolver(4, 36, 22, compact=compact)
+        s.set_image(zb)
+        s.set_fitting(0.8, 0.2)
+        st = s.solve_tol(*PAR, np.float32(0.3), 3000, 1e-3, 5)
+        p1, p2 = s.p()
+        out.append((st, s.u(), s.v(), p1, p2))
+    (sd, *a), (sc, *b) = out
+    assert sc["compact"] == 1 and sd["iters"] == sc["iters"] and sc["converged"] == 1
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)

@@ -106,11 +106,14 @@ def test_state_rows_roundtrip(rds):
         fresh.state_rows(0, 1)
 
 
-@pytest.mark.parametrize("H,W,G,s,K,delta_rel,kf", [(257, 190, 2, 7, 40, 0.3, 7),
-                                                    (300, 129, 3, 5, 33, math.inf, 4),
-                                                    (200, 96, 4, 4, 21, 0.2, 0),
-                                                    (181, 77, 3, 3, 10, 0.4, 3)])
-def test_strips_bitwise_whole_image(rds, H, W, G, s, K, delta_rel, kf):
+@pytest.mark.parametrize("H,W,G,s,K,delta_rel,kf,compact", [(257, 190, 2, 7, 40, 0.3, 7, 0),
+                                                            (300, 129, 3, 5, 33, math.inf, 4, 0),
+                                                            (200, 96, 4, 4, 21, 0.2, 0, 0),
+                                                            (181, 77, 3, 3, 10, 0.4, 3, 0),
+                                                            (240, 200, 3, 6, 30, 0.1, 0, 1)])
+def test_strips_bitwise_whole_image(rds, H, W, G, s, K, delta_rel, kf, compact):
+    """(compact = 1: every strip's first segment on the compacted RD path, the rest dense --
+    the two paths agree value for value, so the strips still equal the whole image)"""
     z = _image(H, W, G * 100 + s)
     ref = rds.Solver(H, W, k_fuse=kf)
     ref.set_image(z)
@@ -122,7 +125,7 @@ def test_strips_bitwise_whole_image(rds, H, W, G, s, K, delta_rel, kf):
     plan = strips.partition(H, G, s)
     engines = []
     for st in plan:
-        e = rds.Solver(st.rows, W, k_fuse=kf)
+        e = rds.Solver(st.rows, W, k_fuse=kf, compact=compact)
         e.set_image(z[st.r0:st.r0 + st.rows])
         e.set_fitting(0.8, 0.2)
         engines.append(e)
