@@ -18,7 +18,8 @@
  *
  * Parity pins: every function below is pinned by a -m "not gpu" test in tests/test_oracle_*.py
  * (closed forms, textbook identities, brute force, invariants).  The intermediate iterate
- * values themselves have no printed value in the paper -- see DESIGN.md "parity unpinned".
+ * values themselves have no printed value in the paper: they are pinned only through those
+ * closed forms, special cases and invariants.
  */
 #include <math.h>
 #include <stdint.h>
