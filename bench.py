@@ -59,6 +59,11 @@ def parse():
     ap.add_argument("--rows", type=int, default=0, help="rows per work item (0=lib default)")
     ap.add_argument("--iters", type=int, default=0, help="override K (diagnostics only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layout", default="replicas", choices=["replicas", "strips"],
+                    help="N>1: independent replicas (default, weak scaling) or one image in "
+                         "row strips with halo exchange (strong scaling)")
+    ap.add_argument("--seg", type=int, default=28, help="strips: iterations between halo "
+                                                       "refreshes")
     ap.add_argument("--no-compact", action="store_true",
                     help="skip the f3 compacted-RD section (restricted_compact)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -545,12 +550,92 @@ def _traffic_from_profile(kf):
     return None
 
 
+# ------------------------------------------------------------------------------------------
+# --layout strips: one image over the ranks (opt-in, strong scaling)
+# ------------------------------------------------------------------------------------------
+
+def run_strips(args, dist):
+    """ONE image split in row strips over the ranks (paper_1807_11534_b200/strips.py: halo
+    exchange by torch.distributed point-to-point, NCCL), the C-config delta sweep as one step.
+    value = whole-image pixel-iterations / max-over-ranks time; strong scaling.  With one rank
+    this times the segmented solve (rds_solve + rds_solve_continue every seg iterations) of a
+    single strip without any exchange."""
+    import torch
+    import torch.distributed as tdist
+
+    assert torch.cuda.is_available(), "bench.py --layout strips needs a CUDA device"
+    torch.cuda.set_device(dist.local)
+    from paper_1807_11534_b200 import strips
+
+    own_pg = not tdist.is_initialized()
+    if own_pg:  # one rank: a single-process group for StripSolver
+        tdist.init_process_group("nccl", store=tdist.HashStore(), rank=0, world_size=1,
+                                 device_id=torch.device("cuda", dist.local))
+    cfg = wl.CONFIGS[args.config]
+    K = args.iters or cfg.iters
+    lam = cfg.lambdas[0]
+    z, P = wl.make_image(cfg)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    zt = torch.from_numpy(z).cuda()
+    Pt = torch.from_numpy(P).cuda() if P is not None else None
+    ss = strips.StripSolver(cfg.H, cfg.W, args.seg)
+    ss.set_image(zt)
+    ss.set_fitting(cfg.c1, cfg.c2, cfg.gamma, Pt)
+    am = ss.absmax()
+    deltas = [wl.band_delta(dr, am) for dr in cfg.delta_rels]
+
+    def step():
+        for d in deltas:
+            ss.solve(lam, cfg.theta, cfg.tau, d, K)
+            ss.energy()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    clocks = Clocks(dist.local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ck = clocks.stop()
+    t_ms = dist.max(ev0.elapsed_time(ev1))
+    work = float(cfg.H * cfg.W) * K * len(deltas) * args.steps
+    me = ss.me
+    line = {
+        "metric": METRIC, "value": throughput(work, t_ms), "unit": UNIT,
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.desc}", "H": cfg.H, "W": cfg.W, "iters": K,
+                   "delta_rels": _js(cfg.delta_rels),
+                   "parallelism": f"row strips x{dist.world}, halo refresh every {args.seg} "
+                                  f"iterations", "rows_held_rank0": me.rows,
+                   "l2": "no flush: per-iteration working set > L2 at C3/C4"},
+        "work_basis": "whole-image pixel-iterations (every tile of C3 is active)",
+        "clocks": ck,
+    }
+    if dist.rank == 0:
+        print(json.dumps(line), flush=True)
+    ss.engine.close()
+    if own_pg:
+        tdist.destroy_process_group()
+
+
 def main():
     args = parse()
     dist = Dist()
     try:
         if args.impl == "reference":
             run_reference(args, dist)
+        elif args.layout == "strips":
+            run_strips(args, dist)
         else:
             run_ours(args, dist)
     finally:
