@@ -832,7 +832,17 @@ static int compact_run(rds_t *h, CompactPlan *cp, int iters, const TolParams &tp
     it.norm_div = tp.norm_div;
     it.part = h->rdc_part;
     it.rec_out = tp.check_every > 0 ? h->stop : nullptr;
-    if (tp.check_every > 0) CK(h, cudaMemsetAsync(h->stop, 0, sizeof(StopRecord), h->stream));
+    if (tp.check_every > 0) {
+        StopRecord r{};
+        if (it.n == 0) {  // nothing iterates: the first check (m or K) sees a zero residual
+            r.flag = 1;
+            r.iters = r.it = tp.check_every < iters ? tp.check_every : iters;
+            r.converged = 1;
+            r.checks = 1;
+        }
+        CK(h, cudaMemcpyAsync(h->stop, &r, sizeof r, cudaMemcpyHostToDevice, h->stream));
+        if (it.n == 0) CK(h, cudaStreamSynchronize(h->stream));  // r lives on this stack
+    }
     CK(h, launch_rdc_iter(it, h->n_sm, h->stream));
     CK(h, launch_rdc_scatter(cp->su, it, h->stream));
     return RDS_OK;

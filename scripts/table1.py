@@ -2,7 +2,8 @@
 study) on the synthetic stand-in images: for each q, the restricted solve (q -> q^ by
 rds_band_for_fraction) run to the paper's delta_stop = 1e-2 with the fused stopping rule,
 E1 (Tanimoto) and E2 (L2) against u^GT = the unrestricted float64 solve to 1e-10
-(rds_solve_gt), and the GPU time of the restricted solve.  One JSON line per q.
+(rds_solve_gt), and the GPU time of the restricted solve -- on the dense stencil and on the
+compacted RD path (f3, RDS_OPT_COMPACT = 1), whose cost follows q.  One JSON line per q.
 The paper's own images are not distributed (PAPER.md:160-195 are [FIGURE] placeholders), so
 its Table 1 values are context, not targets."""
 import argparse
@@ -43,6 +44,9 @@ ev1.record(st)
 ev1.synchronize()
 print(json.dumps({"config": cfg.name, "gt": gt, "gt_ms": ev0.elapsed_time(ev1),
                   "lambda": lam}), flush=True)
+c = rds.Solver(cfg.H, cfg.W, stream=st.cuda_stream, timing=True, compact=1)
+c.set_image(z)
+c.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
 for q in [float(x) for x in args.qs.split(",")]:
     delta = s.band_for_fraction(q)
     r = s.solve_tol(lam, cfg.theta, cfg.tau, delta, args.max_iters, args.stop,
@@ -50,8 +54,15 @@ for q in [float(x) for x in args.qs.split(",")]:
     r = s.solve_tol(lam, cfg.theta, cfg.tau, delta, args.max_iters, args.stop,
                     args.check_every)
     e1, e2 = s.compare_gt(0.5)
+    rc = c.solve_tol(lam, cfg.theta, cfg.tau, delta, args.max_iters, args.stop,
+                     args.check_every)
+    rc = c.solve_tol(lam, cfg.theta, cfg.tau, delta, args.max_iters, args.stop,
+                     args.check_every)
     print(json.dumps({"q": q, "delta": float(delta), "iters": r["iters"],
                       "residual": r["residual"], "E1": e1, "E2": e2,
                       "rd_frac": r["n_rd"] / (cfg.H * cfg.W), "loop_ms": r["loop_ms"],
-                      "setup_ms": r["setup_ms"]}), flush=True)
+                      "setup_ms": r["setup_ms"], "compact_iters": rc["iters"],
+                      "compact_loop_ms": rc["loop_ms"], "compact_setup_ms": rc["setup_ms"]}),
+          flush=True)
 s.close()
+c.close()

@@ -203,3 +203,17 @@ def test_compact_tolerance_batch(rds):
     assert sc["compact"] == 1 and sd["iters"] == sc["iters"] and sc["converged"] == 1
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_compact_tolerance_empty_band(rds):
+    """RD empty (q = 0): both paths report the first check (residual 0, converged) and u0."""
+    z, _ = wl.make_image("C0")
+    out = []
+    for compact in (0, 1):
+        s = rds.Solver(*z.shape, compact=compact)
+        s.set_image(z)
+        s.set_fitting(0.8, 0.2)
+        st = s.solve_tol(*PAR, np.float32(0.0), 500, 1e-2, 10)
+        out.append((st["iters"], st["converged"], st["residual"], s.u()))
+    assert out[0][:3] == out[1][:3] == (10, 1, 0.0)
+    assert np.array_equal(out[0][3], out[1][3])
