@@ -211,9 +211,10 @@ cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s);
 struct F64Args {
     const float *z, *P;        // image and selection map (float planes; P may be null)
     double *f, *u, *v;
+    double *v2;                // second v buffer of the persistent solve (k64_persist), or null
     double *p1[2], *p2[2];     // ping-pong rho
     uint8_t *lab;
-    StopRecord *stop;          // early exit once the stopping rule fired (null: never)
+    StopRecord *stop;          // outcome of the tolerance solve
     int64_t pitch;
     int H, W, img_w;
     float c1, c2, gamma, delta;
@@ -222,9 +223,17 @@ struct F64Args {
 constexpr int F64_BLOCKS = 592;  // fixed grid of the double-precision kernels (4 x 148)
 int f64_grid(int64_t n);
 cudaError_t launch_f64_init(const F64Args &a, cudaStream_t s);
-// one iteration: rho from buffer b into b ^ 1, then u, v; part != null adds the stopping sums
-// (one [du^2, dv^2] pair per CTA of f64_grid)
-cudaError_t launch_f64_iter(const F64Args &a, int b, double *part, cudaStream_t s);
+// the whole fp64 tolerance solve as one cooperative launch (k64_persist)
+constexpr int F64P_THREADS = 256, F64P_MAX_GRID = 2 * 148 * 4;
+struct F64Persist {
+    F64Args a;                 // a.v = v buffer 0 (v^0 after init), a.stop = the outcome
+    double *v[2];
+    int max_iters, check_every;
+    double tol, norm_div;
+    double *part;              // [2 * grid]
+    unsigned *bar;
+};
+cudaError_t launch_f64_persist(const F64Persist &q, int n_sm, cudaStream_t s);
 // E1, E2 of the float u against a double u (out[0], out[1]); part holds 3 doubles per CTA
 cudaError_t launch_compare(const float *u, const double *ugt, int64_t pitch, int H, int W,
                            float eps, double *part, double *out, cudaStream_t s);

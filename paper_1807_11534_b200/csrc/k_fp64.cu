@@ -11,9 +11,9 @@
 //   u   = v - theta div rho on RD, u0 elsewhere                 (Eq. 7)
 //   v   = min(max(u - (theta lambda) f, 0), 1) on RD, u0 elsewhere (Eq. 9)
 // with div rho = ((rho1 - rho1(i-1,j)) + rho2) - rho2(i,j-1) (reading R-C6).  Throughput is
-// not the point here (this is the reference-quality solver of the evaluation protocol, run on
-// the paper's 128 x 128 images), so it is a plain two-kernel-per-iteration scheme on natural-
-// order double planes (padded like the float planes; the frame holds zeros).
+// not the first concern here (this is the reference-quality solver of the evaluation protocol,
+// run on the paper's 128 x 128 images), so it works on natural-order double planes (padded
+// like the float planes; the frame holds zeros), one persistent cooperative launch per solve.
 #include <math.h>
 
 #include "internal.h"
@@ -51,85 +51,189 @@ __global__ void k64_init(const F64Args a) {
         a.lab[o] = rd ? 2 : (f <= 0.0f ? 1 : 0);
         a.u[o] = u0;
         a.v[o] = u0;
+        if (a.v2) a.v2[o] = u0;  // the persistent solve's second v buffer
         a.p1[0][o] = a.p1[1][o] = 0.0;
         a.p2[0][o] = a.p2[1][o] = 0.0;
     }
 }
 
-// rho-step: reads rho (buffer b) and v, writes rho (buffer b ^ 1)
-__global__ void k64_rho(const F64Args a, int b) {
-    if (a.stop != nullptr && *(volatile const int32_t *)&a.stop->flag != 0) return;
-    const int64_t n = (int64_t)a.H * a.W, P = a.pitch;
-    const double *p1 = a.p1[b], *p2 = a.p2[b];
-    double *q1 = a.p1[b ^ 1], *q2 = a.p2[b ^ 1];
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        const int i = (int)(k / a.W), j = (int)(k - (int64_t)i * a.W);
-        const int64_t o = (int64_t)i * P + j;
-        if (a.lab[o] != 2) {
-            q1[o] = 0.0;
-            q2[o] = 0.0;
-            continue;
+// ---------------------------------------------------------------------------------------
+// Persistent form (rds_solve_gt): ONE cooperative launch runs the whole solve, a grid barrier
+// between iterations.  Pass k at pixel x (on RD; pinned pixels never change) computes, from
+// rho^k and v^{k-1}, the u/v step of iteration k at x and at its two forward neighbours
+// (recomputed so one barrier per iteration suffices), then w^k and rho^{k+1}(x) -- exactly
+// operations written out at the top of this file, each in the order written, so the iterates
+// are the same bits as the fp64 oracle's.  At a check iteration the CTAs publish fixed-order partial sums of
+// (u^l - u^{l-1})^2, (v^l - v^{l-1})^2 and, after the barrier, all form the same total and take
+// the same stop decision.
+// ---------------------------------------------------------------------------------------
+
+namespace {
+
+__device__ __forceinline__ void gbar(unsigned *bar, unsigned k) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        const unsigned target = k * gridDim.x;
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double wsum(double x) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// fixed-order CTA sum of two doubles (valid in thread 0)
+__device__ __forceinline__ void cta2(double &a, double &b, double (*sh)[F64P_THREADS / 32]) {
+    a = wsum(a);
+    b = wsum(b);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        sh[0][threadIdx.x >> 5] = a;
+        sh[1][threadIdx.x >> 5] = b;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a = b = 0.0;
+        for (int w = 0; w < F64P_THREADS / 32; ++w) {
+            a += sh[0][w];
+            b += sh[1][w];
         }
-        const double w = __dsub_rn(div64(p1, p2, o, P), __ddiv_rn(a.v[o], a.theta));
-        double g1 = 0.0, g2 = 0.0;
-        if (i < a.H - 1)
-            g1 = __dsub_rn(__dsub_rn(div64(p1, p2, o + P, P), __ddiv_rn(a.v[o + P], a.theta)), w);
-        if (j % a.img_w != a.img_w - 1)
-            g2 = __dsub_rn(__dsub_rn(div64(p1, p2, o + 1, P), __ddiv_rn(a.v[o + 1], a.theta)), w);
-        const double ng = __dsqrt_rn(__dadd_rn(__dmul_rn(g1, g1), __dmul_rn(g2, g2)));
-        const double den = __dadd_rn(1.0, __dmul_rn(a.tau, ng));
-        q1[o] = __ddiv_rn(__dadd_rn(p1[o], __dmul_rn(a.tau, g1)), den);
-        q2[o] = __ddiv_rn(__dadd_rn(p2[o], __dmul_rn(a.tau, g2)), den);
     }
 }
 
-// u- and v-steps from rho (buffer b); with part != null also the stopping sums
-// sum (u - u_prev)^2, sum (v - v_prev)^2 of this iteration, one fixed-order partial per CTA
-__global__ void __launch_bounds__(256) k64_uv(const F64Args a, int b, double *part) {
-    if (a.stop != nullptr && *(volatile const int32_t *)&a.stop->flag != 0) return;
+// v^k at an RD pixel y from v^{k-1}(y) and div rho^k(y): u = v - theta div rho, then the clamp
+__device__ __forceinline__ double v_step(double vp, double d, double f, double theta,
+                                         double theta_lambda, double *u_out) {
+    const double u = __dsub_rn(vp, __dmul_rn(theta, d));
+    const double t = __dsub_rn(u, __dmul_rn(theta_lambda, f));
+    *u_out = u;
+    return t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(F64P_THREADS) k64_persist(const F64Persist q) {
+    const F64Args &a = q.a;
     const int64_t n = (int64_t)a.H * a.W, P = a.pitch;
-    const double *p1 = a.p1[b], *p2 = a.p2[b];
-    double su = 0.0, sv = 0.0;
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-         k += (int64_t)gridDim.x * blockDim.x) {
-        const int i = (int)(k / a.W), j = (int)(k - (int64_t)i * a.W);
-        const int64_t o = (int64_t)i * P + j;
-        if (a.lab[o] != 2) continue;                   // u = v = u0, unchanged
-        const double v = a.v[o];
-        const double u = __dsub_rn(v, __dmul_rn(a.theta, div64(p1, p2, o, P)));
-        const double t = __dsub_rn(u, __dmul_rn(a.theta_lambda, a.f[o]));
-        const double vn = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
-        if (part) {
-            const double du = __dsub_rn(u, a.u[o]), dv = __dsub_rn(vn, v);
-            su = __fma_rn(du, du, su);
-            sv = __fma_rn(dv, dv, sv);
-        }
-        a.u[o] = u;
-        a.v[o] = vn;
-    }
-    if (part) {
-#pragma unroll
-        for (int off = 16; off; off >>= 1) {
-            su += __shfl_xor_sync(0xffffffffu, su, off);
-            sv += __shfl_xor_sync(0xffffffffu, sv, off);
-        }
-        __shared__ double sh[2][8];
-        if ((threadIdx.x & 31) == 0) {
-            sh[0][threadIdx.x >> 5] = su;
-            sh[1][threadIdx.x >> 5] = sv;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double tu = 0.0, tv = 0.0;
-            for (int w = 0; w < 8; ++w) {
-                tu += sh[0][w];
-                tv += sh[1][w];
+    const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t k0 = blockIdx.x * chunk, k1 = min(n, k0 + chunk);
+    const double theta = a.theta, tau = a.tau, tl = a.theta_lambda;
+    __shared__ double sh[2][F64P_THREADS / 32];
+    __shared__ int stop_s;
+    const int K = q.max_iters, m = q.check_every;
+    for (int k = 0; k <= K; ++k) {
+        const bool odd = k & 1;
+        const double *p1 = odd ? a.p1[1] : a.p1[0], *p2 = odd ? a.p2[1] : a.p2[0];
+        double *q1 = odd ? a.p1[0] : a.p1[1], *q2 = odd ? a.p2[0] : a.p2[1];
+        // v^{k-1} in buffer (k-1)&1 (pass 0: v^0 in buffer 0); v^k goes to buffer k&1
+        const double *vp = (k == 0 || odd) ? q.v[0] : q.v[1];
+        double *vo = odd ? q.v[1] : q.v[0];
+        const bool chk = k >= 1 && (k % m == 0 || k == K);
+        double su = 0.0, sv = 0.0;
+        for (int64_t x = k0 + threadIdx.x; x < k1; x += blockDim.x) {
+            const int i = (int)(x / a.W), j = (int)(x - (int64_t)i * a.W);
+            const int64_t o = (int64_t)i * P + j;
+            if (a.lab[o] != 2) continue;  // pinned: rho = 0 and u = v = u0 for good
+            const double dx = div64(p1, p2, o, P);
+            double ux = 0.0, vx = vp[o];
+            if (k >= 1) vx = v_step(vp[o], dx, a.f[o], theta, tl, &ux);
+            if (k >= 1) {
+                if (chk) {
+                    const double du = __dsub_rn(ux, a.u[o]), dv = __dsub_rn(vx, vp[o]);
+                    su = __fma_rn(du, du, su);
+                    sv = __fma_rn(dv, dv, sv);
+                }
+                a.u[o] = ux;
+                vo[o] = vx;
             }
-            part[2 * blockIdx.x] = tu;
-            part[2 * blockIdx.x + 1] = tv;
+            if (k == K) continue;
+            // rho-step of iteration k+1: w = div rho - v / theta, g = grad w, the fixed point
+            const double w = __dsub_rn(dx, __ddiv_rn(vx, theta));
+            double g1 = 0.0, g2 = 0.0;
+            if (i < a.H - 1) {
+                const int64_t y = o + P;
+                const double dy = div64(p1, p2, y, P);
+                double vy = vp[y], uy;
+                if (k >= 1 && a.lab[y] == 2) vy = v_step(vp[y], dy, a.f[y], theta, tl, &uy);
+                g1 = __dsub_rn(__dsub_rn(dy, __ddiv_rn(vy, theta)), w);
+            }
+            if (j % a.img_w != a.img_w - 1) {
+                const int64_t y = o + 1;
+                const double dy = div64(p1, p2, y, P);
+                double vy = vp[y], uy;
+                if (k >= 1 && a.lab[y] == 2) vy = v_step(vp[y], dy, a.f[y], theta, tl, &uy);
+                g2 = __dsub_rn(__dsub_rn(dy, __ddiv_rn(vy, theta)), w);
+            }
+            const double ng = __dsqrt_rn(__dadd_rn(__dmul_rn(g1, g1), __dmul_rn(g2, g2)));
+            const double den = __dadd_rn(1.0, __dmul_rn(tau, ng));
+            q1[o] = __ddiv_rn(__dadd_rn(p1[o], __dmul_rn(tau, g1)), den);
+            q2[o] = __ddiv_rn(__dadd_rn(p2[o], __dmul_rn(tau, g2)), den);
+        }
+        if (chk) {
+            cta2(su, sv, sh);
+            if (threadIdx.x == 0) {
+                q.part[2 * blockIdx.x] = su;
+                q.part[2 * blockIdx.x + 1] = sv;
+            }
+        }
+        if (k < K || chk) gbar(q.bar, (unsigned)(k + 1));
+        if (chk) {
+            double tu = 0.0, tv = 0.0;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+                tu += __ldcg(q.part + 2 * b);
+                tv += __ldcg(q.part + 2 * b + 1);
+            }
+            cta2(tu, tv, sh);
+            if (threadIdx.x == 0) {
+                const double r = fmax(sqrt(tu / q.norm_div), sqrt(tv / q.norm_div));
+                const bool conv = r <= q.tol, fire = conv || k >= K;
+                stop_s = fire;
+                if (blockIdx.x == 0) {
+                    StopRecord *rec = a.stop;
+                    rec->it = k;
+                    rec->residual = r;
+                    rec->checks += 1;
+                    if (fire) {
+                        rec->iters = k;
+                        rec->converged = conv ? 1 : 0;
+                        rec->flag = 1;
+                    }
+                }
+            }
+            __syncthreads();
+            if (stop_s) break;
         }
     }
+}
+
+cudaError_t launch_f64_persist(const F64Persist &q, int n_sm, cudaStream_t s) {
+    static int per_sm = 0;
+    if (per_sm <= 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k64_persist, F64P_THREADS,
+                                                          0) != cudaSuccess ||
+            per_sm < 1) {
+            (void)cudaGetLastError();
+            per_sm = 1;
+        }
+        if (per_sm > 2) per_sm = 2;
+    }
+    const int64_t n = (int64_t)q.a.H * q.a.W;
+    int g = per_sm * n_sm;
+    const int64_t need = (n + F64P_THREADS - 1) / F64P_THREADS;
+    if (g > need) g = (int)need;
+    if (g > F64P_MAX_GRID) g = F64P_MAX_GRID;
+    cudaError_t e = cudaMemsetAsync(q.bar, 0, sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    void *args[] = {const_cast<F64Persist *>(&q)};
+    return cudaLaunchCooperativeKernel((const void *)k64_persist, dim3(g), dim3(F64P_THREADS),
+                                       args, 0, s);
 }
 
 int f64_grid(int64_t n) {
@@ -139,15 +243,6 @@ int f64_grid(int64_t n) {
 
 cudaError_t launch_f64_init(const F64Args &a, cudaStream_t s) {
     k64_init<<<f64_grid((int64_t)a.H * a.W), 256, 0, s>>>(a);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_f64_iter(const F64Args &a, int b, double *part, cudaStream_t s) {
-    const int g = f64_grid((int64_t)a.H * a.W);
-    k64_rho<<<g, 256, 0, s>>>(a, b);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    k64_uv<<<g, 256, 0, s>>>(a, b ^ 1, part);
     return cudaGetLastError();
 }
 

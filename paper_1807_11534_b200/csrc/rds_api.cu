@@ -76,7 +76,7 @@ struct rds_handle {
     double *d64 = nullptr, *part64 = nullptr, *cmp_out = nullptr;
     uint8_t *lab64 = nullptr;
     StopRecord *stop64 = nullptr;
-    int32_t *n64 = nullptr;
+    unsigned *bar64 = nullptr;       // grid-barrier counter of k64_persist
     bool have_gt = false;
     int cur0 = 0;                    // ping-pong buffer at the start of the last solve
     float *scratch = nullptr;        // H*W natural-order staging for swizzled-plane getters
@@ -151,7 +151,7 @@ static void free_all(rds_t *h) {
                      h->items,   h->queue,       h->counts,  h->n_rd_dev,  h->absmax_bits,
                      h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch,
                      h->stop,    h->chk,         h->d64,     h->part64,    h->cmp_out,
-                     h->lab64,   h->stop64,      h->n64,       h->rows_buf,
+                     h->lab64,   h->stop64,      h->bar64,       h->rows_buf,
                      h->rdc_idx, h->rdc_row,     h->rdc_buf,   h->rdc_bar, h->rdc_part};  // rdc_tot points into rdc_row
     for (void *p : other)
         if (p) cudaFree(p);
@@ -1357,24 +1357,22 @@ int rds_solve_gt(rds_t *h, float lambda, float theta, float tau, float delta,
     if (!h->image_ok || !h->p_ok)
         return fail(h, RDS_EINVAL, "rds_solve_gt: image or P has non-finite values");
     NvtxRange nvtx_gt("rds_solve_gt");
-    const int nb = f64_grid(h->H * h->W);
-    if (!h->d64) {
-        CK(h, cudaMalloc(&h->d64, sizeof(double) * h->plane * 7));
-        CK(h, cudaMemsetAsync(h->d64, 0, sizeof(double) * h->plane * 7, h->stream));
+    if (!h->d64) {  // f, u, v, rho1 x2, rho2 x2, v (second buffer): 8 double planes
+        CK(h, cudaMalloc(&h->d64, sizeof(double) * h->plane * 8));
+        CK(h, cudaMemsetAsync(h->d64, 0, sizeof(double) * h->plane * 8, h->stream));
         CK(h, cudaMalloc(&h->lab64, h->plane));
         CK(h, cudaMemsetAsync(h->lab64, 0, h->plane, h->stream));
-        CK(h, cudaMalloc(&h->part64, sizeof(double) * 3 * F64_BLOCKS));
+        CK(h, cudaMalloc(&h->part64, sizeof(double) * 2 * F64P_MAX_GRID));
         CK(h, cudaMalloc(&h->cmp_out, sizeof(double) * 2));
         CK(h, cudaMalloc(&h->stop64, sizeof(StopRecord)));
-        CK(h, cudaMalloc(&h->n64, sizeof(int32_t)));
+        CK(h, cudaMalloc(&h->bar64, sizeof(unsigned)));
     }
-    CK(h, cudaMemcpyAsync(h->n64, &nb, sizeof nb, cudaMemcpyHostToDevice, h->stream));
     CK(h, cudaMemsetAsync(h->stop64, 0, sizeof(StopRecord), h->stream));
     F64Args a{};
     a.z = h->at(h->z);
     a.P = h->gamma != 0.0f ? h->at(h->P) : nullptr;
-    double *pl[7];
-    for (int k = 0; k < 7; ++k) pl[k] = h->d64 + h->plane * k + h->origin;
+    double *pl[8];
+    for (int k = 0; k < 8; ++k) pl[k] = h->d64 + h->plane * k + h->origin;
     a.f = pl[0];
     a.u = pl[1];
     a.v = pl[2];
@@ -1382,6 +1380,7 @@ int rds_solve_gt(rds_t *h, float lambda, float theta, float tau, float delta,
     a.p1[1] = pl[4];
     a.p2[0] = pl[5];
     a.p2[1] = pl[6];
+    a.v2 = pl[7];
     a.lab = h->lab64 + h->origin;
     a.stop = h->stop64;
     a.pitch = h->pitch;
@@ -1396,93 +1395,18 @@ int rds_solve_gt(rds_t *h, float lambda, float theta, float tau, float delta,
     a.theta = (double)theta;
     a.theta_lambda = (double)theta * (double)lambda;
     CK(h, launch_f64_init(a, h->stream));
-    StopCheck c{};
-    c.part = h->part64;
-    c.n_part = h->n64;
-    c.norm_div = h->opt_norm ? (double)h->H * (double)h->W : 1.0;
-    c.tol = tol;
-    c.max_iters = max_iters;
-    c.rec = h->stop64;
-    // One CUDA graph: a while node over whole bodies of checks (two checks when check_every
-    // is odd, so a body keeps the rho ping-pong parity), driven by the body's last
-    // k_stop_check, then a static tail up to max_iters.
-    const int body_checks = (check_every & 1) ? 2 : 1;
-    const int body_iters = body_checks * check_every;
-    const int loop_end = (max_iters / body_iters) * body_iters;
-    c.body_iters = body_iters;
-    c.loop_end = loop_end;
-    auto enqueue_iters = [&](int it0, int it1, bool drive) -> cudaError_t {
-        int last_check = it0;
-        cudaError_t e = cudaSuccess;
-        for (int it = it0; it < it1 && e == cudaSuccess; ++it) {
-            const bool check = ((it + 1) % check_every) == 0 || it + 1 == max_iters;
-            e = launch_f64_iter(a, it & 1, check ? h->part64 : nullptr, h->stream);
-            if (e == cudaSuccess && check) {
-                c.block_iters = it + 1 - last_check;
-                c.set_cond = drive && it + 1 == it1;
-                last_check = it + 1;
-                e = launch_stop_check(c, h->stream);
-            }
-        }
-        return e;
-    };
-    {
-        cudaStream_t cap = nullptr, keep = h->stream;
-        cudaGraph_t g = nullptr, body = nullptr;
-        cudaGraphExec_t ge = nullptr;
-        cudaError_t e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaGraphCreate(&g, 0);
-        if (e == cudaSuccess)
-            e = cudaGraphConditionalHandleCreate(&c.cond, g, loop_end > 0 ? 1 : 0,
-                                                 cudaGraphCondAssignDefault);
-        h->stream = cap;
-        if (e == cudaSuccess)
-            e = cudaStreamBeginCaptureToGraph(cap, g, nullptr, nullptr, 0,
-                                              cudaStreamCaptureModeThreadLocal);
-        if (e == cudaSuccess) e = cudaMemsetAsync(h->stop64, 0, sizeof(StopRecord), cap);
-        if (e == cudaSuccess) {
-            cudaStreamCaptureStatus st;
-            cudaGraph_t cg = nullptr;
-            const cudaGraphNode_t *deps = nullptr;
-            size_t nd = 0;
-            e = cudaStreamGetCaptureInfo(cap, &st, nullptr, &cg, &deps, &nd);
-            cudaGraphNode_t wnode = nullptr;
-            cudaGraphNodeParams cp = {};
-            cp.type = cudaGraphNodeTypeConditional;
-            cp.conditional.handle = c.cond;
-            cp.conditional.type = cudaGraphCondTypeWhile;
-            cp.conditional.size = 1;
-            if (e == cudaSuccess) e = cudaGraphAddNode(&wnode, cg, deps, nd, &cp);
-            if (e == cudaSuccess) {
-                body = cp.conditional.phGraph_out[0];
-                e = cudaStreamUpdateCaptureDependencies(cap, &wnode, 1,
-                                                        cudaStreamSetCaptureDependencies);
-            }
-        }
-        if (e == cudaSuccess) e = enqueue_iters(loop_end, max_iters, false);
-        {
-            cudaGraph_t got = nullptr;
-            const cudaError_t e2 = cudaStreamEndCapture(cap, &got);
-            if (e == cudaSuccess) e = e2;
-        }
-        if (e == cudaSuccess)
-            e = cudaStreamBeginCaptureToGraph(cap, body, nullptr, nullptr, 0,
-                                              cudaStreamCaptureModeThreadLocal);
-        if (e == cudaSuccess) {
-            const cudaError_t e1 = enqueue_iters(0, body_iters, true);
-            cudaGraph_t got = nullptr;
-            const cudaError_t e2 = cudaStreamEndCapture(cap, &got);
-            e = e1 != cudaSuccess ? e1 : e2;
-        }
-        h->stream = keep;
-        if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, g, 0);
-        if (e == cudaSuccess) e = cudaGraphLaunch(ge, h->stream);
-        if (ge) cudaGraphExecDestroy(ge);
-        if (g) cudaGraphDestroy(g);
-        if (cap) cudaStreamDestroy(cap);
-        if (e != cudaSuccess)
-            return fail(h, RDS_ECUDA, "rds_solve_gt: %s", cudaGetErrorString(e));
-    }
+    F64Persist q{};
+    q.a = a;
+    q.a.stop = h->stop64;
+    q.v[0] = pl[2];
+    q.v[1] = pl[7];
+    q.max_iters = max_iters;
+    q.check_every = check_every;
+    q.tol = tol;
+    q.norm_div = h->opt_norm ? (double)h->H * (double)h->W : 1.0;
+    q.part = h->part64;
+    q.bar = h->bar64;
+    CK(h, launch_f64_persist(q, h->n_sm, h->stream));
     StopRecord rec{};
     CK(h, cudaMemcpyAsync(&rec, h->stop64, sizeof rec, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
