@@ -61,9 +61,12 @@ typedef struct rds_handle rds_t;
  *  E_u   = TV(c(u)) + lambda sum f c(u),     c(u) = min(max(u,0),1)
  *  D_p   = sum min(0, lambda f + div rho)    (Lagrangian dual of Eq. 4 over u in [0,1])
  *  gap   = E_v - D_p  (>= 0 by weak duality whenever |rho| <= 1)
- *  TV_v, fit_v = lambda sum f v : the two parts of E_v. */
+ *  TV_v, fit_v = lambda sum f v : the two parts of E_v.
+ *  F_rd  = sum_{RD} |grad u'| + sum |u' - v|^2 / (2 theta) + lambda sum f v with
+ *          u' = v_prev - theta div rho (the last u on RD, u0 - theta div rho off RD): the
+ *          restricted functional that the iteration decreases (reading R-C12). */
 typedef struct {
-    double E_v, E_u, D_p, gap, TV_v, fit_v;
+    double E_v, E_u, D_p, gap, TV_v, fit_v, F_rd;
 } rds_energy_t;
 
 /* Statistics of the last rds_solve. Times are CUDA-event times on the handle's stream and are

@@ -147,12 +147,14 @@ cudaError_t launch_stop_check(const StopCheck &c, cudaStream_t s);
 
 struct EnergyArgs {
     const float *f, *u, *v, *p1, *p2;
+    const uint8_t *lab;           // labels (F^RD: the sum over RD and u0 off RD)
     int64_t pitch;
     int H, W, img_w;
     int row0, row1;     // rows summed: [row0, row1) (rds_set_energy_rows; default [0, H))
-    double *partials;   // [n_blocks * 5]
-    double *out;        // [5]: TV_v, sum f v, TV_cu, sum f cu, sum min(0, lambda f + div p)
-    float lambda;
+    double *partials;   // [n_blocks * 7]
+    double *out;        // [7]: TV_v, sum f v, TV_cu, sum f cu, sum min(0, lambda f + div p),
+                        //      sum_RD |grad u'|, sum (u' - v)^2
+    float lambda, theta;
 };
 constexpr int ENERGY_BLOCKS = 592;  // 4 x 148 SMs
 cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s);

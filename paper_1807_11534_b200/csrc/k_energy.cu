@@ -11,7 +11,7 @@
 
 namespace rds {
 
-constexpr int NE = 5;
+constexpr int NE = 7;
 
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
@@ -21,9 +21,19 @@ __device__ __forceinline__ double warp_sum(double x) {
 
 __device__ __forceinline__ float clamp01(float x) { return fminf(fmaxf(x, 0.0f), 1.0f); }
 
+// u' = v_prev - theta div rho (reading R-C12) at pixel (i, j): the last u on RD (the kernel
+// wrote exactly that), u0 - theta div rho on pinned pixels (v_prev = u0 there)
+__device__ __forceinline__ float u_prime(const EnergyArgs &a, int64_t row, int j) {
+    const int64_t o = row + j, os = row + swz(j);
+    const uint8_t l = a.lab[o];
+    if (l == 2) return a.u[o];
+    const float dv = a.p1[os] - a.p1[os - a.pitch] + a.p2[os] - a.p2[row + swz(j - 1)];
+    return (l == 1 ? 1.0f : 0.0f) - a.theta * dv;
+}
+
 __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
     const int64_t pitch = a.pitch;
-    double acc[NE] = {0, 0, 0, 0, 0};
+    double acc[NE] = {0, 0, 0, 0, 0, 0, 0};
     // fixed pixel -> thread map: CTA b takes rows row0 + b, row0 + b + G, ...; thread t columns t, t + 256, ...
     for (int i = a.row0 + blockIdx.x; i < a.row1; i += gridDim.x) {
         const int64_t row = (int64_t)i * pitch;
@@ -49,6 +59,14 @@ __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
             acc[2] += (double)sqrtf(gu1 * gu1 + gu2 * gu2);
             acc[3] += (double)f * (double)cu;
             acc[4] += (double)fminf(t, 0.0f);
+            // F^RD(u', v) = sum_RD |grad u'| + |u' - v|^2 / (2 theta) + lambda <f, v>
+            const float up = u_prime(a, row, j);
+            if (a.lab[o] == 2) {
+                const float g1 = down ? u_prime(a, row + pitch, j) - up : 0.0f;
+                const float g2 = right ? u_prime(a, row, j + 1) - up : 0.0f;
+                acc[5] += (double)sqrtf(g1 * g1 + g2 * g2);
+            }
+            acc[6] += (double)((up - v) * (up - v));
             jm += 256;
             while (jm >= a.img_w) jm -= a.img_w;
         }
@@ -70,7 +88,7 @@ __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
 __global__ void __launch_bounds__(256) k_energy_final(const double *partials, int nb,
                                                       double *out) {
     __shared__ double sh[8][NE];
-    double acc[NE] = {0, 0, 0, 0, 0};
+    double acc[NE] = {0, 0, 0, 0, 0, 0, 0};
     for (int b = threadIdx.x; b < nb; b += 256)
 #pragma unroll
         for (int q = 0; q < NE; ++q) acc[q] += partials[b * NE + q];

@@ -234,8 +234,8 @@ int rds_create(int64_t H, int64_t W, rds_t **out) {
     A(cudaMalloc(&h->n_rd_dev, sizeof(long long)));
     A(cudaMalloc(&h->absmax_bits, sizeof(unsigned)));
     A(cudaMalloc(&h->flag, sizeof(int)));
-    A(cudaMalloc(&h->e_partials, sizeof(double) * ENERGY_BLOCKS * 5));
-    A(cudaMalloc(&h->e_out, sizeof(double) * 5));
+    A(cudaMalloc(&h->e_partials, sizeof(double) * ENERGY_BLOCKS * 7));
+    A(cudaMalloc(&h->e_out, sizeof(double) * 7));
     for (auto &ev : h->ev) A(cudaEventCreate(&ev));
     A(cudaStreamSynchronize(h->stream));
 #undef A
@@ -1304,9 +1304,11 @@ int rds_energy(rds_t *h, rds_energy_t *out) {
     a.row1 = (int)(h->e_row1 < 0 ? h->H : h->e_row1);
     a.partials = h->e_partials;
     a.out = h->e_out;
+    a.lab = h->at(h->lab);
     a.lambda = h->lambda;
+    a.theta = h->theta;
     CK(h, launch_energy(a, h->stream));
-    double s[5];
+    double s[7];
     CK(h, cudaMemcpyAsync(s, h->e_out, sizeof s, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     const double lam = (double)h->lambda;
@@ -1316,6 +1318,7 @@ int rds_energy(rds_t *h, rds_energy_t *out) {
     out->E_u = s[2] + lam * s[3];
     out->D_p = s[4];
     out->gap = out->E_v - out->D_p;
+    out->F_rd = s[5] + s[6] / (2.0 * (double)h->theta) + lam * s[1];
     return RDS_OK;
 }
 

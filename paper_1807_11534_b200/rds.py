@@ -50,7 +50,8 @@ class RdsError(RuntimeError):
 
 
 class rds_energy_t(ctypes.Structure):
-    _fields_ = [(k, ctypes.c_double) for k in ("E_v", "E_u", "D_p", "gap", "TV_v", "fit_v")]
+    _fields_ = [(k, ctypes.c_double) for k in ("E_v", "E_u", "D_p", "gap", "TV_v", "fit_v",
+                                                "F_rd")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

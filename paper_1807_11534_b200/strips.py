@@ -218,11 +218,13 @@ class StripSolver:
         D(rho), all-reduced (the gap and E(v) recomputed from the sums)."""
         self.engine.set_energy_rows(self.me.owned.start, self.me.owned.stop)
         e = self.engine.energy()
-        t = self.torch.tensor([e["TV_v"], e["fit_v"], e["E_u"], e["D_p"]],
-                              dtype=self.torch.float64, device=self.device)
+        keys = ("TV_v", "fit_v", "E_u", "D_p", "F_rd")
+        t = self.torch.tensor([e.get(k, 0.0) for k in keys], dtype=self.torch.float64,
+                              device=self.device)
         self.dist.all_reduce(t, group=self.group)
-        tv, fit, eu, dp = t.tolist()
-        return dict(E_v=tv + fit, E_u=eu, D_p=dp, gap=tv + fit - dp, TV_v=tv, fit_v=fit)
+        tv, fit, eu, dp, frd = t.tolist()
+        return dict(E_v=tv + fit, E_u=eu, D_p=dp, gap=tv + fit - dp, TV_v=tv, fit_v=fit,
+                    F_rd=frd)
 
     def gather_u(self, dst=0):
         """The whole u on rank `dst` (None elsewhere); strips padded to the tallest."""

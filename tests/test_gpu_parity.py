@@ -610,3 +610,22 @@ def test_frame_untouched(rds, shape, kf):
     s.energy()
     assert s.check_frame() == 0
     s.close()
+
+
+
+@pytest.mark.parametrize("delta_rel,K", [(0.3, 1), (0.3, 60), (math.inf, 40), (0.15, 25)])
+def test_energy_f_rd(rds, orc, delta_rel, K):
+    """F_rd of rds_energy is the oracle's F^RD(u', v) (reading R-C12; u' = v^(K-1) - theta
+    div rho^K on the full grid) at the last iteration, to float32 accuracy."""
+    z = wl.random_image(57, 83, 21)
+    f = orc.fitting(z, 0.75, 0.25)
+    delta = wl.band_delta(delta_rel, orc.absmax(f))
+    s = rds.Solver(57, 83)
+    s.set_image(z)
+    s.set_fitting(0.75, 0.25)
+    s.solve(4.0, 0.1, 0.125, delta, K)
+    e = s.energy()
+    o = orc.solve(f, delta, 4.0, np.float32(0.1), 0.125, K, trace=True)
+    F = o["trace"][K - 1][3]
+    assert abs(e["F_rd"] - F) <= 1e-4 * max(1.0, abs(F)), (e["F_rd"], F)
+    s.close()

@@ -130,7 +130,7 @@ def test_strips_bitwise_whole_image(rds, H, W, G, s, K, delta_rel, kf, compact):
         e.set_fitting(0.8, 0.2)
         engines.append(e)
     strips.solve_local(engines, plan, *PAR, delta, K, s)
-    tot = dict.fromkeys(("TV_v", "fit_v", "E_u", "D_p"), 0.0)
+    tot = dict.fromkeys(("TV_v", "fit_v", "E_u", "D_p", "F_rd"), 0.0)
     for st, e in zip(plan, engines):
         got = _state(e)
         stop = st.owned.stop + (1 if st.bot else 0)   # the row below the owned ones too
