@@ -226,7 +226,7 @@ constexpr int F64_BLOCKS = 592;  // fixed grid of the double-precision kernels (
 int f64_grid(int64_t n);
 cudaError_t launch_f64_init(const F64Args &a, cudaStream_t s);
 // the whole fp64 tolerance solve as one cooperative launch (k64_persist)
-constexpr int F64P_THREADS = 256, F64P_MAX_GRID = 2 * 148 * 4;
+constexpr int F64P_THREADS = 256, F64P_MAX_GRID = 4 * 148 * 4;
 struct F64Persist {
     F64Args a;                 // a.v = v buffer 0 (v^0 after init), a.stop = the outcome
     double *v[2];

@@ -119,6 +119,42 @@ __device__ __forceinline__ double v_step(double vp, double d, double f, double t
 
 }  // namespace
 
+// stop decision after a check (all CTAs, same total in the same order); returns fire
+__device__ __forceinline__ bool f64_check(const F64Persist &q, double su, double sv, int k,
+                                          unsigned &nbar, double (*sh)[F64P_THREADS / 32],
+                                          int *stop_s) {
+    cta2(su, sv, sh);
+    if (threadIdx.x == 0) {
+        q.part[2 * blockIdx.x] = su;
+        q.part[2 * blockIdx.x + 1] = sv;
+    }
+    gbar(q.bar, ++nbar);
+    double tu = 0.0, tv = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
+        tu += __ldcg(q.part + 2 * b);
+        tv += __ldcg(q.part + 2 * b + 1);
+    }
+    cta2(tu, tv, sh);
+    if (threadIdx.x == 0) {
+        const double r = fmax(sqrt(tu / q.norm_div), sqrt(tv / q.norm_div));
+        const bool conv = r <= q.tol, fire = conv || k >= q.max_iters;
+        *stop_s = fire;
+        if (blockIdx.x == 0) {
+            StopRecord *rec = q.a.stop;
+            rec->it = k;
+            rec->residual = r;
+            rec->checks += 1;
+            if (fire) {
+                rec->iters = k;
+                rec->converged = conv ? 1 : 0;
+                rec->flag = 1;
+            }
+        }
+    }
+    __syncthreads();
+    return *stop_s != 0;
+}
+
 __global__ void __launch_bounds__(F64P_THREADS) k64_persist(const F64Persist q) {
     const F64Args &a = q.a;
     const int64_t n = (int64_t)a.H * a.W, P = a.pitch;
@@ -128,6 +164,7 @@ __global__ void __launch_bounds__(F64P_THREADS) k64_persist(const F64Persist q) 
     __shared__ double sh[2][F64P_THREADS / 32];
     __shared__ int stop_s;
     const int K = q.max_iters, m = q.check_every;
+    unsigned nbar = 0;
     for (int k = 0; k <= K; ++k) {
         const bool odd = k & 1;
         const double *p1 = odd ? a.p1[1] : a.p1[0], *p2 = odd ? a.p2[1] : a.p2[0];
@@ -177,43 +214,18 @@ __global__ void __launch_bounds__(F64P_THREADS) k64_persist(const F64Persist q) 
             q2[o] = __ddiv_rn(__dadd_rn(p2[o], __dmul_rn(tau, g2)), den);
         }
         if (chk) {
-            cta2(su, sv, sh);
-            if (threadIdx.x == 0) {
-                q.part[2 * blockIdx.x] = su;
-                q.part[2 * blockIdx.x + 1] = sv;
-            }
-        }
-        if (k < K || chk) gbar(q.bar, (unsigned)(k + 1));
-        if (chk) {
-            double tu = 0.0, tv = 0.0;
-            for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-                tu += __ldcg(q.part + 2 * b);
-                tv += __ldcg(q.part + 2 * b + 1);
-            }
-            cta2(tu, tv, sh);
-            if (threadIdx.x == 0) {
-                const double r = fmax(sqrt(tu / q.norm_div), sqrt(tv / q.norm_div));
-                const bool conv = r <= q.tol, fire = conv || k >= K;
-                stop_s = fire;
-                if (blockIdx.x == 0) {
-                    StopRecord *rec = a.stop;
-                    rec->it = k;
-                    rec->residual = r;
-                    rec->checks += 1;
-                    if (fire) {
-                        rec->iters = k;
-                        rec->converged = conv ? 1 : 0;
-                        rec->flag = 1;
-                    }
-                }
-            }
-            __syncthreads();
-            if (stop_s) break;
+            if (f64_check(q, su, sv, k, nbar, sh, &stop_s)) break;
+        } else if (k < K) {
+            gbar(q.bar, ++nbar);
         }
     }
 }
 
 cudaError_t launch_f64_persist(const F64Persist &q, int n_sm, cudaStream_t s) {
+    // up to 4 CTAs per SM (the occupancy limit at 64 registers): latency hiding for the
+    // dependent fp64 division chains outweighs the extra barrier arrivals (measured: C1 u^GT
+    // 27.8 us per iteration at 4 vs 42.8 at 2; a two-phase variant without the neighbour
+    // recomputation was slower at both C0 and C1)
     static int per_sm = 0;
     if (per_sm <= 0) {
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k64_persist, F64P_THREADS,
@@ -222,7 +234,7 @@ cudaError_t launch_f64_persist(const F64Persist &q, int n_sm, cudaStream_t s) {
             (void)cudaGetLastError();
             per_sm = 1;
         }
-        if (per_sm > 2) per_sm = 2;
+        if (per_sm > 4) per_sm = 4;
     }
     const int64_t n = (int64_t)q.a.H * q.a.W;
     int g = per_sm * n_sm;
@@ -240,7 +252,6 @@ int f64_grid(int64_t n) {
     const int64_t g = (n + 255) / 256;
     return (int)(g < F64_BLOCKS ? g : F64_BLOCKS);
 }
-
 cudaError_t launch_f64_init(const F64Args &a, cudaStream_t s) {
     k64_init<<<f64_grid((int64_t)a.H * a.W), 256, 0, s>>>(a);
     return cudaGetLastError();
