@@ -26,9 +26,8 @@ __device__ __forceinline__ float clamp01(float x) { return fminf(fmaxf(x, 0.0f),
 __device__ __forceinline__ float u_prime(const EnergyArgs &a, int64_t row, int j) {
     const int64_t o = row + j, os = row + swz(j);
     const uint8_t l = a.lab[o];
-    if (l == 2) return a.u[o];
     const float dv = a.p1[os] - a.p1[os - a.pitch] + a.p2[os] - a.p2[row + swz(j - 1)];
-    return (l == 1 ? 1.0f : 0.0f) - a.theta * dv;
+    return l == 2 ? a.u[o] : (l == 1 ? 1.0f : 0.0f) - a.theta * dv;
 }
 
 __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
@@ -60,12 +59,15 @@ __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
             acc[3] += (double)f * (double)cu;
             acc[4] += (double)fminf(t, 0.0f);
             // F^RD(u', v) = sum_RD |grad u'| + |u' - v|^2 / (2 theta) + lambda <f, v>
-            const float up = u_prime(a, row, j);
-            if (a.lab[o] == 2) {
-                const float g1 = down ? u_prime(a, row + pitch, j) - up : 0.0f;
-                const float g2 = right ? u_prime(a, row, j + 1) - up : 0.0f;
-                acc[5] += (double)sqrtf(g1 * g1 + g2 * g2);
-            }
+            // (branch-free: the band is scattered noise at small delta, so a branch on the
+            // label diverges in nearly every warp)
+            const uint8_t lx = a.lab[o];  // u' here reuses the div rho of the D term
+            const float up = lx == 2 ? a.u[o] : (lx == 1 ? 1.0f : 0.0f) - a.theta * dv;
+            const float ud = down ? u_prime(a, row + pitch, j) : up;
+            const float ur = right ? u_prime(a, row, j + 1) : up;
+            const float g1 = ud - up, g2 = ur - up;
+            const float tvp = sqrtf(g1 * g1 + g2 * g2);
+            acc[5] += (double)(lx == 2 ? tvp : 0.0f);
             acc[6] += (double)((up - v) * (up - v));
             jm += 256;
             while (jm >= a.img_w) jm -= a.img_w;

@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 timeout 1500 python -m pytest tests -m gpu -q --durations=5 > gpurun_out/r01k_pytest.log 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r01k_smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/r01k_bench.json 2> gpurun_out/r01k_bench.err
-BCMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e"
+BCMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e --no-compact"
 $BCMD > gpurun_out/r01k_bench_short.json 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r01k_launches.csv $BCMD > gpurun_out/r01k_ncu_launch.log 2>&1
 SCMD="python scripts/sweep.py --kf 7 --rows 0 --iters 70 --reps 1"
