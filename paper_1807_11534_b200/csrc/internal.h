@@ -174,6 +174,7 @@ __host__ __device__ inline unsigned rdc_cls(int code) {
 }
 constexpr int RDC_BAR_BYTES = 128;  // grid barrier counter (one 128-byte line)
 constexpr int RDC_THREADS = 512;
+constexpr int RDC_CLUSTER_MAX = 16;  // CTAs of the one-cluster form (non-portable size)
 constexpr int RDC_MAX_GRID = 4 * 148 * 4;  // bound on k_rdc_iter CTAs (the stopping-sum buffer)
 struct RdcSetup {
     int n, H, W, img_w;

@@ -308,7 +308,15 @@ __device__ __forceinline__ void cta_sum2(double &a, double &b, double (*sh)[RDC_
 // nearby records: L1 reuse).  NPT > 0: every thread owns the fixed pixels
 // start + t + q * blockDim (q < NPT) and keeps their codes in registers for the whole solve;
 // NPT = 0: any n, codes reloaded every pass.
-template <int NPT>
+// Cluster form for small bands (CL): the whole grid is ONE thread-block cluster (<= 16 CTAs,
+// one per SM), so the per-iteration barrier is the hardware cluster barrier (release /
+// acquire at cluster scope) instead of the global-memory grid barrier.
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int NPT, bool CL = false>
 __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
     const int chunk = (a.n + gridDim.x - 1) / gridDim.x;
     const int start = blockIdx.x * chunk;
@@ -352,7 +360,12 @@ __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
                 a.part[2 * blockIdx.x + 1] = dv;
             }
         }
-        if (k < a.K || m > 0) grid_barrier(a.bar, (unsigned)(k + 1));
+        if (k < a.K || m > 0) {
+            if (CL)
+                cluster_barrier();
+            else
+                grid_barrier(a.bar, (unsigned)(k + 1));
+        }
         if (chk) {  // every CTA forms the same total in the same order: one common decision
             double tu = 0.0, tv = 0.0;
             for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
@@ -433,8 +446,36 @@ cudaError_t launch_rdc_scatter(const RdcSetup &a, const RdcIter &it, cudaStream_
     return cudaGetLastError();
 }
 
+// one cluster of g CTAs (g <= RDC_CLUSTER_MAX), NPT pixels per thread
+static cudaError_t launch_cluster(const RdcIter &a, RdcFn fn, int g, cudaStream_t s) {
+    if (g > 8) {
+        cudaError_t e = cudaFuncSetAttribute((const void *)fn,
+                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(g);
+    cfg.blockDim = dim3(RDC_THREADS);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = g;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void *args[] = {const_cast<RdcIter *>(&a)};
+    return cudaLaunchKernelExC(&cfg, (const void *)fn, args);
+}
+
 cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s) {
     if (a.n <= 0) return cudaSuccess;
+    static const bool use_cluster = !getenv("RDS_RDC_CLUSTER") || atoi(getenv("RDS_RDC_CLUSTER"));
+    if (use_cluster && a.n <= RDC_CLUSTER_MAX * RDC_THREADS * 2) {
+        const int npt = a.n <= RDC_CLUSTER_MAX * RDC_THREADS ? 1 : 2;
+        const int g = (a.n + RDC_THREADS * npt - 1) / (RDC_THREADS * npt);
+        return launch_cluster(a, npt == 1 ? k_rdc_iter<1, true> : k_rdc_iter<2, true>, g, s);
+    }
     // the smallest register-resident variant that covers n, else the general one
     RdcFn fn = nullptr;
     int g = 0;
