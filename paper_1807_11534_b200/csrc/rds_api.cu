@@ -756,8 +756,7 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactP
     const int64_t npx = h->H * h->W;
     if (npx > INT32_MAX / 2) return RDS_OK;  // compact indices are int32: keep the dense path
     if (iters > 4000000) return RDS_OK;      // the grid-barrier counter is 32-bit
-    if (!h->rdc_idx) {
-        CK(h, cudaMalloc(&h->rdc_idx, sizeof(int32_t) * npx));
+    if (!h->rdc_row) {  // small buffers; the H x W index map only once the path is taken
         CK(h, cudaMalloc(&h->rdc_row, sizeof(int32_t) * (2 * h->H + 1)));
         CK(h, cudaMalloc(&h->rdc_bar, RDC_BAR_BYTES));
         CK(h, cudaMalloc(&h->rdc_part, sizeof(double) * 2 * RDC_MAX_GRID));
@@ -776,6 +775,7 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactP
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
         if (!compact_pays(n, (int64_t)act * TILE_H * TILE_W, (size_t)l2)) return RDS_OK;
     }
+    if (!h->rdc_idx) CK(h, cudaMalloc(&h->rdc_idx, sizeof(int32_t) * npx));
     // records x2 (float4), packed codes (uint2), list, u
     const size_t nn = (size_t)(n > 0 ? n : 1);
     void *pb = h->rdc_buf;
