@@ -196,37 +196,72 @@ class Clocks:
 # CPU oracle baseline / reference arm
 # ------------------------------------------------------------------------------------------
 
-def oracle_rate(cfg, z, P, deltas_rel, seconds, iters_hint=None):
-    """Time the oracle (as it stands) on the full image with a bounded iteration count.
-    Returns (px-iter/s counted like the GPU metric, cores, sample description)."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_rate(cfg, z, P, deltas_rel, seconds, iters_hint=None, threads=0):
+    """Time the oracle (as it stands) on the full image with a bounded iteration count,
+    following BASELINE.md §3: the timed region is the oracle's K-loop alone
+    (oracle.last_loop_seconds(): no labels, initialisation, allocation or copies); labels and
+    active tiles for the work count are formed outside it.  Returns (px-iter/s counted like
+    the GPU metric, threads used, sample description, loop seconds)."""
     import oracle
 
+    oracle.set_threads(threads or (os.cpu_count() or 1))
     f = oracle.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
     am = oracle.absmax(f)
     lam = cfg.lambdas[0]
-    # calibrate: 1 iteration at delta=inf
-    t0 = time.perf_counter()
-    oracle.solve(f, np.inf, lam, np.float32(cfg.theta), cfg.tau, 1)
-    t1 = time.perf_counter() - t0
-    per_delta = max(1, int(seconds / max(t1, 1e-6) / len(deltas_rel)))
     if iters_hint:
         per_delta = iters_hint
-    work = 0
-    t0 = time.perf_counter()
+    else:  # calibrate on 2 loop iterations at delta = inf
+        oracle.solve(f, np.inf, lam, np.float32(cfg.theta), cfg.tau, 2)
+        t_it = max(oracle.last_loop_seconds() / 2, 1e-6)
+        per_delta = max(2, int(seconds / t_it / len(deltas_rel)))
+    work, dt = 0, 0.0
     for dr in deltas_rel:
         delta = wl.band_delta(dr, am)
-        lab = oracle.labels(f, delta)
-        n_act = len(oracle.tiles(lab, 32, 32)) * 32 * 32
+        n_act = len(oracle.tiles(oracle.labels(f, delta), 32, 32)) * 32 * 32
         oracle.solve(f, delta, lam, np.float32(cfg.theta), cfg.tau, per_delta)
+        dt += oracle.last_loop_seconds()
         work += min(n_act, cfg.H * cfg.W) * per_delta
-    dt = time.perf_counter() - t0
-    sample = (f"oracle fp64 on the full {cfg.H}x{cfg.W} {cfg.name} image, {per_delta} "
-              f"iterations per delta for delta_rel in {list(deltas_rel)} (of K={cfg.iters})")
-    return work / dt, oracle.get_threads(), sample, dt
+    used = oracle.get_threads()
+    sample = (f"oracle fp64 K-loop only (setup excluded) on the full {cfg.H}x{cfg.W} "
+              f"{cfg.name} image, {per_delta} iterations per delta for delta_rel in "
+              f"{_js(list(deltas_rel))} (of K={cfg.iters}), {used} OpenMP threads")
+    return work / dt, used, sample, dt
+
+
+def cpu_baseline(cfg, z, P, seconds):
+    """cpu_baseline object: all host cores; plus one thread for configs up to 2048^2
+    (BASELINE.md §3)."""
+    r, cores, sample, dt = oracle_rate(cfg, z, P, cfg.delta_rels, seconds)
+    out = {"value": r / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+           "loop_s": dt, "cpu_model": cpu_model(), "nproc": os.cpu_count()}
+    if cfg.H * cfg.W <= 2048 * 2048:
+        r1, _, s1, dt1 = oracle_rate(cfg, z, P, cfg.delta_rels, seconds / 2, threads=1)
+        out["single_thread"] = {"value": r1 / 1e9, "unit": UNIT, "cores": 1, "sample": s1,
+                                "loop_s": dt1}
+    import oracle
+
+    oracle.set_threads(os.cpu_count() or 1)
+    return out
+
+
+REF_ITERS_PER_DELTA = 20
 
 
 def run_reference(args, dist):
-    """--impl reference: the CPU oracle as the reference arm (rank 0 only)."""
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only).  Each step runs
+    REF_ITERS_PER_DELTA iterations per delta on the full image; the step time is the sum of
+    the oracle's K-loop times (setup excluded)."""
     if dist.rank != 0:
         return
     cfg = wl.CONFIGS[args.config]
@@ -234,12 +269,12 @@ def run_reference(args, dist):
     import oracle
 
     oracle.build()
-    # each step: a bounded sample (2 iterations per delta on the full image)
     for _ in range(args.warmup):
-        oracle_rate(cfg, z, P, cfg.delta_rels, 0, iters_hint=1)
+        oracle_rate(cfg, z, P, cfg.delta_rels, 0, iters_hint=2)
     times, works = [], []
     for _ in range(args.steps):
-        r, cores, sample, dt = oracle_rate(cfg, z, P, cfg.delta_rels, 0, iters_hint=2)
+        r, cores, sample, dt = oracle_rate(cfg, z, P, cfg.delta_rels, 0,
+                                           iters_hint=REF_ITERS_PER_DELTA)
         times.append(dt)
         works.append(r * dt)
     value = sum(works) / sum(times) / 1e9
@@ -249,9 +284,9 @@ def run_reference(args, dist):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.desc}", "delta_rels": _js(cfg.delta_rels),
-                   "iters_per_step_per_delta": 2, "iters_of_config": cfg.iters},
+                   "iters_per_step_per_delta": REF_ITERS_PER_DELTA, "iters_of_config": cfg.iters},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model(), "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -427,9 +462,7 @@ def run_ours(args, dist):
     if not args.no_compact:
         line["restricted_compact"] = compact_section(cfg, zt, Pt, am, K, lam, sp, per_delta)
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        r, cores, sample, _ = oracle_rate(cfg, z, P, cfg.delta_rels, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": r / 1e9, "unit": UNIT, "cores": cores,
-                                "kind": "oracle", "sample": sample}
+        line["cpu_baseline"] = cpu_baseline(cfg, z, P, args.cpu_seconds)
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
 

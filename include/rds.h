@@ -119,8 +119,8 @@ typedef struct {
                                 pixel as the dense path (results agree value for value); the
                                 solve synchronises once to size the compact arrays; tolerance
                                 solves (rds_solve_tol) evaluate the stopping rule inside the
-                                same persistent kernel; images of more than 2^30 pixels, bands
-                                of 2^26 or more pixels and K > 4e6 stay dense. */
+                                same persistent kernel; images of more than 2^30 pixels and bands
+                                of 2^26 or more pixels stay dense. */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */

@@ -33,13 +33,26 @@ GCC_FLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC", 
              "-Wall"]
 
 
+def _src_hash() -> str:
+    import hashlib
+
+    with open(_SRC, "rb") as fh:
+        return hashlib.sha256(fh.read() + " ".join(GCC_FLAGS).encode()).hexdigest()
+
+
 def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (no contraction, no fast-math)."""
-    if force or not os.path.exists(_LIB_PATH) or \
-            os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+    """Compile liboracle.so with gcc (no contraction, no fast-math); rebuilt whenever the
+    content hash of oracle.c and the flags differs from the one recorded beside it."""
+    stamp = _LIB_PATH + ".srchash"
+    h = _src_hash()
+    stale = not os.path.exists(_LIB_PATH) or not os.path.exists(stamp) or \
+        open(stamp).read().strip() != h
+    if force or stale:
         tmp = _LIB_PATH + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", *GCC_FLAGS, _SRC, "-o", tmp, "-lm"])
         os.replace(tmp, _LIB_PATH)
+        with open(stamp, "w") as fh:
+            fh.write(h)
     return _LIB_PATH
 
 
@@ -86,6 +99,7 @@ def _load():
         lib.orc_band_for_fraction.argtypes = [P, i64, d]
         lib.orc_band_for_fraction.restype = f
         lib.orc_ntrace.restype = i
+        lib.orc_last_loop_seconds.restype = d
         assert lib.orc_ntrace() == NTRACE
         _lib = lib
         return lib
@@ -109,6 +123,11 @@ def set_threads(n: int) -> None:
 
 def get_threads() -> int:
     return int(_load().orc_get_threads())
+
+
+def last_loop_seconds() -> float:
+    """Wall time of the last solve's K-loop alone (no labels, initialisation or copies)."""
+    return float(_load().orc_last_loop_seconds())
 
 
 # ---------------------------------------------------------------------------------------------

@@ -1,13 +1,14 @@
 """Build librds.so (the C-ABI CUDA library) in-tree with nvcc for sm_100a.
 
 Each .cu under csrc/ is compiled to an object in parallel, then linked into
-paper_1807_11534_b200/librds.so (static cudart).  Rebuilds only when a source or header is
-newer than the library.
+paper_1807_11534_b200/librds.so (static cudart).  Rebuilds only when the content hash of the
+sources, headers and flags differs from the one recorded beside the library.
 """
 from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import subprocess
 
@@ -17,6 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "librds.so")
+STAMP = LIB + ".srchash"  # content hash of the sources the library was built from
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -33,11 +35,24 @@ def _deps():
         glob.glob(os.path.join(INCLUDE, "*.h")) + [os.path.abspath(__file__)]
 
 
+def source_hash() -> str:
+    """Hash of every source, header, this script and the extra compile flags: the library is
+    rebuilt whenever they differ from what it was built from (content, not mtimes, so a
+    copied tree with a stale library is caught)."""
+    h = hashlib.sha256()
+    for p in sorted(_deps()):
+        h.update(os.path.relpath(p, ROOT).encode())
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    h.update(os.environ.get("RDS_NVCC_DEFS", "").encode())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in _deps())
+    with open(STAMP) as fh:
+        return fh.read().strip() != source_hash()
 
 
 def _compile(src: str) -> tuple[str, str]:
@@ -71,6 +86,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(source_hash())
     return LIB
 
 

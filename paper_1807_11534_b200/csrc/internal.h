@@ -193,12 +193,13 @@ struct RdcIter {
     float4 *rec[2];               // pass k reads rec[k & 1], writes rec[(k + 1) & 1]
     float *u;
     float tau, theta, inv_theta;
-    unsigned *bar;                // RDC_BAR_BYTES, zeroed per launch
+    unsigned long long *bar;      // RDC_BAR_BYTES, zeroed per launch (64-bit: never wraps)
     // tolerance solves (check_every > 0): per-CTA partial sums, the outcome (StopRecord
     // fields iters, converged, residual, checks, flag; launches = 0)
     int check_every;
     double tol, norm_div;
-    double *part;                 // [2 * grid]
+    double *part;                 // [2][2 * RDC_MAX_GRID]: alternate by check parity (a fast
+                                  // CTA's next check must not overwrite sums still being read)
     StopRecord *rec_out;
 };
 cudaError_t launch_rdc_count(const uint8_t *lab, int64_t pitch, int H, int W, int32_t *rowcnt,
@@ -233,8 +234,8 @@ struct F64Persist {
     double *v[2];
     int max_iters, check_every;
     double tol, norm_div;
-    double *part;              // [2 * grid]
-    unsigned *bar;
+    double *part;              // [2][2 * F64P_MAX_GRID], alternating by check parity
+    unsigned long long *bar;   // 64-bit barrier counter (no wrap at any max_iters)
 };
 cudaError_t launch_f64_persist(const F64Persist &q, int n_sm, cudaStream_t s);
 // E1, E2 of the float u against a double u (out[0], out[1]); part holds 3 doubles per CTA

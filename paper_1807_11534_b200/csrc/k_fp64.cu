@@ -70,14 +70,14 @@ __global__ void k64_init(const F64Args a) {
 
 namespace {
 
-__device__ __forceinline__ void gbar(unsigned *bar, unsigned k) {
+__device__ __forceinline__ void gbar(unsigned long long *bar, unsigned long long k) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-        const unsigned target = k * gridDim.x;
-        unsigned v;
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+        const unsigned long long target = k * gridDim.x;
+        unsigned long long v;
         do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
         } while (v < target);
     }
     __syncthreads();
@@ -121,18 +121,21 @@ __device__ __forceinline__ double v_step(double vp, double d, double f, double t
 
 // stop decision after a check (all CTAs, same total in the same order); returns fire
 __device__ __forceinline__ bool f64_check(const F64Persist &q, double su, double sv, int k,
-                                          unsigned &nbar, double (*sh)[F64P_THREADS / 32],
-                                          int *stop_s) {
+                                          unsigned long long &nbar, int &nchk,
+                                          double (*sh)[F64P_THREADS / 32], int *stop_s) {
+    // two buffers alternating by check parity: with checks one iteration apart no barrier
+    // separates a fast CTA's write for check c+1 from a slow CTA's read for check c
+    double *part = q.part + (nchk++ & 1) * 2 * F64P_MAX_GRID;
     cta2(su, sv, sh);
     if (threadIdx.x == 0) {
-        q.part[2 * blockIdx.x] = su;
-        q.part[2 * blockIdx.x + 1] = sv;
+        part[2 * blockIdx.x] = su;
+        part[2 * blockIdx.x + 1] = sv;
     }
     gbar(q.bar, ++nbar);
     double tu = 0.0, tv = 0.0;
     for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-        tu += __ldcg(q.part + 2 * b);
-        tv += __ldcg(q.part + 2 * b + 1);
+        tu += __ldcg(part + 2 * b);
+        tv += __ldcg(part + 2 * b + 1);
     }
     cta2(tu, tv, sh);
     if (threadIdx.x == 0) {
@@ -164,7 +167,8 @@ __global__ void __launch_bounds__(F64P_THREADS) k64_persist(const F64Persist q) 
     __shared__ double sh[2][F64P_THREADS / 32];
     __shared__ int stop_s;
     const int K = q.max_iters, m = q.check_every;
-    unsigned nbar = 0;
+    unsigned long long nbar = 0;
+    int nchk = 0;
     for (int k = 0; k <= K; ++k) {
         const bool odd = k & 1;
         const double *p1 = odd ? a.p1[1] : a.p1[0], *p2 = odd ? a.p2[1] : a.p2[0];
@@ -214,7 +218,7 @@ __global__ void __launch_bounds__(F64P_THREADS) k64_persist(const F64Persist q) 
             q2[o] = __ddiv_rn(__dadd_rn(p2[o], __dmul_rn(tau, g2)), den);
         }
         if (chk) {
-            if (f64_check(q, su, sv, k, nbar, sh, &stop_s)) break;
+            if (f64_check(q, su, sv, k, nbar, nchk, sh, &stop_s)) break;
         } else if (k < K) {
             gbar(q.bar, ++nbar);
         }
@@ -241,7 +245,7 @@ cudaError_t launch_f64_persist(const F64Persist &q, int n_sm, cudaStream_t s) {
     const int64_t need = (n + F64P_THREADS - 1) / F64P_THREADS;
     if (g > need) g = (int)need;
     if (g > F64P_MAX_GRID) g = F64P_MAX_GRID;
-    cudaError_t e = cudaMemsetAsync(q.bar, 0, sizeof(unsigned), s);
+    cudaError_t e = cudaMemsetAsync(q.bar, 0, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
     void *args[] = {const_cast<F64Persist *>(&q)};
     return cudaLaunchCooperativeKernel((const void *)k64_persist, dim3(g), dim3(F64P_THREADS),

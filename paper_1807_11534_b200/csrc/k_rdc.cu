@@ -189,14 +189,14 @@ __device__ __forceinline__ float4 rec_at(const float4 *B, int code) {
 // then an acquire spin until all gridDim.x CTAs have arrived k times.  (A two-level version
 // with group counters measured slower: its serial fence/atomic chain outweighs the
 // contention of ~300 arrivals on one address.)
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned k) {
+__device__ __forceinline__ void grid_barrier(unsigned long long *bar, unsigned long long k) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-        const unsigned target = k * gridDim.x;
-        unsigned v;
+        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(bar) : "memory");
+        const unsigned long long target = k * gridDim.x;
+        unsigned long long v;
         do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(bar) : "memory");
         } while (v < target);
     }
     __syncthreads();
@@ -331,6 +331,7 @@ __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
     __shared__ double sh[2][RDC_THREADS / 32];
     __shared__ int stop_s;
     const int m = a.check_every;  // tolerance solves: check after iterations m, 2m, ..., K
+    int nchk = 0;                 // checks so far: selects the partial-sum buffer
     for (int k = 0; k <= a.K; ++k) {
         const bool odd = k & 1;  // selects: a runtime index into a.rec would cost a stack copy
         const float4 *B = odd ? a.rec[1] : a.rec[0];
@@ -352,25 +353,29 @@ __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
                 pix_pass(decode(__ldg(a.code + r), r), B, O, a.u, k, a.K, tau, theta,
                          inv_theta, chk, wr_u, su, sv);
         }
+        // two buffers alternating by check parity: when checks are one pass apart no barrier
+        // separates a fast CTA's write for check c+1 from a slow CTA's read for check c
+        double *part = a.part + (nchk & 1) * 2 * RDC_MAX_GRID;
         if (chk) {  // this CTA's partial sums, published by the barrier below
             double du = su, dv = sv;
             cta_sum2(du, dv, sh);
             if (threadIdx.x == 0) {
-                a.part[2 * blockIdx.x] = du;
-                a.part[2 * blockIdx.x + 1] = dv;
+                part[2 * blockIdx.x] = du;
+                part[2 * blockIdx.x + 1] = dv;
             }
+            ++nchk;
         }
         if (k < a.K || m > 0) {
             if (CL)
                 cluster_barrier();
             else
-                grid_barrier(a.bar, (unsigned)(k + 1));
+                grid_barrier(a.bar, (unsigned long long)(k + 1));
         }
         if (chk) {  // every CTA forms the same total in the same order: one common decision
             double tu = 0.0, tv = 0.0;
             for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
-                tu += __ldcg(a.part + 2 * b);
-                tv += __ldcg(a.part + 2 * b + 1);
+                tu += __ldcg(part + 2 * b);
+                tv += __ldcg(part + 2 * b + 1);
             }
             cta_sum2(tu, tv, sh);
             if (threadIdx.x == 0) {
@@ -446,13 +451,40 @@ cudaError_t launch_rdc_scatter(const RdcSetup &a, const RdcIter &it, cudaStream_
     return cudaGetLastError();
 }
 
+// Can one cluster of g CTAs of fn be scheduled on this device (a g > 8 cluster needs the
+// non-portable size; MIG / MPS slices or small GPCs may not hold it)?  Cached per (fn, g).
+static bool cluster_fits(RdcFn fn, int npt_slot, int g) {
+    static signed char ok[2][RDC_CLUSTER_MAX + 1];  // 0 unknown, 1 yes, -1 no
+    signed char &c = ok[npt_slot][g];
+    if (c == 0) {
+        bool fits = true;
+        if (g > 8 && cudaFuncSetAttribute((const void *)fn,
+                                          cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                          1) != cudaSuccess)
+            fits = false;
+        if (fits) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(g);
+            cfg.blockDim = dim3(RDC_THREADS);
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = g;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            int n = 0;
+            fits = cudaOccupancyMaxActiveClusters(&n, (const void *)fn, &cfg) == cudaSuccess &&
+                   n >= 1;
+        }
+        (void)cudaGetLastError();
+        c = fits ? 1 : -1;
+    }
+    return c > 0;
+}
+
 // one cluster of g CTAs (g <= RDC_CLUSTER_MAX), NPT pixels per thread
 static cudaError_t launch_cluster(const RdcIter &a, RdcFn fn, int g, cudaStream_t s) {
-    if (g > 8) {
-        cudaError_t e = cudaFuncSetAttribute((const void *)fn,
-                                             cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g);
     cfg.blockDim = dim3(RDC_THREADS);
@@ -474,7 +506,9 @@ cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s) {
     if (use_cluster && a.n <= RDC_CLUSTER_MAX * RDC_THREADS * 2) {
         const int npt = a.n <= RDC_CLUSTER_MAX * RDC_THREADS ? 1 : 2;
         const int g = (a.n + RDC_THREADS * npt - 1) / (RDC_THREADS * npt);
-        return launch_cluster(a, npt == 1 ? k_rdc_iter<1, true> : k_rdc_iter<2, true>, g, s);
+        RdcFn cf = npt == 1 ? k_rdc_iter<1, true> : k_rdc_iter<2, true>;
+        // not schedulable as one cluster here: fall through to the cooperative grid form
+        if (cluster_fits(cf, npt - 1, g)) return launch_cluster(a, cf, g, s);
     }
     // the smallest register-resident variant that covers n, else the general one
     RdcFn fn = nullptr;

@@ -76,7 +76,7 @@ struct rds_handle {
     double *d64 = nullptr, *part64 = nullptr, *cmp_out = nullptr;
     uint8_t *lab64 = nullptr;
     StopRecord *stop64 = nullptr;
-    unsigned *bar64 = nullptr;       // grid-barrier counter of k64_persist
+    unsigned long long *bar64 = nullptr;  // grid-barrier counter of k64_persist
     bool have_gt = false;
     int cur0 = 0;                    // ping-pong buffer at the start of the last solve
     float *scratch = nullptr;        // H*W natural-order staging for swizzled-plane getters
@@ -103,7 +103,7 @@ struct rds_handle {
     int32_t *rdc_idx = nullptr, *rdc_row = nullptr, *rdc_tot = nullptr;
     void *rdc_buf = nullptr;
     size_t rdc_bytes = 0;
-    unsigned *rdc_bar = nullptr;
+    unsigned long long *rdc_bar = nullptr;
     double *rdc_part = nullptr;       // per-CTA stopping sums of a compact tolerance solve
     rds_stats_t stats{};
 
@@ -755,12 +755,11 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactP
     cp->use = false;
     const int64_t npx = h->H * h->W;
     if (npx > INT32_MAX / 2) return RDS_OK;  // compact indices are int32: keep the dense path
-    if (iters > 4000000) return RDS_OK;      // the grid-barrier counter is 32-bit
-    if (!h->rdc_row) {  // small buffers; the H x W index map only once the path is taken
-        CK(h, cudaMalloc(&h->rdc_row, sizeof(int32_t) * (2 * h->H + 1)));
-        CK(h, cudaMalloc(&h->rdc_bar, RDC_BAR_BYTES));
-        CK(h, cudaMalloc(&h->rdc_part, sizeof(double) * 2 * RDC_MAX_GRID));
-    }
+    // small buffers; the H x W index map only once the path is taken.  Each buffer is
+    // guarded by its own pointer, so a failed allocation is retried, never skipped.
+    if (!h->rdc_row) CK(h, cudaMalloc(&h->rdc_row, sizeof(int32_t) * (2 * h->H + 1)));
+    if (!h->rdc_bar) CK(h, cudaMalloc(&h->rdc_bar, RDC_BAR_BYTES));
+    if (!h->rdc_part) CK(h, cudaMalloc(&h->rdc_part, sizeof(double) * 4 * RDC_MAX_GRID));
     h->rdc_tot = h->rdc_row + 2 * h->H;
     CK(h, launch_rdc_count(h->at(h->lab), h->pitch, (int)h->H, (int)h->W, h->rdc_row,
                            h->rdc_row + h->H, h->rdc_tot, h->stream));
@@ -1360,16 +1359,20 @@ int rds_solve_gt(rds_t *h, float lambda, float theta, float tau, float delta,
     if (!h->image_ok || !h->p_ok)
         return fail(h, RDS_EINVAL, "rds_solve_gt: image or P has non-finite values");
     NvtxRange nvtx_gt("rds_solve_gt");
-    if (!h->d64) {  // f, u, v, rho1 x2, rho2 x2, v (second buffer): 8 double planes
+    // f, u, v, rho1 x2, rho2 x2, v (second buffer): 8 double planes; every buffer guarded by
+    // its own pointer (a failed allocation is retried on the next call, never skipped)
+    if (!h->d64) {
         CK(h, cudaMalloc(&h->d64, sizeof(double) * h->plane * 8));
         CK(h, cudaMemsetAsync(h->d64, 0, sizeof(double) * h->plane * 8, h->stream));
+    }
+    if (!h->lab64) {
         CK(h, cudaMalloc(&h->lab64, h->plane));
         CK(h, cudaMemsetAsync(h->lab64, 0, h->plane, h->stream));
-        CK(h, cudaMalloc(&h->part64, sizeof(double) * 2 * F64P_MAX_GRID));
-        CK(h, cudaMalloc(&h->cmp_out, sizeof(double) * 2));
-        CK(h, cudaMalloc(&h->stop64, sizeof(StopRecord)));
-        CK(h, cudaMalloc(&h->bar64, sizeof(unsigned)));
     }
+    if (!h->part64) CK(h, cudaMalloc(&h->part64, sizeof(double) * 4 * F64P_MAX_GRID));
+    if (!h->cmp_out) CK(h, cudaMalloc(&h->cmp_out, sizeof(double) * 2));
+    if (!h->stop64) CK(h, cudaMalloc(&h->stop64, sizeof(StopRecord)));
+    if (!h->bar64) CK(h, cudaMalloc(&h->bar64, sizeof(unsigned long long)));
     CK(h, cudaMemsetAsync(h->stop64, 0, sizeof(StopRecord), h->stream));
     F64Args a{};
     a.z = h->at(h->z);

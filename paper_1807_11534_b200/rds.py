@@ -458,8 +458,10 @@ class Solver:
 
     def solve_tol(self, lam, theta, tau, delta, max_iters, tol, check_every=0):
         """Stop at the first check (every check_every iterations, and at max_iters) where
-        max(RMS du, RMS dv) <= tol.  Returns the stats dict (iters,
-        converged, residual)."""
+        max(||u^l - u^(l-1)||, ||v^l - v^(l-1)||) <= tol.  The norm is
+        the library default RDS_OPT_STOP_NORM = 0, the Euclidean norm over pixels of unit
+        area (reading R-F2); set_option(RDS_OPT_STOP_NORM, 1) selects the RMS instead.
+        Returns the stats dict (iters, converged, residual)."""
         rds_solve_tol(self.h, lam, theta, tau, math.inf if delta is None else delta,
                       max_iters, tol, check_every)
         return self.stats()
