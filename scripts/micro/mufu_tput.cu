@@ -6,7 +6,8 @@
 __device__ __forceinline__ float sq(float x) { float y; asm volatile("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 __device__ __forceinline__ float rc(float x) { float y; asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x)); return y; }
 // MODE 0: 16 independent MUFU.SQRT per iteration (throughput)
-// MODE 1: 16 independent MUFU.RCP
+// MODE 1: 16 independent MUFU.RCP (each fed through an FADD: a bare rcp(rcp(x)) chain was
+//         eliminated by ptxas in round 1, 0.03 cycles per "instruction")
 // MODE 2: 8 MUFU + 8 FFMA2 interleaved (independent)
 // MODE 3: 8 MUFU + 16 FFMA2
 // MODE 4: dependent chain of FFMA2 (latency), 1 warp per SMSP
@@ -28,17 +29,17 @@ __global__ void k(float *out, int iters) {
             for (int i = 0; i < 16; ++i) a[i] = sq(a[i]) + 1.0f;
         } else if (MODE == 1) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) a[i] = rc(a[i]);
+            for (int i = 0; i < 16; ++i) a[i] = rc(a[i]) + 1.0f;
         } else if (MODE == 2) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                a[i] = rc(a[i]);
+                a[i] = rc(a[i]) + 1.0f;
                 b[i] = __ffma2_rn(b[i], m2, c2);
             }
         } else if (MODE == 3) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                a[i] = rc(a[i]);
+                a[i] = rc(a[i]) + 1.0f;
                 b[i] = __ffma2_rn(b[i], m2, c2);
                 b[i] = __ffma2_rn(b[i], m2, c2);
             }
@@ -50,7 +51,7 @@ __global__ void k(float *out, int iters) {
             for (int i = 0; i < 16; ++i) a[0] = fmaf(a[0], 0.999f, 1e-3f);
         } else if (MODE == 6) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) a[0] = rc(a[0]);
+            for (int i = 0; i < 16; ++i) a[0] = rc(a[0]) + 1.0f;  // MUFU + FADD latency
         } else if (MODE == 8) {  // odd warps: 16 SQRT; even warps: 64 FFMA2 (128 pipe cycles each)
             if ((threadIdx.x >> 5) & 1) {
 #pragma unroll
@@ -105,15 +106,15 @@ int main() {
     float *o; CK(cudaMalloc(&o, 148 * 8 * 256 * 4));
     const int B = 148 * 4, T = 256;  // 8 warps per SMSP
     run<0>("MUFU.SQRT x16 (tput)", B, T, 4000, 16, o);
-    run<1>("MUFU.RCP x16 (tput)", B, T, 4000, 16, o);
-    run<2>("MUFU.RCP x8 + FFMA2 x8 (per MUFU)", B, T, 4000, 8, o);
-    run<3>("MUFU.RCP x8 + FFMA2 x16 (per MUFU)", B, T, 4000, 8, o);
+    run<1>("MUFU.RCP x16 (+FADD) (tput)", B, T, 4000, 16, o);
+    run<2>("MUFU.RCP(+FADD) x8 + FFMA2 x8 (per MUFU)", B, T, 4000, 8, o);
+    run<3>("MUFU.RCP(+FADD) x8 + FFMA2 x16 (per MUFU)", B, T, 4000, 8, o);
     run<8>("half warps SQRT x16 / half FFMA2 x64", B, T, 4000, 16, o);
     run<9>("SQRT x8 + FFMA2 x32 interleaved", B, T, 4000, 8, o);
     run<10>("SQRT x8 (+FADD) only", B, T, 4000, 8, o);
     run<4>("FFMA2 dep chain (latency)", 148, 32 * 4, 4000, 16, o);
     run<5>("FFMA dep chain (latency)", 148, 32 * 4, 4000, 16, o);
-    run<6>("MUFU.RCP dep chain (latency)", 148, 32 * 4, 4000, 16, o);
+    run<6>("MUFU.RCP+FADD dep chain (latency)", 148, 32 * 4, 4000, 16, o);
     run<7>("SHFL dep chain (latency)", 148, 32 * 4, 4000, 16, o);
     return 0;
 }

@@ -19,3 +19,19 @@ def orc():
 
     oracle.build()
     return oracle
+
+
+class _Cache(dict):
+    """Session cache of seeded config images and full-size oracle solves, so that the slow
+    stated-K parity tests (which share images and, for some deltas, oracle runs) build each
+    one once.  Keys are plain tuples; values are whatever the builder returned."""
+
+    def get_or(self, key, build):
+        if key not in self:
+            self[key] = build()
+        return self[key]
+
+
+@pytest.fixture(scope="session")
+def cache():
+    return _Cache()

@@ -138,6 +138,27 @@ def test_compact_c3_full(rds, delta_rel):
     assert np.array_equal(s_c.v(), s_d.v())
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("delta_rel", [0.02, 0.05])
+def test_compact_c3_full_oracle(rds, orc, cache, delta_rel):
+    """The compact path at full C3 (4096^2) and the config's K = 1000, at the thin bands where
+    the bench takes it (restricted_compact), element-wise against the fp64 oracle at the
+    north_star tolerances, labels bit-exact."""
+    cfg = wl.CONFIGS["C3"]
+    z, P = cache.get_or(("C3", "image"), lambda: wl.make_image(cfg))
+    f = orc.fitting(z, cfg.c1, cfg.c2)
+    delta = wl.band_delta(delta_rel, orc.absmax(f))
+    s, g = _run(rds, z, delta, cfg.iters, 1)
+    assert s.stats()["compact"] == 1
+    o = orc.solve(f, delta, *PAR, cfg.iters)
+    assert np.array_equal(g["labels"], o["labels"])
+    for k in ("u", "v", "p1", "p2"):
+        err = np.abs(g[k].astype(np.float64) - o[k]).max()
+        assert err <= 5e-4, (k, err)
+    assert np.mean(g["mask"] != (o["u"] > 0.5)) <= 5e-4
+    s.close()
+
+
 def _resid(a, b):
     return max(float(np.sqrt(np.sum((a[0].astype(np.float64) - b[0]) ** 2))),
                float(np.sqrt(np.sum((a[1].astype(np.float64) - b[1]) ** 2))))

@@ -146,6 +146,39 @@ def test_strips_bitwise_whole_image(rds, H, W, G, s, K, delta_rel, kf, compact):
         assert tot[k] == pytest.approx(e_ref[k], rel=1e-9, abs=1e-9), k
 
 
+@pytest.mark.parametrize("name,G,seg,dr", [("C1", 3, 7, 0.2), ("C2", 4, 28, math.inf),
+                                           ("C2", 2, 14, 0.1)])
+def test_strips_config_vs_oracle(rds, orc, name, G, seg, dr):
+    """Row strips on a BASELINE config at full size and its stated K, compared directly with
+    the whole-image fp64 oracle (not only with the GPU whole-image solve): every strip's owned
+    rows within the north_star tolerances, labels bit-exact."""
+    cfg = wl.CONFIGS[name]
+    z, P = wl.make_image(cfg)
+    f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
+    delta = wl.band_delta(dr, orc.absmax(f))
+    lam, K = cfg.lambdas[0], cfg.iters
+    plan = strips.partition(cfg.H, G, seg)
+    engines = []
+    for st in plan:
+        e = rds.Solver(st.rows, cfg.W)
+        e.set_image(z[st.r0:st.r0 + st.rows])
+        e.set_fitting(cfg.c1, cfg.c2, cfg.gamma,
+                      None if P is None else np.ascontiguousarray(P[st.r0:st.r0 + st.rows]))
+        engines.append(e)
+    strips.solve_local(engines, plan, lam, cfg.theta, cfg.tau, delta, K, seg)
+    o = orc.solve(f, delta, lam, np.float32(cfg.theta), cfg.tau, K)
+    for st, e in zip(plan, engines):
+        got = _state(e)
+        got["labels"] = e.labels()
+        rows = slice(st.lo, st.hi)
+        for k in ("u", "v", "p1", "p2"):
+            err = np.abs(got[k][st.owned].astype(np.float64) - o[k][rows]).max()
+            assert err <= 5e-4, (st.rank, k, err)
+        assert np.array_equal(got["labels"][st.owned], o["labels"][rows])
+        assert np.mean(got["mask"][st.owned] != (o["u"][rows] > 0.5)) <= 5e-4
+        e.close()
+
+
 def test_torch_default_stream(rds):
     """stream=0 (torch's default stream) is the legacy default stream, not the private one:
     work is ordered with torch's (temporary device inputs are safe) and CUDA events on it

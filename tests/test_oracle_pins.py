@@ -493,6 +493,37 @@ def test_dependency_cone_window(orc, delta_rel):
         assert same == exact, (m, same)
 
 
+def _window_exact(orc, f, delta, K, r0, c0, b, top, bot, left, right):
+    full = orc.solve(f, delta, 4.0, np.float32(0.1), 0.125, K)
+    win = orc.solve(np.ascontiguousarray(f[r0 - top:r0 + b + bot, c0 - left:c0 + b + right]),
+                    delta, 4.0, np.float32(0.1), 0.125, K)
+    return all(np.array_equal(win[k][top:top + b, left:left + b], full[k][r0:r0 + b, c0:c0 + b])
+               for k in ("u", "v", "p1", "p2"))
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 9, 20])
+@pytest.mark.parametrize("delta_rel", [0.3, math.inf])
+def test_cone_margin_k_plus_1(orc, K, delta_rel):
+    """The tight margin the stated-K window tests use ("window margin"): the
+    window solve differs from the full one only through its cut rows / columns (rho1 of the
+    row above the top cut and rho2 of the column left of the left cut read as 0; the Neumann
+    conditions forced on the last window row / column).  By induction on the iteration, after
+    k iterations the wrong rho reaches at most k-1 rows (columns) in from the top (left) cut
+    and v at most k, and from the bottom (right) cut at most k-1: so a margin of K+1 on EVERY
+    side reproduces the full-image iterates bit for bit, and (at delta = inf, where no pinned
+    pixel stops the front) a margin of K-1 on the top or the bottom side does not."""
+    rng = np.random.default_rng(11)
+    H, W = 160, 150
+    f = rng.uniform(-1, 1, (H, W)).astype(np.float32)
+    delta = wl.band_delta(delta_rel, orc.absmax(f))
+    r0, c0, b, m = 70, 68, 8, K + 1
+    assert _window_exact(orc, f, delta, K, r0, c0, b, m, m, m, m)
+    if math.isinf(delta_rel) and 2 <= K <= 9:
+        assert not _window_exact(orc, f, delta, K, r0, c0, b, K - 1, m, m, m)
+        assert not _window_exact(orc, f, delta, K, r0, c0, b, m, K - 1, m, m)
+        assert not _window_exact(orc, f, delta, K, r0, c0, b, m, m, K - 1, m)
+
+
 # ------------------------------------------------------------------------------------------
 # f2: the stopping rule (PAPER.md:234-238), RMS norm (reading R-F2)
 # ------------------------------------------------------------------------------------------
