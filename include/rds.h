@@ -90,6 +90,8 @@ typedef struct {
     float residual;          /* rds_solve_tol: max(RMS du, RMS dv) at the last check; else -1 */
     int32_t check_every;     /* rds_solve_tol: iterations between checks; 0 for rds_solve */
     int32_t compact;         /* 1 if the last solve ran the compacted RD iteration (RDS_OPT_COMPACT) */
+    int32_t wave;            /* 1 if the last solve's K-loop ran as the temporal wavefront (RDS_OPT_WAVE) */
+    int32_t resident;        /* 1 if the last solve ran as one resident cluster (RDS_OPT_RESIDENT) */
 } rds_stats_t;
 
 /* Options (rds_set_option). */
@@ -121,6 +123,31 @@ typedef struct {
                                 solves (rds_solve_tol) evaluate the stopping rule inside the
                                 same persistent kernel; images of more than 2^30 pixels and bands
                                 of 2^26 or more pixels stay dense. */
+
+#define RDS_OPT_WAVE 9       /* temporal wavefront for fixed-K solves (rds_solve, rds_solve_q,
+                                rds_solve_continue): the K / k_fuse blocks of k_fuse fused
+                                iterations run as ONE persistent launch in which block b of a
+                                column strip follows block b-1 down the image a few rows behind,
+                                reading its rows from L2 (progress counters per block and strip;
+                                DESIGN.md §5).  Same per-pixel operations as the launch-per-block
+                                form: results are bit-identical.  0 = off; 1 = on whenever it
+                                applies (image widths a multiple of 4, k_fuse 4..7, at least two
+                                full blocks); 2 = on for images above 2^21 pixels.  Default 0:
+                                measured slower than the launch-per-block form on B200 (C3
+                                25.6 vs 16.5 ms, C4 352 vs 268 ms per 1000 iterations; the
+                                chained blocks settle into lock-step polls and the data does not
+                                stay in L2).  With no RDS_OPT_KFUSE set it runs
+                                k_fuse 6. */
+
+#define RDS_OPT_RESIDENT 10  /* small images (the paper's 128 x 128 size) as ONE resident thread-
+                                block cluster: the image in <= 16 horizontal slabs, one CTA each,
+                                the state in shared memory, every iteration of a fixed-K solve in
+                                one launch with one cluster barrier per iteration (k_small.cu,
+                                DESIGN.md §5).  Same per-pixel operations as the stencil (results
+                                bit-identical).  Used for rds_solve / rds_solve_q when the slabs
+                                fit 200 KB of shared memory per CTA (about 300 x 300 pixels) and
+                                the cluster can be scheduled; tolerance solves stay on the
+                                stencil.  0 = off; 1 and 2 (default) = on where it applies. */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */
@@ -271,6 +298,26 @@ int rds_energy(rds_t *h, rds_energy_t *out);
  * the mask at the end).  A tolerance solve's outcome is resolved first (synchronises).
  * iters = 0 is a no-op.  Errors: RDS_ESTATE before a solve; RDS_EINVAL if iters < 0. */
 int rds_solve_continue(rds_t *h, int32_t iters);
+
+/* rds_solve_continue(iters) whose last iteration l also evaluates the two sums of the paper's
+ * stopping rule (§4) over rows [row0, row1) only:
+ *   sums[0] = sum (u^l - u^(l-1))^2,  sums[1] = sum (v^l - v^(l-1))^2   (host, synchronises).
+ * A strip passes its owned rows; the ranks all-reduce the sums and take one decision, so the
+ * rule runs on a strip-decomposed image exactly as on the whole one (strips.StripSolver.
+ * solve_tol).  Errors: RDS_ESTATE before a solve; RDS_EINVAL if iters < 1, sums == NULL or the
+ * rows leave [0, H). */
+int rds_continue_check(rds_t *h, int32_t iters, int64_t row0, int64_t row1, double *sums);
+
+/* One radix-select pass of rds_band_for_fraction over rows [row0, row1): out[d] (256 counts,
+ * host) = #{pixels of those rows whose |f| bit pattern b has (b & mask) == prefix and byte
+ * (b >> shift) & 255 == d}, shift in {24, 16, 8, 0}.  |f| >= 0, so bit patterns order like
+ * the values; summing the strips' histograms (all-reduce) and walking the passes from the
+ * top byte down finds the k-th smallest |f| of the whole image (the q -> q^ rule of
+ * PAPER.md:74, 84; strips.StripSolver.band_for_fraction).  Synchronises.  Errors:
+ * RDS_ESTATE before rds_set_image / rds_set_fitting; RDS_EINVAL on NULL, rows outside
+ * [0, H) or another shift. */
+int rds_abs_histogram(rds_t *h, int64_t row0, int64_t row1, uint32_t prefix, uint32_t mask,
+                      int32_t shift, uint32_t *out);
 
 /* Copy rows [row0, row0 + nrows) of the current state out of / into the handle.  Buffer
  * layout: three planes v, rho1, rho2, each nrows x W float32 row-major (natural column

@@ -41,6 +41,33 @@ __host__ __device__ constexpr int lh_of(int kf) { return 4 * ((kf + 1 + 3) / 4);
 __host__ __device__ constexpr int rh_of(int kf) { return 4 * ((kf + 3) / 4); }
 __host__ __device__ constexpr int wv_of(int kf) { return 128 - lh_of(kf) - rh_of(kf); }
 
+// The next run [b, e) of set bits at or after position *pos in a strip's band bitmask
+// (nbw words); false when there is none.  *pos is left at e.
+__device__ __forceinline__ bool next_run(const uint32_t *bits, int nbw, int *pos, int *b, int *e) {
+    int p = *pos, w = p >> 5;
+    if (w >= nbw) return false;
+    uint32_t x = bits[w] & (0xffffffffu << (p & 31));
+    while (x == 0) {
+        if (++w >= nbw) return false;
+        x = bits[w];
+    }
+    *b = (w << 5) + __ffs(x) - 1;
+    // run end: first clear bit after b
+    p = *b;
+    uint32_t y = ~bits[w] & (0xffffffffu << (p & 31));
+    while (y == 0) {
+        if (++w >= nbw) {
+            *e = nbw << 5;
+            *pos = *e;
+            return true;
+        }
+        y = ~bits[w];
+    }
+    *e = (w << 5) + __ffs(y) - 1;
+    *pos = *e;
+    return true;
+}
+
 // A stencil work item: output columns [strip*WV, (strip+1)*WV) and output rows [r0, r1) --
 // a piece of a vertical run of active 32-row bands, cut at multiples of ITEM_Q rows.
 constexpr int ITEM_Q = 8;
@@ -58,6 +85,7 @@ struct StopRecord {
     double residual;    // ||du||, ||dv|| max at the last check (norm: StopCheck::norm_div)
     int32_t checks;     // checks evaluated
     int32_t it;         // iterations done so far (advanced by every check)
+    double su, sv;      // the last check's sums of (u^l - u^(l-1))^2, (v^l - v^(l-1))^2
 };
 
 // One evaluation of the stopping rule after a block of iterations.
@@ -87,11 +115,49 @@ struct StencilArgs {
     int32_t *queue;                      // this launch's work counter (zeroed before the loop)
     StopRecord *stop;                    // tolerance mode: skip the launch once stop->flag
     double *chk;                         // CHECK launches: [item][2] sums of du^2, dv^2
+    int chk_r0, chk_r1;                  // CHECK launches: rows the sums cover ([0, H) for a
+                                         // whole-image rule; a strip's owned rows)
     int64_t pitch;
     int H, W;
     int img_w;                           // columns per image (W, or the image width of a batch)
     float tau, theta, inv_theta;
 };
+
+// The temporal wavefront (k_wave.cu): nblk blocks of KF iterations of a
+// fixed-K solve in ONE persistent launch; block b of strip s reads ping-pong buffer
+// (c0 + b) & 1 and writes the other, after its producers (block b-1, strips s-1..s+1) have
+// published the rows it needs in prog[(b-1) * n_strips + s'] (rows < value final).
+struct WaveArgs {
+    StencilArgs a;                       // c, pitch, H, W, img_w, tau, theta (planes below)
+    const float *p1[2], *p2[2], *v[2];   // ping-pong plane origins
+    const uint32_t *band_bits;           // active 8-row bands per strip (launch_band_flags)
+    int nbw;                             // bitmask words per strip
+    int32_t *prog;                       // [nblk][n_strips], zeroed before the launch
+    int32_t *queue;                      // task counter, zeroed before the launch
+    int nblk, n_strips, c0;
+};
+cudaError_t launch_wave(int kf, const WaveArgs &w, int grid, cudaStream_t s);
+int wave_blocks_per_sm(int kf);
+bool wave_supported(int kf);
+
+// Small images as one resident cluster (k_small.cu): G slabs of R rows, one CTA
+// each, the whole fixed-K loop in one launch.  Reads the state from the dense ping-pong buffer
+// *_in, writes the final state into *_out and u / the mask of the last iteration.
+constexpr int SMALL_THREADS = 512, SMALL_MAX_CTAS = 16;
+constexpr size_t SMALL_MAX_SMEM = 200 * 1024;
+struct SmallArgs {
+    const float *p1_in, *p2_in, *v_in, *c;   // plane origins (pixel (0,0)), swizzled
+    float *p1_out, *p2_out, *v_out;
+    float *u_out;
+    uint8_t *mask_out;
+    const long long *n_rd;                   // RD pixel count (0: nothing moves), or null
+    int64_t pitch;
+    int H, W, img_w, K, G, R;
+    float tau, theta, inv_theta;
+};
+bool small_plan(int64_t H, int64_t W, int *G, int *R);
+bool small_cluster_fits(const SmallArgs &a);
+cudaError_t launch_small(const SmallArgs &a, cudaStream_t s);
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_fill_frame(float *plane, int64_t n, float value, cudaStream_t s);

@@ -239,6 +239,8 @@ __global__ void __launch_bounds__(256) k_stop_check(const StopCheck c) {
             tv += sh[1][w];
         }
         const double r = fmax(sqrt(tu / c.norm_div), sqrt(tv / c.norm_div));
+        rec->su = tu;
+        rec->sv = tv;
         const int it = rec->it + c.block_iters;
         rec->it = it;
         rec->launches += c.block_launches;

@@ -310,36 +310,10 @@ cudaError_t launch_band_flags(const int32_t *sub_rd, int H, int W, int wv, int n
     return cudaGetLastError();
 }
 
-// The next run [b, e) of set bits at or after position *pos in a strip's band bitmask
-// (nbw words); false when there is none.  *pos is left at e.
-__device__ bool next_run(const uint32_t *bits, int nbw, int *pos, int *b, int *e) {
-    int p = *pos, w = p >> 5;
-    if (w >= nbw) return false;
-    uint32_t x = bits[w] & (0xffffffffu << (p & 31));
-    while (x == 0) {
-        if (++w >= nbw) return false;
-        x = bits[w];
-    }
-    *b = (w << 5) + __ffs(x) - 1;
-    // run end: first clear bit after b
-    p = *b;
-    uint32_t y = ~bits[w] & (0xffffffffu << (p & 31));
-    while (y == 0) {
-        if (++w >= nbw) {
-            *e = nbw << 5;
-            *pos = *e;
-            return true;
-        }
-        y = ~bits[w];
-    }
-    *e = (w << 5) + __ffs(y) - 1;
-    *pos = *e;
-    return true;
-}
-
 // Item rows are cut at multiples of ITEM_Q rows (finer than a 32-row band), so a sparse
 // active set, or a dense one that would overflow the resident warps by a few items, can be
 // spread over every warp.  Candidate item heights (rows) for the makespan model:
+
 __constant__ int kChunkRows[] = {8, 16, 24, 32, 40, 48, 64, 80, 96, 128, 160, 192, 256, 384, 512};
 constexpr int N_CHUNK = 15;
 

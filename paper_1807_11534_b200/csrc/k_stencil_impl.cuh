@@ -112,7 +112,10 @@ __device__ __forceinline__ Q zeroq() {
 // needed (cp.async.wait_group is per-thread).
 constexpr int RING = 4;   // rows of rho1/rho2/v in flight (power of two)
 constexpr int CR = 16;    // rows of c kept (power of two; >= RING + KF + 3)
-constexpr int STENCIL_SMEM = STENCIL_WARPS * (RING * 96 + 2 * CR * 32) * (int)sizeof(float4);
+// Per warp after the row rings: its c ring (2 CR rows of 32 float4) followed by two rows of
+// 32 float4, the wavefront's per-lane 32-byte slots (k_wave; WaveSlot).  CRW = that stride.
+constexpr int CRW = 2 * CR * 32 + 64;
+constexpr int STENCIL_SMEM = STENCIL_WARPS * (RING * 96 + CRW) * (int)sizeof(float4);
 
 // Pipeline split: the S stages are cut into NS+1 chains ([0, sp(1)), [sp(1), sp(2)), ...)
 // joined through one-row delay buffers, so within one row step the chains are independent
@@ -158,6 +161,7 @@ struct Ctx {
     float4 *cring;  // this lane's c slot 0; slot stride 32 float4, 2*CR slots
     int64_t pitch;
     int col, H, R0, Rend, n_last;
+    int chk_r0, chk_r1;  // CHECK mode: rows whose stopping sums are accumulated
     bool store_lane, right_edge;
     Q kx;
     float tau, theta, inv_theta;
@@ -273,6 +277,97 @@ __device__ __forceinline__ void stage(const Q &ap1, const Q &ap2, const Q &av, c
     bw = f.w;
 }
 
+// ---------------------------------------------------------------------------------------
+// Temporal wavefront (k_wave, DESIGN.md §5 "wavefront"): ONE persistent launch runs many
+// KF-iteration blocks of a fixed-K solve.  Task (b, s) = block b of strip s: a warp marches
+// the strip's active runs top to bottom, reading level b*KF from ping-pong buffer (c0+b)&1 and
+// writing level (b+1)*KF into the other.  Block b's row r of strip s may be read only after
+// block b-1 has written it on strips s-1, s, s+1 (the 128 input columns span them), so every
+// task publishes a progress counter (rows < P final) and waits on its three producers'
+// counters before it stages a row.  Tasks are taken in (b, s) order from one queue, so a task
+// waits only on tasks already taken by running warps: no deadlock, no co-residency needed.
+// The waits also order the ping-pong reuse: block b+1 overwrites a row of block b's input
+// only after block b has emitted rows far below it (its march consumed the row by then).
+// Rows outside [0, H) are frame rows (never written) and rows between active runs hold pinned
+// values in both buffers, so neither is waited for.  The hooks run once per two row steps at
+// the march's loop head, so the pipeline body itself has no extra control flow.
+// ---------------------------------------------------------------------------------------
+
+// Registers of a wavefront task; the counter addresses live in the lane's shared-memory slot
+// (WaveSlot, after the warp's c ring) to keep the pipeline free of spills.  Everything here is
+// warp-uniform (every lane loads / stores the same addresses) and branch-free except for
+// vote-controlled loops, so the pipeline's warp shuffles need no divergence handling.
+// rows between progress publications (a gpu-scope fence each); RDS_WAVE_PUB overrides (even)
+#ifndef RDS_WAVE_PUB
+#define RDS_WAVE_PUB 16
+#endif
+constexpr int WAVE_PUB = RDS_WAVE_PUB;
+static_assert(WAVE_PUB >= 2 && WAVE_PUB % 2 == 0, "publication interval");
+
+struct Wave {
+    int avail;  // rows < avail are final on all three producers
+    int pend;   // producers' progress loaded at the previous check
+};
+struct WaveSlot {
+    const int *pin[3];      // progress of the producers on strips s-1, s, s+1 (a cell holding
+                            // INT_MAX where there is none)
+    int *pout;              // this task's progress counter
+    const uint32_t *bits;   // the strip's band bitmask (k_wave's run loop state, kept out of
+    int pos, task;          // registers while the pipeline runs)
+};
+__device__ __forceinline__ WaveSlot *wave_slot(const Ctx &x) {
+    // the warp's slot after its c ring (x.cring is this lane's float4 of the c ring's row 0)
+    return reinterpret_cast<WaveSlot *>(x.cring + 2 * CR * 32 - (threadIdx.x & 31));
+}
+static_assert(sizeof(WaveSlot) <= 64 * sizeof(float4), "wave slot");
+
+__device__ __forceinline__ int ld_relaxed(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int wave_poll(const WaveSlot *w) {
+    return min(ld_relaxed(w->pin[0]), min(ld_relaxed(w->pin[1]), ld_relaxed(w->pin[2])));
+}
+
+// Rows < v of this task are final: make the warp's stores visible at gpu scope, then publish
+// (every lane fences its own stores and writes the same value to the same word).
+__device__ __forceinline__ void wave_publish(const Ctx &x, int v) {
+    __syncwarp();
+#ifndef RDS_WAVE_NOFENCE  // (timing experiment only: without the fence the protocol is unsafe)
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+    __syncwarp();
+    asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(wave_slot(x)->pout), "r"(v)
+                 : "memory");
+}
+
+// The slow path of wave_need: a producer is always a task taken earlier by a running warp, so
+// this wait ends; the bound (~seconds) turns a broken invariant into a launch error instead of
+// a hung GPU.  (Conditions through warp votes: the compiler then knows the loop is uniform.)
+__device__ __forceinline__ int wave_spin(const WaveSlot *ws, int avail, int need) {
+    for (unsigned spins = 0; __any_sync(0xffffffffu, need > avail); ++spins) {
+        if (spins > (1u << 24)) __trap();
+        __nanosleep(128);
+        avail = max(avail, wave_poll(ws));
+    }
+    return avail;
+}
+
+// Before staging input rows <= r: wait until the producers have finalised them.  The poll
+// issued at the previous check is consumed first (its L2 round trip overlapped two row steps of
+// work); the data is then read with cp.async.cg from L2, where the producer's fence put it
+// before the counter.  The copies are issued only after the counter value has been observed
+// (they are control dependent on it).
+__device__ __forceinline__ void wave_need(const Ctx &x, Wave &w, int r) {
+    const int need = min(r + 1, x.H);  // rows >= H are frame rows: never written
+    if (__all_sync(0xffffffffu, w.avail >= x.H)) return;
+    const WaveSlot *ws = wave_slot(x);
+    w.avail = max(w.avail, w.pend);
+    w.pend = wave_poll(ws);
+    if (__any_sync(0xffffffffu, need > w.avail)) w.avail = wave_spin(ws, w.avail, need);
+}
+
 // Launch modes: PLAIN iterates; WRITE_U also writes u and the mask of the last level
 // (the last launch of a solve); CHECK additionally accumulates the paper's stopping
 // quantities sum (u^l - u^(l-1))^2 and sum (v^l - v^(l-1))^2 over the item's output pixels
@@ -287,10 +382,10 @@ struct Extra {  // per-row-step state only the CHECK mode needs
 
 // One row step: consume input row n from the ring, advance all S stages, store the level-S
 // row if it is an output row of this item, then refill the slot with row n+RING.
-template <int S, int MODE, bool ALIGNED, bool LAST>
+template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE>
 __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B,
                                           const Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
-                                          const Ctx &x, float &acc_u, float &acc_v) {
+                                          const Ctx &x, float &acc_u, float &acc_v, Wave &wv) {
     using SPL = Split<S>;
     constexpr bool WRITE_U = MODE != MODE_PLAIN;
     cp_async_wait<RING - 1>();
@@ -342,8 +437,10 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
                     const float2 da = sub2(uu.a, up.a), db = sub2(uu.b, up.b);
                     const Q &av = A.v[S - 1];  // v^(l-1) at row m
                     const float2 ea = sub2(ov.a, av.a), eb = sub2(ov.b, av.b);
-                    acc_u += (da.x * da.x + da.y * da.y) + (db.x * db.x + db.y * db.y);
-                    acc_v += (ea.x * ea.x + ea.y * ea.y) + (eb.x * eb.x + eb.y * eb.y);
+                    if (m >= x.chk_r0 && m < x.chk_r1) {  // the rows the sums cover
+                        acc_u += (da.x * da.x + da.y * da.y) + (db.x * db.x + db.y * db.y);
+                        acc_v += (ea.x * ea.x + ea.y * ea.y) + (eb.x * eb.x + eb.y * eb.y);
+                    }
                 }
                 stq(x.p1o + o, o1);
                 stq(x.p2o + o, o2);
@@ -357,13 +454,18 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
             }
         }
     }
-    // refill the slot just consumed (its values are in registers and already used)
-    if (n + RING <= x.n_last) stage_row(x, n + RING);
+    // refill the slot just consumed (its values are in registers and already used); the
+    // wavefront first waits until the producers have written that row
+    if (n + RING <= x.n_last) {
+        if (WAVE) wave_need(x, wv, n + RING);
+        stage_row(x, n + RING);
+    }
     cp_async_commit();
 }
 
-template <int S, int MODE, bool ALIGNED, bool LAST>
-__device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &acc_v) {
+template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE>
+__device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &acc_v,
+                                      Wave &wv) {
     PipeState<S> A, B;
     Extra<S, MODE> EA, EB;
 #pragma unroll
@@ -374,13 +476,65 @@ __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &
         A.d1[k] = A.d2[k] = A.dv[k] = A.dd[k] = zeroq();
     }
     EA.uprev = zeroq();
-    for (; n <= x.n_last; n += 2) {
-        pipe_step<S, MODE, ALIGNED, LAST>(A, B, EA, EB, n, x, acc_u, acc_v);
-        pipe_step<S, MODE, ALIGNED, LAST>(B, A, EB, EA, n + 1, x, acc_u, acc_v);
+    for (int k = 0; n <= x.n_last; n += 2, ++k) {
+        // wavefront: every second loop head, publish the rows emitted so far (rows < n - S -
+        // NS of this item are final)
+        if (WAVE && (k % (WAVE_PUB / 2)) == WAVE_PUB / 2 - 1)
+            wave_publish(x, min(max(n - S - Split<S>::NS, x.R0), x.Rend));
+        pipe_step<S, MODE, ALIGNED, LAST, WAVE>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
+        pipe_step<S, MODE, ALIGNED, LAST, WAVE>(B, A, EB, EA, n + 1, x, acc_u, acc_v, wv);
     }
 }
 
-// Two CTAs (8 warps) per SM: shared memory (88 KB per CTA) and registers both allow 2.
+// One item: output columns of `strip`, output rows [r0, r1), inputs from the planes p1i /
+// p2i / vi (pixel (0,0) origins).  Sets up the lane geometry, stages the first RING rows and
+// marches (S stages); returns with every cp.async group drained.
+template <int KF, int S, int MODE, bool ALIGNED, bool WAVE>
+__device__ __forceinline__ void run_item(Ctx &x, const StencilArgs &a, int strip, int r0, int r1,
+                                         const float *p1i, const float *p2i, const float *vi,
+                                         float &acc_u, float &acc_v, Wave &wv) {
+    constexpr int LH = lh_of(KF), WV = wv_of(KF);
+    const int lane = threadIdx.x & 31;
+    x.R0 = r0;
+    x.Rend = r1;
+    x.col = strip * WV - LH + 4 * lane;
+    x.store_lane = (4 * lane >= LH) && (4 * lane < LH + WV);
+    // the Neumann column (grad_2 = 0) of every image: W - 1, or with a batch of images
+    // stacked along columns (rds_create_batch) every img_w-th column; the frame columns
+    // left of 0 give negative x.col + e, never an image-last column
+    {
+        const int iw = a.img_w;
+        auto last_col = [&](int c) { return c >= 0 && c < a.W && c % iw == iw - 1; };
+        x.right_edge = last_col(x.col + 3);
+        x.kx.a = make_float2(last_col(x.col) ? 0.0f : 1.0f, last_col(x.col + 2) ? 0.0f : 1.0f);
+        x.kx.b = make_float2(last_col(x.col + 1) ? 0.0f : 1.0f, last_col(x.col + 3) ? 0.0f : 1.0f);
+    }
+    x.p1i = p1i + x.col;
+    x.p2i = p2i + x.col;
+    x.vi = vi + x.col;
+    x.ci = a.c + x.col;
+    // input rows [n, n_last]; the cone reaches S+1 rows up and S rows down, the delay
+    // buffer adds one row of latency.  The step count is made even (one extra warm-up
+    // row) for the two-state unrolled loop.
+    x.n_last = x.Rend - 1 + S + Split<S>::NS;
+    int n = x.R0 - (S + 1);
+    if (((x.n_last - n + 1) & 1) != 0) --n;
+    if (WAVE) wave_need(x, wv, min(n + RING - 1, x.n_last));
+#pragma unroll
+    for (int r = 0; r < RING; ++r) {
+        if (n + r <= x.n_last) stage_row(x, n + r);
+        cp_async_commit();
+    }
+    // the Neumann row H-1 matters whenever the march (cone included) reaches it
+    if (x.n_last >= a.H - 1)
+        march<S, MODE, ALIGNED, true, WAVE>(x, n, acc_u, acc_v, wv);
+    else
+        march<S, MODE, ALIGNED, false, WAVE>(x, n, acc_u, acc_v, wv);
+    cp_async_wait<0>();
+    __syncwarp();
+}
+
+// Two CTAs (8 warps) per SM: shared memory (94 KB per CTA) and registers both allow 2.
 template <int S>
 struct MinBlocks {
     static constexpr int value = 2;
@@ -391,8 +545,7 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
     k_stencil(const StencilArgs a) {
     static_assert(S >= 1 && S <= KF && KF + 3 <= PAD_R, "stage count");
     static_assert(RING + KF + 3 <= CR, "c ring too short for the stage lags");
-    constexpr int LH = lh_of(KF), WV = wv_of(KF);
-    extern __shared__ float4 smem[];  // [warps][RING][3][32] then [warps][2 CR][32]
+    extern __shared__ float4 smem[];  // [warps][RING][3][32] then [warps][CRW]
     // launched as a programmatic dependent of the previous stencil launch: nothing below may
     // run before that grid has completed (its planes, the stop flag)
     asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -411,50 +564,21 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
     x.vo = a.v_out;
     x.uo = a.u_out;
     x.mo = a.mask_out;
+    x.chk_r0 = a.chk_r0;
+    x.chk_r1 = a.chk_r1;
     x.ring = smem + warp * RING * 96 + lane;
-    x.cring = smem + STENCIL_WARPS * RING * 96 + warp * 2 * CR * 32 + lane;
+    x.cring = smem + STENCIL_WARPS * RING * 96 + warp * CRW + lane;
     // persistent warps: fetch items from this launch's queue until it is drained
+    Wave wv{};
     for (;;) {
         int it = 0;
         if (lane == 0) it = atomicAdd(a.queue, 1);
         it = __shfl_sync(0xffffffffu, it, 0);
         if (it >= n_items) break;  // warp-uniform
         const Item item = a.items[it];
-        x.R0 = item.r0;
-        x.Rend = item.r1;
-        x.col = item.strip * WV - LH + 4 * lane;
-        x.store_lane = (4 * lane >= LH) && (4 * lane < LH + WV);
-        // the Neumann column (grad_2 = 0) of every image: W - 1, or with a batch of images
-        // stacked along columns (rds_create_batch) every img_w-th column; the frame columns
-        // left of 0 give negative x.col + e, never an image-last column
-        {
-            const int iw = a.img_w;
-            auto last_col = [&](int c) { return c >= 0 && c < a.W && c % iw == iw - 1; };
-            x.right_edge = last_col(x.col + 3);
-            x.kx.a = make_float2(last_col(x.col) ? 0.0f : 1.0f, last_col(x.col + 2) ? 0.0f : 1.0f);
-            x.kx.b = make_float2(last_col(x.col + 1) ? 0.0f : 1.0f, last_col(x.col + 3) ? 0.0f : 1.0f);
-        }
-        x.p1i = a.p1_in + x.col;
-        x.p2i = a.p2_in + x.col;
-        x.vi = a.v_in + x.col;
-        x.ci = a.c + x.col;
-        // input rows [n, n_last]; the cone reaches S+1 rows up and S rows down, the delay
-        // buffer adds one row of latency.  The step count is made even (one extra warm-up
-        // row) for the two-state unrolled loop.
-        x.n_last = x.Rend - 1 + S + Split<S>::NS;
-        int n = x.R0 - (S + 1);
-        if (((x.n_last - n + 1) & 1) != 0) --n;
-#pragma unroll
-        for (int r = 0; r < RING; ++r) {
-            if (n + r <= x.n_last) stage_row(x, n + r);
-            cp_async_commit();
-        }
         float acc_u = 0.0f, acc_v = 0.0f;
-        // the Neumann row H-1 matters whenever the march (cone included) reaches it
-        if (x.n_last >= a.H - 1)
-            march<S, MODE, ALIGNED, true>(x, n, acc_u, acc_v);
-        else
-            march<S, MODE, ALIGNED, false>(x, n, acc_u, acc_v);
+        run_item<KF, S, MODE, ALIGNED, false>(x, a, item.strip, item.r0, item.r1, a.p1_in,
+                                              a.p2_in, a.v_in, acc_u, acc_v, wv);
         if (MODE == MODE_CHECK) {  // per-item partial sums, fixed lane order (deterministic)
             double su = acc_u, sv = acc_v;
 #pragma unroll
@@ -467,8 +591,6 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
                 a.chk[2 * it + 1] = sv;
             }
         }
-        cp_async_wait<0>();
-        __syncwarp();
     }
 }
 

@@ -36,6 +36,9 @@ struct NvtxRange {
 constexpr int kDefaultKF = 7, kSmallKF = 4;
 constexpr int64_t kSmallPixels = int64_t(1) << 21;
 static int default_kf(int64_t H, int64_t W) { return H * W <= kSmallPixels ? kSmallKF : kDefaultKF; }
+// k_fuse of the temporal wavefront (k_wave.cu) when none is set: 6 (the 7-stage pipeline
+// spills once the wavefront's waits are added; 6 has the same 112 output columns per strip)
+constexpr int kWaveKF = 6;
 
 }  // namespace
 
@@ -99,6 +102,13 @@ struct rds_handle {
     int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1, opt_ctas = 0;
     int opt_norm = 0;  // stopping-rule norm: 0 Euclidean over pixels, 1 RMS (R-F2)
     int opt_compact = 0;  // f3: 0 dense stencil, 1 compacted RD iteration, 2 auto (RDS_OPT_COMPACT)
+    int opt_wave = 0;     // temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto (RDS_OPT_WAVE)
+    bool wave_ok = false; // the last solve's set-up allows the wavefront (aligned, supported kf)
+    int opt_resident = 2; // small images as one resident cluster: 0 off, 1 on, 2 auto (RDS_OPT_RESIDENT)
+    int resident_fit = 0; // cached cluster schedulability for (resident_G, resident_R): 1 / -1
+    int resident_G = 0, resident_R = 0;
+    int32_t *wave_prog = nullptr;  // progress counters [blocks][strips] of k_wave
+    size_t wave_prog_bytes = 0;
     // compacted RD iteration (k_rdc.cu): index map, row counts/offsets, total, compact arrays
     int32_t *rdc_idx = nullptr, *rdc_row = nullptr, *rdc_tot = nullptr;
     void *rdc_buf = nullptr;
@@ -110,7 +120,7 @@ struct rds_handle {
     // cached CUDA graph of the K-loop
     cudaGraphExec_t graph = nullptr;
     struct Key {
-        int kf, iters, cur0, max_items, check_every, norm;
+        int kf, iters, cur0, max_items, check_every, norm, wave;
         float tau, theta, tol;
         bool operator==(const Key &o) const { return memcmp(this, &o, sizeof(Key)) == 0; }
     } gkey{};
@@ -152,7 +162,8 @@ static void free_all(rds_t *h) {
                      h->flag,    h->e_partials,  h->e_out,   h->hist,    h->scratch,
                      h->stop,    h->chk,         h->d64,     h->part64,    h->cmp_out,
                      h->lab64,   h->stop64,      h->bar64,       h->rows_buf,
-                     h->rdc_idx, h->rdc_row,     h->rdc_buf,   h->rdc_bar, h->rdc_part};  // rdc_tot points into rdc_row
+                     h->rdc_idx, h->rdc_row,     h->rdc_buf,   h->rdc_bar, h->rdc_part,
+                     h->wave_prog};  // rdc_tot points into rdc_row
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -308,6 +319,16 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             if (value < 0 || value > 2)
                 return fail(h, RDS_EINVAL, "rds_set_option: compact=%lld", (long long)value);
             h->opt_compact = (int)value;
+            return RDS_OK;
+        case RDS_OPT_RESIDENT:
+            if (value < 0 || value > 2)
+                return fail(h, RDS_EINVAL, "rds_set_option: resident=%lld", (long long)value);
+            h->opt_resident = (int)value;
+            return RDS_OK;
+        case RDS_OPT_WAVE:
+            if (value < 0 || value > 2)
+                return fail(h, RDS_EINVAL, "rds_set_option: wave=%lld", (long long)value);
+            h->opt_wave = (int)value;
             return RDS_OK;
         case RDS_OPT_STOP_NORM:
             if (value != 0 && value != 1)
@@ -542,6 +563,7 @@ struct TolParams {
     float tol = 0.0f;
     int max_iters = 0;     // K
     double norm_div = 1.0;
+    int row0 = 0, row1 = -1;  // rows the stopping sums cover (row1 < 0: every row)
 };
 
 // Enqueue plan[0..n) on h->stream starting from ping-pong buffer `cur`, using work counters
@@ -566,6 +588,8 @@ static cudaError_t enqueue_plan(rds_t *h, const LaunchPlan *plan, int n, int kf,
     a.inv_theta = 1.0f / theta;
     a.stop = tp.check_every > 0 ? h->stop : nullptr;
     a.chk = h->chk;
+    a.chk_r0 = tp.row0;
+    a.chk_r1 = tp.row1 < 0 ? (int)h->H : tp.row1;
     int prev_it = n > 0 ? plan[0].it_end - plan[0].stages : 0, prev_l = 0;
     cudaError_t e = cudaSuccess;
     for (int l = 0; l < n && e == cudaSuccess; ++l) {
@@ -604,10 +628,90 @@ static cudaError_t enqueue_plan(rds_t *h, const LaunchPlan *plan, int n, int kf,
     return e;
 }
 
+// Blocks of the temporal wavefront for a fixed-K solve of `iters` iterations: the remainder
+// K mod kf runs first as one ordinary launch, the last kf iterations as the ordinary launch
+// that writes u and the mask, and the nblk = K / kf - 1 blocks between them as ONE k_wave
+// launch.  0 when the wavefront does not apply (fewer than one middle block).
+static int wave_blocks(const rds_t *h, int kf, int iters, int check_every) {
+    if (!h->wave_ok || check_every > 0 || kf < 1) return 0;
+    const int nblk = iters / kf - 1;
+    return nblk >= 1 ? nblk : 0;
+}
+
+static int wave_strips(const rds_t *h, int kf) {
+    const int wv = wv_of(kf);
+    return (int)((h->W + wv - 1) / wv);
+}
+
+// The wavefront K-loop (k_wave.cu): remainder launch, zeroed progress counters, the k_wave
+// launch, the final u/mask launch.  Ping-pong parity is that of the ceil(K/kf)-launch plan.
+static cudaError_t enqueue_wave(rds_t *h, int kf, int iters, int nblk, int max_items,
+                                float tau, float theta) {
+    StencilArgs a{};
+    a.c = h->at(h->c);
+    a.u_out = h->at(h->u);
+    a.mask_out = h->at(h->mask);
+    a.items = h->items;
+    a.n_items = h->counts + 1;
+    a.pitch = h->pitch;
+    a.H = (int)h->H;
+    a.W = (int)h->W;
+    a.img_w = (int)h->img_w;
+    a.tau = tau;
+    a.theta = theta;
+    a.inv_theta = 1.0f / theta;
+    const int ns = wave_strips(h, kf);
+    cudaError_t e = cudaMemsetAsync(h->queue, 0, sizeof(int32_t) * 3, h->stream);
+    int cur = h->cur;
+    auto ordinary = [&](int stages, int mode, int q) {
+        a.p1_in = h->at(h->p1[cur]);
+        a.p2_in = h->at(h->p2[cur]);
+        a.v_in = h->at(h->v[cur]);
+        a.p1_out = h->at(h->p1[cur ^ 1]);
+        a.p2_out = h->at(h->p2[cur ^ 1]);
+        a.v_out = h->at(h->v[cur ^ 1]);
+        a.queue = h->queue + q;
+        int grid = h->n_sm * blocks_per_sm(h, kf, stages);
+        const int need = (max_items + STENCIL_WARPS - 1) / STENCIL_WARPS;
+        if (grid > need) grid = need;
+        cur ^= 1;
+        return launch_stencil(kf, stages, mode, a, grid, h->stream);
+    };
+    const int r = iters % kf;
+    if (e == cudaSuccess && r > 0) e = ordinary(r, 0, 0);  // mode 0: iterate
+    if (e == cudaSuccess)
+        e = cudaMemsetAsync(h->wave_prog, 0, sizeof(int32_t) * (size_t)nblk * ns, h->stream);
+    if (e == cudaSuccess) {
+        WaveArgs w{};
+        w.a = a;
+        for (int k = 0; k < 2; ++k) {
+            w.p1[k] = h->at(h->p1[k]);
+            w.p2[k] = h->at(h->p2[k]);
+            w.v[k] = h->at(h->v[k]);
+        }
+        w.band_bits = h->band_flag;
+        w.nbw = (int)(((h->H + BAND_H - 1) / BAND_H + 31) / 32);
+        w.prog = h->wave_prog;
+        w.queue = h->queue + 1;
+        w.nblk = nblk;
+        w.n_strips = ns;
+        w.c0 = cur;
+        int grid = h->n_sm * wave_blocks_per_sm(kf);
+        const int need = (nblk * ns + STENCIL_WARPS - 1) / STENCIL_WARPS;
+        if (grid > need) grid = need;
+        e = launch_wave(kf, w, grid, h->stream);
+        cur = (cur + nblk) & 1;
+    }
+    if (e == cudaSuccess) e = ordinary(kf, 1, 2);  // mode 1: + u and the mask
+    return e;
+}
+
 // Static K-loop: zero the work counters (and the stop record), then every planned launch.
 // A tolerance solve enqueued this way runs its remaining launches as immediate exits.
 static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, float tau,
                                 float theta, const TolParams &tp) {
+    const int nblk = wave_blocks(h, kf, iters, tp.check_every);
+    if (nblk > 0) return enqueue_wave(h, kf, iters, nblk, max_items, tau, theta);
     const int launches = make_plan(kf, iters, tp.check_every, nullptr, 0);
     LaunchPlan *plan = new (std::nothrow) LaunchPlan[launches > 0 ? launches : 1];
     if (!plan) return cudaErrorMemoryAllocation;
@@ -863,7 +967,14 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     if (!h->image_ok || !h->p_ok)
         return fail(h, RDS_EINVAL, "rds_solve: image or P has non-finite values");
 
-    const int kf = h->opt_kf ? h->opt_kf : default_kf(h->H, h->W);
+    // the temporal wavefront (k_wave) runs fixed-K solves when it applies: packed (aligned)
+    // columns, a k_fuse it is built for, and, in auto mode, images above the small-image
+    // size (where the launch-per-block form's item latency already binds less)
+    const int kf_wave = h->opt_kf ? h->opt_kf : kWaveKF;
+    h->wave_ok = h->opt_wave != 0 && check_every == 0 && (h->img_w & 3) == 0 &&
+                 wave_supported(kf_wave) &&
+                 (h->opt_wave == 1 || h->H * h->W > kSmallPixels);
+    const int kf = h->wave_ok ? kf_wave : (h->opt_kf ? h->opt_kf : default_kf(h->H, h->W));
     const int wv = wv_of(kf);
     const int n_strips = (int)((h->W + wv - 1) / wv);
     const int n_bands = (int)((h->H + BAND_H - 1) / BAND_H);
@@ -895,7 +1006,15 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
                 h->graph = nullptr;
             }
         }
-        if ((realloc_items || realloc_queue) && h->graph) {
+        bool realloc_prog = false;
+        if (h->wave_ok) {
+            const int nblk = wave_blocks(h, kf, iters, check_every);
+            void *pp = h->wave_prog;
+            realloc_prog = sizeof(int32_t) * (size_t)nblk * n_strips > h->wave_prog_bytes;
+            CK(h, grow(&pp, &h->wave_prog_bytes, sizeof(int32_t) * ((size_t)nblk * n_strips + 1)));
+            h->wave_prog = (int32_t *)pp;
+        }
+        if ((realloc_items || realloc_queue || realloc_prog) && h->graph) {
             cudaGraphExecDestroy(h->graph);
             h->graph = nullptr;
         }
@@ -955,7 +1074,43 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     h->cur = 0;
     if (h->opt_timing) CK(h, cudaEventRecord(h->ev[1], h->stream));
 
-    if (iters > 0 && cplan.use) {
+    // small images: the whole fixed-K loop in one resident cluster (k_small.cu) when the image
+    // fits one cluster's shared memory and such a cluster can be scheduled here
+    SmallArgs sa{};
+    bool small_use = false;
+    if (iters > 0 && !cplan.use && check_every == 0 && h->opt_resident &&
+        small_plan(h->H, h->W, &sa.G, &sa.R)) {
+        sa.p1_in = h->at(h->p1[h->cur]);
+        sa.p2_in = h->at(h->p2[h->cur]);
+        sa.v_in = h->at(h->v[h->cur]);
+        sa.c = h->at(h->c);
+        sa.p1_out = h->at(h->p1[h->cur]);
+        sa.p2_out = h->at(h->p2[h->cur]);
+        sa.v_out = h->at(h->v[h->cur]);
+        sa.u_out = h->at(h->u);
+        sa.mask_out = h->at(h->mask);
+        sa.n_rd = h->n_rd_dev;
+        sa.pitch = h->pitch;
+        sa.H = (int)h->H;
+        sa.W = (int)h->W;
+        sa.img_w = (int)h->img_w;
+        sa.K = iters;
+        sa.tau = tau;
+        sa.theta = theta;
+        sa.inv_theta = 1.0f / theta;
+        if (h->resident_G != sa.G || h->resident_R != sa.R || h->resident_fit == 0) {
+            h->resident_G = sa.G;
+            h->resident_R = sa.R;
+            h->resident_fit = small_cluster_fits(sa) ? 1 : -1;
+        }
+        small_use = h->resident_fit > 0;
+    }
+
+    if (small_use) {
+        NvtxRange nvtx_small("rds_solve (resident cluster)");
+        CK(h, launch_small(sa, h->stream));
+        h->cur0 = h->cur;  // the final state is written back into the same buffer
+    } else if (iters > 0 && cplan.use) {
         NvtxRange nvtx_rdc("rds_solve (compact RD)");
         TolParams tp;
         tp.check_every = check_every;
@@ -972,8 +1127,8 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
         tp.tol = tol;
         tp.max_iters = iters;
         tp.norm_div = h->opt_norm ? (double)h->H * (double)h->W : 1.0;
-        rds_handle::Key key{kf, iters, h->cur, max_items, check_every, h->opt_norm, tau, theta,
-                            tol};
+        rds_handle::Key key{kf,       iters,      h->cur, max_items, check_every,
+                            h->opt_norm, h->wave_ok, tau,    theta,     tol};
         if (h->opt_graph && (launches > 1 || check_every > 0)) {
             if (!h->graph || !(h->gkey == key)) {
                 if (h->graph) {
@@ -1034,8 +1189,10 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     st.n_items = (int64_t)n_strips * n_bands;
     st.iters = iters;
     st.k_fuse = kf;
-    st.launches = cplan.use ? 1 : launches;
+    st.launches = (cplan.use || small_use) ? 1 : launches;
     st.compact = cplan.use ? 1 : 0;
+    st.wave = (!cplan.use && !small_use && wave_blocks(h, kf, iters, check_every) > 0) ? 1 : 0;
+    st.resident = small_use ? 1 : 0;
     st.converged = 0;
     st.residual = -1.0f;
     st.check_every = check_every;
@@ -1145,10 +1302,16 @@ int rds_solve_continue(rds_t *h, int32_t iters) {
     const int launches = make_plan(kf, iters, 0, nullptr, 0);
     {
         void *pq = h->queue;
-        const bool realloc_queue = sizeof(int32_t) * (size_t)launches > h->queue_bytes;
-        CK(h, grow(&pq, &h->queue_bytes, sizeof(int32_t) * (size_t)launches));
+        const bool realloc_queue = sizeof(int32_t) * (size_t)(launches + 3) > h->queue_bytes;
+        CK(h, grow(&pq, &h->queue_bytes, sizeof(int32_t) * (size_t)(launches + 3)));
         h->queue = (int32_t *)pq;
-        if (realloc_queue && h->graph) {  // the cached K-loop graph points at the old counters
+        const int nblk = wave_blocks(h, kf, iters, 0);
+        void *pp = h->wave_prog;
+        const size_t pb = sizeof(int32_t) * ((size_t)nblk * wave_strips(h, kf) + 1);
+        const bool realloc_prog = nblk > 0 && pb > h->wave_prog_bytes;
+        if (nblk > 0) CK(h, grow(&pp, &h->wave_prog_bytes, pb));
+        h->wave_prog = (int32_t *)pp;
+        if ((realloc_queue || realloc_prog) && h->graph) {  // the cached graph points at them
             cudaGraphExecDestroy(h->graph);
             h->graph = nullptr;
         }
@@ -1168,6 +1331,74 @@ int rds_solve_continue(rds_t *h, int32_t iters) {
     h->stats.converged = 0;
     h->stats.residual = -1.0f;
     h->stats.check_every = 0;
+    return RDS_OK;
+}
+
+int rds_continue_check(rds_t *h, int32_t iters, int64_t row0, int64_t row1, double *sums) {
+    NEED_SOLVED("rds_continue_check");
+    if (iters < 1) return fail(h, RDS_EINVAL, "rds_continue_check: iters=%d must be >= 1", iters);
+    if (!sums) return fail(h, RDS_EINVAL, "rds_continue_check: NULL sums");
+    if (row0 < 0 || row1 > h->H || row0 > row1)
+        return fail(h, RDS_EINVAL, "rds_continue_check: rows [%lld, %lld) outside [0, %lld)",
+                    (long long)row0, (long long)row1, (long long)h->H);
+    if (h->tol_pending) {  // a tolerance solve's state: bring its outcome to the host first
+        const int rc = resolve(h);
+        if (rc) return rc;
+    }
+    const int kf = h->last_kf;
+    const int launches = make_plan(kf, iters, iters, nullptr, 0);
+    {
+        void *pq = h->queue, *pc = h->chk;
+        const bool realloc_queue = sizeof(int32_t) * (size_t)launches > h->queue_bytes;
+        CK(h, grow(&pq, &h->queue_bytes, sizeof(int32_t) * (size_t)launches));
+        h->queue = (int32_t *)pq;
+        const bool realloc_chk = 2 * sizeof(double) * (size_t)h->last_max_items > h->chk_bytes;
+        CK(h, grow(&pc, &h->chk_bytes, 2 * sizeof(double) * (size_t)h->last_max_items));
+        h->chk = (double *)pc;
+        if (!h->stop) CK(h, cudaMalloc(&h->stop, sizeof(StopRecord)));
+        if ((realloc_queue || realloc_chk) && h->graph) {
+            cudaGraphExecDestroy(h->graph);
+            h->graph = nullptr;
+        }
+    }
+    NvtxRange nvtx("rds_continue_check");
+    TolParams tp;
+    tp.check_every = iters;  // one check, after the last iteration
+    tp.tol = -1.0f;          // never "converged": only the sums are wanted
+    tp.max_iters = iters;
+    tp.row0 = (int)row0;
+    tp.row1 = (int)row1;
+    CK(h, enqueue_loop(h, kf, iters, h->last_max_items, h->last_tau, h->theta, tp));
+    StopRecord rec{};
+    CK(h, cudaMemcpyAsync(&rec, h->stop, sizeof rec, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    if (launches & 1) h->cur ^= 1;
+    sums[0] = rec.su;
+    sums[1] = rec.sv;
+    h->stats.iters += iters;
+    h->stats.launches += launches;
+    return RDS_OK;
+}
+
+int rds_abs_histogram(rds_t *h, int64_t row0, int64_t row1, uint32_t prefix, uint32_t mask,
+                      int32_t shift, uint32_t *out) {
+    if (!h || !out) return fail(h, RDS_EINVAL, "rds_abs_histogram: NULL argument");
+    if (!h->have_image || !h->have_fitting || !h->image_ok || !h->p_ok)
+        return fail(h, RDS_ESTATE, "rds_abs_histogram: image and fitting must be set");
+    if (row0 < 0 || row1 > h->H || row0 > row1 || (shift != 0 && shift != 8 && shift != 16 &&
+                                                   shift != 24))
+        return fail(h, RDS_EINVAL, "rds_abs_histogram: rows [%lld, %lld) or shift %d invalid",
+                    (long long)row0, (long long)row1, shift);
+    if (!h->hist) CK(h, cudaMalloc(&h->hist, sizeof(unsigned) * 256));
+    CK(h, cudaMemsetAsync(h->hist, 0, sizeof(unsigned) * 256, h->stream));
+    if (row1 > row0)
+        CK(h, launch_abs_hist(h->at(h->z) + row0 * h->pitch,
+                              h->gamma != 0.0f ? h->at(h->P) + row0 * h->pitch : nullptr,
+                              h->pitch, (int)(row1 - row0), (int)h->W, h->c1, h->c2, h->gamma,
+                              prefix, mask, shift, h->hist, h->stream));
+    CK(h, cudaMemcpyAsync(out, h->hist, sizeof(unsigned) * 256, cudaMemcpyDeviceToHost,
+                          h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
     return RDS_OK;
 }
 

@@ -25,6 +25,8 @@ RDS_OPT_KFUSE, RDS_OPT_ITEM_ROWS, RDS_OPT_TIMING, RDS_OPT_SKIP, RDS_OPT_GRAPH = 
 RDS_OPT_CTAS_PER_SM = 6
 RDS_OPT_STOP_NORM = 7  # 0 Euclidean over pixels (default), 1 RMS
 RDS_OPT_COMPACT = 8    # f3: 0 dense stencil (default), 1 compacted RD iteration, 2 auto
+RDS_OPT_WAVE = 9       # temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto
+RDS_OPT_RESIDENT = 10  # small images as one resident cluster: 0 off, 1 / 2 (default) on
 
 EXPORTS = (
     "rds_create", "rds_create_batch", "rds_destroy", "rds_set_stream", "rds_set_option",
@@ -35,7 +37,7 @@ EXPORTS = (
     "rds_kfuse_supported", "rds_last_error", "rds_version", "rds_band_for_fraction",
     "rds_solve_q", "rds_solve_tol", "rds_solve_gt", "rds_get_u_gt", "rds_compare_gt",
     "rds_check_frame", "rds_solve_continue", "rds_get_state_rows", "rds_set_state_rows",
-    "rds_set_energy_rows",
+    "rds_set_energy_rows", "rds_continue_check", "rds_abs_histogram",
     "rds3_create", "rds3_destroy", "rds3_set_stream", "rds3_set_kz", "rds3_set_image",
     "rds3_set_fitting",
     "rds3_fitting_absmax", "rds3_solve", "rds3_get_u", "rds3_get_v", "rds3_get_p",
@@ -75,7 +77,8 @@ class rds_stats_t(ctypes.Structure):
                 ("item_cols", ctypes.c_int32), ("converged", ctypes.c_int32),
                 ("setup_ms", ctypes.c_float), ("loop_ms", ctypes.c_float),
                 ("residual", ctypes.c_float), ("check_every", ctypes.c_int32),
-                ("compact", ctypes.c_int32)]
+                ("compact", ctypes.c_int32), ("wave", ctypes.c_int32),
+                ("resident", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -122,6 +125,9 @@ def _load():
         "rds_get_state_rows": [P, i64, i64, P, i],
         "rds_set_state_rows": [P, i64, i64, P, i],
         "rds_set_energy_rows": [P, i64, i64],
+        "rds_continue_check": [P, i32, i64, i64, ctypes.POINTER(ctypes.c_double)],
+        "rds_abs_histogram": [P, i64, i64, ctypes.c_uint32, ctypes.c_uint32, i32,
+                              ctypes.POINTER(ctypes.c_uint32)],
         "rds3_create": [i64, i64, i64, ctypes.POINTER(P)],
         "rds3_destroy": [P],
         "rds3_set_stream": [P, P],
@@ -290,6 +296,21 @@ def rds_set_energy_rows(h, row0, row1):
     _check(_lib.rds_set_energy_rows(h, int(row0), int(row1)), h)
 
 
+def rds_continue_check(h, iters, row0, row1):
+    """(sum du^2, sum dv^2) of the last of `iters` continued iterations over rows [row0, row1)."""
+    out = (ctypes.c_double * 2)()
+    _check(_lib.rds_continue_check(h, int(iters), int(row0), int(row1), out), h)
+    return out[0], out[1]
+
+
+def rds_abs_histogram(h, row0, row1, prefix, mask, shift):
+    """256 counts of byte `shift` of |f|'s bit pattern over rows [row0, row1) (radix pass)."""
+    out = (ctypes.c_uint32 * 256)()
+    _check(_lib.rds_abs_histogram(h, int(row0), int(row1), int(prefix), int(mask), int(shift),
+                                  out), h)
+    return np.frombuffer(out, dtype=np.uint32).copy()
+
+
 def _get(fn, h, out, dtype, shape):
     p, dev, _keep = _buf(out, dtype, shape, writable=True)
     _check(fn(h, p, dev), h)
@@ -376,7 +397,7 @@ class Solver:
     """One librds handle for an H x W image.  Host (numpy) or device (torch) buffers."""
 
     def __init__(self, H, W, stream=None, k_fuse=0, item_rows=0, timing=False, skip=True,
-                 graph=True, batch=None, compact=0):
+                 graph=True, batch=None, compact=0, wave=None, resident=None):
         self.shape = (int(H) * (int(batch) if batch else 1), int(W))
         if batch is not None:
             h = ctypes.c_void_p()
@@ -395,6 +416,10 @@ class Solver:
         rds_set_option(self.h, RDS_OPT_GRAPH, int(graph))
         if compact:
             rds_set_option(self.h, RDS_OPT_COMPACT, int(compact))
+        if wave is not None:
+            rds_set_option(self.h, RDS_OPT_WAVE, int(wave))
+        if resident is not None:
+            rds_set_option(self.h, RDS_OPT_RESIDENT, int(resident))
 
     def close(self):
         if self.h is not None:
@@ -455,6 +480,15 @@ class Solver:
 
     def set_energy_rows(self, row0, row1=-1):
         rds_set_energy_rows(self.h, row0, row1)
+
+    def continue_check(self, iters, row0, row1):
+        """`iters` more iterations; returns the stopping-rule sums (du^2, dv^2) of the last one
+        over rows [row0, row1) (row strips: all-reduce them, strips.StripSolver.solve_tol)."""
+        return rds_continue_check(self.h, iters, row0, row1)
+
+    def abs_histogram(self, row0, row1, prefix, mask, shift):
+        """One radix pass of the q -> q^ search over rows [row0, row1) (256 counts)."""
+        return rds_abs_histogram(self.h, row0, row1, prefix, mask, shift)
 
     def solve_tol(self, lam, theta, tau, delta, max_iters, tol, check_every=0):
         """Stop at the first check (every check_every iterations, and at max_iters) where

@@ -121,6 +121,125 @@ def solve_local(engines, plan, lam, theta, tau, delta, iters, seg_iters, device=
             e.solve_continue(it)
 
 
+# ---- the paper's q -> q^ knob and stopping rule on a strip-decomposed image ----------------
+# Both are global quantities (q^ is set by the fraction of ALL pixels;
+# the norms run over the whole image), so every strip contributes its owned
+# rows and the ranks combine them before a common decision.  The combination step is passed
+# in (`allreduce`), so the same code runs over torch.distributed (StripSolver) and for several
+# strip handles on one device (the *_local forms used by the tests).
+
+def band_from_histograms(q, N, hist_pass):
+    """q -> q^ as rds_band_for_fraction computes it: the smallest float32 q^ with
+    #{|f| < q^} >= k = ceil(q N), i.e. the next float above the k-th smallest |f| (ties at the
+    k-th value join RD).  `hist_pass(prefix, mask, shift)` returns the 256-bin histogram of
+    byte `shift` of the |f| bit patterns matching `prefix` under `mask`, summed over the whole
+    image; four passes from the top byte down find the k-th smallest bit pattern."""
+    import math
+
+    k = int(math.ceil(q * float(N)))
+    k = min(k, N)
+    if k <= 0:
+        return np.float32(0.0)
+    prefix, mask, rank = 0, 0, k
+    for shift in (24, 16, 8, 0):
+        hh = np.asarray(hist_pass(prefix, mask, shift), dtype=np.int64)
+        c = np.cumsum(hh)
+        d = int(np.searchsorted(c, rank))  # first bin whose cumulative count reaches rank
+        if d >= 256:
+            raise RuntimeError("histogram inconsistent")
+        rank -= int(c[d - 1]) if d > 0 else 0
+        prefix |= d << shift
+        mask |= 255 << shift
+    a = np.array([prefix], dtype=np.uint32).view(np.float32)[0]
+    return np.nextafter(a, np.float32(np.inf), dtype=np.float32)
+
+
+def tolerance_loop(run, allreduce, max_iters, tol, check_every, norm_div):
+    """The stopping rule of PAPER.md:234-238 over strips: checks after iterations m, 2m, ...
+    and at max_iters (m = check_every, reading R-F2), each on the all-reduced sums of the
+    strips' owned rows.  `run(n, check)` advances every strip by n iterations (exchanging
+    halos as it must) and, if check, returns this rank's (sum du^2, sum dv^2) of the last one.
+    Returns dict(iters, residual, converged)."""
+    import math
+
+    done, r = 0, -1.0
+    while done < max_iters:
+        block = min(check_every, max_iters - done)
+        su, sv = allreduce(run(block, True))
+        done += block
+        r = max(math.sqrt(su / norm_div), math.sqrt(sv / norm_div))
+        if r <= tol:
+            return dict(iters=done, residual=r, converged=1)
+    return dict(iters=done, residual=r, converged=0)
+
+
+def _chunks(n, seg_iters):
+    """A block of n iterations as segments of at most seg_iters (a halo refresh before each
+    but the first of the solve)."""
+    out = []
+    while n > 0:
+        out.append(min(seg_iters, n))
+        n -= out[-1]
+    return out
+
+
+def band_for_fraction_local(engines, plan, q, H, W):
+    """q -> q^ of the whole image from strip handles on one device (histograms summed)."""
+    def hist_pass(prefix, mask, shift):
+        return sum(e.abs_histogram(st.owned.start, st.owned.stop, prefix, mask, shift)
+                   .astype(np.int64) for st, e in zip(plan, engines))
+    return band_from_histograms(q, H * W, hist_pass)
+
+
+def solve_tol_local(engines, plan, lam, theta, tau, delta, max_iters, tol, check_every,
+                    seg_iters, norm="l2"):
+    """The tolerance solve of a strip-decomposed image with all strips in one process
+    (exchange through host buffers, sums added in rank order)."""
+    xplan = exchange_plan(plan)
+    state = {"started": False}
+
+    def exchange():
+        bufs = [(d, dr, engines[s].state_rows(sr, m)) for s, sr, d, dr, m in xplan]
+        for d, dr, buf in bufs:
+            engines[d].set_state_rows(dr, buf)
+
+    def run(n, check):
+        chunks = _chunks(n, seg_iters)
+        sums = None
+        for k, it in enumerate(chunks):
+            sums = _advance(engines, plan, state, exchange, lam, theta, tau, delta, it,
+                            check and k == len(chunks) - 1)
+        return sums
+
+    def allreduce(parts):
+        return tuple(float(sum(p[i] for p in parts)) for i in range(2))
+
+    H = sum(st.hi - st.lo for st in plan)
+    W = engines[0].shape[1]
+    return tolerance_loop(run, allreduce, max_iters, tol, check_every,
+                          float(H * W) if norm == "rms" else 1.0)
+
+
+def _advance(engines, plan, state, exchange, lam, theta, tau, delta, it, check):
+    """Advance this process's strips (`engines`, their `plan` entries) by `it` iterations: the
+    solve's first segment sets up, later ones refresh the halos first.  With check, return
+    every strip's owned-row sums (du^2, dv^2) of the last iteration."""
+    if not state["started"]:
+        for e in engines:
+            e.solve(lam, theta, tau, delta, it - 1 if check else it)
+        state["started"] = True
+        if not check:
+            return None
+        it = 1  # the checked iteration continues the first segment (no refresh needed)
+    else:
+        exchange()
+    if not check:
+        for e in engines:
+            e.solve_continue(it)
+        return None
+    return [e.continue_check(it, st.owned.start, st.owned.stop) for st, e in zip(plan, engines)]
+
+
 class StripSolver:
     """This rank's strip of an H x W image, one process per GPU (torch.distributed
     initialised by the caller).  `engine` defaults to an `rds.Solver` on torch's current
@@ -205,6 +324,48 @@ class StripSolver:
             else:
                 self._exchange()
                 self.engine.solve_continue(it)
+
+    def band_for_fraction(self, q):
+        """q -> q^ over the WHOLE image: each rank's radix-select histogram
+        of its owned rows, all-reduced per pass -- the same q^ as rds_band_for_fraction on the
+        whole image."""
+        torch, dist = self.torch, self.dist
+
+        def hist_pass(prefix, mask, shift):
+            h = self.engine.abs_histogram(self.me.owned.start, self.me.owned.stop, prefix, mask,
+                                          shift)
+            t = torch.as_tensor(np.asarray(h, np.int64), device=self.device)
+            dist.all_reduce(t, group=self.group)
+            return t.cpu().numpy()
+
+        return band_from_histograms(q, self.H * self.W, hist_pass)
+
+    def solve_q(self, lam, theta, tau, q, iters):
+        self.solve(lam, theta, tau, self.band_for_fraction(q), iters)
+
+    def solve_tol(self, lam, theta, tau, delta, max_iters, tol, check_every, norm="l2"):
+        """The paper's stopping rule on the strip-decomposed image: checks
+        after every check_every iterations and at max_iters, each deciding on the all-reduced
+        owned-row sums, so every rank stops at the same iteration as a whole-image solve
+        (reading R-F2: Euclidean norm, or "rms").  Returns dict(iters, residual, converged)."""
+        torch, dist = self.torch, self.dist
+        state = {"started": False}
+
+        def run(n, check):
+            chunks = _chunks(n, self.seg_iters)
+            sums = None
+            for k, it in enumerate(chunks):
+                sums = _advance([self.engine], [self.me], state, self._exchange, lam, theta,
+                                tau, delta, it, check and k == len(chunks) - 1)
+            return sums[0] if sums else None
+
+        def allreduce(s):
+            t = torch.tensor([float(s[0]), float(s[1])], dtype=torch.float64, device=self.device)
+            dist.all_reduce(t, group=self.group)
+            return tuple(t.tolist())
+
+        return tolerance_loop(run, allreduce, int(max_iters), float(tol), int(check_every),
+                              float(self.H * self.W) if norm == "rms" else 1.0)
 
     # -- outputs: owned rows ----------------------------------------------------------------
     def u(self):

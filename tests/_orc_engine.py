@@ -44,6 +44,25 @@ class OracleEngine:
         for k, name in enumerate(("v", "p1", "p2")):
             self.st[name][r0:r0 + buf.shape[1]] = buf[k]
 
+    def continue_check(self, iters, r0, r1):
+        """rds_continue_check: `iters` more iterations, then the stopping-rule sums of the
+        last one over rows [r0, r1)."""
+        if iters > 1:
+            self.solve_continue(iters - 1)
+        up, vp = self.st["u"].copy(), self.st["v"].copy()
+        self.solve_continue(1)
+        du = self.st["u"][r0:r1] - up[r0:r1]
+        dv = self.st["v"][r0:r1] - vp[r0:r1]
+        return float(np.sum(du * du)), float(np.sum(dv * dv))
+
+    def abs_histogram(self, r0, r1, prefix, mask, shift):
+        """rds_abs_histogram: byte `shift` of the |f| bit patterns of rows [r0, r1) matching
+        prefix under mask."""
+        b = np.abs(self.f[r0:r1]).view(np.uint32).ravel()
+        b = b[(b & np.uint32(mask)) == np.uint32(prefix)]
+        return np.bincount((b >> np.uint32(shift)) & np.uint32(255), minlength=256).astype(
+            np.int64)
+
     def u(self):
         return self.st["u"]
 

@@ -197,15 +197,19 @@ def test_c4_full_size(rds, orc, c4, dr):
 SHAPES = [(1, 1), (1, 7), (9, 1), (5, 3), (33, 129), (100, 77), (130, 250), (257, 131)]
 
 
+@pytest.mark.parametrize("resident", [0, 2])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_ragged_shapes(rds, orc, shape):
+def test_ragged_shapes(rds, orc, shape, resident):
+    """(resident = 0: the stencil; 2: the library default, the resident cluster where the
+    shape fits one)"""
     H, W = shape
     z = wl.random_image(H, W, seed=H * 1000 + W)
     for dr in (0.0, 0.3, math.inf):
         f = orc.fitting(z, 0.8, 0.2)
         delta = wl.band_delta(dr, orc.absmax(f))
         for iters in (1, 8, 23):
-            g = gpu_solve(rds, z, None, 0.8, 0.2, 0.0, 5.0, 0.1, 0.125, delta, iters)
+            g = gpu_solve(rds, z, None, 0.8, 0.2, 0.0, 5.0, 0.1, 0.125, delta, iters,
+                          resident=resident)
             o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, iters)
             assert np.array_equal(g["labels"], o["labels"])
             compare(g, o, tol=1e-5, mask_frac=0.0 if H * W < 2000 else MASK_FRAC,
@@ -222,7 +226,7 @@ def test_every_fusion_depth(rds, orc, kf):
     delta = wl.band_delta(0.4, orc.absmax(f))
     for iters in (kf, 2 * kf + 1, 3 * kf + kf - 1):
         g = gpu_solve(rds, z, None, 0.75, 0.25, 0.0, 2.0, 0.1, 0.125, delta, iters, k_fuse=kf,
-                      item_rows=40)
+                      item_rows=40, resident=0)
         o = orc.solve(f, delta, 2.0, np.float32(0.1), 0.125, iters)
         compare(g, o, tol=1e-5, ctx=f"kf={kf} K={iters}")
 
@@ -238,7 +242,7 @@ def test_warm_start_random_state(rds, orc):
         delta = wl.band_delta(dr, orc.absmax(f))
         for iters in (1, 2, 9):
             g = gpu_solve(rds, z, None, 0.8, 0.2, 0.0, 5.0, 0.1, 0.125, delta, iters,
-                          init=(v, p1, p2))
+                          init=(v, p1, p2), resident=0)
             o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, iters,
                           init=(v.astype(np.float64), p1.astype(np.float64),
                                 p2.astype(np.float64)))
@@ -290,13 +294,14 @@ def test_skip_equivalence_and_determinism(rds):
 # configs at their stated sizes / iteration counts
 # ------------------------------------------------------------------------------------------
 
-def _run_cfg(rds, orc, name, lam, dr, iters=None):
+def _run_cfg(rds, orc, name, lam, dr, iters=None, **opt):
     cfg = wl.CONFIGS[name]
     z, P = wl.make_image(cfg)
     f = orc.fitting(z, cfg.c1, cfg.c2, cfg.gamma, P)
     delta = wl.band_delta(dr, orc.absmax(f))
     K = cfg.iters if iters is None else iters
-    g = gpu_solve(rds, z, P, cfg.c1, cfg.c2, cfg.gamma, lam, cfg.theta, cfg.tau, delta, K)
+    g = gpu_solve(rds, z, P, cfg.c1, cfg.c2, cfg.gamma, lam, cfg.theta, cfg.tau, delta, K,
+                  **opt)
     o = orc.solve(f, delta, lam, np.float32(cfg.theta), cfg.tau, K)
     assert np.array_equal(g["labels"], o["labels"])
     assert np.array_equal(g["tiles"], orc.tiles(o["labels"], 32, 32))
@@ -304,9 +309,11 @@ def _run_cfg(rds, orc, name, lam, dr, iters=None):
     return g, o
 
 
+@pytest.mark.parametrize("resident", [0, 2])
 @pytest.mark.parametrize("dr", [0.2, math.inf])
-def test_c0(rds, orc, dr):
-    g, o = _run_cfg(rds, orc, "C0", 5.0, dr)
+def test_c0(rds, orc, dr, resident):
+    g, o = _run_cfg(rds, orc, "C0", 5.0, dr, resident=resident)
+    assert g["stats"]["resident"] == (1 if resident else 0)
 
 
 @pytest.mark.parametrize("lam,dr", [(5.0, 0.05), (5.0, 0.1), (5.0, 0.2), (5.0, 0.4),

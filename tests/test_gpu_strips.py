@@ -202,3 +202,85 @@ def test_torch_default_stream(rds):
         torch.cuda.synchronize()
     assert a.elapsed_time(b) > 0.05
     assert np.array_equal(s.u(), ref.u())
+
+
+@pytest.mark.parametrize("G,s,m,tol,norm", [(3, 7, 10, 2e-2, "l2"), (4, 5, 7, 3e-4, "rms"),
+                                            (2, 14, 14, 5e-2, "l2")])
+def test_strips_global_q_and_stop(rds, orc, G, s, m, tol, norm):
+    """The paper's q -> q^ knob and stopping rule on a strip-decomposed image (PAPER.md:74-84,
+    234-238): summed radix histograms of the strips' owned rows give the whole image's q^
+    bit for bit, and the tolerance solve over strips (owned-row sums of rds_continue_check,
+    added over strips) stops at the iteration of the whole-image fp64 oracle, with the
+    whole-image GPU state on every owned row."""
+    cfg = wl.CONFIGS["C1"]
+    z, P = wl.make_image(cfg)
+    z = z[:300, :257].copy()
+    H, W = z.shape
+    f = orc.fitting(z, cfg.c1, cfg.c2)
+    plan = strips.partition(H, G, s)
+    engines = []
+    for st in plan:
+        e = rds.Solver(st.rows, W)
+        e.set_image(z[st.r0:st.r0 + st.rows])
+        e.set_fitting(cfg.c1, cfg.c2)
+        engines.append(e)
+    for q in (0.0, 0.02, 0.3, 1.0):
+        assert strips.band_for_fraction_local(engines, plan, q, H, W) == \
+            orc.band_for_fraction(f, q), q
+    delta = orc.band_for_fraction(f, 0.3)
+    st = strips.solve_tol_local(engines, plan, 5.0, cfg.theta, cfg.tau, delta, 600, tol, m, s,
+                                norm)
+    ref = orc.solve_tol(f, delta, 5.0, np.float32(cfg.theta), cfg.tau, 600, tol, m, norm)
+    assert st["iters"] == ref["iters"] and st["converged"] == ref["converged"], (st, ref["iters"])
+    assert abs(st["residual"] - ref["residual"]) <= 2e-2 * ref["residual"]
+    whole = rds.Solver(H, W, resident=0)
+    whole.set_image(z)
+    whole.set_fitting(cfg.c1, cfg.c2)
+    whole.solve(5.0, cfg.theta, cfg.tau, delta, st["iters"])
+    want = _state(whole)
+    for stp, e in zip(plan, engines):
+        got = _state(e)
+        for k in ("u", "v", "p1", "p2"):
+            assert np.array_equal(got[k][stp.owned], want[k][stp.lo:stp.hi]), (stp.rank, k)
+        e.close()
+
+
+def test_abs_histogram_and_continue_check(rds, orc):
+    """rds_abs_histogram over a row range equals numpy's count of the |f| bit bytes, and
+    rds_continue_check's sums equal (u^l - u^(l-1))^2, (v^l - v^(l-1))^2 summed over the rows
+    (from two fixed-K solves of the same handle shape)."""
+    H, W = 90, 70
+    z = _image(H, W, 4)
+    s = rds.Solver(H, W, resident=0)
+    s.set_image(z)
+    s.set_fitting(0.8, 0.2)
+    f = orc.fitting(z, 0.8, 0.2)
+    b = np.abs(f).view(np.uint32)
+    for r0, r1, prefix, mask, shift in ((0, H, 0, 0, 24), (13, 57, 0x3e000000, 0xff000000, 16),
+                                        (40, 41, 0, 0, 0), (5, 5, 0, 0, 8)):
+        h = s.abs_histogram(r0, r1, prefix, mask, shift)
+        sel = b[r0:r1].ravel()
+        sel = sel[(sel & np.uint32(mask)) == np.uint32(prefix)]
+        want = np.bincount((sel >> np.uint32(shift)) & np.uint32(255), minlength=256)
+        assert np.array_equal(h, want), (r0, r1, prefix, mask, shift)
+    delta = np.float32(0.4 * float(orc.absmax(f)))
+    s.solve(5.0, 0.1, 0.125, delta, 11)
+    ua, va = s.u().astype(np.float64), s.v().astype(np.float64)
+    su, sv = s.continue_check(1, 20, 71)
+    ub, vb = s.u().astype(np.float64), s.v().astype(np.float64)
+    assert su == pytest.approx(((ub - ua)[20:71] ** 2).sum(), rel=1e-6)
+    assert sv == pytest.approx(((vb - va)[20:71] ** 2).sum(), rel=1e-6)
+    ref = rds.Solver(H, W, resident=0)
+    ref.set_image(z)
+    ref.set_fitting(0.8, 0.2)
+    ref.solve(5.0, 0.1, 0.125, delta, 12)
+    assert np.array_equal(ref.u(), s.u()) and np.array_equal(ref.v(), s.v())
+    s.continue_check(9, 0, H)   # a multi-launch block
+    ref.solve_continue(9)
+    assert np.array_equal(ref.u(), s.u()) and np.array_equal(ref.v(), s.v())
+    with pytest.raises(rds.RdsError):
+        s.continue_check(0, 0, H)
+    with pytest.raises(rds.RdsError):
+        s.abs_histogram(0, H + 1, 0, 0, 24)
+    s.close()
+    ref.close()

@@ -93,3 +93,32 @@ def test_strips_need_the_halo(orc):
     engines = _strip_solve(z, short, (0.8, 0.2), np.float32(np.inf), K, s, (5.0, 0.1, 0.125))
     st, e = short[1], engines[1]
     assert not np.array_equal(e.st["u"][st.owned], ref["u"][st.lo:st.hi])
+
+
+@pytest.mark.parametrize("G,s", [(2, 4), (3, 2), (4, 5)])
+def test_local_q_and_tolerance(orc, G, s):
+    """One process, G strip engines (the oracle): the summed radix histograms give the whole
+    image's q^, and the strip tolerance solve stops where the whole-image oracle does, with
+    its state on every owned row."""
+    H, W = 61, 27
+    z = wl.gen_voronoi(N=61, seed=G * 10 + s, n_sites=8)[:H, :W].copy()
+    f = orc.fitting(z, 0.8, 0.2)
+    plan = strips.partition(H, G, s)
+    engines = []
+    for st in plan:
+        e = OracleEngine(st.rows, W)
+        e.set_image(z[st.r0:st.r0 + st.rows])
+        e.set_fitting(0.8, 0.2)
+        engines.append(e)
+    for q in (0.0, 0.05, 0.5, 0.999, 1.0):
+        assert strips.band_for_fraction_local(engines, plan, q, H, W) == \
+            orc.band_for_fraction(f, q), q
+    delta = orc.band_for_fraction(f, 0.45)
+    for m, tol, norm in ((5, 2e-3, "l2"), (3, 1e-4, "rms")):
+        st = strips.solve_tol_local(engines, plan, 5.0, 0.1, 0.125, delta, 150, tol, m, s,
+                                    norm)
+        ref = orc.solve_tol(f, delta, 5.0, 0.1, 0.125, 150, tol, m, norm)
+        assert st["iters"] == ref["iters"], (m, st, ref["iters"])
+        assert abs(st["residual"] - ref["residual"]) <= 1e-12 * max(ref["residual"], 1e-300)
+        for stp, e in zip(plan, engines):
+            assert np.array_equal(e.u()[stp.owned], ref["u"][stp.lo:stp.hi])
