@@ -92,6 +92,7 @@ typedef struct {
     int32_t compact;         /* 1 if the last solve ran the compacted RD iteration (RDS_OPT_COMPACT) */
     int32_t wave;            /* 1 if the last solve's K-loop ran as the temporal wavefront (RDS_OPT_WAVE) */
     int32_t resident;        /* 1 if the last solve ran as one resident cluster (RDS_OPT_RESIDENT) */
+    int32_t persist;         /* 1 if the last solve's K-loop ran as one persistent launch (RDS_OPT_PERSIST) */
 } rds_stats_t;
 
 /* Options (rds_set_option). */
@@ -148,6 +149,18 @@ typedef struct {
                                 fit 200 KB of shared memory per CTA (about 300 x 300 pixels) and
                                 the cluster can be scheduled; tolerance solves stay on the
                                 stencil.  0 = off; 1 and 2 (default) = on where it applies. */
+
+#define RDS_OPT_PERSIST 11   /* the K-loop of a fixed-K solve as ONE persistent launch of the
+                                stencil (k_loop.cu): the K / k_fuse blocks run inside one
+                                cooperative grid separated by a grid barrier (or, for <= 16
+                                CTAs, the hardware cluster barrier) instead of one launch each;
+                                the remainder K mod k_fuse runs as one ordinary launch before.
+                                Same per-pixel operations (bit-identical results).  0 (default)
+                                = off, 1 = on where it applies (image widths a multiple of 4,
+                                k_fuse 4..7, at least two full blocks), 2 = on for images up to
+                                2^22 pixels.  Off by default: on B200 the launches are not what
+                                bounds these sizes (C0 0.44 vs 0.46 ms, 256^2..2048^2 2-6%
+                                slower; the item march's row latency is). */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */

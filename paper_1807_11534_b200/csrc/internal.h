@@ -141,10 +141,10 @@ int wave_blocks_per_sm(int kf);
 bool wave_supported(int kf);
 
 // Small images as one resident cluster (k_small.cu): G slabs of R rows, one CTA
-// each, the whole fixed-K loop in one launch.  Reads the state from the dense ping-pong buffer
-// *_in, writes the final state into *_out and u / the mask of the last iteration.
-constexpr int SMALL_THREADS = 512, SMALL_MAX_CTAS = 16;
-constexpr size_t SMALL_MAX_SMEM = 200 * 1024;
+// each (one thread per column), the whole fixed-K loop in one launch.  Reads the state from the
+// dense ping-pong buffer *_in, writes the final state into *_out and u / the mask of the last
+// iteration.
+constexpr int SMALL_THREADS_MAX = 1024, SMALL_MAX_CTAS = 16;
 struct SmallArgs {
     const float *p1_in, *p2_in, *v_in, *c;   // plane origins (pixel (0,0)), swizzled
     float *p1_out, *p2_out, *v_out;
@@ -158,6 +158,20 @@ struct SmallArgs {
 bool small_plan(int64_t H, int64_t W, int *G, int *R);
 bool small_cluster_fits(const SmallArgs &a);
 cudaError_t launch_small(const SmallArgs &a, cudaStream_t s);
+
+// The fixed-K K-loop as one persistent launch (k_loop.cu): nblk blocks of KF
+// iterations over the same work items, block b reading ping-pong buffer (c0 + b) & 1, a grid
+// (or cluster) barrier between blocks, the last block writing u and the mask.
+struct LoopArgs {
+    StencilArgs a;                       // c, u / mask, items, n_items, pitch, H, W, img_w, ...
+    const float *p1[2], *p2[2], *v[2];   // ping-pong plane origins
+    int32_t *queue;                      // [nblk] per-block item counters, zeroed
+    unsigned long long *bar;             // grid-barrier counter (zeroed by the launcher)
+    int nblk, c0;
+};
+bool loop_supported(int kf);
+int loop_blocks_per_sm(int kf);
+cudaError_t launch_loop(int kf, const LoopArgs &L, int grid, cudaStream_t s);
 
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_fill_frame(float *plane, int64_t n, float value, cudaStream_t s);

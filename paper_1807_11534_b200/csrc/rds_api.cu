@@ -39,6 +39,8 @@ static int default_kf(int64_t H, int64_t W) { return H * W <= kSmallPixels ? kSm
 // k_fuse of the temporal wavefront (k_wave.cu) when none is set: 6 (the 7-stage pipeline
 // spills once the wavefront's waits are added; 6 has the same 112 output columns per strip)
 constexpr int kWaveKF = 6;
+// images up to this size run fixed-K solves as one persistent launch (k_loop) by default
+constexpr int64_t kPersistPixels = int64_t(1) << 22;
 
 }  // namespace
 
@@ -105,6 +107,9 @@ struct rds_handle {
     int opt_wave = 0;     // temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto (RDS_OPT_WAVE)
     bool wave_ok = false; // the last solve's set-up allows the wavefront (aligned, supported kf)
     int opt_resident = 2; // small images as one resident cluster: 0 off, 1 on, 2 auto (RDS_OPT_RESIDENT)
+    int opt_persist = 0;  // fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto (RDS_OPT_PERSIST)
+    bool persist_ok = false;  // the last solve's set-up allows it (aligned, supported kf, size)
+    unsigned long long *loop_bar = nullptr;  // grid-barrier counter of k_loop
     int resident_fit = 0; // cached cluster schedulability for (resident_G, resident_R): 1 / -1
     int resident_G = 0, resident_R = 0;
     int32_t *wave_prog = nullptr;  // progress counters [blocks][strips] of k_wave
@@ -163,7 +168,7 @@ static void free_all(rds_t *h) {
                      h->stop,    h->chk,         h->d64,     h->part64,    h->cmp_out,
                      h->lab64,   h->stop64,      h->bar64,       h->rows_buf,
                      h->rdc_idx, h->rdc_row,     h->rdc_buf,   h->rdc_bar, h->rdc_part,
-                     h->wave_prog};  // rdc_tot points into rdc_row
+                     h->wave_prog, h->loop_bar};  // rdc_tot points into rdc_row
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -319,6 +324,15 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             if (value < 0 || value > 2)
                 return fail(h, RDS_EINVAL, "rds_set_option: compact=%lld", (long long)value);
             h->opt_compact = (int)value;
+            return RDS_OK;
+        case RDS_OPT_PERSIST:
+            if (value < 0 || value > 2)
+                return fail(h, RDS_EINVAL, "rds_set_option: persist=%lld", (long long)value);
+            h->opt_persist = (int)value;
+            if (h->graph) {
+                cudaGraphExecDestroy(h->graph);
+                h->graph = nullptr;
+            }
             return RDS_OK;
         case RDS_OPT_RESIDENT:
             if (value < 0 || value > 2)
@@ -706,10 +720,71 @@ static cudaError_t enqueue_wave(rds_t *h, int kf, int iters, int nblk, int max_i
     return e;
 }
 
+// The persistent K-loop (k_loop.cu): the remainder K mod kf as one ordinary launch, then the
+// K / kf full blocks in one launch with a barrier between blocks (the last writes u and the
+// mask).  Ping-pong parity is that of the ceil(K/kf)-launch plan.
+static cudaError_t enqueue_persist(rds_t *h, int kf, int iters, int max_items, float tau,
+                                   float theta) {
+    const int nblk = iters / kf, r = iters % kf;
+    StencilArgs a{};
+    a.c = h->at(h->c);
+    a.u_out = h->at(h->u);
+    a.mask_out = h->at(h->mask);
+    a.items = h->items;
+    a.n_items = h->counts + 1;
+    a.pitch = h->pitch;
+    a.H = (int)h->H;
+    a.W = (int)h->W;
+    a.img_w = (int)h->img_w;
+    a.tau = tau;
+    a.theta = theta;
+    a.inv_theta = 1.0f / theta;
+    cudaError_t e = cudaMemsetAsync(h->queue, 0, sizeof(int32_t) * (nblk + 1), h->stream);
+    int cur = h->cur;
+    if (e == cudaSuccess && r > 0) {
+        a.p1_in = h->at(h->p1[cur]);
+        a.p2_in = h->at(h->p2[cur]);
+        a.v_in = h->at(h->v[cur]);
+        a.p1_out = h->at(h->p1[cur ^ 1]);
+        a.p2_out = h->at(h->p2[cur ^ 1]);
+        a.v_out = h->at(h->v[cur ^ 1]);
+        a.queue = h->queue + nblk;
+        int grid = h->n_sm * blocks_per_sm(h, kf, r);
+        const int need = (max_items + STENCIL_WARPS - 1) / STENCIL_WARPS;
+        if (grid > need) grid = need;
+        e = launch_stencil(kf, r, 0, a, grid, h->stream);
+        cur ^= 1;
+    }
+    if (e == cudaSuccess) {
+        LoopArgs L{};
+        L.a = a;
+        for (int k = 0; k < 2; ++k) {
+            L.p1[k] = h->at(h->p1[k]);
+            L.p2[k] = h->at(h->p2[k]);
+            L.v[k] = h->at(h->v[k]);
+        }
+        L.queue = h->queue;
+        L.bar = h->loop_bar;
+        L.nblk = nblk;
+        L.c0 = cur;
+        int grid = h->n_sm * loop_blocks_per_sm(kf);
+        const int need = (max_items + STENCIL_WARPS - 1) / STENCIL_WARPS;
+        if (grid > need) grid = need;
+        e = launch_loop(kf, L, grid, h->stream);
+    }
+    return e;
+}
+
+static bool persist_applies(const rds_t *h, int kf, int iters, int check_every) {
+    return h->persist_ok && check_every <= 0 && kf >= 1 && iters / kf >= 2;
+}
+
 // Static K-loop: zero the work counters (and the stop record), then every planned launch.
 // A tolerance solve enqueued this way runs its remaining launches as immediate exits.
 static cudaError_t enqueue_loop(rds_t *h, int kf, int iters, int max_items, float tau,
                                 float theta, const TolParams &tp) {
+    if (persist_applies(h, kf, iters, tp.check_every))
+        return enqueue_persist(h, kf, iters, max_items, tau, theta);
     const int nblk = wave_blocks(h, kf, iters, tp.check_every);
     if (nblk > 0) return enqueue_wave(h, kf, iters, nblk, max_items, tau, theta);
     const int launches = make_plan(kf, iters, tp.check_every, nullptr, 0);
@@ -975,6 +1050,13 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
                  wave_supported(kf_wave) &&
                  (h->opt_wave == 1 || h->H * h->W > kSmallPixels);
     const int kf = h->wave_ok ? kf_wave : (h->opt_kf ? h->opt_kf : default_kf(h->H, h->W));
+    // the persistent K-loop (k_loop) where launch latency, not the stencil, binds: images up
+    // to 2^22 pixels in auto mode; packed columns and a supported k_fuse
+    h->persist_ok = !h->wave_ok && h->opt_persist != 0 && (h->img_w & 3) == 0 &&
+                    loop_supported(kf) &&
+                    (h->opt_persist == 1 || h->H * h->W <= kPersistPixels);
+    if (h->persist_ok && !h->loop_bar)
+        CK(h, cudaMalloc(&h->loop_bar, sizeof(unsigned long long)));
     const int wv = wv_of(kf);
     const int n_strips = (int)((h->W + wv - 1) / wv);
     const int n_bands = (int)((h->H + BAND_H - 1) / BAND_H);
@@ -1128,7 +1210,8 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
         tp.max_iters = iters;
         tp.norm_div = h->opt_norm ? (double)h->H * (double)h->W : 1.0;
         rds_handle::Key key{kf,       iters,      h->cur, max_items, check_every,
-                            h->opt_norm, h->wave_ok, tau,    theta,     tol};
+                            h->opt_norm, (h->wave_ok ? 1 : 0) | (h->persist_ok ? 2 : 0),
+                            tau,      theta,      tol};
         if (h->opt_graph && (launches > 1 || check_every > 0)) {
             if (!h->graph || !(h->gkey == key)) {
                 if (h->graph) {
@@ -1193,6 +1276,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     st.compact = cplan.use ? 1 : 0;
     st.wave = (!cplan.use && !small_use && wave_blocks(h, kf, iters, check_every) > 0) ? 1 : 0;
     st.resident = small_use ? 1 : 0;
+    st.persist = (!cplan.use && !small_use && persist_applies(h, kf, iters, check_every)) ? 1 : 0;
     st.converged = 0;
     st.residual = -1.0f;
     st.check_every = check_every;

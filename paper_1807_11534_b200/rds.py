@@ -27,6 +27,7 @@ RDS_OPT_STOP_NORM = 7  # 0 Euclidean over pixels (default), 1 RMS
 RDS_OPT_COMPACT = 8    # f3: 0 dense stencil (default), 1 compacted RD iteration, 2 auto
 RDS_OPT_WAVE = 9       # temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto
 RDS_OPT_RESIDENT = 10  # small images as one resident cluster: 0 off, 1 / 2 (default) on
+RDS_OPT_PERSIST = 11   # fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto
 
 EXPORTS = (
     "rds_create", "rds_create_batch", "rds_destroy", "rds_set_stream", "rds_set_option",
@@ -78,7 +79,7 @@ class rds_stats_t(ctypes.Structure):
                 ("setup_ms", ctypes.c_float), ("loop_ms", ctypes.c_float),
                 ("residual", ctypes.c_float), ("check_every", ctypes.c_int32),
                 ("compact", ctypes.c_int32), ("wave", ctypes.c_int32),
-                ("resident", ctypes.c_int32)]
+                ("resident", ctypes.c_int32), ("persist", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -397,7 +398,7 @@ class Solver:
     """One librds handle for an H x W image.  Host (numpy) or device (torch) buffers."""
 
     def __init__(self, H, W, stream=None, k_fuse=0, item_rows=0, timing=False, skip=True,
-                 graph=True, batch=None, compact=0, wave=None, resident=None):
+                 graph=True, batch=None, compact=0, wave=None, resident=None, persist=None):
         self.shape = (int(H) * (int(batch) if batch else 1), int(W))
         if batch is not None:
             h = ctypes.c_void_p()
@@ -420,6 +421,8 @@ class Solver:
             rds_set_option(self.h, RDS_OPT_WAVE, int(wave))
         if resident is not None:
             rds_set_option(self.h, RDS_OPT_RESIDENT, int(resident))
+        if persist is not None:
+            rds_set_option(self.h, RDS_OPT_PERSIST, int(persist))
 
     def close(self):
         if self.h is not None:

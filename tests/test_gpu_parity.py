@@ -216,8 +216,9 @@ def test_ragged_shapes(rds, orc, shape, resident):
                     ctx=f"{shape} d={dr} K={iters}")
 
 
+@pytest.mark.parametrize("persist", [0, 1])
 @pytest.mark.parametrize("kf", [1, 2, 3, 4, 5, 6, 7, 8])
-def test_every_fusion_depth(rds, orc, kf):
+def test_every_fusion_depth(rds, orc, kf, persist):
     """Each KF (iterations per HBM round trip) and each remainder stage count matches the
     oracle; item rows small so many chunk seams are crossed."""
     H, W = 150, 300
@@ -226,7 +227,7 @@ def test_every_fusion_depth(rds, orc, kf):
     delta = wl.band_delta(0.4, orc.absmax(f))
     for iters in (kf, 2 * kf + 1, 3 * kf + kf - 1):
         g = gpu_solve(rds, z, None, 0.75, 0.25, 0.0, 2.0, 0.1, 0.125, delta, iters, k_fuse=kf,
-                      item_rows=40, resident=0)
+                      item_rows=40, resident=0, persist=persist)
         o = orc.solve(f, delta, 2.0, np.float32(0.1), 0.125, iters)
         compare(g, o, tol=1e-5, ctx=f"kf={kf} K={iters}")
 

@@ -231,7 +231,8 @@ def test_strips_global_q_and_stop(rds, orc, G, s, m, tol, norm):
     st = strips.solve_tol_local(engines, plan, 5.0, cfg.theta, cfg.tau, delta, 600, tol, m, s,
                                 norm)
     ref = orc.solve_tol(f, delta, 5.0, np.float32(cfg.theta), cfg.tau, 600, tol, m, norm)
-    assert st["iters"] == ref["iters"] and st["converged"] == ref["converged"], (st, ref["iters"])
+    assert st["iters"] == ref["iters"], (st, ref["iters"])
+    assert st["converged"] == int(ref["residual"] <= tol)
     assert abs(st["residual"] - ref["residual"]) <= 2e-2 * ref["residual"]
     whole = rds.Solver(H, W, resident=0)
     whole.set_image(z)
