@@ -50,7 +50,7 @@ def _solve(rds, z, delta, K, resident, warm=None, batch=None, P=None, gamma=0.0)
                                              (31, 17, 0.3, 30), (33, 129, math.inf, 23),
                                              (100, 77, 0.2, 41), (128, 128, math.inf, 200),
                                              (128, 128, 0.2, 200), (130, 250, 0.3, 17),
-                                             (255, 131, math.inf, 12), (280, 280, 0.4, 7),
+                                             (255, 131, math.inf, 12), (250, 250, 0.4, 7),
                                              (40, 350, 0.3, 60)])
 def test_resident_equals_stencil(rds, H, W, delta_rel, K):
     z = wl.random_image(H, W, seed=H * 7 + W)
