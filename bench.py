@@ -382,12 +382,14 @@ def run_ours(args, dist):
         n_items = st["n_active_cells"]
         item_px = n_items * st["item_rows"] * st["item_cols"]
         launches = st["launches"]
-        launch_ms_all.append(lm / launches)
         px = act_px[dr]
-        bytes_all.append(BYTES_PER_PX_ITER * px * K / launches)
-        pxit_all.append(px * K / launches)
+        path = "compact" if st["compact"] else ("resident" if st.get("resident") else "stencil")
+        if path == "stencil":  # the stencil's roofline: its launches only
+            launch_ms_all.append(lm / launches)
+            bytes_all.append(BYTES_PER_PX_ITER * px * K / launches)
+            pxit_all.append(px * K / launches)
         per_delta.append({
-            "delta_rel": "inf" if math.isinf(dr) else dr,
+            "delta_rel": "inf" if math.isinf(dr) else dr, "path": path,
             "loop_ms": lm, "setup_ms": sm,
             "active_tile_frac": st["n_active_tiles"] / st["n_tiles"],
             "rd_frac": st["n_rd"] / (cfg.H * cfg.W),
@@ -434,7 +436,10 @@ def run_ours(args, dist):
                           f"time / peak; peak = MEASURED_PEAKS.json hbm_gbs (measured copy)")},
     }
 
-    launches_per_step = sum(st["launches"] + 4 + 2 for _, st, _ in info)
+    # K1, K2, band flags, items; energy partial + final; the compact path's index build,
+    # gather and scatter
+    launches_per_step = sum(st["launches"] + 4 + 2 + (5 if st["compact"] else 0)
+                            for _, st, _ in info)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,

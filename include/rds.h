@@ -115,10 +115,11 @@ typedef struct {
 #define RDS_OPT_COMPACT 8    /* f3: iterate on the RD pixels alone, stored compactly
                                 in row-major RD order with their stencil neighbours' indices, in
                                 one persistent cooperative kernel (k_rdc.cu) instead of the dense
-                                temporally blocked stencil.  0 (default) = dense; 1 = compact for
-                                every rds_solve / rds_solve_q / rds_solve_tol; 2 = compact where
-                                a cost model predicts it faster (thin scattered bands, e.g. C3
-                                up to delta ~ 0.1 max|f|, and small images).  Same float operations per
+                                temporally blocked stencil.  0 = dense; 1 = compact for every
+                                rds_solve / rds_solve_q / rds_solve_tol; 2 (default) = compact
+                                where a cost model predicts it at least 10% faster (thin
+                                scattered bands, e.g. C3 up to delta ~ 0.1 max|f|, and small
+                                images).  Same float operations per
                                 pixel as the dense path (results agree value for value); the
                                 solve synchronises once to size the compact arrays; tolerance
                                 solves (rds_solve_tol) evaluate the stopping rule inside the

@@ -236,7 +236,8 @@ struct EnergyArgs {
                         //      sum_RD |grad u'|, sum (u' - v)^2
     float lambda, theta;
 };
-constexpr int ENERGY_BLOCKS = 592;  // 4 x 148 SMs
+constexpr int ENERGY_BLOCKS = 592;  // 4 x 148 SMs (k_energy_partial)
+constexpr int ENERGY_WARPS = 8192;  // bound on k_energy_strip's warps (its partials)
 cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s);
 
 // f3: compacted restricted-domain iteration (k_rdc.cu).  Neighbour codes: >= 0 compact index

@@ -87,6 +87,131 @@ __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Streaming form (round 2): one warp per 120-column strip x row chunk marches down its rows,
+// each lane holding a quad of columns (float4 / uchar4 loads: 21 bytes per pixel, every row
+// read once; the quad-swizzled v, rho undone in registers).  Lane 0 and lane 31 only supply
+// the left / right neighbour quads (the strips overlap by one quad on each side); rows i-1 ..
+// i+1 of what the terms need are carried from row to row.  Same per-pixel float terms as
+// k_energy_partial; per-warp fp64 sums in a fixed lane order, warps combined in a fixed order
+// by k_energy_final, so the result is bit-reproducible.
+// ---------------------------------------------------------------------------------------
+constexpr int ESTRIP = 120;  // output columns per warp (30 lanes x 4)
+
+struct Q4 {
+    float x[4];
+};
+__device__ __forceinline__ Q4 ld_nat(const float *p) {  // natural-order quad
+    const float4 q = *reinterpret_cast<const float4 *>(p);
+    return Q4{{q.x, q.y, q.z, q.w}};
+}
+__device__ __forceinline__ Q4 ld_swz(const float *p) {  // quad-swizzled: x0 x2 x1 x3 in memory
+    const float4 q = *reinterpret_cast<const float4 *>(p);
+    return Q4{{q.x, q.z, q.y, q.w}};
+}
+
+__global__ void __launch_bounds__(256) k_energy_strip(const EnergyArgs a, int n_strips,
+                                                      int chunk, int n_items) {
+    const int lane = threadIdx.x & 31;
+    const int item = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (item >= n_items) return;  // warp-uniform
+    const int s = item % n_strips, c = item / n_strips;
+    const int r0 = a.row0 + c * chunk, r1 = min(a.row1, r0 + chunk);
+    const int j0 = s * ESTRIP - 4 + 4 * lane;  // this lane's first column
+    const bool out_lane = lane >= 1 && lane <= 30;
+    const int64_t pitch = a.pitch;
+    const float lambda = a.lambda, theta = a.theta;
+    // per column: in the image and not an image's last column (grad_2 exists)
+    bool inc[4], right[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int j = j0 + e;
+        inc[e] = out_lane && j >= 0 && j < a.W;
+        right[e] = j >= 0 && j < a.W && (j % a.img_w) != a.img_w - 1;
+    }
+    auto div_row = [&](const Q4 &p1, const Q4 &p1up, const Q4 &p2, Q4 &d) {
+        // div rho = rho1 - rho1(i-1) + rho2 - rho2(j-1); the left neighbour of x0 is the
+        // previous lane's x3 (lane 0: its own left quad's value is never used)
+        const float l2 = __shfl_up_sync(0xffffffffu, p2.x[3], 1);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            d.x[e] = p1.x[e] - p1up.x[e] + p2.x[e] - (e == 0 ? l2 : p2.x[e - 1]);
+    };
+    auto uprime = [&](const uchar4 &lb, const Q4 &u, const Q4 &d, Q4 &up) {
+        const uint8_t l[4] = {lb.x, lb.y, lb.z, lb.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            up.x[e] = l[e] == 2 ? u.x[e] : (l[e] == 1 ? 1.0f : 0.0f) - theta * d.x[e];
+    };
+    // row r0 - 1 (rho1 only) and row r0
+    int64_t row = (int64_t)r0 * pitch + j0;
+    Q4 p1m = ld_swz(a.p1 + row - pitch);
+    Q4 v = ld_swz(a.v + row), p1 = ld_swz(a.p1 + row), p2 = ld_swz(a.p2 + row);
+    Q4 u = ld_nat(a.u + row);
+    uchar4 lab = *reinterpret_cast<const uchar4 *>(a.lab + row);
+    Q4 d, up;
+    div_row(p1, p1m, p2, d);
+    uprime(lab, u, d, up);
+    double acc[NE] = {0, 0, 0, 0, 0, 0, 0};
+    for (int i = r0; i < r1; ++i) {
+        const bool down = i < a.H - 1;
+        const int64_t rn = row + pitch;
+        // row i + 1 (a frame row past H - 1: pinned zeros, unused where !down)
+        const Q4 vd = ld_swz(a.v + rn), p1d = ld_swz(a.p1 + rn), p2d = ld_swz(a.p2 + rn);
+        const Q4 ud = ld_nat(a.u + rn);
+        const uchar4 labd = *reinterpret_cast<const uchar4 *>(a.lab + rn);
+        const Q4 f = ld_nat(a.f + row);
+        Q4 dd, upd;
+        div_row(p1d, p1, p2d, dd);
+        uprime(labd, ud, dd, upd);
+        // right neighbours of x3: the next lane's x0
+        const float vr = __shfl_down_sync(0xffffffffu, v.x[0], 1);
+        const float ur = __shfl_down_sync(0xffffffffu, u.x[0], 1);
+        const float upr = __shfl_down_sync(0xffffffffu, up.x[0], 1);
+        const uint8_t l[4] = {lab.x, lab.y, lab.z, lab.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (!inc[e]) continue;
+            const float vx = v.x[e], ux = u.x[e], fx = f.x[e];
+            const float vnext = e < 3 ? v.x[e + 1] : vr;
+            const float unext = e < 3 ? u.x[e + 1] : ur;
+            const float upnext = e < 3 ? up.x[e + 1] : upr;
+            const float gv1 = down ? vd.x[e] - vx : 0.0f;
+            const float gv2 = right[e] ? vnext - vx : 0.0f;
+            const float cu = clamp01(ux);
+            const float gu1 = down ? clamp01(ud.x[e]) - cu : 0.0f;
+            const float gu2 = right[e] ? clamp01(unext) - cu : 0.0f;
+            const float t = lambda * fx + d.x[e];
+            acc[0] += (double)sqrtf(gv1 * gv1 + gv2 * gv2);
+            acc[1] += (double)fx * (double)vx;
+            acc[2] += (double)sqrtf(gu1 * gu1 + gu2 * gu2);
+            acc[3] += (double)fx * (double)cu;
+            acc[4] += (double)fminf(t, 0.0f);
+            const float upx = up.x[e];
+            const float g1 = (down ? upd.x[e] : upx) - upx;
+            const float g2 = (right[e] ? upnext : upx) - upx;
+            const float tvp = sqrtf(g1 * g1 + g2 * g2);
+            acc[5] += (double)(l[e] == 2 ? tvp : 0.0f);
+            acc[6] += (double)((upx - vx) * (upx - vx));
+        }
+        // carry row i + 1
+        p1m = p1;
+        v = vd;
+        p1 = p1d;
+        p2 = p2d;
+        u = ud;
+        lab = labd;
+        d = dd;
+        up = upd;
+        row = rn;
+    }
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+        const double sum = warp_sum(acc[q]);
+        if (lane == 0) a.partials[(int64_t)item * NE + q] = sum;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_energy_final(const double *partials, int nb,
                                                       double *out) {
     __shared__ double sh[8][NE];
@@ -195,10 +320,30 @@ cudaError_t launch_unswizzle(const float *plane, int64_t pitch, int H, int W, fl
 }
 
 cudaError_t launch_energy(const EnergyArgs &a, cudaStream_t s) {
-    k_energy_partial<<<ENERGY_BLOCKS, 256, 0, s>>>(a);
+    // strips of ESTRIP columns x row chunks, at most ENERGY_WARPS warps (the partials buffer)
+    const int n_strips = (a.W + ESTRIP - 1) / ESTRIP;
+    const int rows = a.row1 - a.row0;
+    if (rows <= 0 || n_strips <= 0) {
+        k_energy_final<<<1, 256, 0, s>>>(a.partials, 0, a.out);
+        return cudaGetLastError();
+    }
+    int chunks = ENERGY_WARPS / n_strips;
+    if (chunks < 1) chunks = 1;
+    int chunk = (rows + chunks - 1) / chunks;
+    if (chunk < 16) chunk = 16;  // short chunks: the first-row loads would dominate
+    chunks = (rows + chunk - 1) / chunk;
+    if ((int64_t)chunks * n_strips > ENERGY_WARPS) {  // very wide images: the old kernel
+        k_energy_partial<<<ENERGY_BLOCKS, 256, 0, s>>>(a);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        k_energy_final<<<1, 256, 0, s>>>(a.partials, ENERGY_BLOCKS, a.out);
+        return cudaGetLastError();
+    }
+    const int n_items = chunks * n_strips;
+    k_energy_strip<<<(n_items + 7) / 8, 256, 0, s>>>(a, n_strips, chunk, n_items);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    k_energy_final<<<1, 256, 0, s>>>(a.partials, ENERGY_BLOCKS, a.out);
+    k_energy_final<<<1, 256, 0, s>>>(a.partials, n_items, a.out);
     return cudaGetLastError();
 }
 

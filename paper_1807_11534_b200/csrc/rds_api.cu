@@ -103,7 +103,7 @@ struct rds_handle {
 
     int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1, opt_ctas = 0;
     int opt_norm = 0;  // stopping-rule norm: 0 Euclidean over pixels, 1 RMS (R-F2)
-    int opt_compact = 0;  // f3: 0 dense stencil, 1 compacted RD iteration, 2 auto (RDS_OPT_COMPACT)
+    int opt_compact = 2;  // f3: 0 dense stencil, 1 compacted RD iteration, 2 auto (default; RDS_OPT_COMPACT)
     int opt_wave = 0;     // temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto (RDS_OPT_WAVE)
     bool wave_ok = false; // the last solve's set-up allows the wavefront (aligned, supported kf)
     int opt_resident = 2; // small images as one resident cluster: 0 off, 1 on, 2 auto (RDS_OPT_RESIDENT)
@@ -250,7 +250,7 @@ int rds_create(int64_t H, int64_t W, rds_t **out) {
     A(cudaMalloc(&h->n_rd_dev, sizeof(long long)));
     A(cudaMalloc(&h->absmax_bits, sizeof(unsigned)));
     A(cudaMalloc(&h->flag, sizeof(int)));
-    A(cudaMalloc(&h->e_partials, sizeof(double) * ENERGY_BLOCKS * 7));
+    A(cudaMalloc(&h->e_partials, sizeof(double) * ENERGY_WARPS * 7));
     A(cudaMalloc(&h->e_out, sizeof(double) * 7));
     for (auto &ev : h->ev) A(cudaEventCreate(&ev));
     A(cudaStreamSynchronize(h->stream));

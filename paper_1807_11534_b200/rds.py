@@ -24,7 +24,7 @@ RDS_LABEL_BG, RDS_LABEL_FG, RDS_LABEL_RD = 0, 1, 2
 RDS_OPT_KFUSE, RDS_OPT_ITEM_ROWS, RDS_OPT_TIMING, RDS_OPT_SKIP, RDS_OPT_GRAPH = 1, 2, 3, 4, 5
 RDS_OPT_CTAS_PER_SM = 6
 RDS_OPT_STOP_NORM = 7  # 0 Euclidean over pixels (default), 1 RMS
-RDS_OPT_COMPACT = 8    # f3: 0 dense stencil (default), 1 compacted RD iteration, 2 auto
+RDS_OPT_COMPACT = 8    # f3: 0 dense stencil, 1 compacted RD iteration, 2 auto (default)
 RDS_OPT_WAVE = 9       # temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto
 RDS_OPT_RESIDENT = 10  # small images as one resident cluster: 0 off, 1 / 2 (default) on
 RDS_OPT_PERSIST = 11   # fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto
@@ -398,7 +398,8 @@ class Solver:
     """One librds handle for an H x W image.  Host (numpy) or device (torch) buffers."""
 
     def __init__(self, H, W, stream=None, k_fuse=0, item_rows=0, timing=False, skip=True,
-                 graph=True, batch=None, compact=0, wave=None, resident=None, persist=None):
+                 graph=True, batch=None, compact=None, wave=None, resident=None,
+                 persist=None):
         self.shape = (int(H) * (int(batch) if batch else 1), int(W))
         if batch is not None:
             h = ctypes.c_void_p()
@@ -415,7 +416,7 @@ class Solver:
         rds_set_option(self.h, RDS_OPT_TIMING, int(timing))
         rds_set_option(self.h, RDS_OPT_SKIP, int(skip))
         rds_set_option(self.h, RDS_OPT_GRAPH, int(graph))
-        if compact:
+        if compact is not None:  # None: the library default (2, auto)
             rds_set_option(self.h, RDS_OPT_COMPACT, int(compact))
         if wave is not None:
             rds_set_option(self.h, RDS_OPT_WAVE, int(wave))

@@ -227,7 +227,7 @@ def test_every_fusion_depth(rds, orc, kf, persist):
     delta = wl.band_delta(0.4, orc.absmax(f))
     for iters in (kf, 2 * kf + 1, 3 * kf + kf - 1):
         g = gpu_solve(rds, z, None, 0.75, 0.25, 0.0, 2.0, 0.1, 0.125, delta, iters, k_fuse=kf,
-                      item_rows=40, resident=0, persist=persist)
+                      item_rows=40, resident=0, persist=persist, compact=0)
         o = orc.solve(f, delta, 2.0, np.float32(0.1), 0.125, iters)
         compare(g, o, tol=1e-5, ctx=f"kf={kf} K={iters}")
 
@@ -258,7 +258,7 @@ def test_fusion_depth_equivalence(rds):
     res = []
     for kf in (1, 3, 7):
         g = gpu_solve(rds, z, P, cfg.c1, cfg.c2, cfg.gamma, 5.0, cfg.theta, cfg.tau,
-                      np.float32(0.2), 23, k_fuse=kf)
+                      np.float32(0.2), 23, k_fuse=kf, compact=0)
         res.append(g)
     for g in res[1:]:
         for k in ("u", "v", "p1", "p2", "mask"):
@@ -271,7 +271,7 @@ def test_skip_equivalence_and_determinism(rds):
     cfg = wl.CONFIGS["C2"]
     z, P = wl.make_image(cfg)
     am = np.float32(0)
-    s = rds.Solver(cfg.H, cfg.W)
+    s = rds.Solver(cfg.H, cfg.W, compact=0)
     s.set_image(z)
     s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
     am = s.absmax()
@@ -549,7 +549,7 @@ def test_solve_tol_schedules(rds, orc, m, kf, max_iters, tol):
     rng = np.random.default_rng(m * 100 + kf)
     z = rng.uniform(0, 1, (75, 133)).astype(np.float32)
     s, st = _tol_case(rds, orc, z, None, cfg, 5.0, np.float32(0.3), max_iters, tol, m,
-                      f"m={m} kf={kf} K={max_iters} tol={tol}", k_fuse=kf)
+                      f"m={m} kf={kf} K={max_iters} tol={tol}", k_fuse=kf, compact=0)
     if tol == 0.0:
         assert st["iters"] == max_iters and st["converged"] == 0
     # graph replay and a fixed-K solve on the same handle afterwards
@@ -642,7 +642,7 @@ def test_frame_untouched(rds, shape, kf):
     padded frame around the image has changed (rds_check_frame)."""
     H, W = shape
     z = np.random.default_rng(H * W).uniform(0, 1, shape).astype(np.float32)
-    s = rds.Solver(H, W, k_fuse=kf)
+    s = rds.Solver(H, W, k_fuse=kf, compact=0)
     s.set_image(z)
     s.set_fitting(0.75, 0.25, 1.5, np.random.default_rng(1).uniform(0, 1, shape).astype(np.float32))
     d = 0.3 * s.absmax()
