@@ -1146,29 +1146,22 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
                                  max_chunk,
                                  2 * kf + 4, h->items, h->counts, h->stream));
     }
-    CompactPlan cplan;
-    if (iters > 0 && h->opt_compact) {
-        const int rc = compact_prepare(h, tau, theta, iters, &cplan);
-        if (rc) return rc;
-    }
-    h->warm_pending = false;
-    h->tol_pending = false;
-    h->cur = 0;
-    if (h->opt_timing) CK(h, cudaEventRecord(h->ev[1], h->stream));
-
     // small images: the whole fixed-K loop in one resident cluster (k_small.cu) when the image
     // fits one cluster's shared memory and such a cluster can be scheduled here
     SmallArgs sa{};
     bool small_use = false;
-    if (iters > 0 && !cplan.use && check_every == 0 && h->opt_resident &&
+    // (ahead of the compact path's auto mode, which it beats where it fits; a forced compact
+    // path, RDS_OPT_COMPACT = 1, still wins).  K1 put the initial state in both buffers; the
+    // final state is written back into buffer 0.
+    if (iters > 0 && check_every == 0 && h->opt_resident && h->opt_compact != 1 &&
         small_plan(h->H, h->W, &sa.G, &sa.R)) {
-        sa.p1_in = h->at(h->p1[h->cur]);
-        sa.p2_in = h->at(h->p2[h->cur]);
-        sa.v_in = h->at(h->v[h->cur]);
+        sa.p1_in = h->at(h->p1[0]);
+        sa.p2_in = h->at(h->p2[0]);
+        sa.v_in = h->at(h->v[0]);
         sa.c = h->at(h->c);
-        sa.p1_out = h->at(h->p1[h->cur]);
-        sa.p2_out = h->at(h->p2[h->cur]);
-        sa.v_out = h->at(h->v[h->cur]);
+        sa.p1_out = h->at(h->p1[0]);
+        sa.p2_out = h->at(h->p2[0]);
+        sa.v_out = h->at(h->v[0]);
         sa.u_out = h->at(h->u);
         sa.mask_out = h->at(h->mask);
         sa.n_rd = h->n_rd_dev;
@@ -1187,6 +1180,16 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
         }
         small_use = h->resident_fit > 0;
     }
+
+    CompactPlan cplan;
+    if (iters > 0 && h->opt_compact && !small_use) {
+        const int rc = compact_prepare(h, tau, theta, iters, &cplan);
+        if (rc) return rc;
+    }
+    h->warm_pending = false;
+    h->tol_pending = false;
+    h->cur = 0;
+    if (h->opt_timing) CK(h, cudaEventRecord(h->ev[1], h->stream));
 
     if (small_use) {
         NvtxRange nvtx_small("rds_solve (resident cluster)");
