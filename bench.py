@@ -399,6 +399,14 @@ def run_ours(args, dist):
             "speedup_vs_full": (t_full / lm) if t_full else None,
             "gap": e["gap"], "E_v": e["E_v"],
         })
+    kernel = "k_stencil"
+    if not launch_ms_all:  # no delta ran on the stencil (small images: the resident cluster)
+        kernel = "+".join(sorted({p["path"] for p in per_delta}))
+        for p in per_delta:
+            px = act_px[p["delta_rel"] if p["delta_rel"] != "inf" else math.inf]
+            launch_ms_all.append(p["loop_ms"])
+            bytes_all.append(BYTES_PER_PX_ITER * px * K)
+            pxit_all.append(px * K)
     launch_ms = statistics.mean(launch_ms_all)
     bytes_per_launch = statistics.mean(bytes_all)
     achieved_gbs = bytes_per_launch / (launch_ms * 1e-3) / 1e9
@@ -416,7 +424,7 @@ def run_ours(args, dist):
     # HBM roofline of the minimum-traffic one-iteration-per-pass schedule (north_star, SURVEY
     # §8(d) R1) is reported beside it and exceeds 1 by design.
     roofline = {
-        "bound": "alu", "kernel": "k_stencil", "achieved": achieved_px, "peak": alu_peak,
+        "bound": "alu", "kernel": kernel, "achieved": achieved_px, "peak": alu_peak,
         "unit": "Gpixel-iter/s", "frac": achieved_px / alu_peak,
         "traffic": traffic,
         "basis": (f"active pixel-iterations per launch / mean launch time {launch_ms:.4f} ms; "

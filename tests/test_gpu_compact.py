@@ -28,10 +28,11 @@ def rds():
     return _rds
 
 
-def _run(rds, z, delta, K, compact, batch=None, kf=0, lam=5.0, warm=None, P=None, gamma=0.0):
+def _run(rds, z, delta, K, compact, batch=None, kf=0, lam=5.0, warm=None, P=None, gamma=0.0,
+         resident=None):
     H, W = z.shape[-2:] if batch else z.shape
-    s = rds.BatchSolver(batch, H, W, compact=compact, k_fuse=kf) if batch else \
-        rds.Solver(H, W, compact=compact, k_fuse=kf)
+    kw = dict(compact=compact, k_fuse=kf, resident=resident)
+    s = rds.BatchSolver(batch, H, W, **kw) if batch else rds.Solver(H, W, **kw)
     s.set_image(z)
     s.set_fitting(0.8, 0.2, gamma, P)
     if warm is not None:
@@ -96,8 +97,10 @@ def test_compact_variants(rds):
     _, c = _run(rds, z, np.float32(0.2), 15, 1, warm=warm)
     _same(d, c)
     for d in (np.float32(math.inf), np.float32(0.01)):  # small image: dense is launch bound
-        s, _ = _run(rds, z, d, 5, 2)
+        s, _ = _run(rds, z, d, 5, 2, resident=0)
         assert s.stats()["compact"] == 1
+        s, _ = _run(rds, z, d, 5, 2)               # ... and the resident cluster beats both
+        assert s.stats()["compact"] == 0 and s.stats()["resident"] == 1
     z3, _ = wl.make_image("C3")                        # thin scattered band on 4096^2: compact
     s3 = rds.Solver(*z3.shape, compact=2)
     s3.set_image(z3)
