@@ -11,6 +11,15 @@
 
 namespace rds {
 
+// |grad| in the energies: MUFU.SQRT (sqrt.approx, relative error < 2^-23, measured:
+// profiles/micro_mufu_err.txt); the IEEE sqrtf's slow-path branch made K5 issue-bound.  The
+// energies are sums of 10^7 terms compared at 1e-5 relative, far above that error.
+__device__ __forceinline__ float esqrt(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 constexpr int NE = 7;
 
 __device__ __forceinline__ double warp_sum(double x) {
@@ -53,9 +62,9 @@ __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
             // holds 0
             const float dv = a.p1[os] - a.p1[os - pitch] + a.p2[os] - a.p2[row + swz(j - 1)];
             const float t = a.lambda * f + dv;
-            acc[0] += (double)sqrtf(gv1 * gv1 + gv2 * gv2);
+            acc[0] += (double)esqrt(gv1 * gv1 + gv2 * gv2);
             acc[1] += (double)f * (double)v;
-            acc[2] += (double)sqrtf(gu1 * gu1 + gu2 * gu2);
+            acc[2] += (double)esqrt(gu1 * gu1 + gu2 * gu2);
             acc[3] += (double)f * (double)cu;
             acc[4] += (double)fminf(t, 0.0f);
             // F^RD(u', v) = sum_RD |grad u'| + |u' - v|^2 / (2 theta) + lambda <f, v>
@@ -66,7 +75,7 @@ __global__ void __launch_bounds__(256) k_energy_partial(const EnergyArgs a) {
             const float ud = down ? u_prime(a, row + pitch, j) : up;
             const float ur = right ? u_prime(a, row, j + 1) : up;
             const float g1 = ud - up, g2 = ur - up;
-            const float tvp = sqrtf(g1 * g1 + g2 * g2);
+            const float tvp = esqrt(g1 * g1 + g2 * g2);
             acc[5] += (double)(lx == 2 ? tvp : 0.0f);
             acc[6] += (double)((up - v) * (up - v));
             jm += 256;
@@ -143,24 +152,37 @@ __global__ void __launch_bounds__(256) k_energy_strip(const EnergyArgs a, int n_
         for (int e = 0; e < 4; ++e)
             up.x[e] = l[e] == 2 ? u.x[e] : (l[e] == 1 ? 1.0f : 0.0f) - theta * d.x[e];
     };
-    // row r0 - 1 (rho1 only) and row r0
+    // row r0 - 1 (rho1 only) and row r0; rows are software-pipelined one ahead: the loads
+    // of row i + 2 are in flight while row i's terms are formed (row i + 1's are carried)
     int64_t row = (int64_t)r0 * pitch + j0;
     Q4 p1m = ld_swz(a.p1 + row - pitch);
     Q4 v = ld_swz(a.v + row), p1 = ld_swz(a.p1 + row), p2 = ld_swz(a.p2 + row);
     Q4 u = ld_nat(a.u + row);
     uchar4 lab = *reinterpret_cast<const uchar4 *>(a.lab + row);
+    Q4 f = ld_nat(a.f + row);
+    // row r0 + 1 (a frame row past H - 1 holds pinned zeros; the chunk's rows are < H)
+    Q4 vd = ld_swz(a.v + row + pitch), p1d = ld_swz(a.p1 + row + pitch),
+       p2d = ld_swz(a.p2 + row + pitch), ud = ld_nat(a.u + row + pitch);
+    uchar4 labd = *reinterpret_cast<const uchar4 *>(a.lab + row + pitch);
     Q4 d, up;
     div_row(p1, p1m, p2, d);
     uprime(lab, u, d, up);
     double acc[NE] = {0, 0, 0, 0, 0, 0, 0};
     for (int i = r0; i < r1; ++i) {
         const bool down = i < a.H - 1;
-        const int64_t rn = row + pitch;
-        // row i + 1 (a frame row past H - 1: pinned zeros, unused where !down)
-        const Q4 vd = ld_swz(a.v + rn), p1d = ld_swz(a.p1 + rn), p2d = ld_swz(a.p2 + rn);
-        const Q4 ud = ld_nat(a.u + rn);
-        const uchar4 labd = *reinterpret_cast<const uchar4 *>(a.lab + rn);
-        const Q4 f = ld_nat(a.f + row);
+        const int64_t rn = row + pitch, rnn = rn + pitch;
+        // prefetch row i + 2 (and f of row i + 1); rows past the frame are not read
+        const bool pre = i + 2 <= a.H && i + 1 < r1;
+        Q4 vn, p1n, p2n, un, fn;
+        uchar4 labn = make_uchar4(0, 0, 0, 0);
+        if (pre) {
+            vn = ld_swz(a.v + rnn);
+            p1n = ld_swz(a.p1 + rnn);
+            p2n = ld_swz(a.p2 + rnn);
+            un = ld_nat(a.u + rnn);
+            labn = *reinterpret_cast<const uchar4 *>(a.lab + rnn);
+        }
+        if (i + 1 < r1) fn = ld_nat(a.f + rn);
         Q4 dd, upd;
         div_row(p1d, p1, p2d, dd);
         uprime(labd, ud, dd, upd);
@@ -169,9 +191,10 @@ __global__ void __launch_bounds__(256) k_energy_strip(const EnergyArgs a, int n_
         const float ur = __shfl_down_sync(0xffffffffu, u.x[0], 1);
         const float upr = __shfl_down_sync(0xffffffffu, up.x[0], 1);
         const uint8_t l[4] = {lab.x, lab.y, lab.z, lab.w};
+        // the row's four columns are summed in fp32 (selects, no branches), then once in fp64
+        float r[NE] = {0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-            if (!inc[e]) continue;
             const float vx = v.x[e], ux = u.x[e], fx = f.x[e];
             const float vnext = e < 3 ? v.x[e + 1] : vr;
             const float unext = e < 3 ? u.x[e + 1] : ur;
@@ -182,19 +205,22 @@ __global__ void __launch_bounds__(256) k_energy_strip(const EnergyArgs a, int n_
             const float gu1 = down ? clamp01(ud.x[e]) - cu : 0.0f;
             const float gu2 = right[e] ? clamp01(unext) - cu : 0.0f;
             const float t = lambda * fx + d.x[e];
-            acc[0] += (double)sqrtf(gv1 * gv1 + gv2 * gv2);
-            acc[1] += (double)fx * (double)vx;
-            acc[2] += (double)sqrtf(gu1 * gu1 + gu2 * gu2);
-            acc[3] += (double)fx * (double)cu;
-            acc[4] += (double)fminf(t, 0.0f);
             const float upx = up.x[e];
             const float g1 = (down ? upd.x[e] : upx) - upx;
             const float g2 = (right[e] ? upnext : upx) - upx;
-            const float tvp = sqrtf(g1 * g1 + g2 * g2);
-            acc[5] += (double)(l[e] == 2 ? tvp : 0.0f);
-            acc[6] += (double)((upx - vx) * (upx - vx));
+            const float tvp = esqrt(g1 * g1 + g2 * g2);
+            const bool in = inc[e];
+            r[0] += in ? esqrt(gv1 * gv1 + gv2 * gv2) : 0.0f;
+            r[1] += in ? fx * vx : 0.0f;
+            r[2] += in ? esqrt(gu1 * gu1 + gu2 * gu2) : 0.0f;
+            r[3] += in ? fx * cu : 0.0f;
+            r[4] += in ? fminf(t, 0.0f) : 0.0f;
+            r[5] += in && l[e] == 2 ? tvp : 0.0f;
+            r[6] += in ? (upx - vx) * (upx - vx) : 0.0f;
         }
-        // carry row i + 1
+#pragma unroll
+        for (int q = 0; q < NE; ++q) acc[q] += (double)r[q];
+        // carry rows i + 1 and i + 2
         p1m = p1;
         v = vd;
         p1 = p1d;
@@ -203,6 +229,12 @@ __global__ void __launch_bounds__(256) k_energy_strip(const EnergyArgs a, int n_
         lab = labd;
         d = dd;
         up = upd;
+        f = fn;
+        vd = vn;
+        p1d = p1n;
+        p2d = p2n;
+        ud = un;
+        labd = labn;
         row = rn;
     }
 #pragma unroll

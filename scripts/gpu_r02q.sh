@@ -2,6 +2,9 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r02q_build.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_vol.py -q > gpurun_out/r02q_pytest_vol.log 2>&1
 tail -3 gpurun_out/r02q_pytest_vol.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_compact.py tests/test_gpu_batch.py -q -k "energy or compact or batch" > gpurun_out/r02q_pytest_energy.log 2>&1
+tail -3 gpurun_out/r02q_pytest_energy.log
+timeout 300 python scripts/energy_time.py C3 C4 > gpurun_out/r02q_energy.jsonl 2>&1; cat gpurun_out/r02q_energy.jsonl
 RDS_VOL_RPT=1 timeout 300 python scripts/bench3d.py > gpurun_out/r02q_bench3d_rpt1.jsonl 2>&1
 timeout 300 python scripts/bench3d.py > gpurun_out/r02q_bench3d_rpt2.jsonl 2>&1
 cat gpurun_out/r02q_bench3d_rpt1.jsonl gpurun_out/r02q_bench3d_rpt2.jsonl
