@@ -91,7 +91,8 @@ typedef struct {
     int32_t check_every;     /* rds_solve_tol: iterations between checks; 0 for rds_solve */
     int32_t compact;         /* 1 if the last solve ran the compacted RD iteration (RDS_OPT_COMPACT) */
     int32_t wave;            /* 1 if the last solve's K-loop ran as the temporal wavefront (RDS_OPT_WAVE) */
-    int32_t resident;        /* 1 if the last solve ran as one resident cluster (RDS_OPT_RESIDENT) */
+    int32_t resident;        /* 1 if the last solve ran as one resident cluster (RDS_OPT_RESIDENT),
+                                2 if resident on the whole GPU (RDS_OPT_GRID), else 0 */
     int32_t persist;         /* 1 if the last solve's K-loop ran as one persistent launch (RDS_OPT_PERSIST) */
 } rds_stats_t;
 
@@ -162,6 +163,22 @@ typedef struct {
                                 2^22 pixels.  Off by default: on B200 the launches are not what
                                 bounds these sizes (C0 0.44 vs 0.46 ms, 256^2..2048^2 2-6%
                                 slower; the item march's row latency is). */
+
+#define RDS_OPT_GRID 12      /* mid-size images (up to 1024 columns and 8 x #SM rows: C1's
+                                1024 x 1024) resident on the whole GPU: every iteration of a
+                                fixed-K solve in ONE cooperative launch, the image in G <= #SM
+                                horizontal slabs of R <= 8 rows, one CTA per SM, the state in
+                                registers, the slab halos exchanged every iteration through an L2
+                                mailbox of {value, tag} words that each thread polls for its own
+                                columns (no grid barrier, no fence; k_grid.cu).
+                                Same per-pixel operations as the stencil (results bit-identical).
+                                Applies to rds_solve / rds_solve_q when the resident cluster
+                                (RDS_OPT_RESIDENT) does not and the G CTAs can be co-resident;
+                                tolerance solves stay on the stencil.  0 (default) = off, 1 and
+                                2 = on where it applies.  Off by default: measured on B200 the
+                                per-iteration exchange (~1 us) plus the barrier-separated short
+                                phases make it slower than the stencil at C1 (3.9 vs 3.0 us per
+                                iteration). */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */

@@ -159,6 +159,25 @@ bool small_plan(int64_t H, int64_t W, int *G, int *R);
 bool small_cluster_fits(const SmallArgs &a);
 cudaError_t launch_small(const SmallArgs &a, cudaStream_t s);
 
+// Mid-size images resident on the whole GPU (k_grid.cu): G <= #SM slabs of R
+// rows, one cooperative CTA each, halos through an L2 mailbox of {value, tag} words.
+struct GridArgs {
+    const float *p1_in, *p2_in, *v_in, *c;   // plane origins (pixel (0,0)), swizzled
+    float *p1_out, *p2_out, *v_out;
+    float *u_out;
+    uint8_t *mask_out;
+    const long long *n_rd;                   // RD pixel count (0: nothing moves), or null
+    unsigned long long *mail;                // [2][G][7][2 * threads] {value, tag} words
+    unsigned tag0;                           // tag of iteration 0 (grows across launches)
+    int64_t pitch;
+    int H, W, img_w, K, G, R;
+    float tau, theta, inv_theta;
+};
+bool grid_plan(int64_t H, int64_t W, int n_sm, int *G, int *R);
+size_t grid_mail_words(int G, int W);
+bool grid_fits(const GridArgs &a);
+cudaError_t launch_grid(const GridArgs &a, cudaStream_t s);
+
 // The fixed-K K-loop as one persistent launch (k_loop.cu): nblk blocks of KF
 // iterations over the same work items, block b reading ping-pong buffer (c0 + b) & 1, a grid
 // (or cluster) barrier between blocks, the last block writing u and the mask.

@@ -112,6 +112,12 @@ struct rds_handle {
     unsigned long long *loop_bar = nullptr;  // grid-barrier counter of k_loop
     int resident_fit = 0; // cached cluster schedulability for (resident_G, resident_R): 1 / -1
     int resident_G = 0, resident_R = 0;
+    int opt_grid = 0;     // mid-size images resident on the whole GPU: 0 off (default), 1 / 2 on (RDS_OPT_GRID)
+    int grid_fit = 0;     // cached co-residency of (grid_G, grid_R): 1 / -1
+    int grid_G = 0, grid_R = 0;
+    unsigned long long *grid_mail = nullptr;  // k_grid's halo mailbox ({value, tag} words)
+    size_t grid_mail_n = 0;
+    unsigned grid_tag = 1;       // tag of the next k_grid launch's iteration 0
     int32_t *wave_prog = nullptr;  // progress counters [blocks][strips] of k_wave
     size_t wave_prog_bytes = 0;
     // compacted RD iteration (k_rdc.cu): index map, row counts/offsets, total, compact arrays
@@ -168,7 +174,7 @@ static void free_all(rds_t *h) {
                      h->stop,    h->chk,         h->d64,     h->part64,    h->cmp_out,
                      h->lab64,   h->stop64,      h->bar64,       h->rows_buf,
                      h->rdc_idx, h->rdc_row,     h->rdc_buf,   h->rdc_bar, h->rdc_part,
-                     h->wave_prog, h->loop_bar};  // rdc_tot points into rdc_row
+                     h->wave_prog, h->loop_bar, h->grid_mail};  // rdc_tot points into rdc_row
     for (void *p : other)
         if (p) cudaFree(p);
     if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -338,6 +344,11 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             if (value < 0 || value > 2)
                 return fail(h, RDS_EINVAL, "rds_set_option: resident=%lld", (long long)value);
             h->opt_resident = (int)value;
+            return RDS_OK;
+        case RDS_OPT_GRID:
+            if (value < 0 || value > 2)
+                return fail(h, RDS_EINVAL, "rds_set_option: grid=%lld", (long long)value);
+            h->opt_grid = (int)value;
             return RDS_OK;
         case RDS_OPT_WAVE:
             if (value < 0 || value > 2)
@@ -1181,8 +1192,62 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
         small_use = h->resident_fit > 0;
     }
 
+    // mid-size images: the whole fixed-K loop resident on the GPU (k_grid.cu), G <= #SM slabs
+    // with L2-mailbox halos, where the small-image cluster does not apply
+    GridArgs ga{};
+    bool grid_use = false;
+    if (iters > 0 && check_every == 0 && h->opt_grid && h->opt_compact != 1 && !small_use &&
+        grid_plan(h->H, h->W, h->n_sm, &ga.G, &ga.R)) {
+        ga.p1_in = h->at(h->p1[0]);
+        ga.p2_in = h->at(h->p2[0]);
+        ga.v_in = h->at(h->v[0]);
+        ga.c = h->at(h->c);
+        ga.p1_out = h->at(h->p1[0]);
+        ga.p2_out = h->at(h->p2[0]);
+        ga.v_out = h->at(h->v[0]);
+        ga.u_out = h->at(h->u);
+        ga.mask_out = h->at(h->mask);
+        ga.n_rd = h->n_rd_dev;
+        ga.pitch = h->pitch;
+        ga.H = (int)h->H;
+        ga.W = (int)h->W;
+        ga.img_w = (int)h->img_w;
+        ga.K = iters;
+        ga.tau = tau;
+        ga.theta = theta;
+        ga.inv_theta = 1.0f / theta;
+        if (h->grid_G != ga.G || h->grid_R != ga.R || h->grid_fit == 0) {
+            h->grid_G = ga.G;
+            h->grid_R = ga.R;
+            h->grid_fit = grid_fits(ga) ? 1 : -1;
+        }
+        grid_use = h->grid_fit > 0;
+        if (grid_use) {
+            const size_t n = grid_mail_words(ga.G, ga.W);
+            if (n > h->grid_mail_n) {
+                if (h->grid_mail) cudaFree(h->grid_mail);
+                h->grid_mail = nullptr;
+                h->grid_mail_n = 0;
+                CK(h, cudaMalloc(&h->grid_mail, sizeof(unsigned long long) * n));
+                CK(h, cudaMemsetAsync(h->grid_mail, 0, sizeof(unsigned long long) * n,
+                                      h->stream));
+                h->grid_mail_n = n;
+                h->grid_tag = 1;
+            }
+            if ((unsigned long long)h->grid_tag + (unsigned)iters + 1 >= (1ull << 31)) {
+                // tags would wrap: start over from a cleared mailbox
+                CK(h, cudaMemsetAsync(h->grid_mail, 0, sizeof(unsigned long long) * h->grid_mail_n,
+                                      h->stream));
+                h->grid_tag = 1;
+            }
+            ga.mail = h->grid_mail;
+            ga.tag0 = h->grid_tag;
+            h->grid_tag += (unsigned)iters + 1;
+        }
+    }
+
     CompactPlan cplan;
-    if (iters > 0 && h->opt_compact && !small_use) {
+    if (iters > 0 && h->opt_compact && !small_use && !grid_use) {
         const int rc = compact_prepare(h, tau, theta, iters, &cplan);
         if (rc) return rc;
     }
@@ -1195,6 +1260,10 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
         NvtxRange nvtx_small("rds_solve (resident cluster)");
         CK(h, launch_small(sa, h->stream));
         h->cur0 = h->cur;  // the final state is written back into the same buffer
+    } else if (grid_use) {
+        NvtxRange nvtx_grid("rds_solve (resident grid)");
+        CK(h, launch_grid(ga, h->stream));
+        h->cur0 = h->cur;
     } else if (iters > 0 && cplan.use) {
         NvtxRange nvtx_rdc("rds_solve (compact RD)");
         TolParams tp;
@@ -1275,11 +1344,11 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     st.n_items = (int64_t)n_strips * n_bands;
     st.iters = iters;
     st.k_fuse = kf;
-    st.launches = (cplan.use || small_use) ? 1 : launches;
+    st.launches = (cplan.use || small_use || grid_use) ? 1 : launches;
     st.compact = cplan.use ? 1 : 0;
-    st.wave = (!cplan.use && !small_use && wave_blocks(h, kf, iters, check_every) > 0) ? 1 : 0;
-    st.resident = small_use ? 1 : 0;
-    st.persist = (!cplan.use && !small_use && persist_applies(h, kf, iters, check_every)) ? 1 : 0;
+    st.wave = (!cplan.use && !small_use && !grid_use && wave_blocks(h, kf, iters, check_every) > 0) ? 1 : 0;
+    st.resident = small_use ? 1 : grid_use ? 2 : 0;
+    st.persist = (!cplan.use && !small_use && !grid_use && persist_applies(h, kf, iters, check_every)) ? 1 : 0;
     st.converged = 0;
     st.residual = -1.0f;
     st.check_every = check_every;

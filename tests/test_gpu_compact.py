@@ -29,9 +29,9 @@ def rds():
 
 
 def _run(rds, z, delta, K, compact, batch=None, kf=0, lam=5.0, warm=None, P=None, gamma=0.0,
-         resident=None):
+         resident=None, grid=None):
     H, W = z.shape[-2:] if batch else z.shape
-    kw = dict(compact=compact, k_fuse=kf, resident=resident)
+    kw = dict(compact=compact, k_fuse=kf, resident=resident, grid=grid)
     s = rds.BatchSolver(batch, H, W, **kw) if batch else rds.Solver(H, W, **kw)
     s.set_image(z)
     s.set_fitting(0.8, 0.2, gamma, P)
@@ -97,7 +97,7 @@ def test_compact_variants(rds):
     _, c = _run(rds, z, np.float32(0.2), 15, 1, warm=warm)
     _same(d, c)
     for d in (np.float32(math.inf), np.float32(0.01)):  # small image: dense is launch bound
-        s, _ = _run(rds, z, d, 5, 2, resident=0)
+        s, _ = _run(rds, z, d, 5, 2, resident=0, grid=0)
         assert s.stats()["compact"] == 1
         s, _ = _run(rds, z, d, 5, 2)               # ... and the resident cluster beats both
         assert s.stats()["compact"] == 0 and s.stats()["resident"] == 1

@@ -197,21 +197,24 @@ def test_c4_full_size(rds, orc, c4, dr):
 SHAPES = [(1, 1), (1, 7), (9, 1), (5, 3), (33, 129), (100, 77), (130, 250), (257, 131)]
 
 
-@pytest.mark.parametrize("resident", [0, 2])
+@pytest.mark.parametrize("path", ["stencil", "grid", "default"])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_ragged_shapes(rds, orc, shape, resident):
-    """(resident = 0: the stencil; 2: the library default, the resident cluster where the
-    shape fits one)"""
+def test_ragged_shapes(rds, orc, shape, path):
+    """(stencil: the tiled stencil; grid: resident on the whole GPU, k_grid; default: the
+    library's choice, the resident cluster where the shape fits one)"""
+    opt = {"stencil": dict(resident=0, grid=0, compact=0), "grid": dict(resident=0, grid=1),
+           "default": {}}[path]
     H, W = shape
     z = wl.random_image(H, W, seed=H * 1000 + W)
     for dr in (0.0, 0.3, math.inf):
         f = orc.fitting(z, 0.8, 0.2)
         delta = wl.band_delta(dr, orc.absmax(f))
         for iters in (1, 8, 23):
-            g = gpu_solve(rds, z, None, 0.8, 0.2, 0.0, 5.0, 0.1, 0.125, delta, iters,
-                          resident=resident)
+            g = gpu_solve(rds, z, None, 0.8, 0.2, 0.0, 5.0, 0.1, 0.125, delta, iters, **opt)
             o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, iters)
             assert np.array_equal(g["labels"], o["labels"])
+            if path == "grid":
+                assert g["stats"]["resident"] == 2
             compare(g, o, tol=1e-5, mask_frac=0.0 if H * W < 2000 else MASK_FRAC,
                     ctx=f"{shape} d={dr} K={iters}")
 
@@ -227,7 +230,7 @@ def test_every_fusion_depth(rds, orc, kf, persist):
     delta = wl.band_delta(0.4, orc.absmax(f))
     for iters in (kf, 2 * kf + 1, 3 * kf + kf - 1):
         g = gpu_solve(rds, z, None, 0.75, 0.25, 0.0, 2.0, 0.1, 0.125, delta, iters, k_fuse=kf,
-                      item_rows=40, resident=0, persist=persist, compact=0)
+                      item_rows=40, resident=0, grid=0, persist=persist, compact=0)
         o = orc.solve(f, delta, 2.0, np.float32(0.1), 0.125, iters)
         compare(g, o, tol=1e-5, ctx=f"kf={kf} K={iters}")
 
@@ -243,7 +246,7 @@ def test_warm_start_random_state(rds, orc):
         delta = wl.band_delta(dr, orc.absmax(f))
         for iters in (1, 2, 9):
             g = gpu_solve(rds, z, None, 0.8, 0.2, 0.0, 5.0, 0.1, 0.125, delta, iters,
-                          init=(v, p1, p2), resident=0)
+                          init=(v, p1, p2), resident=0, grid=0)
             o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, iters,
                           init=(v.astype(np.float64), p1.astype(np.float64),
                                 p2.astype(np.float64)))
@@ -258,7 +261,7 @@ def test_fusion_depth_equivalence(rds):
     res = []
     for kf in (1, 3, 7):
         g = gpu_solve(rds, z, P, cfg.c1, cfg.c2, cfg.gamma, 5.0, cfg.theta, cfg.tau,
-                      np.float32(0.2), 23, k_fuse=kf, compact=0)
+                      np.float32(0.2), 23, k_fuse=kf, compact=0, grid=0)
         res.append(g)
     for g in res[1:]:
         for k in ("u", "v", "p1", "p2", "mask"):
@@ -313,14 +316,18 @@ def _run_cfg(rds, orc, name, lam, dr, iters=None, **opt):
 @pytest.mark.parametrize("resident", [0, 2])
 @pytest.mark.parametrize("dr", [0.2, math.inf])
 def test_c0(rds, orc, dr, resident):
-    g, o = _run_cfg(rds, orc, "C0", 5.0, dr, resident=resident)
+    g, o = _run_cfg(rds, orc, "C0", 5.0, dr, resident=resident, grid=0)
     assert g["stats"]["resident"] == (1 if resident else 0)
 
 
+@pytest.mark.parametrize("grid", [0, 1])
 @pytest.mark.parametrize("lam,dr", [(5.0, 0.05), (5.0, 0.1), (5.0, 0.2), (5.0, 0.4),
                                     (2.0, 0.2), (10.0, 0.2), (5.0, math.inf)])
-def test_c1(rds, orc, lam, dr):
-    _run_cfg(rds, orc, "C1", lam, dr)
+def test_c1(rds, orc, lam, dr, grid):
+    """(grid 0: the default, the stencil or the compact path; 1: resident on the GPU)"""
+    g, _ = _run_cfg(rds, orc, "C1", lam, dr, grid=grid)
+    if grid:
+        assert g["stats"]["resident"] == 2
 
 
 @pytest.mark.parametrize("dr", [0.05, 0.1, 0.2, 0.4, math.inf])
@@ -634,15 +641,16 @@ def test_solve_tol_c3_full_size(rds, orc):
     s.close()
 
 
+@pytest.mark.parametrize("grid", [0, 1])
 @pytest.mark.parametrize("shape,kf", [((37, 61), 0), ((64, 128), 7), ((5, 3), 2),
                                       ((130, 250), 5), ((33, 129), 8)])
-def test_frame_untouched(rds, shape, kf):
+def test_frame_untouched(rds, shape, kf, grid):
     """Memory safety without a sanitizer (compute-sanitizer is closed on this pool): after
     solves in every launch mode, warm starts, tolerance and fp64 solves, no element of the
     padded frame around the image has changed (rds_check_frame)."""
     H, W = shape
     z = np.random.default_rng(H * W).uniform(0, 1, shape).astype(np.float32)
-    s = rds.Solver(H, W, k_fuse=kf, compact=0)
+    s = rds.Solver(H, W, k_fuse=kf, compact=0, resident=0, grid=grid)
     s.set_image(z)
     s.set_fitting(0.75, 0.25, 1.5, np.random.default_rng(1).uniform(0, 1, shape).astype(np.float32))
     d = 0.3 * s.absmax()

@@ -30,7 +30,7 @@ def rds():
 
 def _solve(rds, z, delta, K, persist, kf=0, warm=None, batch=None, cont=0):
     H, W = z.shape[-2:] if batch else z.shape
-    kw = dict(k_fuse=kf, persist=persist, resident=0, compact=0)
+    kw = dict(k_fuse=kf, persist=persist, resident=0, grid=0, compact=0)
     s = rds.BatchSolver(batch, H, W, **kw) if batch else rds.Solver(H, W, **kw)
     s.set_image(z)
     s.set_fitting(0.8, 0.2)

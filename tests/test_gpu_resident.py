@@ -31,8 +31,8 @@ def rds():
 
 def _solve(rds, z, delta, K, resident, warm=None, batch=None, P=None, gamma=0.0):
     H, W = z.shape[-2:] if batch else z.shape
-    s = rds.BatchSolver(batch, H, W, resident=resident) if batch else \
-        rds.Solver(H, W, resident=resident)
+    kw = dict(resident=resident, grid=0 if resident == 0 else None)
+    s = rds.BatchSolver(batch, H, W, **kw) if batch else rds.Solver(H, W, **kw)
     s.set_image(z)
     s.set_fitting(0.8, 0.2, gamma, P)
     if warm is not None:
@@ -109,7 +109,8 @@ def test_resident_warm_batch_selection(rds):
 
 
 def test_resident_not_taken(rds):
-    """Tolerance solves and images too large for one cluster stay on the stencil."""
+    """Tolerance solves stay on the stencil; images too large for one cluster go to the stencil,
+    or resident on the whole GPU with RDS_OPT_GRID on (k_grid, stats resident = 2)."""
     z = wl.random_image(128, 128, seed=1)
     s = rds.Solver(128, 128)
     s.set_image(z)
@@ -119,10 +120,11 @@ def test_resident_not_taken(rds):
     s.solve(*PAR, math.inf, 10)
     assert s.stats()["resident"] == 1
     s.close()
-    zb = wl.random_image(300, 300, seed=2)   # slabs of 19 x 300 exceed 200 KB per CTA
-    s = rds.Solver(300, 300)
-    s.set_image(zb)
-    s.set_fitting(0.8, 0.2)
-    s.solve(*PAR, math.inf, 10)
-    assert s.stats()["resident"] == 0
-    s.close()
+    zb = wl.random_image(300, 300, seed=2)   # more than 16 slabs: no single cluster
+    for grid, want in ((None, 0), (1, 2)):
+        s = rds.Solver(300, 300, grid=grid)
+        s.set_image(zb)
+        s.set_fitting(0.8, 0.2)
+        s.solve(*PAR, math.inf, 10)
+        assert s.stats()["resident"] == want
+        s.close()

@@ -32,8 +32,8 @@ def rds():
 
 def _solve(rds, z, delta, K, wave, kf, warm=None, batch=None, cont=0, skip=True):
     H, W = z.shape[-2:] if batch else z.shape
-    s = rds.BatchSolver(batch, H, W, k_fuse=kf, wave=wave, skip=skip, resident=0, compact=0) if batch \
-        else rds.Solver(H, W, k_fuse=kf, wave=wave, skip=skip, resident=0, compact=0)
+    s = rds.BatchSolver(batch, H, W, k_fuse=kf, wave=wave, skip=skip, resident=0, grid=0, compact=0) if batch \
+        else rds.Solver(H, W, k_fuse=kf, wave=wave, skip=skip, resident=0, grid=0, compact=0)
     s.set_image(z)
     s.set_fitting(0.8, 0.2)
     if warm is not None:
@@ -112,7 +112,7 @@ def test_wave_not_taken(rds):
     """No wavefront where it does not apply: a tolerance solve, fewer than two full blocks,
     an unsupported k_fuse, a width that is not a multiple of 4."""
     z = wl.gen_voronoi(N=200, seed=1, n_sites=8)[:200, :200].copy()
-    s = rds.Solver(200, 200, wave=1, k_fuse=6, resident=0, compact=0)
+    s = rds.Solver(200, 200, wave=1, k_fuse=6, resident=0, grid=0, compact=0)
     s.set_image(z)
     s.set_fitting(0.8, 0.2)
     s.solve(*PAR, np.float32(0.3), 11)
@@ -122,13 +122,13 @@ def test_wave_not_taken(rds):
     st = s.solve_tol(*PAR, np.float32(0.3), 100, 1e-3, 6)
     assert st["wave"] == 0
     s.close()
-    s = rds.Solver(200, 198, wave=1, k_fuse=6, resident=0, compact=0)
+    s = rds.Solver(200, 198, wave=1, k_fuse=6, resident=0, grid=0, compact=0)
     s.set_image(z[:, :198].copy())
     s.set_fitting(0.8, 0.2)
     s.solve(*PAR, np.float32(0.3), 40)
     assert s.stats()["wave"] == 0
     s.close()
-    s = rds.Solver(200, 200, wave=1, k_fuse=3, resident=0, compact=0)
+    s = rds.Solver(200, 200, wave=1, k_fuse=3, resident=0, grid=0, compact=0)
     s.set_image(z)
     s.set_fitting(0.8, 0.2)
     s.solve(*PAR, np.float32(0.3), 40)
