@@ -119,7 +119,10 @@ __device__ __forceinline__ Q4 ld_swz(const float *p) {  // quad-swizzled: x0 x2 
     return Q4{{q.x, q.z, q.y, q.w}};
 }
 
-__global__ void __launch_bounds__(256) k_energy_strip(const EnergyArgs a, int n_strips,
+#ifndef RDS_ENERGY_MINB
+#define RDS_ENERGY_MINB 1
+#endif
+__global__ void __launch_bounds__(256, RDS_ENERGY_MINB) k_energy_strip(const EnergyArgs a, int n_strips,
                                                       int chunk, int n_items) {
     const int lane = threadIdx.x & 31;
     const int item = blockIdx.x * 8 + (threadIdx.x >> 5);
