@@ -389,15 +389,20 @@ const char *rds_version(void);
  * The same method on a D x H x W volume (plane-major, row-major planes): voxel labels and
  * fitting term as above; grad = forward differences along rows, columns and planes with a
  * zero last row / column / plane, div = -grad^T, rho = (rho1 rows, rho2 columns, rho3 planes)
- * (reading R-F4).  tau must be in (0, 1/12] (||grad||^2 <= 12 in 3-D).  One fused
- * pass per iteration (k_vol_step), the K-loop replayed from a CUDA graph.  Errors as for the
- * 2-D calls; the buffers are D*H*W elements. */
+ * (reading R-F4).  tau must be in (0, 1/12] (||grad||^2 <= 12 in 3-D).  k_fuse
+ * iterations per fused pass over the volume (1, the default: k_vol_step, one pass per
+ * iteration; 2-3: k_vol_tb, temporal blocking along the plane axis, measured slower on B200),
+ * the K-loop replayed from a CUDA graph.
+ * Errors as for the 2-D calls; the buffers are D*H*W elements. */
 typedef struct rds3_handle rds3_t;
 int rds3_create(int64_t D, int64_t H, int64_t W, rds3_t **out);
 int rds3_destroy(rds3_t *h);
 int rds3_set_stream(rds3_t *h, void *stream);
-/* planes per CTA z-chunk of k_vol_step (0 = automatic); a tuning knob, results identical */
+/* planes per CTA z-chunk (0 = automatic); a tuning knob, results identical */
 int rds3_set_kz(rds3_t *h, int32_t kz);
+/* iterations per pass over the volume, 1 .. 3 (0 = automatic: 1); every value gives the same
+ * bits (the passes run the same per-voxel operations in the same order); RDS_EINVAL outside */
+int rds3_set_kfuse(rds3_t *h, int32_t kf);
 int rds3_set_image(rds3_t *h, const float *z, int on_device);
 int rds3_set_fitting(rds3_t *h, float c1, float c2, float gamma, const float *P, int on_device);
 int rds3_fitting_absmax(rds3_t *h, float *out);

@@ -344,7 +344,8 @@ cudaError_t launch_compare(const float *u, const double *ugt, int64_t pitch, int
 
 // f4: 3-D volumes (k_vol.cu).  Padded volume: VOL_PZ frame planes before/after, VOL_PY_TOP
 // rows above and VOL_PY_BOT below each plane, VOL_PX_L columns left, >= VOL_PX_R right.
-constexpr int VOL_PZ = 2, VOL_PY_TOP = 2, VOL_PY_BOT = 32, VOL_PX_L = 4, VOL_PX_R = 32;
+constexpr int VOL_PZ = 4, VOL_PY_TOP = 8, VOL_PY_BOT = 32, VOL_PX_L = 8, VOL_PX_R = 32;
+constexpr int VOL_TB_MAX = 3, VOL_TB_DEFAULT = 1;  // k_vol_tb measured slower on B200  // iterations per pass of k_vol_tb (frame: VOL_PZ >= S + 1, 2S rows / columns)
 struct VolArgs {
     const float *p1_in, *p2_in, *p3_in, *v_in, *c;   // voxel (0,0,0) origins
     float *p1_out, *p2_out, *p3_out, *v_out, *u_out;
@@ -364,6 +365,10 @@ struct VolSetupArgs {
 };
 cudaError_t launch_vol_step(const VolArgs &a, bool write_u, cudaStream_t s);
 int64_t vol_tiles(int64_t H, int64_t W);  // CTA (i, j) tiles of k_vol_step
+// S iterations per pass (k_vol_tb, S = 1 .. VOL_TB_MAX): launch, (i, j) tiles, CTAs per SM
+cudaError_t launch_vol_tb(const VolArgs &a, int S, bool write_u, cudaStream_t s);
+int64_t vol_tb_tiles(int S, int64_t H, int64_t W);
+int vol_tb_blocks_per_sm(int S);
 cudaError_t launch_vol_setup(const VolSetupArgs &a, cudaStream_t s);
 cudaError_t launch_vol_absmax(const float *z, const float *P, int64_t plane, int64_t pitch,
                               int D, int H, int W, float c1, float c2, float gamma,

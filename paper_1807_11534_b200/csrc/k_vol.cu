@@ -258,6 +258,259 @@ __global__ void __launch_bounds__(VT_X * VT2_Y) k_vol_step2(const VolArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// k_vol_tb<S>: S iterations per pass over the volume (temporal blocking along the plane
+// axis).  The S stages of a CTA are a software pipeline: at plane step n stage s takes the
+// state of level s at plane n - 2s (stage 0 from HBM, stage s > 0 from the registers stage s-1
+// filled at step n - 1), runs the three phases of k_vol_step2 on it (w of that plane, the rho
+// update of the plane before it, the u- and v-steps of that plane) and hands the new level-
+// (s+1) state of plane n - 2s - 1 to stage s+1; the last stage writes it out.  All stages share
+// the phase barriers (three per plane step).  A window of 32 x TY columns loses 2 rows /
+// columns on its low side and 1 on its high side per stage (the dependency cone), so it writes
+// a (32 - 3S) x (TY - 3S) tile; along the planes stage s produces valid state from plane
+// k0 - S + s + 1 on, so the pass starts S planes before its z-chunk and reads up to S - 1
+// planes past it (the frame, VOL_PZ >= S + 1).  Every float operation is k_vol_step's in the
+// same order: S passes of k_vol_tb<1-stage> == S launches of k_vol_step, bit for bit (tested).
+// ---------------------------------------------------------------------------------------
+template <int S, int TY, bool WRITE_U>
+#ifndef RDS_VTB_MINB
+#define RDS_VTB_MINB 1
+#endif
+__global__ void __launch_bounds__(VT_X * TY / 2, RDS_VTB_MINB) k_vol_tb(const VolArgs a) {
+    extern __shared__ float vsm[];
+    constexpr int PL = TY * VT_X;           // one window plane
+    constexpr int OX = VT_X - 3 * S, OY = TY - 3 * S;
+    // per stage: s1, s2 (rho1, rho2 of its plane), sw[2] (w of its plane and the one before),
+    // q1s, q2s (new rho1, rho2 of the plane before)
+    auto S1 = [&](int st) { return vsm + (st * 6 + 0) * PL; };
+    auto S2 = [&](int st) { return vsm + (st * 6 + 1) * PL; };
+    auto SW = [&](int st, int c) { return vsm + (st * 6 + 2 + c) * PL; };
+    auto Q1 = [&](int st) { return vsm + (st * 6 + 4) * PL; };
+    auto Q2 = [&](int st) { return vsm + (st * 6 + 5) * PL; };
+    const int tx = threadIdx.x, ty0 = 2 * threadIdx.y;  // local rows ty0, ty0 + 1
+    const int j = blockIdx.x * OX - 2 * S + tx, i0 = blockIdx.y * OY - 2 * S + ty0;
+    const int k0 = blockIdx.z * a.kz, k1 = min(k0 + a.kz, a.D);
+    const float tau = a.tau, theta = a.theta, inv_theta = a.inv_theta;
+    bool in_w[2], in_q[2], in_o[2], last_i[2];
+    int64_t col[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int ty = ty0 + r, i = i0 + r;
+        col[r] = (int64_t)i * a.pitch + j;
+        in_w[r] = ty >= 1 && tx >= 1;
+        in_q[r] = ty >= 1 && ty <= TY - 2 && tx >= 1 && tx <= VT_X - 2;
+        in_o[r] = ty >= 2 * S && ty <= TY - 1 - S && tx >= 2 * S && tx <= VT_X - 1 - S &&
+                  i < a.H && j < a.W;
+        last_i[r] = i == a.H - 1;
+    }
+    const bool last_j = j == a.W - 1;
+    // per stage and row: the state of the plane before the stage's current one (pp*, pv, pc),
+    // rho3 new of the plane before that (q3prev), and the stage's output of the last step
+    float pp1[S][2], pp2[S][2], pp3[S][2], pv[S][2], pc[S][2], q3prev[S][2];
+    float o1[S][2], o2[S][2], o3[S][2], ov[S][2], oc[S][2];
+#pragma unroll
+    for (int st = 0; st < S; ++st)
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            pp1[st][r] = pp2[st][r] = pp3[st][r] = pv[st][r] = q3prev[st][r] = 0.f;
+            pc[st][r] = INFINITY;
+            o1[st][r] = o2[st][r] = o3[st][r] = ov[st][r] = 0.f;
+            oc[st][r] = INFINITY;
+        }
+    // stage 0 reads planes n0 .. nl (one ahead, in registers); planes past nl are not needed
+    // by any valid output and read as the pinned frame
+    const int n0 = k0 - S - 1, nl = k1 + S - 1, n1 = k1 + 2 * S - 2;
+    float x1[2], x2[2], x3[2], xv[2], xc[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int64_t o = (int64_t)n0 * a.plane + col[r];
+        x1[r] = a.p1_in[o];
+        x2[r] = a.p2_in[o];
+        x3[r] = a.p3_in[o];
+        xv[r] = a.v_in[o];
+        xc[r] = a.c[o];
+    }
+    int cur = 0;
+    for (int n = n0; n <= n1; ++n) {
+        // L: each stage's current plane (stage 0: HBM; stage s: stage s-1's last output)
+        float p1n[S][2], p2n[S][2], p3n[S][2], vn[S][2], cn[S][2];
+#pragma unroll
+        for (int st = S - 1; st >= 0; --st)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                if (st == 0) {
+                    p1n[0][r] = x1[r];
+                    p2n[0][r] = x2[r];
+                    p3n[0][r] = x3[r];
+                    vn[0][r] = xv[r];
+                    cn[0][r] = xc[r];
+                    if (n < nl) {
+                        const int64_t o = (int64_t)(n + 1) * a.plane + col[r];
+                        x1[r] = a.p1_in[o];
+                        x2[r] = a.p2_in[o];
+                        x3[r] = a.p3_in[o];
+                        xv[r] = a.v_in[o];
+                        xc[r] = a.c[o];
+                    } else {
+                        x1[r] = x2[r] = x3[r] = xv[r] = 0.f;
+                        xc[r] = INFINITY;
+                    }
+                } else {
+                    p1n[st][r] = o1[st - 1][r];
+                    p2n[st][r] = o2[st - 1][r];
+                    p3n[st][r] = o3[st - 1][r];
+                    vn[st][r] = ov[st - 1][r];
+                    cn[st][r] = oc[st - 1][r];
+                }
+                S1(st)[(ty0 + r) * VT_X + tx] = p1n[st][r];
+                S2(st)[(ty0 + r) * VT_X + tx] = p2n[st][r];
+            }
+        __syncthreads();
+        // W: w of each stage's current plane
+        float wn[S][2];
+#pragma unroll
+        for (int st = 0; st < S; ++st)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int ty = ty0 + r;
+                wn[st][r] = 0.f;
+                if (in_w[r]) {
+                    const float up1 = r == 1 ? p1n[st][0] : S1(st)[(ty - 1) * VT_X + tx];
+                    const float d = (p1n[st][r] - up1) + (p2n[st][r] - S2(st)[ty * VT_X + tx - 1]) +
+                                    (p3n[st][r] - pp3[st][r]);
+                    wn[st][r] = fmaf(vn[st][r], -inv_theta, d);
+                }
+                SW(st, cur)[ty * VT_X + tx] = wn[st][r];
+            }
+        __syncthreads();
+        // Q: the rho update of each stage's plane before (its plane index m - 1, m = n - 2 st)
+        float q1[S][2], q2[S][2], q3[S][2];
+#pragma unroll
+        for (int st = 0; st < S; ++st) {
+            const bool last_k = n - 2 * st - 1 == a.D - 1;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int ty = ty0 + r;
+                q1[st][r] = q2[st][r] = q3[st][r] = 0.f;
+                if (in_q[r]) {
+                    const float *sw = SW(st, cur ^ 1);
+                    const float w0 = sw[ty * VT_X + tx];
+                    const float g1 = last_i[r] ? 0.f : sw[(ty + 1) * VT_X + tx] - w0;
+                    const float g2 = last_j ? 0.f : sw[ty * VT_X + tx + 1] - w0;
+                    const float g3 = last_k ? 0.f : wn[st][r] - w0;
+                    const float s_ = fmaf(g1, g1, fmaf(g2, g2, fmaf(g3, g3, fabsf(pc[st][r]))));
+                    const float rr = vrcp(fmaf(tau, vsqrt(s_), 1.0f));
+                    q1[st][r] = fmaf(tau, g1, pp1[st][r]) * rr;
+                    q2[st][r] = fmaf(tau, g2, pp2[st][r]) * rr;
+                    q3[st][r] = fmaf(tau, g3, pp3[st][r]) * rr;
+                }
+                Q1(st)[ty * VT_X + tx] = q1[st][r];
+                Q2(st)[ty * VT_X + tx] = q2[st][r];
+            }
+        }
+        __syncthreads();
+        // O: u, v' of each stage's plane before; the new state goes to the next stage (or out)
+#pragma unroll
+        for (int st = 0; st < S; ++st) {
+            const int m = n - 2 * st - 1;  // the plane this stage finishes
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int ty = ty0 + r;
+                float vnew = 0.f, u = 0.f;
+                if (in_w[r]) {
+                    const float qup = r == 1 ? q1[st][0] : Q1(st)[(ty - 1) * VT_X + tx];
+                    const float d = (q1[st][r] - qup) + (q2[st][r] - Q2(st)[ty * VT_X + tx - 1]) +
+                                    (q3[st][r] - q3prev[st][r]);
+                    u = fmaf(-theta, d, pv[st][r]);
+                    vnew = __saturatef(fmaf(pc[st][r], -0x1p100f, u));
+                }
+                if (st == S - 1) {
+                    if (in_o[r] && m >= k0 && m < k1) {
+                        const int64_t oo = (int64_t)m * a.plane + col[r];
+                        a.p1_out[oo] = q1[st][r];
+                        a.p2_out[oo] = q2[st][r];
+                        a.p3_out[oo] = q3[st][r];
+                        a.v_out[oo] = vnew;
+                        if (WRITE_U) {
+                            const float uu = fabsf(pc[st][r]) < INFINITY ? u : pv[st][r];
+                            a.u_out[oo] = uu;
+                            a.mask_out[oo] = uu > 0.5f;
+                        }
+                    }
+                } else {
+                    o1[st][r] = q1[st][r];
+                    o2[st][r] = q2[st][r];
+                    o3[st][r] = q3[st][r];
+                    ov[st][r] = vnew;
+                    oc[st][r] = pc[st][r];
+                }
+                pp1[st][r] = p1n[st][r];
+                pp2[st][r] = p2n[st][r];
+                pp3[st][r] = p3n[st][r];
+                pv[st][r] = vn[st][r];
+                pc[st][r] = cn[st][r];
+                q3prev[st][r] = q3[st][r];
+            }
+        }
+        cur ^= 1;
+    }
+}
+
+#ifndef RDS_VTB_TY
+#define RDS_VTB_TY 32
+#endif
+constexpr int VTB_TY = RDS_VTB_TY;  // window rows of k_vol_tb (32 x 32 columns, 512 threads)
+
+static size_t vol_tb_smem(int S) { return sizeof(float) * 6 * (size_t)S * VTB_TY * VT_X; }
+
+template <int S>
+static cudaError_t launch_tb(const VolArgs &a, bool write_u, cudaStream_t s) {
+    constexpr int OX = VT_X - 3 * S, OY = VTB_TY - 3 * S;
+    dim3 grid((a.W + OX - 1) / OX, (a.H + OY - 1) / OY, (a.D + a.kz - 1) / a.kz);
+    dim3 block(VT_X, VTB_TY / 2);
+    const size_t sm = vol_tb_smem(S);
+    auto fn = write_u ? k_vol_tb<S, VTB_TY, true> : k_vol_tb<S, VTB_TY, false>;
+    cudaError_t e = cudaFuncSetAttribute((const void *)fn,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, block, sm, s>>>(a);
+    return cudaGetLastError();
+}
+
+int64_t vol_tb_tiles(int S, int64_t H, int64_t W) {
+    const int OX = VT_X - 3 * S, OY = VTB_TY - 3 * S;
+    return ((W + OX - 1) / OX) * ((H + OY - 1) / OY);
+}
+
+int vol_tb_blocks_per_sm(int S) {
+    static int cache[VOL_TB_MAX + 1] = {0};
+    if (S < 1 || S > VOL_TB_MAX) return 0;
+    if (cache[S] == 0) {
+        const void *fn = S == 1   ? (const void *)k_vol_tb<1, VTB_TY, false>
+                         : S == 2 ? (const void *)k_vol_tb<2, VTB_TY, false>
+                                  : (const void *)k_vol_tb<3, VTB_TY, false>;
+        int b = 0;
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)vol_tb_smem(S)) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, VT_X * VTB_TY / 2,
+                                                          vol_tb_smem(S)) != cudaSuccess ||
+            b < 1)
+            b = 1;
+        (void)cudaGetLastError();
+        cache[S] = b;
+    }
+    return cache[S];
+}
+
+cudaError_t launch_vol_tb(const VolArgs &a, int S, bool write_u, cudaStream_t s) {
+    switch (S) {
+        case 1: return launch_tb<1>(a, write_u, s);
+        case 2: return launch_tb<2>(a, write_u, s);
+        case 3: return launch_tb<3>(a, write_u, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
 // K1 of the volume path: f (R-A1 order), label, c', u0 / mask, v0 and rho0 = 0 into both
 // buffers; frame voxels are never touched (they keep the allocation-time pinned values).
 __global__ void k_vol_setup(const VolSetupArgs a) {

@@ -29,11 +29,13 @@ struct rds3_handle {
     cudaStream_t own = nullptr, stream = nullptr;
     cudaEvent_t ev[2] = {};
     cudaGraphExec_t graph = nullptr;
-    int gkey_iters = -1, gkey_kz = -1;
+    int gkey_iters = -1, gkey_kz = -1, gkey_kf = -1, gkey_kzt = -1;
+    int launches = 0;                       // launches of the cached K-loop (final buffer)
     float gkey_tau = 0, gkey_theta = 0;
     bool have_image = false, have_fitting = false, solved = false;
     float c1 = 0, c2 = 0, gamma = 0;
     int cur = 0, kz = 0, iters = 0, opt_kz = 0;
+    int opt_kf = 0, kf = 1, kz_tb = 0;     // iterations per pass (k_vol_tb) and its z-chunk
     std::string err;
     float *at(float *b) const { return b + origin; }
     uint8_t *at(uint8_t *b) const { return b + origin; }
@@ -158,6 +160,14 @@ int rds3_set_kz(rds3_t *h, int32_t kz) {
     return RDS_OK;
 }
 
+int rds3_set_kfuse(rds3_t *h, int32_t kf) {
+    if (!h) return RDS_EINVAL;
+    if (kf < 0 || kf > VOL_TB_MAX)
+        return fail3(h, RDS_EINVAL, "rds3_set_kfuse: k_fuse=%d not in 0 .. %d", kf, VOL_TB_MAX);
+    h->opt_kf = kf;
+    return RDS_OK;
+}
+
 // 1 if every value of a padded volume (frame included: zeros) is finite
 static int vol_finite(rds3_t *h, const float *vol, bool *ok) {
     int *flag = nullptr;
@@ -229,7 +239,10 @@ int rds3_fitting_absmax(rds3_t *h, float *out) {
     return RDS_OK;
 }
 
-static cudaError_t enqueue3(rds3_t *h, int iters, float tau, float theta) {
+// The K-loop: kf = 1 one k_vol_step launch per iteration; kf > 1 k_vol_tb launches of kf
+// iterations each (the last one of iters mod kf), ping-ponging the state buffers; the last
+// launch writes u and the mask.  Returns the launch count in *launches.
+static cudaError_t enqueue3(rds3_t *h, int iters, float tau, float theta, int *launches) {
     VolArgs a{};
     a.c = h->at(h->c);
     a.u_out = h->at(h->u);
@@ -239,12 +252,12 @@ static cudaError_t enqueue3(rds3_t *h, int iters, float tau, float theta) {
     a.D = (int)h->D;
     a.H = (int)h->H;
     a.W = (int)h->W;
-    a.kz = h->kz;
     a.tau = tau;
     a.theta = theta;
     a.inv_theta = 1.0f / theta;
-    int cur = h->cur;
-    for (int it = 0; it < iters; ++it) {
+    int cur = h->cur, n = 0;
+    for (int it = 0; it < iters;) {
+        const int step = h->kf > 1 ? (iters - it < h->kf ? iters - it : h->kf) : 1;
         a.p1_in = h->at(h->p1[cur]);
         a.p2_in = h->at(h->p2[cur]);
         a.p3_in = h->at(h->p3[cur]);
@@ -253,11 +266,46 @@ static cudaError_t enqueue3(rds3_t *h, int iters, float tau, float theta) {
         a.p2_out = h->at(h->p2[cur ^ 1]);
         a.p3_out = h->at(h->p3[cur ^ 1]);
         a.v_out = h->at(h->v[cur ^ 1]);
-        const cudaError_t e = launch_vol_step(a, it == iters - 1, h->stream);
+        const bool last = it + step == iters;
+        cudaError_t e;
+        if (h->kf > 1) {
+            a.kz = h->kz_tb;
+            e = launch_vol_tb(a, step, last, h->stream);
+        } else {
+            a.kz = h->kz;
+            e = launch_vol_step(a, last, h->stream);
+        }
         if (e != cudaSuccess) return e;
         cur ^= 1;
+        it += step;
+        ++n;
     }
+    *launches = n;
     return cudaSuccess;
+}
+
+// z-chunk of k_vol_tb<S>: the chunk count whose waves of CTAs (tiles x chunks over the
+// resident slots) times the per-CTA plane steps (kz + 3S) is least
+static int plan_kz_tb(rds3_t *h, int S) {
+    if (h->opt_kz > 0) return (int)(h->opt_kz < h->D ? h->opt_kz : h->D);
+    int dev = 0, n_sm = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    (void)cudaGetLastError();
+    const int64_t tiles = vol_tb_tiles(S, h->H, h->W);
+    const int64_t slots = (int64_t)n_sm * vol_tb_blocks_per_sm(S);
+    int best_kz = (int)h->D;
+    double best = 1e300;
+    for (int64_t c = 1; c <= h->D && c <= 512; ++c) {
+        const int64_t kz = (h->D + c - 1) / c, ce = (h->D + kz - 1) / kz;
+        const int64_t waves = (tiles * ce + slots - 1) / slots;
+        const double cost = (double)waves * (double)(kz + 3 * S);
+        if (cost < best - 1e-9) {
+            best = cost;
+            best_kz = (int)kz;
+        }
+    }
+    return best_kz;
 }
 
 int rds3_solve(rds3_t *h, float lambda, float theta, float tau, float delta, int32_t iters) {
@@ -282,6 +330,8 @@ int rds3_solve(rds3_t *h, float lambda, float theta, float tau, float delta, int
         if (kz < 8 && h->opt_kz <= 0) kz = 8;
         if (kz > h->D) kz = (int)h->D;
         h->kz = kz;
+        h->kf = h->opt_kf > 0 ? h->opt_kf : VOL_TB_DEFAULT;
+        h->kz_tb = h->kf > 1 ? plan_kz_tb(h, h->kf) : 0;
     }
     CK3(h, cudaEventRecord(h->ev[0], h->stream));
     VolSetupArgs s{};
@@ -316,6 +366,7 @@ int rds3_solve(rds3_t *h, float lambda, float theta, float tau, float delta, int
     h->cur = 0;
     if (iters > 0) {
         const bool same = h->graph && h->gkey_iters == iters && h->gkey_kz == h->kz &&
+                          h->gkey_kf == h->kf && h->gkey_kzt == h->kz_tb &&
                           h->gkey_tau == tau && h->gkey_theta == theta;
         if (!same) {
             if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -327,7 +378,7 @@ int rds3_solve(rds3_t *h, float lambda, float theta, float tau, float delta, int
             if (e == cudaSuccess) {
                 cudaStream_t keep = h->stream;
                 h->stream = cap;
-                const cudaError_t e2 = enqueue3(h, iters, tau, theta);
+                const cudaError_t e2 = enqueue3(h, iters, tau, theta, &h->launches);
                 h->stream = keep;
                 e = cudaStreamEndCapture(cap, &g);
                 if (e == cudaSuccess) e = e2;
@@ -341,11 +392,13 @@ int rds3_solve(rds3_t *h, float lambda, float theta, float tau, float delta, int
             }
             h->gkey_iters = iters;
             h->gkey_kz = h->kz;
+            h->gkey_kf = h->kf;
+            h->gkey_kzt = h->kz_tb;
             h->gkey_tau = tau;
             h->gkey_theta = theta;
         }
         CK3(h, cudaGraphLaunch(h->graph, h->stream));
-        if (iters & 1) h->cur = 1;
+        if (h->launches & 1) h->cur = 1;
     }
     CK3(h, cudaEventRecord(h->ev[1], h->stream));
     h->iters = iters;
@@ -413,7 +466,7 @@ int rds3_get_stats(rds3_t *h, int64_t *n_rd, int32_t *iters, int32_t *kz, float 
     CK3(h, cudaStreamSynchronize(h->stream));
     if (n_rd) *n_rd = (int64_t)nrd;
     if (iters) *iters = h->iters;
-    if (kz) *kz = h->kz;
+    if (kz) *kz = h->kf > 1 ? h->kz_tb : h->kz;
     if (loop_ms) CK3(h, cudaEventElapsedTime(loop_ms, h->ev[0], h->ev[1]));
     return RDS_OK;
 }

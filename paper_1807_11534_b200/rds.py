@@ -40,7 +40,8 @@ EXPORTS = (
     "rds_solve_q", "rds_solve_tol", "rds_solve_gt", "rds_get_u_gt", "rds_compare_gt",
     "rds_check_frame", "rds_solve_continue", "rds_get_state_rows", "rds_set_state_rows",
     "rds_set_energy_rows", "rds_continue_check", "rds_abs_histogram",
-    "rds3_create", "rds3_destroy", "rds3_set_stream", "rds3_set_kz", "rds3_set_image",
+    "rds3_create", "rds3_destroy", "rds3_set_stream", "rds3_set_kz", "rds3_set_kfuse",
+    "rds3_set_image",
     "rds3_set_fitting",
     "rds3_fitting_absmax", "rds3_solve", "rds3_get_u", "rds3_get_v", "rds3_get_p",
     "rds3_get_mask", "rds3_get_labels", "rds3_get_stats", "rds3_last_error",
@@ -134,6 +135,7 @@ def _load():
         "rds3_destroy": [P],
         "rds3_set_stream": [P, P],
         "rds3_set_kz": [P, i32],
+        "rds3_set_kfuse": [P, i32],
         "rds3_set_image": [P, P, i],
         "rds3_set_fitting": [P, f, f, f, P, i],
         "rds3_fitting_absmax": [P, ctypes.POINTER(f)],
@@ -592,6 +594,10 @@ class Solver3:
 
     def set_kz(self, kz):
         _check3(_lib.rds3_set_kz(self.h, int(kz)), self.h)
+
+    def set_kfuse(self, kf):
+        """Iterations per pass over the volume (1 .. 3; 0 = automatic, 1)."""
+        _check3(_lib.rds3_set_kfuse(self.h, int(kf)), self.h)
 
     def set_image(self, z):
         p, dev, _k = _buf(z, np.float32, self.shape)

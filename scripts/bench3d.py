@@ -19,6 +19,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="V1")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--kz", default="0", help="comma list of planes per z-chunk (0 = auto)")
+ap.add_argument("--kf", default="0", help="comma list of iterations per pass (0 = auto)")
 args = ap.parse_args()
 cfg = wl.VOL_CONFIGS[args.config]
 z = wl.make_volume(cfg)
@@ -30,7 +31,9 @@ am = s.absmax()
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)
 n = cfg.D * cfg.H * cfg.W
-for kz, dr in [(int(k), dr) for k in args.kz.split(",") for dr in cfg.delta_rels]:
+for kf, kz, dr in [(int(f), int(k), dr) for f in args.kf.split(",") for k in args.kz.split(",")
+                   for dr in cfg.delta_rels]:
+    s.set_kfuse(kf)
     s.set_kz(kz)
     d = wl.band_delta(dr, am)
     s.solve(cfg.lam, cfg.theta, cfg.tau, d, cfg.iters)  # warm (graph capture)
@@ -46,7 +49,7 @@ for kz, dr in [(int(k), dr) for k in args.kz.split(",") for dr in cfg.delta_rels
     info = s.stats()
     gv = n * cfg.iters / (ms * 1e-3) / 1e9
     print(json.dumps({"config": cfg.name, "delta_rel": "inf" if math.isinf(dr) else dr,
-                      "iters": cfg.iters, "ms": ms, "gvoxel_iter_s": gv,
+                      "kf": kf, "iters": cfg.iters, "ms": ms, "gvoxel_iter_s": gv,
                       "rd_frac": info["n_rd"] / n, "kz": info["kz"],
                       "hbm_roofline": {"achieved_gbs": 36 * gv, "peak": peak,
                                        "frac": 36 * gv / peak}}), flush=True)

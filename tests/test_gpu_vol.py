@@ -140,3 +140,41 @@ def test_vol_errors(rds):
     s.solve(1.0, 0.1, 1 / 12, 0.5, 10)
     assert s.u().shape == (4, 5, 6)
     s.close()
+
+
+@pytest.mark.parametrize("shape", [(3, 5, 7), (9, 17, 40), (40, 14, 70), (33, 61, 29),
+                                   (70, 40, 100)])
+def test_vol_kfuse_bitwise(rds, shape):
+    """k_fuse 1, 2, 3 iterations per pass over the volume (k_vol_step / k_vol_tb) and
+    several z-chunk sizes give the same bits: the temporally blocked passes run the same
+    per-voxel operations in the same order; K not a multiple of k_fuse exercises the
+    remainder pass."""
+    rng = np.random.default_rng(sum(shape) + 7)
+    z = rng.uniform(0, 1, shape).astype(np.float32)
+    res = {}
+    for kf, kz in ((1, 0), (2, 0), (3, 0), (2, 5), (3, 8)):
+        for K in (1, 2, 5, 7):
+            s = rds.Solver3(*shape)
+            s.set_kfuse(kf)
+            s.set_kz(kz)
+            s.set_image(z)
+            s.set_fitting(0.75, 0.25)
+            d = 0.3 * s.absmax()
+            s.solve(4.0, 0.1, TAU3, d, K)
+            p1, p2, p3 = s.p()
+            out = (s.u(), s.v(), p1, p2, p3, s.mask())
+            s.close()
+            if K in res:
+                for a, b in zip(res[K], out):
+                    assert np.array_equal(a, b), (shape, kf, kz, K)
+            else:
+                res[K] = out
+
+
+def test_vol_kfuse_errors(rds):
+    s = rds.Solver3(4, 5, 6)
+    for bad in (-1, 4):
+        with pytest.raises(rds.RdsError) as ei:
+            s.set_kfuse(bad)
+        assert ei.value.code == rds.RDS_EINVAL
+    s.close()
