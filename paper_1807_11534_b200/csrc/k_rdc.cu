@@ -413,8 +413,9 @@ static int grid_of(int n_sm) {
             (void)cudaGetLastError();
             b = 1;
         }
-        static const int cap = getenv("RDS_RDC_MAXB") ? atoi(getenv("RDS_RDC_MAXB")) : 3;
-        if (b > cap) b = cap;  // fewer CTAs: a cheaper grid barrier (one atomic per CTA)
+        static const int cap = getenv("RDS_RDC_MAXB") ? atoi(getenv("RDS_RDC_MAXB")) : 2;
+        if (b > cap) b = cap;  // fewer CTAs: a cheaper grid barrier (2 per SM: C3 δ = .1 -5%,
+                               // profiles/r02/r02aj_compact_maxb.txt)
     }
     return b * n_sm;
 }
