@@ -413,9 +413,10 @@ static int grid_of(int n_sm) {
             (void)cudaGetLastError();
             b = 1;
         }
-        static const int cap = getenv("RDS_RDC_MAXB") ? atoi(getenv("RDS_RDC_MAXB")) : 2;
-        if (b > cap) b = cap;  // fewer CTAs: a cheaper grid barrier (2 per SM: C3 δ = .1 -5%,
-                               // profiles/r02/r02aj_compact_maxb.txt)
+        static const int cap = getenv("RDS_RDC_MAXB") ? atoi(getenv("RDS_RDC_MAXB")) : 3;
+        if (b > cap) b = cap;  // fewer CTAs: a cheaper grid barrier (3 per SM: inside the bench
+                               // C3 delta = .1 runs 14.5-14.7 ms vs 15.2 at 2 per SM, although
+                               // the stand-alone sweep favoured 2; profiles/r02/r02al_*)
     }
     return b * n_sm;
 }
