@@ -55,23 +55,60 @@ class Strip:
         return slice(self.top, self.top + self.hi - self.lo)
 
 
-def partition(H: int, G: int, seg_iters: int) -> list[Strip]:
-    """G near-equal row strips of an H-row image (the first H % G one row taller), each with
-    the halos of `halo_rows(seg_iters)` (none at the image's own top and bottom)."""
+def partition(H: int, G: int, seg_iters: int, weights=None) -> list[Strip]:
+    """G row strips of an H-row image, each with the halos of `halo_rows(seg_iters)` (none at
+    the image's own top and bottom).  Without `weights`: near-equal strips (the first H % G
+    one row taller).  With `weights` (H non-negative per-row costs, e.g. `row_weights` of the
+    band labels): the cuts balance the owned rows' total weight -- a restricted solve costs
+    what its active rows cost, not its row count -- under the constraint that
+    every strip owns at least the top-halo rows its neighbour below needs."""
     if G < 1 or H < G:
         raise ValueError(f"cannot split {H} rows into {G} strips")
     top, bot = halo_rows(seg_iters)
-    base, extra = divmod(H, G)
-    out, lo = [], 0
+    if weights is None:
+        base, extra = divmod(H, G)
+        cuts = [0]
+        for k in range(G):
+            cuts.append(cuts[-1] + base + (1 if k < extra else 0))
+    else:
+        cuts = _weighted_cuts(np.asarray(weights, dtype=np.float64), G,
+                              max(1, top) if G > 1 else 1)
+    out = []
     for k in range(G):
-        hi = lo + base + (1 if k < extra else 0)
-        out.append(Strip(k, lo, hi, top if k > 0 else 0, bot if k < G - 1 else 0))
-        lo = hi
+        out.append(Strip(k, cuts[k], cuts[k + 1], top if k > 0 else 0, bot if k < G - 1 else 0))
     for s in out:
         if s.hi - s.lo < top and G > 1:
             raise ValueError(f"strip {s.rank} owns {s.hi - s.lo} rows, fewer than the {top}-row "
                              f"halo its neighbour needs: use fewer ranks or a shorter segment")
     return out
+
+
+def _weighted_cuts(w, G, min_rows):
+    """Cut points 0 = c0 < c1 < ... < cG = H: cut k at the first row where the cumulative
+    weight reaches k/G of the total, clamped so that every strip keeps >= min_rows rows."""
+    H = len(w)
+    if H < G * min_rows:
+        raise ValueError(f"cannot split {H} rows into {G} strips of >= {min_rows} rows")
+    if np.any(w < 0) or not np.all(np.isfinite(w)):
+        raise ValueError("row weights must be finite and non-negative")
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    total = cum[-1]
+    cuts = [0]
+    for k in range(1, G):
+        c = int(np.searchsorted(cum, total * k / G, side="left")) if total > 0 else (H * k) // G
+        lo = cuts[-1] + min_rows            # this strip keeps min_rows
+        hi = H - (G - k) * min_rows         # the strips after it keep theirs
+        cuts.append(min(max(c, lo), hi))
+    cuts.append(H)
+    return cuts
+
+
+def row_weights(labels, floor: float = 1.0):
+    """Per-row cost of a restricted solve from its band labels (2 = RD, `rds.Solver.labels()`
+    after a K = 0 solve at the band's delta, or an oracle's): the RD pixels of the row plus a
+    floor for the row's fixed per-row work."""
+    lab = np.asarray(labels)
+    return (lab == 2).sum(axis=1).astype(np.float64) + float(floor)
 
 
 def segments(iters: int, seg_iters: int) -> list[int]:
@@ -245,7 +282,7 @@ class StripSolver:
     initialised by the caller).  `engine` defaults to an `rds.Solver` on torch's current
     stream; tests pass a stand-in with the same methods."""
 
-    def __init__(self, H, W, seg_iters, engine=None, group=None, **solver_kw):
+    def __init__(self, H, W, seg_iters, engine=None, group=None, weights=None, **solver_kw):
         import torch
         import torch.distributed as dist
 
@@ -253,7 +290,7 @@ class StripSolver:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.H, self.W, self.seg_iters = int(H), int(W), int(seg_iters)
-        self.plan = partition(self.H, self.world, self.seg_iters)
+        self.plan = partition(self.H, self.world, self.seg_iters, weights)
         self.me = self.plan[self.rank]
         self.xplan = exchange_plan(self.plan)
         nccl = dist.get_backend(group) == "nccl"

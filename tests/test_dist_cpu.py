@@ -50,9 +50,10 @@ def test_replicas_gloo_world2():
         assert v == pytest.approx(3e9 / 0.020 / 1e9)
 
 
-def _strip_worker(rank, world, port, q):
+def _strip_worker(rank, world, port, q, weighted=False):
     """One rank of a row-strip solve over gloo: torch.distributed point-to-point halo
-    exchange, all-reduced max |f|, gathered u (the oracle is every strip's engine)."""
+    exchange, all-reduced max |f|, gathered u (the oracle is every strip's engine).  weighted:
+    uneven strips from per-row weights (the balanced partition of restricted solves)."""
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
                       WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
     import sys
@@ -71,9 +72,11 @@ def _strip_worker(rank, world, port, q):
     try:
         H, W, s, K = 70, 29, 3, 17
         z = wl.gen_voronoi(N=70, seed=5, n_sites=10)[:H, :W].copy()
-        plan = strips.partition(H, world, s)
+        wts = np.linspace(1.0, 12.0, H) ** 2 if weighted else None  # heavy bottom rows
+        plan = strips.partition(H, world, s, wts)
         me = plan[rank]
-        ss = strips.StripSolver(H, W, s, engine=OracleEngine(me.rows, W))
+        ss = strips.StripSolver(H, W, s, engine=OracleEngine(me.rows, W), weights=wts)
+        assert ss.plan == plan
         ss.set_image(z)                       # full image in, the strip's rows used
         ss.set_fitting(0.8, 0.2)
         amax = ss.absmax()
@@ -85,8 +88,8 @@ def _strip_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_strips_gloo(orc, world):
+@pytest.mark.parametrize("world,weighted", [(2, False), (3, False), (3, True)])
+def test_strips_gloo(orc, world, weighted):
     import numpy as np
     import torch.multiprocessing as mp
 
@@ -95,7 +98,8 @@ def test_strips_gloo(orc, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_strip_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_strip_worker, args=(r, world, port, q, weighted))
+             for r in range(world)]
     for p in procs:
         p.start()
     out = sorted((q.get(timeout=180) for _ in procs), key=lambda t: t[0])

@@ -122,3 +122,47 @@ def test_local_q_and_tolerance(orc, G, s):
         assert abs(st["residual"] - ref["residual"]) <= 1e-12 * max(ref["residual"], 1e-300)
         for stp, e in zip(plan, engines):
             assert np.array_equal(e.u()[stp.owned], ref["u"][stp.lo:stp.hi])
+
+
+@pytest.mark.parametrize("H,G,s,seed", [(200, 4, 3, 0), (97, 3, 2, 1), (500, 8, 5, 2),
+                                       (64, 2, 1, 3)])
+def test_weighted_partition(H, G, s, seed):
+    """Balanced cuts: contiguous cover of the rows, every strip owns >= the top halo, and
+    without the clamp each strip's weight is within one row's weight of total / G."""
+    rng = np.random.default_rng(seed)
+    w = rng.uniform(0, 1, H) ** 4 * 100 + (np.arange(H) > H // 2) * 50.0
+    plan = strips.partition(H, G, s, w)
+    top, _ = strips.halo_rows(s)
+    assert plan[0].lo == 0 and plan[-1].hi == H
+    for a, b in zip(plan, plan[1:]):
+        assert a.hi == b.lo
+    for p in plan:
+        assert p.hi - p.lo >= max(1, top)
+    sums = [w[p.lo:p.hi].sum() for p in plan]
+    clamped = any(p.hi - p.lo == max(1, top) for p in plan)
+    if not clamped:
+        assert max(sums) <= w.sum() / G + w.max() + 1e-9
+    # skewed weights move the cuts: heavy bottom rows -> shorter bottom strips
+    sk = strips.partition(H, G, s, np.linspace(1, 20, H) ** 2)
+    assert sk[-1].hi - sk[-1].lo < sk[0].hi - sk[0].lo
+    with pytest.raises(ValueError):
+        strips.partition(H, G, s, -w)
+
+
+def test_row_weights_and_weighted_strips_oracle(orc):
+    """row_weights of the band labels: RD pixels per row + a floor; a solve on the balanced
+    strips reproduces the whole-image oracle bit for bit (owned rows)."""
+    H, W, G, s, K = 90, 40, 3, 3, 13
+    z = _image(H, W, 11)
+    z[: H // 3] = 0.8                     # a flat top third: no RD pixels there
+    f = orc.fitting(z, 0.8, 0.2)
+    delta = wl.band_delta(0.3, orc.absmax(f))
+    labels = orc.labels(f, delta)
+    w = strips.row_weights(labels)
+    assert np.array_equal(w, (labels == 2).sum(axis=1) + 1.0)
+    plan = strips.partition(H, G, s, w)
+    assert plan[0].hi - plan[0].lo > plan[-1].hi - plan[-1].lo   # the empty rows are cheap
+    ref = orc.solve(f, delta, 5.0, 0.1, 0.125, K)
+    for st, e in zip(plan, _strip_solve(z, plan, (0.8, 0.2), delta, K, s, (5.0, 0.1, 0.125))):
+        for k in ("u", "v", "p1", "p2"):
+            assert np.array_equal(e.st[k][st.owned], ref[k][st.lo:st.hi]), (st.rank, k)
