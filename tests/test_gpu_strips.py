@@ -285,3 +285,32 @@ def test_abs_histogram_and_continue_check(rds, orc):
         s.abs_histogram(0, H + 1, 0, 0, 24)
     s.close()
     ref.close()
+
+
+def test_strips_weighted_cuts_bitwise(rds):
+    """Balanced cuts from the GPU's own band labels (a K = 0 solve, strips.row_weights):
+    uneven strips, still bit-identical to the whole-image solve."""
+    H, W, G, s, K = 300, 160, 3, 5, 27
+    z = _image(H, W, 77)
+    z[: H // 2] = 0.8                          # flat upper half: no RD pixels there
+    ref = rds.Solver(H, W)
+    ref.set_image(z)
+    ref.set_fitting(0.8, 0.2)
+    delta = wl.band_delta(0.3, ref.absmax())
+    ref.solve(*PAR, delta, 0)
+    w = strips.row_weights(ref.labels())
+    plan = strips.partition(H, G, s, w)
+    assert plan[0].hi - plan[0].lo > plan[-1].hi - plan[-1].lo
+    ref.solve(*PAR, delta, K)
+    want = _state(ref)
+    engines = []
+    for st in plan:
+        e = rds.Solver(st.rows, W)
+        e.set_image(z[st.r0:st.r0 + st.rows])
+        e.set_fitting(0.8, 0.2)
+        engines.append(e)
+    strips.solve_local(engines, plan, *PAR, delta, K, s)
+    for st, e in zip(plan, engines):
+        got = _state(e)
+        for k in got:
+            assert np.array_equal(got[k][st.owned], want[k][st.lo:st.hi]), (st.rank, k)
