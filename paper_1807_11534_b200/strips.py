@@ -103,12 +103,23 @@ def _weighted_cuts(w, G, min_rows):
     return cuts
 
 
-def row_weights(labels, floor: float = 1.0):
-    """Per-row cost of a restricted solve from its band labels (2 = RD, `rds.Solver.labels()`
-    after a K = 0 solve at the band's delta, or an oracle's): the RD pixels of the row plus a
-    floor for the row's fixed per-row work."""
-    lab = np.asarray(labels)
-    return (lab == 2).sum(axis=1).astype(np.float64) + float(floor)
+def row_weights(labels, floor: float = 1.0, cell=(8, 112)):
+    """Per-row cost of a restricted solve from its band labels (2 = RD; `rds.Solver.labels()`
+    after a K = 0 solve at the band's delta, or an oracle's).  cell = (rows, cols): the
+    stencil's work unit, a band of `rows` rows by `cols` output columns, runs whole when it
+    holds any RD pixel, so a row costs the active cells of its band, plus a
+    floor for fixed per-row work.  cell = None: the row's RD pixel count (the compact path's
+    cost)."""
+    lab = np.asarray(labels) == 2
+    if cell is None:
+        return lab.sum(axis=1).astype(np.float64) + float(floor)
+    ch, cw = int(cell[0]), int(cell[1])
+    H, W = lab.shape
+    nb, ns = -(-H // ch), -(-W // cw)
+    pad = np.zeros((nb * ch, ns * cw), dtype=bool)
+    pad[:H, :W] = lab
+    active = pad.reshape(nb, ch, ns, cw).any(axis=(1, 3)).sum(axis=1).astype(np.float64)
+    return np.repeat(active, ch)[:H] + float(floor)
 
 
 def segments(iters: int, seg_iters: int) -> list[int]:

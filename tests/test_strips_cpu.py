@@ -159,7 +159,10 @@ def test_row_weights_and_weighted_strips_oracle(orc):
     delta = wl.band_delta(0.3, orc.absmax(f))
     labels = orc.labels(f, delta)
     w = strips.row_weights(labels)
-    assert np.array_equal(w, (labels == 2).sum(axis=1) + 1.0)
+    assert np.array_equal(strips.row_weights(labels, cell=None), (labels == 2).sum(axis=1) + 1.0)
+    # cells: rows of a band share its count of active 8 x 112 cells
+    band = (labels[:8] == 2).any()
+    assert w[0] == w[7] == float(band) + 1.0
     plan = strips.partition(H, G, s, w)
     assert plan[0].hi - plan[0].lo > plan[-1].hi - plan[-1].lo   # the empty rows are cheap
     ref = orc.solve(f, delta, 5.0, 0.1, 0.125, K)
