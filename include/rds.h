@@ -180,6 +180,15 @@ typedef struct {
                                 phases make it slower than the stencil at C1 (3.9 vs 3.0 us per
                                 iteration). */
 
+#define RDS_OPT_WS 13        /* warp-specialised stencil (k_stencil_ws.cu): the S-stage pipeline of
+                                a full-depth iterating launch split into 2-3-stage chains run by
+                                different warps of a CTA, joined through shared-memory hand-off
+                                slots one row step apart (the same one-row delay the single-warp
+                                kernel's chain split has), so each warp holds 2-3 stages of state
+                                and 3-5 CTAs share an SM.  Same per-pixel operations (results
+                                bit-identical).  1 (default) = on for image widths a multiple of
+                                4 and k_fuse 6..8, 0 = off. */
+
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */
 int rds_create(int64_t H, int64_t W, rds_t **out);

@@ -121,6 +121,7 @@ struct StencilArgs {
     int H, W;
     int img_w;                           // columns per image (W, or the image width of a batch)
     float tau, theta, inv_theta;
+    int ws;                              // full-depth PLAIN launches on k_stencil_ws (RDS_OPT_WS)
 };
 
 // The temporal wavefront (k_wave.cu): nblk blocks of KF iterations of a
@@ -239,6 +240,12 @@ cudaError_t launch_build_items(const uint32_t *band_bits, int n_strips, int n_ba
 cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a,
                            int grid, cudaStream_t s);
 int stencil_blocks_per_sm(int kf, int stages, bool aligned);
+// concurrent stencil workers per SM for full-depth launches (warps, or CTAs of k_stencil_ws)
+int stencil_workers_per_sm(int kf, bool aligned, bool ws);
+// k_stencil_ws.cu: warp-specialised stage chains (MODE_PLAIN, aligned, stages == k_fuse)
+bool ws_available(int stages);
+int ws_blocks_per_sm(int stages);
+cudaError_t launch_stencil_ws(int stages, const StencilArgs &a, int grid, cudaStream_t s);
 bool kf_supported(int kf);
 int kf_list(int32_t *out, int cap);
 // Stopping rule after a block of iterations (k_energy.cu).

@@ -60,8 +60,36 @@ int stencil_blocks_per_sm(int kf, int stages, bool aligned) {
     return nb;
 }
 
+// Warp-specialised stage chains (k_stencil_ws.cu) for the full-depth iterating launches
+// (RDS_OPT_WS), where an instantiation exists.
+static bool ws_on(int kf, int stages, int mode, bool aligned, bool ws) {
+    return ws && mode == MODE_PLAIN && aligned && stages == kf && ws_available(stages);
+}
+
+static int n_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 1;
+    }
+    return n;
+}
+
+int stencil_workers_per_sm(int kf, bool aligned, bool ws) {
+    if (ws_on(kf, kf, MODE_PLAIN, aligned, ws)) return ws_blocks_per_sm(kf);
+    return stencil_blocks_per_sm(kf, kf, aligned) * STENCIL_WARPS;
+}
+
 cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a, int grid,
                            cudaStream_t s) {
+    if (ws_on(kf, stages, mode, (a.img_w & 3) == 0, a.ws != 0)) {
+        // one item per CTA at a time: as many CTAs as the caller's warps had items
+        int g = n_sms() * ws_blocks_per_sm(stages);
+        if (g > grid * STENCIL_WARPS) g = grid * STENCIL_WARPS;
+        return launch_stencil_ws(stages, a, g, s);
+    }
     // the packed path needs every image-last column at lane position 3 of a quad
     StencilFn fn = lookup(kf, stages, mode, (a.img_w & 3) == 0);
     if (!fn) return cudaErrorInvalidValue;

@@ -99,6 +99,13 @@ __device__ __forceinline__ Q ldq(const float4 &m) {
 __device__ __forceinline__ void stq(float *p, const Q &x) {  // swizzled store
     *reinterpret_cast<float4 *>(p) = make_float4(x.a.x, x.a.y, x.b.x, x.b.y);
 }
+__device__ __forceinline__ void st_pred(float *p, const Q &x, bool pr) {  // swizzled, predicated
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n"
+        " @p st.global.v4.f32 [%1], {%2, %3, %4, %5};\n}\n" ::"r"((int)pr),
+        "l"(p), "f"(x.a.x), "f"(x.a.y), "f"(x.b.x), "f"(x.b.y)
+        : "memory");
+}
 __device__ __forceinline__ Q zeroq() {
     return Q{make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 }
@@ -143,6 +150,23 @@ struct Split {
             if (sp(k) == t) return k;
         return 0;
     }
+};
+
+// Warm-up skip (the trapezoid of the vertical cone).  Level S is stored on rows [R0, Rend);
+// one iteration reads rows m-1 .. m+1 of rho and m .. m+1 of v, w (div rho at m needs rho1 at
+// m-1), so level t is needed on rows >= R0 - 1 - (S - t) for rho and >= R0 - (S - t) for v.
+// Stage t emits level t+1 at row m = n - t - 1 - lag(t) in row step n, so its rows are needed
+// from row step n = R0 - S + 2t + 1 + lag(t) on; before that (the first 2t + 2 + lag(t) steps
+// of a march) it only carries its state (the row it received and its w) and passes its input
+// through.  Nothing computed before that step reaches a needed value: at the first active step
+// the stage's own previous row (q1, rho1 of level t+1 at row m-1) is a placeholder, but it
+// enters only v and div rho of level t+1 at row m, which are needed one row lower.
+template <int S, class SP = Split<S>>
+struct Act {
+    // first row step (relative to R0) in which stage t does its work
+    __host__ __device__ static constexpr int first(int t) { return 1 - S + 2 * t + SP::lag(t); }
+    // from this step (relative to R0) on every stage is active
+    __host__ __device__ static constexpr int all() { return first(S - 1); }
 };
 
 template <int S>
@@ -202,7 +226,7 @@ struct Front {
 };
 template <bool ALIGNED, bool LAST>
 __device__ __forceinline__ Front front(const Q &aw, const Q &inv, const Q &ind, const Q &c, int m,
-                                       const Ctx &x) {
+                                       const Ctx &x, bool act) {
     constexpr unsigned FULL = 0xffffffffu;
     Front f;
     f.w.a = fma2(inv.a, -x.inv_theta, ind.a);
@@ -219,8 +243,13 @@ __device__ __forceinline__ Front front(const Q &aw, const Q &inv, const Q &ind, 
         f.g2.b = mul2(f.g2.b, x.kx.b);
     }
     // |grad w|^2 + |c'|: |c'| is +inf off RD (rr = 0) and <= 2^-80 on RD (see stage())
-    f.rr.a = rr_of(fma2(f.g1.a, f.g1.a, fma2(f.g2.a, f.g2.a, absq(c.a))), x.tau);
-    f.rr.b = rr_of(fma2(f.g1.b, f.g1.b, fma2(f.g2.b, f.g2.b, absq(c.b))), x.tau);
+    // (act = false: a warm-up row outside the cone, whose values are never used)
+    if (act) {
+        f.rr.a = rr_of(fma2(f.g1.a, f.g1.a, fma2(f.g2.a, f.g2.a, absq(c.a))), x.tau);
+        f.rr.b = rr_of(fma2(f.g1.b, f.g1.b, fma2(f.g2.b, f.g2.b, absq(c.b))), x.tau);
+    } else {
+        f.rr = zeroq();
+    }
     return f;
 }
 
@@ -266,10 +295,10 @@ template <bool WRITE_U, bool ALIGNED, bool LAST>
 __device__ __forceinline__ void stage(const Q &ap1, const Q &ap2, const Q &av, const Q &aw,
                                       const Q &q1, const Q &in1, const Q &in2, const Q &inv,
                                       const Q &ind, const float4 &c4, int m, const Ctx &x,
-                                      Q &bp1, Q &bp2, Q &bv, Q &bw, Q &o1, Q &o2, Q &ov, Q &od,
+                                      bool act, Q &bp1, Q &bp2, Q &bv, Q &bw, Q &o1, Q &o2, Q &ov, Q &od,
                                       Q &ou) {
     const Q c = ldq(c4);
-    const Front f = front<ALIGNED, LAST>(aw, inv, ind, c, m, x);
+    const Front f = front<ALIGNED, LAST>(aw, inv, ind, c, m, x, act);
     back<WRITE_U>(f.g1, f.g2, f.rr, ap1, ap2, av, q1, c, x, o1, o2, ov, od, ou);
     bp1 = in1;
     bp2 = in2;
@@ -382,7 +411,7 @@ struct Extra {  // per-row-step state only the CHECK mode needs
 
 // One row step: consume input row n from the ring, advance all S stages, store the level-S
 // row if it is an output row of this item, then refill the slot with row n+RING.
-template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE>
+template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE, bool WARM>
 __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B,
                                           const Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
                                           const Ctx &x, float &acc_u, float &acc_v, Wave &wv) {
@@ -414,9 +443,11 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
                       : SPL::at(t + 1)      ? A.d1[SPL::at(t + 1) > 0 ? SPL::at(t + 1) - 1 : 0]
                                             : A.p1[(t + 1 < S) ? t + 1 : 0];
         const float4 c4 = crow[-32 * (n - m)];  // n - m is a compile-time lag
+        // warm-up: a row outside the cone (Act) skips the stage's MUFU work (warp-uniform)
+        const bool act = !WARM || n - x.R0 >= Act<S>::first(t);
         stage<WRITE_U, ALIGNED, LAST>(A.p1[t], A.p2[t], A.v[t], A.w[t], q1, in1, in2, inv, ind,
-                                      c4, m, x, B.p1[t], B.p2[t], B.v[t], B.w[t], o1, o2, ov, od,
-                                      uu);
+                                      c4, m, x, act, B.p1[t], B.p2[t], B.v[t], B.w[t], o1, o2,
+                                      ov, od, uu);
         in1 = o1;
         in2 = o2;
         inv = ov;
@@ -424,6 +455,15 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
         if (MODE == MODE_CHECK && S >= 2 && t == S - 2) EB.uprev = uu;  // u^(l-1), row m
         if (t == S - 1) {
             B.q1 = o1;
+#ifndef RDS_NO_PRED_STORE
+            if (MODE == MODE_PLAIN) {  // predicated stores instead of a divergent branch
+                const bool st = x.store_lane && m >= x.R0 && m < x.Rend;
+                const int64_t o = (int64_t)m * x.pitch + x.col;
+                st_pred(x.p1o + o, o1, st);
+                st_pred(x.p2o + o, o2, st);
+                st_pred(x.vo + o, ov, st);
+            } else
+#endif
             if (x.store_lane && m >= x.R0 && m < x.Rend) {
                 const int64_t o = (int64_t)m * x.pitch + x.col;
                 if (MODE == MODE_CHECK) {
@@ -476,13 +516,25 @@ __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &
         A.d1[k] = A.d2[k] = A.dv[k] = A.dd[k] = zeroq();
     }
     EA.uprev = zeroq();
-    for (int k = 0; n <= x.n_last; n += 2, ++k) {
+    int k = 0;
+#ifdef RDS_WARMSKIP  // (measured: no gain in the single-warp kernel)
+    // the first row steps, in which the later stages are still above their cone (Act)
+    if (!WAVE) {
+        for (; n <= x.n_last && n < x.R0 + Act<S>::all(); n += 2, ++k) {
+            pipe_step<S, MODE, ALIGNED, LAST, WAVE, true>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
+            pipe_step<S, MODE, ALIGNED, LAST, WAVE, true>(B, A, EB, EA, n + 1, x, acc_u, acc_v,
+                                                          wv);
+        }
+    }
+#endif
+    for (; n <= x.n_last; n += 2, ++k) {
         // wavefront: every second loop head, publish the rows emitted so far (rows < n - S -
         // NS of this item are final)
         if (WAVE && (k % (WAVE_PUB / 2)) == WAVE_PUB / 2 - 1)
             wave_publish(x, min(max(n - S - Split<S>::NS, x.R0), x.Rend));
-        pipe_step<S, MODE, ALIGNED, LAST, WAVE>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
-        pipe_step<S, MODE, ALIGNED, LAST, WAVE>(B, A, EB, EA, n + 1, x, acc_u, acc_v, wv);
+        pipe_step<S, MODE, ALIGNED, LAST, WAVE, false>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
+        pipe_step<S, MODE, ALIGNED, LAST, WAVE, false>(B, A, EB, EA, n + 1, x, acc_u, acc_v,
+                                                       wv);
     }
 }
 

@@ -107,6 +107,7 @@ struct rds_handle {
     int opt_wave = 0;     // temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto (RDS_OPT_WAVE)
     bool wave_ok = false; // the last solve's set-up allows the wavefront (aligned, supported kf)
     int opt_resident = 2; // small images as one resident cluster: 0 off, 1 on, 2 auto (RDS_OPT_RESIDENT)
+    int opt_ws = 1;       // full-depth launches on the warp-specialised stencil (RDS_OPT_WS)
     int opt_persist = 0;  // fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto (RDS_OPT_PERSIST)
     bool persist_ok = false;  // the last solve's set-up allows it (aligned, supported kf, size)
     unsigned long long *loop_bar = nullptr;  // grid-barrier counter of k_loop
@@ -330,6 +331,15 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             if (value < 0 || value > 2)
                 return fail(h, RDS_EINVAL, "rds_set_option: compact=%lld", (long long)value);
             h->opt_compact = (int)value;
+            return RDS_OK;
+        case RDS_OPT_WS:
+            if (value < 0 || value > 1)
+                return fail(h, RDS_EINVAL, "rds_set_option: ws=%lld", (long long)value);
+            h->opt_ws = (int)value;
+            if (h->graph) {
+                cudaGraphExecDestroy(h->graph);
+                h->graph = nullptr;
+            }
             return RDS_OK;
         case RDS_OPT_PERSIST:
             if (value < 0 || value > 2)
@@ -605,6 +615,7 @@ static cudaError_t enqueue_plan(rds_t *h, const LaunchPlan *plan, int n, int kf,
     a.items = h->items;
     a.n_items = h->counts + 1;
     a.pitch = h->pitch;
+    a.ws = h->opt_ws;
     a.H = (int)h->H;
     a.W = (int)h->W;
     a.img_w = (int)h->img_w;
@@ -679,6 +690,7 @@ static cudaError_t enqueue_wave(rds_t *h, int kf, int iters, int nblk, int max_i
     a.items = h->items;
     a.n_items = h->counts + 1;
     a.pitch = h->pitch;
+    a.ws = h->opt_ws;
     a.H = (int)h->H;
     a.W = (int)h->W;
     a.img_w = (int)h->img_w;
@@ -744,6 +756,7 @@ static cudaError_t enqueue_persist(rds_t *h, int kf, int iters, int max_items, f
     a.items = h->items;
     a.n_items = h->counts + 1;
     a.pitch = h->pitch;
+    a.ws = h->opt_ws;
     a.H = (int)h->H;
     a.W = (int)h->W;
     a.img_w = (int)h->img_w;
@@ -1151,7 +1164,10 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     CK(h, launch_band_flags(h->sub_rd, (int)h->H, (int)h->W, wv, n_strips, h->opt_skip,
                             h->band_flag, h->stream));
     {
-        const int slots = h->n_sm * blocks_per_sm(h, kf, kf) * STENCIL_WARPS;
+        const int slots = h->opt_ctas > 0
+                              ? h->n_sm * blocks_per_sm(h, kf, kf) * STENCIL_WARPS
+                              : h->n_sm * stencil_workers_per_sm(kf, (h->img_w & 3) == 0,
+                                                                 h->opt_ws != 0);
         const int max_chunk = 1 << 30;
         CK(h, launch_build_items(h->band_flag, n_strips, n_bands, (int)h->H, slots, fixed_chunk,
                                  max_chunk,

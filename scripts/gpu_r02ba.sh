@@ -1,0 +1,18 @@
+# Warm-up MUFU skip (Act) and predicated stores: parity subset, then an alternating A/B of the
+# C3 K-loop (delta = inf and .2) against the round-2 kernel (RDS_NO_WARMSKIP).
+mkdir -p gpurun_out
+OUT=gpurun_out/r02ba_ab.log
+: > $OUT
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r02ba_build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "ragged or fusion or skip_equiv or c0 or c1 or c2 or warm_start or schedules or frame" > gpurun_out/r02ba_pytest.log 2>&1
+tail -2 gpurun_out/r02ba_pytest.log >> $OUT
+for rep in 1 2; do
+for defs in "-DRDS_NO_WARMSKIP" "-DRDS_WS=1" "-DRDS_PRED_STORE" "-DRDS_PRED_STORE,-DRDS_NO_WARMSKIP"; do
+  d="${defs//,/ } -DRDS_KF_LIST(X)=X(7)"
+  RDS_NVCC_DEFS="$d" python paper_1807_11534_b200/_build.py --force > /dev/null 2>>$OUT || { echo "build failed: $d" >> $OUT; continue; }
+  for dl in inf 0.2; do
+    echo "rep=$rep defs=$defs delta=$dl" >> $OUT
+    RDS_NVCC_DEFS="$d" timeout 300 python scripts/sweep.py --kf 7 --rows 0 --delta $dl --reps 5 >> $OUT 2>&1
+  done
+done; done
+cat $OUT
