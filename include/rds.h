@@ -186,8 +186,12 @@ typedef struct {
                                 slots one row step apart (the same one-row delay the single-warp
                                 kernel's chain split has), so each warp holds 2-3 stages of state
                                 and 3-5 CTAs share an SM.  Same per-pixel operations (results
-                                bit-identical).  1 (default) = on for image widths a multiple of
-                                4 and k_fuse 6..8, 0 = off. */
+                                bit-identical).  0 (default) = off, 1 = on for image widths a
+                                multiple of 4 and k_fuse 6..8.  Off by default: measured on B200
+                                it is slower (C3 K-loop 21-25 ms vs 16.3 ms): each warp's one
+                                chain is a serial dependency chain, and 3-4 such warps per SM
+                                sub-partition hide less latency than 2 warps that interleave
+                                three independent chains each. */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */

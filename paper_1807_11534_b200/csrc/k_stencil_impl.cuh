@@ -167,6 +167,10 @@ struct Act {
     __host__ __device__ static constexpr int first(int t) { return 1 - S + 2 * t + SP::lag(t); }
     // from this step (relative to R0) on every stage is active
     __host__ __device__ static constexpr int all() { return first(S - 1); }
+    // prologue length of a march starting at R0 - S - 2: up to all(), rounded up to even
+    __host__ __device__ static constexpr int prologue() {
+        return ((all() + S + 2) + 1) & ~1;
+    }
 };
 
 template <int S>
@@ -411,7 +415,7 @@ struct Extra {  // per-row-step state only the CHECK mode needs
 
 // One row step: consume input row n from the ring, advance all S stages, store the level-S
 // row if it is an output row of this item, then refill the slot with row n+RING.
-template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE, bool WARM>
+template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE, int KST = -1>
 __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B,
                                           const Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
                                           const Ctx &x, float &acc_u, float &acc_v, Wave &wv) {
@@ -443,11 +447,25 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
                       : SPL::at(t + 1)      ? A.d1[SPL::at(t + 1) > 0 ? SPL::at(t + 1) - 1 : 0]
                                             : A.p1[(t + 1 < S) ? t + 1 : 0];
         const float4 c4 = crow[-32 * (n - m)];  // n - m is a compile-time lag
-        // warm-up: a row outside the cone (Act) skips the stage's MUFU work (warp-uniform)
-        const bool act = !WARM || n - x.R0 >= Act<S>::first(t);
-        stage<WRITE_U, ALIGNED, LAST>(A.p1[t], A.p2[t], A.v[t], A.w[t], q1, in1, in2, inv, ind,
-                                      c4, m, x, act, B.p1[t], B.p2[t], B.v[t], B.w[t], o1, o2,
-                                      ov, od, uu);
+        // prologue step KST >= 0 (row step n = R0 - S - 2 + KST, compile time): a stage still
+        // above its cone (Act) is elided -- it only carries its state and passes its input on
+        const bool act = KST < 0 || KST - (S + 2) >= Act<S>::first(t);
+        if (act) {
+            stage<WRITE_U, ALIGNED, LAST>(A.p1[t], A.p2[t], A.v[t], A.w[t], q1, in1, in2, inv,
+                                          ind, c4, m, x, true, B.p1[t], B.p2[t], B.v[t], B.w[t],
+                                          o1, o2, ov, od, uu);
+        } else {
+            B.p1[t] = in1;
+            B.p2[t] = in2;
+            B.v[t] = inv;
+            B.w[t].a = fma2(inv.a, -x.inv_theta, ind.a);  // (dead unless the stage starts next)
+            B.w[t].b = fma2(inv.b, -x.inv_theta, ind.b);
+            o1 = in1;
+            o2 = in2;
+            ov = inv;
+            od = ind;
+            uu = inv;
+        }
         in1 = o1;
         in2 = o2;
         inv = ov;
@@ -503,6 +521,28 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
     cp_async_commit();
 }
 
+// The prologue: row steps K, K+1, ... < P of a march that starts at n = R0 - S - 2, unrolled
+// (each step's set of live stages is a compile-time constant).  P is even, so the state ends
+// in A as after the loop's step pairs.
+template <int S, int MODE, bool ALIGNED, int K, int P>
+struct Prologue {
+    __device__ static __forceinline__ void run(PipeState<S> &A, PipeState<S> &B,
+                                               Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
+                                               const Ctx &x, float &acc_u, float &acc_v,
+                                               Wave &wv) {
+        pipe_step<S, MODE, ALIGNED, false, false, K>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
+        pipe_step<S, MODE, ALIGNED, false, false, K + 1>(B, A, EB, EA, n + 1, x, acc_u, acc_v,
+                                                         wv);
+        Prologue<S, MODE, ALIGNED, K + 2, P>::run(A, B, EA, EB, n + 2, x, acc_u, acc_v, wv);
+    }
+};
+template <int S, int MODE, bool ALIGNED, int P>
+struct Prologue<S, MODE, ALIGNED, P, P> {
+    __device__ static __forceinline__ void run(PipeState<S> &, PipeState<S> &, Extra<S, MODE> &,
+                                               Extra<S, MODE> &, int, const Ctx &, float &,
+                                               float &, Wave &) {}
+};
+
 template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE>
 __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &acc_v,
                                       Wave &wv) {
@@ -517,14 +557,13 @@ __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &
     }
     EA.uprev = zeroq();
     int k = 0;
-#ifdef RDS_WARMSKIP  // (measured: no gain in the single-warp kernel)
-    // the first row steps, in which the later stages are still above their cone (Act)
-    if (!WAVE) {
-        for (; n <= x.n_last && n < x.R0 + Act<S>::all(); n += 2, ++k) {
-            pipe_step<S, MODE, ALIGNED, LAST, WAVE, true>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
-            pipe_step<S, MODE, ALIGNED, LAST, WAVE, true>(B, A, EB, EA, n + 1, x, acc_u, acc_v,
-                                                          wv);
-        }
+#ifndef RDS_NO_PROLOGUE
+    // the first row steps as straight-line code without the stages above their cone (Act);
+    // run_item started the march at n = R0 - S - 2 for this
+    if (!WAVE && !LAST) {
+        Prologue<S, MODE, ALIGNED, 0, Act<S>::prologue()>::run(A, B, EA, EB, n, x, acc_u, acc_v,
+                                                               wv);
+        n += Act<S>::prologue();
     }
 #endif
     for (; n <= x.n_last; n += 2, ++k) {
@@ -532,9 +571,8 @@ __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &
         // NS of this item are final)
         if (WAVE && (k % (WAVE_PUB / 2)) == WAVE_PUB / 2 - 1)
             wave_publish(x, min(max(n - S - Split<S>::NS, x.R0), x.Rend));
-        pipe_step<S, MODE, ALIGNED, LAST, WAVE, false>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
-        pipe_step<S, MODE, ALIGNED, LAST, WAVE, false>(B, A, EB, EA, n + 1, x, acc_u, acc_v,
-                                                       wv);
+        pipe_step<S, MODE, ALIGNED, LAST, WAVE>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
+        pipe_step<S, MODE, ALIGNED, LAST, WAVE>(B, A, EB, EA, n + 1, x, acc_u, acc_v, wv);
     }
 }
 
@@ -570,6 +608,12 @@ __device__ __forceinline__ void run_item(Ctx &x, const StencilArgs &a, int strip
     // row) for the two-state unrolled loop.
     x.n_last = x.Rend - 1 + S + Split<S>::NS;
     int n = x.R0 - (S + 1);
+#ifndef RDS_NO_PROLOGUE
+    if (!WAVE && x.n_last < a.H - 1) {  // the prologue's fixed start; one extra step at the end
+        n = x.R0 - S - 2;               // when the count would be odd
+        if (((x.n_last - n + 1) & 1) != 0) ++x.n_last;
+    }
+#endif
     if (((x.n_last - n + 1) & 1) != 0) --n;
     if (WAVE) wave_need(x, wv, min(n + RING - 1, x.n_last));
 #pragma unroll

@@ -107,7 +107,7 @@ struct rds_handle {
     int opt_wave = 0;     // temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto (RDS_OPT_WAVE)
     bool wave_ok = false; // the last solve's set-up allows the wavefront (aligned, supported kf)
     int opt_resident = 2; // small images as one resident cluster: 0 off, 1 on, 2 auto (RDS_OPT_RESIDENT)
-    int opt_ws = 1;       // full-depth launches on the warp-specialised stencil (RDS_OPT_WS)
+    int opt_ws = 0;       // full-depth launches on the warp-specialised stencil (RDS_OPT_WS)
     int opt_persist = 0;  // fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto (RDS_OPT_PERSIST)
     bool persist_ok = false;  // the last solve's set-up allows it (aligned, supported kf, size)
     unsigned long long *loop_bar = nullptr;  // grid-barrier counter of k_loop

@@ -27,7 +27,7 @@ RDS_OPT_STOP_NORM = 7  # 0 Euclidean over pixels (default), 1 RMS
 RDS_OPT_COMPACT = 8    # f3: 0 dense stencil, 1 compacted RD iteration, 2 auto (default)
 RDS_OPT_WAVE = 9       # temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto
 RDS_OPT_RESIDENT = 10  # small images as one resident cluster: 0 off, 1 / 2 (default) on
-RDS_OPT_WS = 13        # full-depth launches on the warp-specialised stencil: 1 on (default), 0 off
+RDS_OPT_WS = 13        # full-depth launches on the warp-specialised stencil: 0 off (default), 1 on
 RDS_OPT_PERSIST = 11   # fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto
 RDS_OPT_GRID = 12      # mid-size images resident on the whole GPU: 0 off (default), 1 / 2 on
 
