@@ -91,7 +91,7 @@ __device__ __forceinline__ void ws_step(const WsState<SplitWS<S, NC>::sp(C + 1) 
         const float4 c4 = crow[-32 * (n - m)];
         const bool act = !WARM || n - x.R0 >= Act<S, SP>::first(t);
         Q o1, o2, ov, od;
-        stage<false, true, LAST>(A.p1[i], A.p2[i], A.v[i], A.w[i], q1, in1, in2, inv, ind, c4, m,
+        stage<false, true, LAST ? 3 : 2>(A.p1[i], A.p2[i], A.v[i], A.w[i], q1, in1, in2, inv, ind, c4, m,
                                  x, act, B.p1[i], B.p2[i], B.v[i], B.w[i], o1, o2, ov, od, uu);
         in1 = o1;
         in2 = o2;
@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(NC * 32, RDS_WS_MINB) k_stencil_ws(const Stenc
     float4 *hand = smem + RING * 96 + 2 * CR * 32;
     Ctx x;
     x.pitch = a.pitch;
+    x.pitch32 = (int)a.pitch;
     x.H = a.H;
     x.tau = a.tau;
     x.theta = a.theta;
@@ -215,10 +216,17 @@ __global__ void __launch_bounds__(NC * 32, RDS_WS_MINB) k_stencil_ws(const Stenc
             x.kx.a = make_float2(1.0f, 1.0f);  // (ALIGNED: the packed edge uses right_edge)
             x.kx.b = make_float2(1.0f, 1.0f);
         }
+#ifndef RDS_ADDR32
         x.p1i = a.p1_in + x.col;
         x.p2i = a.p2_in + x.col;
         x.vi = a.v_in + x.col;
         x.ci = a.c + x.col;
+#else
+        x.p1i = a.p1_in;
+        x.p2i = a.p2_in;
+        x.vi = a.v_in;
+        x.ci = a.c;
+#endif
         x.n_last = x.Rend - 1 + S + SP::NS;
         int n = x.R0 - (S + 1);
         if (((x.n_last - n + 1) & 1) != 0) --n;
