@@ -279,10 +279,12 @@ constexpr unsigned RDC_IDX_MASK = (1u << RDC_IDX_BITS) - 1u;
 __host__ __device__ inline unsigned rdc_cls(int code) {
     return code >= 0 ? RDC_C_RD : (code == RDC_FG ? RDC_C_FG : (code == RDC_EDGE ? RDC_C_EDGE : RDC_C_BG));
 }
-constexpr int RDC_BAR_BYTES = 128;  // grid barrier counter (one 128-byte line)
+constexpr int RDC_MAX_GRID = 4 * 148 * 4;  // bound on k_rdc_iter CTAs (the stopping-sum buffer)
+// grid barrier counter (one 128-byte line), then the per-CTA pass counters of the neighbour
+// synchronisation (k_rdc_iter NB form)
+constexpr int RDC_BAR_BYTES = 128 + 4 * RDC_MAX_GRID;
 constexpr int RDC_THREADS = 512;
 constexpr int RDC_CLUSTER_MAX = 16;  // CTAs of the one-cluster form (non-portable size)
-constexpr int RDC_MAX_GRID = 4 * 148 * 4;  // bound on k_rdc_iter CTAs (the stopping-sum buffer)
 struct RdcSetup {
     int n, H, W, img_w;
     int64_t pitch;

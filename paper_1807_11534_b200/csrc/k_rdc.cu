@@ -316,9 +316,37 @@ __device__ __forceinline__ void cluster_barrier() {
                  "barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int NPT, bool CL = false>
+// Neighbour synchronisation (NB form, fixed-K solves): instead of a grid barrier, a CTA
+// publishes "pass k done" in its own counter (release) and, before pass k + 1, waits only for
+// the CTAs that own records its pixels read (acquire).  The owner relation is symmetric (the
+// six stencil neighbours come in pairs up/down, ur/dl, left/right), so the same wait also
+// guarantees that those CTAs have finished READING this CTA's records of pass k before pass
+// k + 1 overwrites that ping-pong buffer, and any two CTAs that read a common record are at
+// most one pass apart -- they then read different buffers.  Ranges are whole 128-byte lines
+// of records (multiples of 8), so no L1 line mixes two CTAs' records either: a line that
+// another CTA of the same SM brings into L1 holds the data of the pass this CTA reads or of
+// the other buffer, never a stale copy of the same one.
+__device__ __forceinline__ void nbr_sync(int *prog, int lo, int hi, int k1) {
+    __syncthreads();
+    if (threadIdx.x == 0)
+        asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(prog + blockIdx.x), "r"(k1)
+                     : "memory");
+    const int c = lo + (int)threadIdx.x;
+    if (c <= hi && c != (int)blockIdx.x) {
+        int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(prog + c)
+                         : "memory");
+        } while (v < k1);
+    }
+    __syncthreads();
+}
+
+template <int NPT, bool CL = false, bool NB = false>
 __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
-    const int chunk = (a.n + gridDim.x - 1) / gridDim.x;
+    // (NB: CTA ranges of whole 128-byte record lines)
+    const int chunk = NB ? (((a.n + gridDim.x - 1) / gridDim.x + 7) & ~7)
+                         : (a.n + gridDim.x - 1) / gridDim.x;
     const int start = blockIdx.x * chunk;
     const int stop = min(a.n, start + chunk);
     const float tau = a.tau, theta = a.theta, inv_theta = a.inv_theta;
@@ -330,6 +358,35 @@ __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
     }
     __shared__ double sh[2][RDC_THREADS / 32];
     __shared__ int stop_s;
+    // NB: the CTAs owning a record some pixel of this CTA reads (always including itself)
+    int dep_lo = blockIdx.x, dep_hi = blockIdx.x;
+    int *prog = reinterpret_cast<int *>(reinterpret_cast<char *>(a.bar) + 128);
+    if (NB) {
+        __shared__ int s_lo, s_hi;
+        if (threadIdx.x == 0) {
+            s_lo = a.n;
+            s_hi = -1;
+        }
+        __syncthreads();
+        int lo = a.n, hi = -1;
+        for (int r = start + threadIdx.x; r < stop; r += blockDim.x) {
+            const PixConst q = decode(__ldg(a.code + r), r);
+            const int nb[6] = {q.up, q.ur, q.lf, q.dn, q.dl, q.rt};
+#pragma unroll
+            for (int e = 0; e < 6; ++e)
+                if (nb[e] >= 0) {
+                    lo = min(lo, nb[e]);
+                    hi = max(hi, nb[e]);
+                }
+        }
+        atomicMin(&s_lo, lo);
+        atomicMax(&s_hi, hi);
+        __syncthreads();
+        if (s_hi >= 0) {
+            dep_lo = min(dep_lo, s_lo / chunk);
+            dep_hi = max(dep_hi, s_hi / chunk);
+        }
+    }
     const int m = a.check_every;  // tolerance solves: check after iterations m, 2m, ..., K
     int nchk = 0;                 // checks so far: selects the partial-sum buffer
     for (int k = 0; k <= a.K; ++k) {
@@ -368,6 +425,8 @@ __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
         if (k < a.K || m > 0) {
             if (CL)
                 cluster_barrier();
+            else if (NB)
+                nbr_sync(prog, dep_lo, dep_hi, k + 1);
             else
                 grid_barrier(a.bar, (unsigned long long)(k + 1));
         }
@@ -512,33 +571,41 @@ cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s) {
         // not schedulable as one cluster here: fall through to the cooperative grid form
         if (cluster_fits(cf, npt - 1, g)) return launch_cluster(a, cf, g, s);
     }
-    // the smallest register-resident variant that covers n, else the general one
+    // the smallest register-resident variant that covers n, else the general one; fixed-K
+    // solves synchronise with their neighbour CTAs only (NB), RDS_RDC_NB=0 restores the grid
+    // barrier
+    static const bool nb_env = !getenv("RDS_RDC_NB") || atoi(getenv("RDS_RDC_NB"));
+    const bool nb = nb_env && a.check_every <= 0;
     RdcFn fn = nullptr;
     int g = 0;
     const int64_t n = a.n;
     static const int max_npt = getenv("RDS_RDC_MAXNPT") ? atoi(getenv("RDS_RDC_MAXNPT")) : 2;
     if (n <= (int64_t)grid_of<1>(n_sm) * RDC_THREADS) {
-        fn = k_rdc_iter<1>;
+        fn = nb ? k_rdc_iter<1, false, true> : k_rdc_iter<1>;
         g = grid_of<1>(n_sm);
     } else if (max_npt >= 2 && n <= (int64_t)grid_of<2>(n_sm) * RDC_THREADS * 2) {
-        fn = k_rdc_iter<2>;
+        fn = nb ? k_rdc_iter<2, false, true> : k_rdc_iter<2>;
         g = grid_of<2>(n_sm);
     } else if (max_npt >= 4 && n <= (int64_t)grid_of<4>(n_sm) * RDC_THREADS * 4) {
-        fn = k_rdc_iter<4>;
+        fn = nb ? k_rdc_iter<4, false, true> : k_rdc_iter<4>;
         g = grid_of<4>(n_sm);
     } else if (max_npt >= 8 && n <= (int64_t)grid_of<8>(n_sm) * RDC_THREADS * 8) {
-        fn = k_rdc_iter<8>;
+        fn = nb ? k_rdc_iter<8, false, true> : k_rdc_iter<8>;
         g = grid_of<8>(n_sm);
     } else if (max_npt >= 16 && n <= (int64_t)grid_of<16>(n_sm) * RDC_THREADS * 16) {
-        fn = k_rdc_iter<16>;
+        fn = nb ? k_rdc_iter<16, false, true> : k_rdc_iter<16>;
         g = grid_of<16>(n_sm);
     } else {
-        fn = k_rdc_iter<0>;
+        fn = nb ? k_rdc_iter<0, false, true> : k_rdc_iter<0>;
         g = grid_of<0>(n_sm);
     }
     const int64_t need = (n + RDC_THREADS - 1) / RDC_THREADS;
     if (g > need) g = (int)need;
     if (g > RDC_MAX_GRID) g = RDC_MAX_GRID;
+    if (nb) {  // ranges of whole 8-record lines: no more CTAs than ranges
+        const int64_t per = ((n + g - 1) / g + 7) & ~7;
+        g = (int)((n + per - 1) / per);
+    }
     void *args[] = {const_cast<RdcIter *>(&a)};
     cudaError_t e = cudaMemsetAsync(a.bar, 0, RDC_BAR_BYTES, s);
     if (e != cudaSuccess) return e;
