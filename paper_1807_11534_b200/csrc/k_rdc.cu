@@ -333,11 +333,14 @@ __device__ __forceinline__ void nbr_sync(int *prog, int lo, int hi, int k1) {
                      : "memory");
     const int c = lo + (int)threadIdx.x;
     if (c <= hi && c != (int)blockIdx.x) {
+        // spin relaxed (an acquire load also invalidates the SM's L1, which the CTAs still
+        // computing on this SM depend on), then one acquire once the count is reached
         int v;
         do {
-            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(prog + c)
+            asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(prog + c)
                          : "memory");
         } while (v < k1);
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(prog + c) : "memory");
     }
     __syncthreads();
 }
@@ -571,10 +574,10 @@ cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s) {
         // not schedulable as one cluster here: fall through to the cooperative grid form
         if (cluster_fits(cf, npt - 1, g)) return launch_cluster(a, cf, g, s);
     }
-    // the smallest register-resident variant that covers n, else the general one; fixed-K
-    // solves synchronise with their neighbour CTAs only (NB), RDS_RDC_NB=0 restores the grid
-    // barrier
-    static const bool nb_env = !getenv("RDS_RDC_NB") || atoi(getenv("RDS_RDC_NB"));
+    // the smallest register-resident variant that covers n, else the general one.  RDS_RDC_NB=1:
+    // fixed-K solves synchronise with their neighbour CTAs only (NB form; off by default:
+    // measured 3% faster at C3 delta = .1 but 1.3-4x slower at thinner bands)
+    static const bool nb_env = getenv("RDS_RDC_NB") && atoi(getenv("RDS_RDC_NB"));
     const bool nb = nb_env && a.check_every <= 0;
     RdcFn fn = nullptr;
     int g = 0;

@@ -47,6 +47,12 @@ __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n"
                  "barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 // store a float into the same shared-memory offset of CTA `rank` of the cluster
 __device__ __forceinline__ void st_remote(float *local_addr, unsigned rank, float v) {
     unsigned a = (unsigned)__cvta_generic_to_shared(local_addr), ra;
@@ -115,11 +121,12 @@ __global__ void __launch_bounds__(SmallCols<R>::value, 1) k_small(const SmallArg
         // A: w on rows -1 .. R; rho2 of the column to the left.  Lane 0 takes the warp to the
         // left's lane 31: rows -1 .. R-1 from `edge` (its rho2' of the previous iteration's phase
         // B; row -1 recomputed there bit-identically to the neighbour's), row R from the halo
-        // slot that the CTA below filled for that column
+        // slot that the CTA below filled for that column.  The interior rows 1 .. R-1 (r = 3 ..
+        // NR-2) need no halo row: they run while the cluster barrier of the previous iteration
+        // completes (split arrive / wait), the rows -1, 0 and R after it.
         const float *hp = halo + ((k - 1) & 1) * 7 * NT;
         float w[NR];
-#pragma unroll
-        for (int r = 1; r < NR; ++r) {
+        auto w_row = [&](int r) {
             float l2 = __shfl_up_sync(FULL, p2[r], 1);
             if (lane == 0) {
                 if (warp == 0)
@@ -131,7 +138,30 @@ __global__ void __launch_bounds__(SmallCols<R>::value, 1) k_small(const SmallArg
             }
             const float d = __fadd_rn(__fsub_rn(p1[r], p1[r - 1]), __fsub_rn(p2[r], l2));
             w[r] = __fmaf_rn(v[r], -inv_theta, d);
+        };
+#pragma unroll
+        for (int r = 3; r < NR - 1; ++r) w_row(r);
+        if (k > 0) {
+#ifdef RDS_SMALL_NOCLUSTER
+            __syncthreads();
+#else
+            cluster_wait();
+#endif
+            if (rank > 0) {  // the halo rows of the new state (pushed in iteration k-1)
+                p1[0] = hp[0 * NT + t];
+                p1[1] = hp[1 * NT + t];
+                p2[1] = hp[3 * NT + t];
+                v[1] = hp[5 * NT + t];
+            }
+            if (rank + 1 < G) {
+                p1[NR - 1] = hp[2 * NT + t];
+                p2[NR - 1] = hp[4 * NT + t];
+                v[NR - 1] = hp[6 * NT + t];
+            }
         }
+        w_row(1);
+        w_row(2);
+        w_row(NR - 1);
         // lane 0 publishes its w for the warp to the left
 #ifndef RDS_SMALL_NOBAR
         __syncthreads();  // (the previous reads of edge are done)
@@ -200,24 +230,10 @@ __global__ void __launch_bounds__(SmallCols<R>::value, 1) k_small(const SmallArg
             }
         }
 #endif
-#ifdef RDS_SMALL_NOCLUSTER
-        __syncthreads();
-#else
-        cluster_sync();
+        // arrive now (the pushes released), wait at the next iteration's phase A
+#ifndef RDS_SMALL_NOCLUSTER
+        if (k + 1 < K) cluster_arrive();
 #endif
-        if (k + 1 < K) {
-            if (rank > 0) {
-                p1[0] = hs[0 * NT + t];
-                p1[1] = hs[1 * NT + t];
-                p2[1] = hs[3 * NT + t];
-                v[1] = hs[5 * NT + t];
-            }
-            if (rank + 1 < G) {
-                p1[NR - 1] = hs[2 * NT + t];
-                p2[NR - 1] = hs[4 * NT + t];
-                v[NR - 1] = hs[6 * NT + t];
-            }
-        }
     }
     // outputs: u and the mask of the last iteration (u0 = v when nothing moved), the state
     if (!col_ok) return;

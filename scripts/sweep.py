@@ -22,7 +22,7 @@ ap.add_argument("--delta", type=float, default=math.inf)
 ap.add_argument("--iters", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--ctas", default="0", help="cap on stencil CTAs per SM (0 = occupancy)")
-ap.add_argument("--ws", default="1", help="RDS_OPT_WS values (warp-specialised stencil)")
+ap.add_argument("--ws", default="0", help="RDS_OPT_WS values (warp-specialised stencil)")
 args = ap.parse_args()
 
 cfg = wl.CONFIGS[args.config]
