@@ -43,7 +43,6 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, 2) k_loop(const LoopArgs L
     const int n_items = *a.n_items;
     Ctx x;
     x.pitch = a.pitch;
-    x.pitch32 = (int)a.pitch;
     x.H = a.H;
     x.tau = a.tau;
     x.theta = a.theta;

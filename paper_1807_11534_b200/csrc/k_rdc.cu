@@ -578,7 +578,9 @@ cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s) {
     // fixed-K solves synchronise with their neighbour CTAs only (NB form; off by default:
     // measured 3% faster at C3 delta = .1 but 1.3-4x slower at thinner bands)
     static const bool nb_env = getenv("RDS_RDC_NB") && atoi(getenv("RDS_RDC_NB"));
-    const bool nb = nb_env && a.check_every <= 0;
+    // (NB needs both record buffers on 128-byte lines: ranges of whole lines, see nbr_sync)
+    const bool nb = nb_env && a.check_every <= 0 && (a.rec[1] - a.rec[0]) % 8 == 0 &&
+                    (reinterpret_cast<uintptr_t>(a.rec[0]) & 127) == 0;
     RdcFn fn = nullptr;
     int g = 0;
     const int64_t n = a.n;

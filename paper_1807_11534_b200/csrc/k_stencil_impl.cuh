@@ -99,13 +99,6 @@ __device__ __forceinline__ Q ldq(const float4 &m) {
 __device__ __forceinline__ void stq(float *p, const Q &x) {  // swizzled store
     *reinterpret_cast<float4 *>(p) = make_float4(x.a.x, x.a.y, x.b.x, x.b.y);
 }
-__device__ __forceinline__ void st_pred(float *p, const Q &x, bool pr) {  // swizzled, predicated
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n"
-        " @p st.global.v4.f32 [%1], {%2, %3, %4, %5};\n}\n" ::"r"((int)pr),
-        "l"(p), "f"(x.a.x), "f"(x.a.y), "f"(x.b.x), "f"(x.b.y)
-        : "memory");
-}
 __device__ __forceinline__ Q zeroq() {
     return Q{make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f)};
 }
@@ -152,27 +145,6 @@ struct Split {
     }
 };
 
-// Warm-up skip (the trapezoid of the vertical cone).  Level S is stored on rows [R0, Rend);
-// one iteration reads rows m-1 .. m+1 of rho and m .. m+1 of v, w (div rho at m needs rho1 at
-// m-1), so level t is needed on rows >= R0 - 1 - (S - t) for rho and >= R0 - (S - t) for v.
-// Stage t emits level t+1 at row m = n - t - 1 - lag(t) in row step n, so its rows are needed
-// from row step n = R0 - S + 2t + 1 + lag(t) on; before that (the first 2t + 2 + lag(t) steps
-// of a march) it only carries its state (the row it received and its w) and passes its input
-// through.  Nothing computed before that step reaches a needed value: at the first active step
-// the stage's own previous row (q1, rho1 of level t+1 at row m-1) is a placeholder, but it
-// enters only v and div rho of level t+1 at row m, which are needed one row lower.
-template <int S, class SP = Split<S>>
-struct Act {
-    // first row step (relative to R0) in which stage t does its work
-    __host__ __device__ static constexpr int first(int t) { return 1 - S + 2 * t + SP::lag(t); }
-    // from this step (relative to R0) on every stage is active
-    __host__ __device__ static constexpr int all() { return first(S - 1); }
-    // prologue length of a march starting at R0 - S - 2: up to all(), rounded up to even
-    __host__ __device__ static constexpr int prologue() {
-        return ((all() + S + 2) + 1) & ~1;
-    }
-};
-
 template <int S>
 struct PipeState {
     static constexpr int ND = Split<S>::NS > 0 ? Split<S>::NS : 1;
@@ -188,7 +160,6 @@ struct Ctx {
     float4 *ring;   // this lane's slot 0, plane 0; slot stride 96 float4, plane stride 32
     float4 *cring;  // this lane's c slot 0; slot stride 32 float4, 2*CR slots
     int64_t pitch;
-    int pitch32;
     int col, H, R0, Rend, n_last;
     int chk_r0, chk_r1;  // CHECK mode: rows whose stopping sums are accumulated
     bool store_lane, right_edge;
@@ -200,11 +171,7 @@ __device__ __forceinline__ void stage_row(const Ctx &x, int r) {
     const int rr = r & (RING - 1);  // two's complement: also right for r < 0
     const int rc = r & (CR - 1);
     float4 *slot = x.ring + rr * 96;
-#ifndef RDS_ADDR32  // per-lane 64-bit row pointers (32-bit element offsets measured 5% slower)
     const int64_t off = (int64_t)r * x.pitch;
-#else
-    const int off = r * x.pitch32 + x.col;  // (planes below 2^31 elements)
-#endif
     cp_async16(slot, x.p1i + off);
     cp_async16(slot + 32, x.p2i + off);
     cp_async16(slot + 64, x.vi + off);
@@ -233,23 +200,18 @@ __device__ __forceinline__ Q div_q(const Q &p1, const Q &p1up, const Q &p2) {
 struct Front {
     Q w, g1, g2, rr;
 };
-// EDGE: bit 0 = the march may reach row H-1 (grad_1 = 0 there), bit 1 = a lane of the warp
-// holds an image-last column (grad_2 = 0 there); items away from both skip the checks.
-template <bool ALIGNED, int EDGE>
+template <bool ALIGNED, bool LAST>
 __device__ __forceinline__ Front front(const Q &aw, const Q &inv, const Q &ind, const Q &c, int m,
-                                       const Ctx &x, bool act) {
+                                       const Ctx &x) {
     constexpr unsigned FULL = 0xffffffffu;
     Front f;
     f.w.a = fma2(inv.a, -x.inv_theta, ind.a);
     f.w.b = fma2(inv.b, -x.inv_theta, ind.b);
     float wr = __shfl_down_sync(FULL, aw.a.x, 1);  // x4 of this lane = x0 of the next
-#ifndef RDS_EDGE_ALWAYS
-#define RDS_EDGE_ALWAYS 0  // 1: every packed march checks the right edge (A/B of the split)
-#endif
-    if (ALIGNED && ((EDGE & 2) || RDS_EDGE_ALWAYS) && x.right_edge) wr = aw.b.y;  // grad_2 = 0
+    if (ALIGNED && x.right_edge) wr = aw.b.y;      // grad_2 = 0 on an image's column W-1
     f.g1.a = sub2(f.w.a, aw.a);
     f.g1.b = sub2(f.w.b, aw.b);
-    if ((EDGE & 1) && m == x.H - 1) f.g1 = zeroq();  // grad_1 = 0 on row H-1
+    if (LAST && m == x.H - 1) f.g1 = zeroq();      // grad_1 = 0 on row H-1
     f.g2.a = sub2(aw.b, aw.a);
     f.g2.b = sub2(make_float2(aw.a.y, wr), aw.b);
     if (!ALIGNED) {
@@ -257,13 +219,8 @@ __device__ __forceinline__ Front front(const Q &aw, const Q &inv, const Q &ind, 
         f.g2.b = mul2(f.g2.b, x.kx.b);
     }
     // |grad w|^2 + |c'|: |c'| is +inf off RD (rr = 0) and <= 2^-80 on RD (see stage())
-    // (act = false: a warm-up row outside the cone, whose values are never used)
-    if (act) {
-        f.rr.a = rr_of(fma2(f.g1.a, f.g1.a, fma2(f.g2.a, f.g2.a, absq(c.a))), x.tau);
-        f.rr.b = rr_of(fma2(f.g1.b, f.g1.b, fma2(f.g2.b, f.g2.b, absq(c.b))), x.tau);
-    } else {
-        f.rr = zeroq();
-    }
+    f.rr.a = rr_of(fma2(f.g1.a, f.g1.a, fma2(f.g2.a, f.g2.a, absq(c.a))), x.tau);
+    f.rr.b = rr_of(fma2(f.g1.b, f.g1.b, fma2(f.g2.b, f.g2.b, absq(c.b))), x.tau);
     return f;
 }
 
@@ -305,14 +262,14 @@ __device__ __forceinline__ void back(const Q &g1, const Q &g2, const Q &rr, cons
 // (rho = 0 on Fg u Bg, Eq. 8) without predicates or extra instructions (|c'| is an FFMA2
 // operand modifier); u - c = fma(c', -2^100, u) exactly, and FFMA.SAT reproduces the pinned
 // 0 / 1 off RD (Eq. 9).
-template <bool WRITE_U, bool ALIGNED, int EDGE>
+template <bool WRITE_U, bool ALIGNED, bool LAST>
 __device__ __forceinline__ void stage(const Q &ap1, const Q &ap2, const Q &av, const Q &aw,
                                       const Q &q1, const Q &in1, const Q &in2, const Q &inv,
                                       const Q &ind, const float4 &c4, int m, const Ctx &x,
-                                      bool act, Q &bp1, Q &bp2, Q &bv, Q &bw, Q &o1, Q &o2, Q &ov, Q &od,
+                                      Q &bp1, Q &bp2, Q &bv, Q &bw, Q &o1, Q &o2, Q &ov, Q &od,
                                       Q &ou) {
     const Q c = ldq(c4);
-    const Front f = front<ALIGNED, EDGE>(aw, inv, ind, c, m, x, act);
+    const Front f = front<ALIGNED, LAST>(aw, inv, ind, c, m, x);
     back<WRITE_U>(f.g1, f.g2, f.rr, ap1, ap2, av, q1, c, x, o1, o2, ov, od, ou);
     bp1 = in1;
     bp2 = in2;
@@ -425,7 +382,7 @@ struct Extra {  // per-row-step state only the CHECK mode needs
 
 // One row step: consume input row n from the ring, advance all S stages, store the level-S
 // row if it is an output row of this item, then refill the slot with row n+RING.
-template <int S, int MODE, bool ALIGNED, int EDGE, bool WAVE, int KST = -1>
+template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE>
 __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B,
                                           const Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
                                           const Ctx &x, float &acc_u, float &acc_v, Wave &wv) {
@@ -457,25 +414,9 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
                       : SPL::at(t + 1)      ? A.d1[SPL::at(t + 1) > 0 ? SPL::at(t + 1) - 1 : 0]
                                             : A.p1[(t + 1 < S) ? t + 1 : 0];
         const float4 c4 = crow[-32 * (n - m)];  // n - m is a compile-time lag
-        // prologue step KST >= 0 (row step n = R0 - S - 2 + KST, compile time): a stage still
-        // above its cone (Act) is elided -- it only carries its state and passes its input on
-        const bool act = KST < 0 || KST - (S + 2) >= Act<S>::first(t);
-        if (act) {
-            stage<WRITE_U, ALIGNED, EDGE>(A.p1[t], A.p2[t], A.v[t], A.w[t], q1, in1, in2, inv,
-                                          ind, c4, m, x, true, B.p1[t], B.p2[t], B.v[t], B.w[t],
-                                          o1, o2, ov, od, uu);
-        } else {
-            B.p1[t] = in1;
-            B.p2[t] = in2;
-            B.v[t] = inv;
-            B.w[t].a = fma2(inv.a, -x.inv_theta, ind.a);  // (dead unless the stage starts next)
-            B.w[t].b = fma2(inv.b, -x.inv_theta, ind.b);
-            o1 = in1;
-            o2 = in2;
-            ov = inv;
-            od = ind;
-            uu = inv;
-        }
+        stage<WRITE_U, ALIGNED, LAST>(A.p1[t], A.p2[t], A.v[t], A.w[t], q1, in1, in2, inv, ind,
+                                      c4, m, x, B.p1[t], B.p2[t], B.v[t], B.w[t], o1, o2, ov, od,
+                                      uu);
         in1 = o1;
         in2 = o2;
         inv = ov;
@@ -483,15 +424,6 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
         if (MODE == MODE_CHECK && S >= 2 && t == S - 2) EB.uprev = uu;  // u^(l-1), row m
         if (t == S - 1) {
             B.q1 = o1;
-#ifndef RDS_NO_PRED_STORE
-            if (MODE == MODE_PLAIN) {  // predicated stores instead of a divergent branch
-                const bool st = x.store_lane && m >= x.R0 && m < x.Rend;
-                const int64_t o = (int64_t)m * x.pitch + x.col;
-                st_pred(x.p1o + o, o1, st);
-                st_pred(x.p2o + o, o2, st);
-                st_pred(x.vo + o, ov, st);
-            } else
-#endif
             if (x.store_lane && m >= x.R0 && m < x.Rend) {
                 const int64_t o = (int64_t)m * x.pitch + x.col;
                 if (MODE == MODE_CHECK) {
@@ -531,29 +463,7 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
     cp_async_commit();
 }
 
-// The prologue: row steps K, K+1, ... < P of a march that starts at n = R0 - S - 2, unrolled
-// (each step's set of live stages is a compile-time constant).  P is even, so the state ends
-// in A as after the loop's step pairs.
-template <int S, int MODE, bool ALIGNED, int K, int P>
-struct Prologue {
-    __device__ static __forceinline__ void run(PipeState<S> &A, PipeState<S> &B,
-                                               Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
-                                               const Ctx &x, float &acc_u, float &acc_v,
-                                               Wave &wv) {
-        pipe_step<S, MODE, ALIGNED, 0, false, K>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
-        pipe_step<S, MODE, ALIGNED, 0, false, K + 1>(B, A, EB, EA, n + 1, x, acc_u, acc_v,
-                                                         wv);
-        Prologue<S, MODE, ALIGNED, K + 2, P>::run(A, B, EA, EB, n + 2, x, acc_u, acc_v, wv);
-    }
-};
-template <int S, int MODE, bool ALIGNED, int P>
-struct Prologue<S, MODE, ALIGNED, P, P> {
-    __device__ static __forceinline__ void run(PipeState<S> &, PipeState<S> &, Extra<S, MODE> &,
-                                               Extra<S, MODE> &, int, const Ctx &, float &,
-                                               float &, Wave &) {}
-};
-
-template <int S, int MODE, bool ALIGNED, int EDGE, bool WAVE>
+template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE>
 __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &acc_v,
                                       Wave &wv) {
     PipeState<S> A, B;
@@ -566,23 +476,13 @@ __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &
         A.d1[k] = A.d2[k] = A.dv[k] = A.dd[k] = zeroq();
     }
     EA.uprev = zeroq();
-    int k = 0;
-#ifndef RDS_NO_PROLOGUE
-    // the first row steps as straight-line code without the stages above their cone (Act);
-    // run_item started the march at n = R0 - S - 2 for this
-    if (!WAVE && EDGE == 0) {
-        Prologue<S, MODE, ALIGNED, 0, Act<S>::prologue()>::run(A, B, EA, EB, n, x, acc_u, acc_v,
-                                                               wv);
-        n += Act<S>::prologue();
-    }
-#endif
-    for (; n <= x.n_last; n += 2, ++k) {
+    for (int k = 0; n <= x.n_last; n += 2, ++k) {
         // wavefront: every second loop head, publish the rows emitted so far (rows < n - S -
         // NS of this item are final)
         if (WAVE && (k % (WAVE_PUB / 2)) == WAVE_PUB / 2 - 1)
             wave_publish(x, min(max(n - S - Split<S>::NS, x.R0), x.Rend));
-        pipe_step<S, MODE, ALIGNED, EDGE, WAVE>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
-        pipe_step<S, MODE, ALIGNED, EDGE, WAVE>(B, A, EB, EA, n + 1, x, acc_u, acc_v, wv);
+        pipe_step<S, MODE, ALIGNED, LAST, WAVE>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
+        pipe_step<S, MODE, ALIGNED, LAST, WAVE>(B, A, EB, EA, n + 1, x, acc_u, acc_v, wv);
     }
 }
 
@@ -609,30 +509,15 @@ __device__ __forceinline__ void run_item(Ctx &x, const StencilArgs &a, int strip
         x.kx.a = make_float2(last_col(x.col) ? 0.0f : 1.0f, last_col(x.col + 2) ? 0.0f : 1.0f);
         x.kx.b = make_float2(last_col(x.col + 1) ? 0.0f : 1.0f, last_col(x.col + 3) ? 0.0f : 1.0f);
     }
-#ifndef RDS_ADDR32
     x.p1i = p1i + x.col;
     x.p2i = p2i + x.col;
     x.vi = vi + x.col;
     x.ci = a.c + x.col;
-#else
-    x.p1i = p1i;
-    x.p2i = p2i;
-    x.vi = vi;
-    x.ci = a.c;
-#endif
     // input rows [n, n_last]; the cone reaches S+1 rows up and S rows down, the delay
     // buffer adds one row of latency.  The step count is made even (one extra warm-up
     // row) for the two-state unrolled loop.
     x.n_last = x.Rend - 1 + S + Split<S>::NS;
     int n = x.R0 - (S + 1);
-#ifndef RDS_NO_PROLOGUE
-    // a warp holding an image-last column (the packed path checks it per stage)
-    const bool redge = __any_sync(0xffffffffu, x.right_edge) || !ALIGNED;
-    if (!WAVE && !redge && x.n_last < a.H - 1) {  // the prologue's fixed start; one extra step
-        n = x.R0 - S - 2;               // at the end when the count would be odd
-        if (((x.n_last - n + 1) & 1) != 0) ++x.n_last;
-    }
-#endif
     if (((x.n_last - n + 1) & 1) != 0) --n;
     if (WAVE) wave_need(x, wv, min(n + RING - 1, x.n_last));
 #pragma unroll
@@ -642,11 +527,9 @@ __device__ __forceinline__ void run_item(Ctx &x, const StencilArgs &a, int strip
     }
     // the Neumann row H-1 matters whenever the march (cone included) reaches it
     if (x.n_last >= a.H - 1)
-        march<S, MODE, ALIGNED, 3, WAVE>(x, n, acc_u, acc_v, wv);
-    else if (redge)
-        march<S, MODE, ALIGNED, 2, WAVE>(x, n, acc_u, acc_v, wv);
+        march<S, MODE, ALIGNED, true, WAVE>(x, n, acc_u, acc_v, wv);
     else
-        march<S, MODE, ALIGNED, 0, WAVE>(x, n, acc_u, acc_v, wv);
+        march<S, MODE, ALIGNED, false, WAVE>(x, n, acc_u, acc_v, wv);
     cp_async_wait<0>();
     __syncwarp();
 }
@@ -672,7 +555,6 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
     const int n_items = *a.n_items;
     Ctx x;
     x.pitch = a.pitch;
-    x.pitch32 = (int)a.pitch;
     x.H = a.H;
     x.tau = a.tau;
     x.theta = a.theta;

@@ -15,7 +15,7 @@
 //   C = 0   : takes input row n (rho1, rho2, v) from its cp.async ring and forms div rho there;
 //   C > 0   : takes chain C-1's emission of row step n-1 (rho1, rho2, v, div rho) from slot
 //             (C-1, (n-1) & 1) of the hand-off buffer;
-//   runs its stages (warm-up rows above the cone skip their MUFU work, Act);
+//   runs its stages;
 //   C < NC-1: writes its emission to slot (C, n & 1); the last chain stores the level-S row;
 //   C = 0   : refills the ring with row n + RING (rho1, rho2, v and c');
 //   then one CTA barrier: after it, the slots written in step n and the c' rows warp 0 waited
@@ -39,6 +39,14 @@ struct SplitWS {
     }
 };
 
+__device__ __forceinline__ void ws_st_pred(float *p, const Q &x, bool pr) {  // swizzled
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %0, 0;\n"
+        " @p st.global.v4.f32 [%1], {%2, %3, %4, %5};\n}\n" ::"r"((int)pr),
+        "l"(p), "f"(x.a.x), "f"(x.a.y), "f"(x.b.x), "f"(x.b.y)
+        : "memory");
+}
+
 constexpr int WS_HAND = 4 * 32;  // float4 per hand-off slot: rho1, rho2, v, div rho x 32 lanes
 // shared memory in float4: rho/v ring (warp 0), c' ring (doubled), hand-off slots, item word
 __host__ __device__ constexpr int ws_smem_f4(int nc) {
@@ -60,7 +68,7 @@ __device__ __forceinline__ void bar_rows(int nthreads) {  // named barrier 1: th
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-template <int S, int NC, int C, bool LAST, bool WARM>
+template <int S, int NC, int C, bool LAST>
 __device__ __forceinline__ void ws_step(const WsState<SplitWS<S, NC>::sp(C + 1) - SplitWS<S, NC>::sp(C)> &A,
                                         WsState<SplitWS<S, NC>::sp(C + 1) - SplitWS<S, NC>::sp(C)> &B,
                                         int n, const Ctx &x, const float4 *hin, float4 *hout) {
@@ -89,10 +97,9 @@ __device__ __forceinline__ void ws_step(const WsState<SplitWS<S, NC>::sp(C + 1) 
         const int m = n - t - 1 - SP::lag(t);  // row emitted (level t+1)
         const Q &q1 = (i == N - 1) ? A.q1 : A.p1[(i + 1 < N) ? i + 1 : 0];
         const float4 c4 = crow[-32 * (n - m)];
-        const bool act = !WARM || n - x.R0 >= Act<S, SP>::first(t);
         Q o1, o2, ov, od;
-        stage<false, true, LAST ? 3 : 2>(A.p1[i], A.p2[i], A.v[i], A.w[i], q1, in1, in2, inv, ind, c4, m,
-                                 x, act, B.p1[i], B.p2[i], B.v[i], B.w[i], o1, o2, ov, od, uu);
+        stage<false, true, LAST>(A.p1[i], A.p2[i], A.v[i], A.w[i], q1, in1, in2, inv, ind, c4, m,
+                                 x, B.p1[i], B.p2[i], B.v[i], B.w[i], o1, o2, ov, od, uu);
         in1 = o1;
         in2 = o2;
         inv = ov;
@@ -109,9 +116,9 @@ __device__ __forceinline__ void ws_step(const WsState<SplitWS<S, NC>::sp(C + 1) 
         const int m = n - S - SP::NS;  // the level-S row of this step
         const bool st = x.store_lane && m >= x.R0 && m < x.Rend;
         const int64_t o = (int64_t)m * x.pitch + x.col;
-        st_pred(x.p1o + o, in1, st);
-        st_pred(x.p2o + o, in2, st);
-        st_pred(x.vo + o, inv, st);
+        ws_st_pred(x.p1o + o, in1, st);
+        ws_st_pred(x.p2o + o, in2, st);
+        ws_st_pred(x.vo + o, inv, st);
     }
     if (C == 0) {
         if (n + RING <= x.n_last) stage_row(x, n + RING);
@@ -128,17 +135,9 @@ __device__ __forceinline__ void ws_march(const Ctx &x, int n, const float4 *hin,
 #pragma unroll
     for (int i = 0; i < N; ++i) A.p1[i] = A.p2[i] = A.v[i] = A.w[i] = zeroq();
     A.q1 = zeroq();
-    // warm-up: this chain's stages above their cone skip the MUFU work (Act)
-#ifdef RDS_WS_NOWARM
-    if (false)
-#endif
-    for (; n <= x.n_last && n < x.R0 + Act<S, SP>::first(SP::sp(C + 1) - 1); n += 2) {
-        ws_step<S, NC, C, LAST, true>(A, B, n, x, hin, hout);
-        ws_step<S, NC, C, LAST, true>(B, A, n + 1, x, hin, hout);
-    }
     for (; n <= x.n_last; n += 2) {
-        ws_step<S, NC, C, LAST, false>(A, B, n, x, hin, hout);
-        ws_step<S, NC, C, LAST, false>(B, A, n + 1, x, hin, hout);
+        ws_step<S, NC, C, LAST>(A, B, n, x, hin, hout);
+        ws_step<S, NC, C, LAST>(B, A, n + 1, x, hin, hout);
     }
 }
 
@@ -182,7 +181,6 @@ __global__ void __launch_bounds__(NC * 32, RDS_WS_MINB) k_stencil_ws(const Stenc
     float4 *hand = smem + RING * 96 + 2 * CR * 32;
     Ctx x;
     x.pitch = a.pitch;
-    x.pitch32 = (int)a.pitch;
     x.H = a.H;
     x.tau = a.tau;
     x.theta = a.theta;
@@ -216,17 +214,10 @@ __global__ void __launch_bounds__(NC * 32, RDS_WS_MINB) k_stencil_ws(const Stenc
             x.kx.a = make_float2(1.0f, 1.0f);  // (ALIGNED: the packed edge uses right_edge)
             x.kx.b = make_float2(1.0f, 1.0f);
         }
-#ifndef RDS_ADDR32
         x.p1i = a.p1_in + x.col;
         x.p2i = a.p2_in + x.col;
         x.vi = a.v_in + x.col;
         x.ci = a.c + x.col;
-#else
-        x.p1i = a.p1_in;
-        x.p2i = a.p2_in;
-        x.vi = a.v_in;
-        x.ci = a.c;
-#endif
         x.n_last = x.Rend - 1 + S + SP::NS;
         int n = x.R0 - (S + 1);
         if (((x.n_last - n + 1) & 1) != 0) --n;

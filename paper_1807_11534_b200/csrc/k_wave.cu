@@ -25,7 +25,6 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, 2) k_wave(const WaveArgs w
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     Ctx x;
     x.pitch = a.pitch;
-    x.pitch32 = (int)a.pitch;
     x.H = a.H;
     x.tau = a.tau;
     x.theta = a.theta;

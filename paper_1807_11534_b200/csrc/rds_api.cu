@@ -979,7 +979,7 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactP
     }
     if (!h->rdc_idx) CK(h, cudaMalloc(&h->rdc_idx, sizeof(int32_t) * npx));
     // records x2 (float4), packed codes (uint2), list, u
-    const size_t nn = ((size_t)(n > 0 ? n : 1) + 7) & ~(size_t)7;  // rec1 on a 128-byte line
+    const size_t nn = (size_t)(n > 0 ? n : 1);
     void *pb = h->rdc_buf;
     CK(h, grow(&pb, &h->rdc_bytes, nn * (16 * 2 + 8 + 4 + 4)));
     h->rdc_buf = pb;
