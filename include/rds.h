@@ -193,6 +193,14 @@ typedef struct {
                                 sub-partition hide less latency than 2 warps that interleave
                                 three independent chains each. */
 
+#define RDS_OPT_PROLOGUE 14  /* the iterating stencil launches in their prologue form: the first
+                                2k+4 row steps of every work item as straight-line code in which
+                                the stages still above their dependency cone are elided (6-7% of
+                                the stage-rows at k_fuse 7, more for short items).  Same values
+                                (bit-identical).  0 = off, 1 = on, 2 (default) = on for images of
+                                at most 2^22 pixels, where items are short (C1 -8.6%); off above,
+                                where the larger kernel measured no gain. */
+
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */
 int rds_create(int64_t H, int64_t W, rds_t **out);

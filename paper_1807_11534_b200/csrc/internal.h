@@ -122,6 +122,7 @@ struct StencilArgs {
     int img_w;                           // columns per image (W, or the image width of a batch)
     float tau, theta, inv_theta;
     int ws;                              // full-depth PLAIN launches on k_stencil_ws (RDS_OPT_WS)
+    int pro;                             // PLAIN launches in the prologue form (RDS_OPT_PROLOGUE)
 };
 
 // The temporal wavefront (k_wave.cu): nblk blocks of KF iterations of a

@@ -16,25 +16,31 @@ namespace rds {
 
 static const int kKfMax = STENCIL_KF_MAX;
 
-static StencilFn lookup(int kf, int stages, int mode, bool aligned) {
+static StencilFn lookup(int kf, int stages, int mode, bool aligned, bool pro = false) {
     static StencilFn table[kKfMax + 1][kKfMax + 1][3][2];
+    static StencilFn ptable[kKfMax + 1][kKfMax + 1][2];
     static bool init = false;
     if (!init) {
-#define RDS_FILL(K) stencil_fill_kf##K(table[K]);
+#define RDS_FILL(K) stencil_fill_kf##K(table[K], ptable[K]);
         RDS_KF_LIST(RDS_FILL)
 #undef RDS_FILL
+        auto attr = [](StencilFn f) {
+            if (f)
+                cudaFuncSetAttribute((const void *)f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     STENCIL_SMEM);
+        };
         for (auto &a : table)
             for (auto &b : a)
                 for (auto &c : b)
-                    for (StencilFn f : c)
-                        if (f)
-                            cudaFuncSetAttribute((const void *)f,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 STENCIL_SMEM);
+                    for (StencilFn f : c) attr(f);
+        for (auto &a : ptable)
+            for (auto &b : a)
+                for (StencilFn f : b) attr(f);
         init = true;
     }
     if (kf < 1 || kf > kKfMax || stages < 1 || stages > kf || mode < 0 || mode > 2)
         return nullptr;
+    if (pro && mode == MODE_PLAIN) return ptable[kf][stages][aligned ? 1 : 0];
     return table[kf][stages][mode][aligned ? 1 : 0];
 }
 
@@ -90,8 +96,9 @@ cudaError_t launch_stencil(int kf, int stages, int mode, const StencilArgs &a, i
         if (g > grid * STENCIL_WARPS) g = grid * STENCIL_WARPS;
         return launch_stencil_ws(stages, a, g, s);
     }
-    // the packed path needs every image-last column at lane position 3 of a quad
-    StencilFn fn = lookup(kf, stages, mode, (a.img_w & 3) == 0);
+    // the packed path needs every image-last column at lane position 3 of a quad; the prologue
+    // form where the caller asks for it (a.pro, RDS_OPT_PROLOGUE)
+    StencilFn fn = lookup(kf, stages, mode, (a.img_w & 3) == 0, a.pro != 0);
     if (!fn) return cudaErrorInvalidValue;
     if (grid <= 0) return cudaSuccess;
     // Programmatic dependent launch: the next stencil launch of the K loop is set up while the

@@ -145,6 +145,23 @@ struct Split {
     }
 };
 
+// Warm-up elision (the trapezoid of the vertical cone; the "prologue" kernels k_stencil_pro,
+// DESIGN.md §5).  Level S is stored on rows [R0, Rend); one iteration reads rows m-1 .. m+1
+// of rho and m .. m+1 of v, w (div rho at m needs rho1 at m-1), so level t is needed on rows
+// >= R0 - 1 - (S - t) for rho and >= R0 - (S - t) for v.  Stage t emits level t+1 at row
+// m = n - t - 1 - lag(t) in row step n, so its rows are needed from row step
+// n = R0 - S + 2t + 1 + lag(t) on; before that it only carries its state (the row it received
+// and its w) and passes its input through.  At the first active step the stage's own previous
+// row (q1, rho1 of level t+1 at row m-1) is a placeholder, but it enters only v and div rho of
+// level t+1 at row m, which are needed one row lower.
+template <int S>
+struct Act {
+    // first row step (relative to R0) in which stage t does its work
+    __host__ __device__ static constexpr int first(int t) { return 1 - S + 2 * t + Split<S>::lag(t); }
+    // prologue length of a march starting at R0 - S - 2: until every stage is active, even
+    __host__ __device__ static constexpr int prologue() { return ((first(S - 1) + S + 2) + 1) & ~1; }
+};
+
 template <int S>
 struct PipeState {
     static constexpr int ND = Split<S>::NS > 0 ? Split<S>::NS : 1;
@@ -382,7 +399,7 @@ struct Extra {  // per-row-step state only the CHECK mode needs
 
 // One row step: consume input row n from the ring, advance all S stages, store the level-S
 // row if it is an output row of this item, then refill the slot with row n+RING.
-template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE>
+template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE, int KST = -1>
 __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B,
                                           const Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
                                           const Ctx &x, float &acc_u, float &acc_v, Wave &wv) {
@@ -414,9 +431,24 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
                       : SPL::at(t + 1)      ? A.d1[SPL::at(t + 1) > 0 ? SPL::at(t + 1) - 1 : 0]
                                             : A.p1[(t + 1 < S) ? t + 1 : 0];
         const float4 c4 = crow[-32 * (n - m)];  // n - m is a compile-time lag
-        stage<WRITE_U, ALIGNED, LAST>(A.p1[t], A.p2[t], A.v[t], A.w[t], q1, in1, in2, inv, ind,
-                                      c4, m, x, B.p1[t], B.p2[t], B.v[t], B.w[t], o1, o2, ov, od,
-                                      uu);
+        // prologue step KST >= 0 (row step n = R0 - S - 2 + KST, compile time): a stage still
+        // above its cone (Act) is elided -- it carries its state and passes its input on
+        if (KST < 0 || KST - (S + 2) >= Act<S>::first(t)) {
+            stage<WRITE_U, ALIGNED, LAST>(A.p1[t], A.p2[t], A.v[t], A.w[t], q1, in1, in2, inv,
+                                          ind, c4, m, x, B.p1[t], B.p2[t], B.v[t], B.w[t], o1,
+                                          o2, ov, od, uu);
+        } else {
+            B.p1[t] = in1;
+            B.p2[t] = in2;
+            B.v[t] = inv;
+            B.w[t].a = fma2(inv.a, -x.inv_theta, ind.a);  // (dead unless the stage starts next)
+            B.w[t].b = fma2(inv.b, -x.inv_theta, ind.b);
+            o1 = in1;
+            o2 = in2;
+            ov = inv;
+            od = ind;
+            uu = inv;
+        }
         in1 = o1;
         in2 = o2;
         inv = ov;
@@ -463,7 +495,29 @@ __device__ __forceinline__ void pipe_step(const PipeState<S> &A, PipeState<S> &B
     cp_async_commit();
 }
 
-template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE>
+// The prologue: row steps K, K+1, ... < P of a march that starts at n = R0 - S - 2, unrolled
+// (each step's set of live stages is a compile-time constant); P is even, so the state ends in
+// A as after the loop's step pairs.
+template <int S, int MODE, bool ALIGNED, int K, int P>
+struct Prologue {
+    __device__ static __forceinline__ void run(PipeState<S> &A, PipeState<S> &B,
+                                               Extra<S, MODE> &EA, Extra<S, MODE> &EB, int n,
+                                               const Ctx &x, float &acc_u, float &acc_v,
+                                               Wave &wv) {
+        pipe_step<S, MODE, ALIGNED, false, false, K>(A, B, EA, EB, n, x, acc_u, acc_v, wv);
+        pipe_step<S, MODE, ALIGNED, false, false, K + 1>(B, A, EB, EA, n + 1, x, acc_u, acc_v,
+                                                         wv);
+        Prologue<S, MODE, ALIGNED, K + 2, P>::run(A, B, EA, EB, n + 2, x, acc_u, acc_v, wv);
+    }
+};
+template <int S, int MODE, bool ALIGNED, int P>
+struct Prologue<S, MODE, ALIGNED, P, P> {
+    __device__ static __forceinline__ void run(PipeState<S> &, PipeState<S> &, Extra<S, MODE> &,
+                                               Extra<S, MODE> &, int, const Ctx &, float &,
+                                               float &, Wave &) {}
+};
+
+template <int S, int MODE, bool ALIGNED, bool LAST, bool WAVE, bool PRO = false>
 __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &acc_v,
                                       Wave &wv) {
     PipeState<S> A, B;
@@ -476,6 +530,11 @@ __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &
         A.d1[k] = A.d2[k] = A.dv[k] = A.dd[k] = zeroq();
     }
     EA.uprev = zeroq();
+    if (PRO && !LAST && !WAVE) {  // run_item started the march at R0 - S - 2 for this
+        Prologue<S, MODE, ALIGNED, 0, Act<S>::prologue()>::run(A, B, EA, EB, n, x, acc_u, acc_v,
+                                                               wv);
+        n += Act<S>::prologue();
+    }
     for (int k = 0; n <= x.n_last; n += 2, ++k) {
         // wavefront: every second loop head, publish the rows emitted so far (rows < n - S -
         // NS of this item are final)
@@ -489,7 +548,7 @@ __device__ __forceinline__ void march(const Ctx &x, int n, float &acc_u, float &
 // One item: output columns of `strip`, output rows [r0, r1), inputs from the planes p1i /
 // p2i / vi (pixel (0,0) origins).  Sets up the lane geometry, stages the first RING rows and
 // marches (S stages); returns with every cp.async group drained.
-template <int KF, int S, int MODE, bool ALIGNED, bool WAVE>
+template <int KF, int S, int MODE, bool ALIGNED, bool WAVE, bool PRO = false>
 __device__ __forceinline__ void run_item(Ctx &x, const StencilArgs &a, int strip, int r0, int r1,
                                          const float *p1i, const float *p2i, const float *vi,
                                          float &acc_u, float &acc_v, Wave &wv) {
@@ -518,6 +577,11 @@ __device__ __forceinline__ void run_item(Ctx &x, const StencilArgs &a, int strip
     // row) for the two-state unrolled loop.
     x.n_last = x.Rend - 1 + S + Split<S>::NS;
     int n = x.R0 - (S + 1);
+    const bool pro = PRO && !WAVE && x.n_last < a.H - 1;
+    if (pro) {  // the prologue's fixed start; one extra step at the end when the count is odd
+        n = x.R0 - S - 2;
+        if (((x.n_last - n + 1) & 1) != 0) ++x.n_last;
+    }
     if (((x.n_last - n + 1) & 1) != 0) --n;
     if (WAVE) wave_need(x, wv, min(n + RING - 1, x.n_last));
 #pragma unroll
@@ -528,6 +592,8 @@ __device__ __forceinline__ void run_item(Ctx &x, const StencilArgs &a, int strip
     // the Neumann row H-1 matters whenever the march (cone included) reaches it
     if (x.n_last >= a.H - 1)
         march<S, MODE, ALIGNED, true, WAVE>(x, n, acc_u, acc_v, wv);
+    else if (PRO && pro)
+        march<S, MODE, ALIGNED, false, WAVE, true>(x, n, acc_u, acc_v, wv);
     else
         march<S, MODE, ALIGNED, false, WAVE>(x, n, acc_u, acc_v, wv);
     cp_async_wait<0>();
@@ -540,7 +606,9 @@ struct MinBlocks {
     static constexpr int value = 2;
 };
 
-template <int KF, int S, int MODE, bool ALIGNED>
+// PRO: the prologue form (warm-up stages elided, Act), instantiated for MODE_PLAIN and chosen
+// per image size at launch
+template <int KF, int S, int MODE, bool ALIGNED, bool PRO = false>
 __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
     k_stencil(const StencilArgs a) {
     static_assert(S >= 1 && S <= KF && KF + 3 <= PAD_R, "stage count");
@@ -577,8 +645,8 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
         if (it >= n_items) break;  // warp-uniform
         const Item item = a.items[it];
         float acc_u = 0.0f, acc_v = 0.0f;
-        run_item<KF, S, MODE, ALIGNED, false>(x, a, item.strip, item.r0, item.r1, a.p1_in,
-                                              a.p2_in, a.v_in, acc_u, acc_v, wv);
+        run_item<KF, S, MODE, ALIGNED, false, PRO>(x, a, item.strip, item.r0, item.r1, a.p1_in,
+                                                   a.p2_in, a.v_in, acc_u, acc_v, wv);
         if (MODE == MODE_CHECK) {  // per-item partial sums, fixed lane order (deterministic)
             double su = acc_u, sv = acc_v;
 #pragma unroll
@@ -597,33 +665,36 @@ __global__ void __launch_bounds__(STENCIL_WARPS * 32, MinBlocks<S>::value)
 
 typedef void (*StencilFn)(const StencilArgs);
 
-// Fills t[S][mode][aligned] for S = 1..KF with the kernel instantiations of one k_fuse.
+// Fills t[S][mode][aligned] for S = 1..KF with the kernel instantiations of one k_fuse, and
+// pro[S][aligned] with the prologue forms of the plain mode.
 template <int KF, int S>
 struct Table {
-    static void fill(StencilFn (*t)[3][2]) {
+    static void fill(StencilFn (*t)[3][2], StencilFn (*pro)[2]) {
+        pro[S][0] = k_stencil<KF, S, MODE_PLAIN, false, true>;
+        pro[S][1] = k_stencil<KF, S, MODE_PLAIN, true, true>;
         t[S][0][0] = k_stencil<KF, S, MODE_PLAIN, false>;
         t[S][1][0] = k_stencil<KF, S, MODE_WRITE_U, false>;
         t[S][2][0] = k_stencil<KF, S, MODE_CHECK, false>;
         t[S][0][1] = k_stencil<KF, S, MODE_PLAIN, true>;
         t[S][1][1] = k_stencil<KF, S, MODE_WRITE_U, true>;
         t[S][2][1] = k_stencil<KF, S, MODE_CHECK, true>;
-        Table<KF, S - 1>::fill(t);
+        Table<KF, S - 1>::fill(t, pro);
     }
 };
 template <int KF>
 struct Table<KF, 0> {
-    static void fill(StencilFn (*)[3][2]) {}
+    static void fill(StencilFn (*)[3][2], StencilFn (*)[2]) {}
 };
 
 constexpr int STENCIL_KF_MAX = 8;
 // defined in k_stencil_kf<K>.cu
-void stencil_fill_kf1(StencilFn (*t)[3][2]);
-void stencil_fill_kf2(StencilFn (*t)[3][2]);
-void stencil_fill_kf3(StencilFn (*t)[3][2]);
-void stencil_fill_kf4(StencilFn (*t)[3][2]);
-void stencil_fill_kf5(StencilFn (*t)[3][2]);
-void stencil_fill_kf6(StencilFn (*t)[3][2]);
-void stencil_fill_kf7(StencilFn (*t)[3][2]);
-void stencil_fill_kf8(StencilFn (*t)[3][2]);
+void stencil_fill_kf1(StencilFn (*t)[3][2], StencilFn (*pro)[2]);
+void stencil_fill_kf2(StencilFn (*t)[3][2], StencilFn (*pro)[2]);
+void stencil_fill_kf3(StencilFn (*t)[3][2], StencilFn (*pro)[2]);
+void stencil_fill_kf4(StencilFn (*t)[3][2], StencilFn (*pro)[2]);
+void stencil_fill_kf5(StencilFn (*t)[3][2], StencilFn (*pro)[2]);
+void stencil_fill_kf6(StencilFn (*t)[3][2], StencilFn (*pro)[2]);
+void stencil_fill_kf7(StencilFn (*t)[3][2], StencilFn (*pro)[2]);
+void stencil_fill_kf8(StencilFn (*t)[3][2], StencilFn (*pro)[2]);
 
 }  // namespace rds

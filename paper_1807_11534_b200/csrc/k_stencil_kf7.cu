@@ -4,6 +4,8 @@
 
 namespace rds {
 
-void stencil_fill_kf7(StencilFn (*t)[3][2]) { Table<7, 7>::fill(t); }
+void stencil_fill_kf7(StencilFn (*t)[3][2], StencilFn (*pro)[2]) {
+    Table<7, 7>::fill(t, pro);
+}
 
 }  // namespace rds

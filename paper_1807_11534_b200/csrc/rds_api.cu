@@ -108,6 +108,7 @@ struct rds_handle {
     bool wave_ok = false; // the last solve's set-up allows the wavefront (aligned, supported kf)
     int opt_resident = 2; // small images as one resident cluster: 0 off, 1 on, 2 auto (RDS_OPT_RESIDENT)
     int opt_ws = 0;       // full-depth launches on the warp-specialised stencil (RDS_OPT_WS)
+    int opt_pro = 2;      // plain launches in the prologue form: 0 off, 1 on, 2 auto (RDS_OPT_PROLOGUE)
     int opt_persist = 0;  // fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto (RDS_OPT_PERSIST)
     bool persist_ok = false;  // the last solve's set-up allows it (aligned, supported kf, size)
     unsigned long long *loop_bar = nullptr;  // grid-barrier counter of k_loop
@@ -331,6 +332,15 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             if (value < 0 || value > 2)
                 return fail(h, RDS_EINVAL, "rds_set_option: compact=%lld", (long long)value);
             h->opt_compact = (int)value;
+            return RDS_OK;
+        case RDS_OPT_PROLOGUE:
+            if (value < 0 || value > 2)
+                return fail(h, RDS_EINVAL, "rds_set_option: prologue=%lld", (long long)value);
+            h->opt_pro = (int)value;
+            if (h->graph) {
+                cudaGraphExecDestroy(h->graph);
+                h->graph = nullptr;
+            }
             return RDS_OK;
         case RDS_OPT_WS:
             if (value < 0 || value > 1)
@@ -616,6 +626,7 @@ static cudaError_t enqueue_plan(rds_t *h, const LaunchPlan *plan, int n, int kf,
     a.n_items = h->counts + 1;
     a.pitch = h->pitch;
     a.ws = h->opt_ws;
+    a.pro = h->opt_pro == 1 || (h->opt_pro == 2 && h->H * h->W <= (int64_t(1) << 22));
     a.H = (int)h->H;
     a.W = (int)h->W;
     a.img_w = (int)h->img_w;
@@ -691,6 +702,7 @@ static cudaError_t enqueue_wave(rds_t *h, int kf, int iters, int nblk, int max_i
     a.n_items = h->counts + 1;
     a.pitch = h->pitch;
     a.ws = h->opt_ws;
+    a.pro = h->opt_pro == 1 || (h->opt_pro == 2 && h->H * h->W <= (int64_t(1) << 22));
     a.H = (int)h->H;
     a.W = (int)h->W;
     a.img_w = (int)h->img_w;
@@ -757,6 +769,7 @@ static cudaError_t enqueue_persist(rds_t *h, int kf, int iters, int max_items, f
     a.n_items = h->counts + 1;
     a.pitch = h->pitch;
     a.ws = h->opt_ws;
+    a.pro = h->opt_pro == 1 || (h->opt_pro == 2 && h->H * h->W <= (int64_t(1) << 22));
     a.H = (int)h->H;
     a.W = (int)h->W;
     a.img_w = (int)h->img_w;

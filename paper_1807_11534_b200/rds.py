@@ -27,6 +27,7 @@ RDS_OPT_STOP_NORM = 7  # 0 Euclidean over pixels (default), 1 RMS
 RDS_OPT_COMPACT = 8    # f3: 0 dense stencil, 1 compacted RD iteration, 2 auto (default)
 RDS_OPT_WAVE = 9       # temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto
 RDS_OPT_RESIDENT = 10  # small images as one resident cluster: 0 off, 1 / 2 (default) on
+RDS_OPT_PROLOGUE = 14  # plain stencil launches in the prologue form: 0 off, 1 on, 2 auto (default)
 RDS_OPT_WS = 13        # full-depth launches on the warp-specialised stencil: 0 off (default), 1 on
 RDS_OPT_PERSIST = 11   # fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto
 RDS_OPT_GRID = 12      # mid-size images resident on the whole GPU: 0 off (default), 1 / 2 on
@@ -403,7 +404,7 @@ class Solver:
 
     def __init__(self, H, W, stream=None, k_fuse=0, item_rows=0, timing=False, skip=True,
                  graph=True, batch=None, compact=None, wave=None, resident=None,
-                 persist=None, grid=None, ws=None):
+                 persist=None, grid=None, ws=None, prologue=None):
         self.shape = (int(H) * (int(batch) if batch else 1), int(W))
         if batch is not None:
             h = ctypes.c_void_p()
@@ -432,6 +433,8 @@ class Solver:
             rds_set_option(self.h, RDS_OPT_GRID, int(grid))
         if ws is not None:
             rds_set_option(self.h, RDS_OPT_WS, int(ws))
+        if prologue is not None:
+            rds_set_option(self.h, RDS_OPT_PROLOGUE, int(prologue))
 
     def close(self):
         if self.h is not None:

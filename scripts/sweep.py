@@ -23,6 +23,7 @@ ap.add_argument("--iters", type=int, default=0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--ctas", default="0", help="cap on stencil CTAs per SM (0 = occupancy)")
 ap.add_argument("--ws", default="0", help="RDS_OPT_WS values (warp-specialised stencil)")
+ap.add_argument("--pro", default="2", help="RDS_OPT_PROLOGUE values (prologue form)")
 args = ap.parse_args()
 
 cfg = wl.CONFIGS[args.config]
@@ -34,11 +35,13 @@ s.set_image(torch.from_numpy(z).cuda())
 s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, torch.from_numpy(P).cuda() if P is not None else None)
 am = s.absmax()
 delta = wl.band_delta(args.delta, am)
-for kf, rows, ctas, ws in [(int(a), int(b), int(c), int(d)) for a in args.kf.split(",")
-                           for b in args.rows.split(",") for c in args.ctas.split(",")
-                           for d in args.ws.split(",")]:
+for kf, rows, ctas, ws, pro in [(int(a), int(b), int(c), int(d), int(e))
+                                for a in args.kf.split(",") for b in args.rows.split(",")
+                                for c in args.ctas.split(",") for d in args.ws.split(",")
+                                for e in args.pro.split(",")]:
     if True:
         s.set_option(rds.RDS_OPT_WS, ws)
+        s.set_option(rds.RDS_OPT_PROLOGUE, pro)
         s.set_option(rds.RDS_OPT_KFUSE, kf)
         s.set_option(rds.RDS_OPT_ITEM_ROWS, rows)
         s.set_option(rds.RDS_OPT_CTAS_PER_SM, ctas)
@@ -51,7 +54,7 @@ for kf, rows, ctas, ws in [(int(a), int(b), int(c), int(d)) for a in args.kf.spl
         info = s.stats()
         lm = statistics.median(ts)
         px = info["n_active_tiles"] * 1024
-        print(json.dumps({"config": args.config, "kf": kf, "rows": rows, "ctas": ctas, "ws": ws,
+        print(json.dumps({"config": args.config, "kf": kf, "rows": rows, "ctas": ctas, "ws": ws, "pro": pro,
                           "defs": os.environ.get("RDS_NVCC_DEFS", ""), "loop_ms": lm,
                           "gpix_iter_s": px * K / lm / 1e6, "items": info["n_active_items"],
                           "launches": info["launches"]}), flush=True)
