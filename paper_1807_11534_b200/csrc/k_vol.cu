@@ -258,6 +258,139 @@ __global__ void __launch_bounds__(VT_X * VT2_Y) k_vol_step2(const VolArgs a) {
     }
 }
 
+// Two barriers per plane step (RDS_VOL_2BAR): rho1 / rho2 of plane n + 1 go into the other of
+// two shared slots during step n's rho phase, so the barrier that publishes the new rho also
+// publishes them and the next step's w phase needs no barrier of its own.  Same operations.
+template <bool WRITE_U>
+__global__ void __launch_bounds__(VT_X * VT2_Y) k_vol_step2b(const VolArgs a) {
+    __shared__ float s1[2][VT_Y][VT_X], s2[2][VT_Y][VT_X];  // rho1, rho2 of planes n, n+1
+    __shared__ float sw[2][VT_Y][VT_X];                // w of planes n-1, n (alternating)
+    __shared__ float q1s[VT_Y][VT_X], q2s[VT_Y][VT_X]; // rho1, rho2 new of plane n-1
+    const int tx = threadIdx.x, ty0 = 2 * threadIdx.y;  // local rows ty0, ty0 + 1
+    const int j = blockIdx.x * VO_X - 2 + tx, i0 = blockIdx.y * VO_Y - 2 + ty0;
+    const int k0 = blockIdx.z * a.kz, k1 = min(k0 + a.kz, a.D);
+    const float tau = a.tau, theta = a.theta, inv_theta = a.inv_theta;
+    bool in_w[2], in_q[2], in_o[2], last_i[2];
+    int64_t col[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        const int ty = ty0 + r, i = i0 + r;
+        col[r] = (int64_t)i * a.pitch + j;
+        in_w[r] = ty >= 1 && tx >= 1;
+        in_q[r] = ty >= 1 && ty <= VT_Y - 2 && tx >= 1 && tx <= VT_X - 2;
+        in_o[r] = ty >= 2 && ty <= VT_Y - 2 && tx >= 2 && tx <= VT_X - 2 && i < a.H && j < a.W;
+        last_i[r] = i == a.H - 1;
+    }
+    const bool last_j = j == a.W - 1;
+    float pp1[2] = {0.f, 0.f}, pp2[2] = {0.f, 0.f}, pv[2] = {0.f, 0.f};
+    float pc[2] = {INFINITY, INFINITY}, q3prev[2] = {0.f, 0.f}, pp3[2];
+    float x1[2], x2[2], x3[2], xv[2], xc[2];
+    int64_t o_next[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        pp3[r] = a.p3_in[(int64_t)(k0 - 2) * a.plane + col[r]];
+        o_next[r] = (int64_t)(k0 - 1) * a.plane + col[r];
+        x1[r] = a.p1_in[o_next[r]];
+        x2[r] = a.p2_in[o_next[r]];
+        x3[r] = a.p3_in[o_next[r]];
+        xv[r] = a.v_in[o_next[r]];
+        xc[r] = a.c[o_next[r]];
+    }
+    // plane k0 - 1 into its rho1 / rho2 slot (the loop stores plane n + 1 during step n)
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+        s1[(k0 - 1) & 1][ty0 + r][tx] = x1[r];
+        s2[(k0 - 1) & 1][ty0 + r][tx] = x2[r];
+    }
+    __syncthreads();
+    int cur = 0;
+    for (int n = k0 - 1; n <= k1; ++n) {
+        const int sb = n & 1;
+        float p1n[2], p2n[2], p3n[2], vn[2], cn[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            p1n[r] = x1[r];
+            p2n[r] = x2[r];
+            p3n[r] = x3[r];
+            vn[r] = xv[r];
+            cn[r] = xc[r];
+            if (n < k1) {
+                o_next[r] += a.plane;
+                x1[r] = a.p1_in[o_next[r]];
+                x2[r] = a.p2_in[o_next[r]];
+                x3[r] = a.p3_in[o_next[r]];
+                xv[r] = a.v_in[o_next[r]];
+                xc[r] = a.c[o_next[r]];
+            }
+        }
+        float wn[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int ty = ty0 + r;
+            wn[r] = 0.f;
+            if (in_w[r]) {
+                const float up1 = r == 1 ? p1n[0] : s1[sb][ty - 1][tx];
+                const float d =
+                    (p1n[r] - up1) + (p2n[r] - s2[sb][ty][tx - 1]) + (p3n[r] - pp3[r]);
+                wn[r] = fmaf(vn[r], -inv_theta, d);
+            }
+            sw[cur][ty][tx] = wn[r];
+        }
+        __syncthreads();
+        float q1[2], q2[2], q3[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int ty = ty0 + r;
+            q1[r] = q2[r] = q3[r] = 0.f;
+            if (in_q[r]) {
+                const float w0 = sw[cur ^ 1][ty][tx];
+                const float g1 = last_i[r] ? 0.f : sw[cur ^ 1][ty + 1][tx] - w0;
+                const float g2 = last_j ? 0.f : sw[cur ^ 1][ty][tx + 1] - w0;
+                const float g3 = (n - 1 == a.D - 1) ? 0.f : wn[r] - w0;
+                const float s = fmaf(g1, g1, fmaf(g2, g2, fmaf(g3, g3, fabsf(pc[r]))));
+                const float rr = vrcp(fmaf(tau, vsqrt(s), 1.0f));
+                q1[r] = fmaf(tau, g1, pp1[r]) * rr;
+                q2[r] = fmaf(tau, g2, pp2[r]) * rr;
+                q3[r] = fmaf(tau, g3, pp3[r]) * rr;
+            }
+            q1s[ty][tx] = q1[r];
+            q2s[ty][tx] = q2[r];
+            // plane n + 1 (prefetched at the top of this step) into the other slot: the
+            // barrier below also publishes it for the next step's w
+            s1[sb ^ 1][ty][tx] = x1[r];
+            s2[sb ^ 1][ty][tx] = x2[r];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int ty = ty0 + r;
+            if (in_o[r] && n - 1 >= k0) {
+                const float qup = r == 1 ? q1[0] : q1s[ty - 1][tx];
+                const float d = (q1[r] - qup) + (q2[r] - q2s[ty][tx - 1]) + (q3[r] - q3prev[r]);
+                const float u = fmaf(-theta, d, pv[r]);
+                const float vnew = __saturatef(fmaf(pc[r], -0x1p100f, u));
+                const int64_t oo = (int64_t)(n - 1) * a.plane + col[r];
+                a.p1_out[oo] = q1[r];
+                a.p2_out[oo] = q2[r];
+                a.p3_out[oo] = q3[r];
+                a.v_out[oo] = vnew;
+                if (WRITE_U) {
+                    const float uu = fabsf(pc[r]) < INFINITY ? u : pv[r];
+                    a.u_out[oo] = uu;
+                    a.mask_out[oo] = uu > 0.5f;
+                }
+            }
+            pp1[r] = p1n[r];
+            pp2[r] = p2n[r];
+            pp3[r] = p3n[r];
+            pv[r] = vn[r];
+            pc[r] = cn[r];
+            q3prev[r] = q3[r];
+        }
+        cur ^= 1;
+    }
+}
+
 // ---------------------------------------------------------------------------------------
 // k_vol_tb<S>: S iterations per pass over the volume (temporal blocking along the plane
 // axis).  The S stages of a CTA are a software pipeline: at plane step n stage s takes the
@@ -596,9 +729,15 @@ cudaError_t launch_vol_step(const VolArgs &a, bool write_u, cudaStream_t s) {
     } else {
         dim3 block(VT_X, VT2_Y);
         if (write_u)
+#ifdef RDS_VOL_2BAR
+            k_vol_step2b<true><<<grid, block, 0, s>>>(a);
+        else
+            k_vol_step2b<false><<<grid, block, 0, s>>>(a);
+#else
             k_vol_step2<true><<<grid, block, 0, s>>>(a);
         else
             k_vol_step2<false><<<grid, block, 0, s>>>(a);
+#endif
     }
     return cudaGetLastError();
 }
