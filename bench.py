@@ -393,6 +393,7 @@ def run_ours(args, dist):
             "loop_ms": lm, "setup_ms": sm,
             "active_tile_frac": st["n_active_tiles"] / st["n_tiles"],
             "rd_frac": st["n_rd"] / (cfg.H * cfg.W),
+            "rd_decoupled_frac": st["rdc_decoupled"] / max(1, st["n_rd"]),
             "active_cell_frac": n_items / st["n_items"], "work_items": st["n_active_items"],
             "tile_gpix_iter_s": px * K / (lm * 1e-3) / 1e9,
             "rd_gpix_iter_s": st["n_rd"] * K / (lm * 1e-3) / 1e9,
@@ -445,9 +446,10 @@ def run_ours(args, dist):
     }
 
     # K1, K2, band flags, items; energy partial + final; the compact path's index build,
-    # gather and scatter
+    # gather and scatter (+ the coupled / decoupled split: count, scan, fill; st["launches"]
+    # counts its k_rdc_iso launch)
     launches_per_step = sum(st["launches"] + 4 + 2 + (5 if st["compact"] else 0)
-                            for _, st, _ in info)
+                            + (3 if st.get("rdc_decoupled", 0) else 0) for _, st, _ in info)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -548,6 +550,7 @@ def compact_section(cfg, zt, Pt, am, K, lam, sp, per_delta):
         row = {"delta_rel": "inf" if math.isinf(dr) else dr,
                "path": "compact" if st["compact"] else "dense",
                "rd_frac": st["n_rd"] / (cfg.H * cfg.W), "solve_ms": t,
+               "rd_decoupled_frac": st["rdc_decoupled"] / max(1, st["n_rd"]),
                "speedup_vs_full": t_full / t,
                "rd_gpix_iter_s": st["n_rd"] * K / (t * 1e-3) / 1e9}
         if st["compact"]:

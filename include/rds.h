@@ -94,6 +94,8 @@ typedef struct {
     int32_t resident;        /* 1 if the last solve ran as one resident cluster (RDS_OPT_RESIDENT),
                                 2 if resident on the whole GPU (RDS_OPT_GRID), else 0 */
     int32_t persist;         /* 1 if the last solve's K-loop ran as one persistent launch (RDS_OPT_PERSIST) */
+    int32_t rdc_decoupled;   /* compact fixed-K solves: RD pixels with no RD neighbour, iterated
+                                independently of the grid-barrier kernel (k_rdc_iso); else 0 */
 } rds_stats_t;
 
 /* Options (rds_set_option). */
@@ -200,6 +202,13 @@ typedef struct {
                                 (bit-identical).  0 = off, 1 = on, 2 (default) = on for images of
                                 at most 2^22 pixels, where items are short (C1 -8.6%); off above,
                                 where the larger kernel measured no gain. */
+
+#define RDS_OPT_RDC_SPLIT 15 /* compact fixed-K solves (RDS_OPT_COMPACT): RD pixels none of whose six
+                                stencil neighbours is RD read no other record and are read by
+                                none (the neighbour relation is symmetric), so they iterate as
+                                independent threads with the record in registers (k_rdc_iso) and
+                                only the coupled rest pays the grid barrier per pass.  Same
+                                values (bit-identical).  1 (default) = on, 0 = off. */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */

@@ -311,6 +311,7 @@ struct RdcIter {
     double *part;                 // [2][2 * RDC_MAX_GRID]: alternate by check parity (a fast
                                   // CTA's next check must not overwrite sums still being read)
     StopRecord *rec_out;
+    const int32_t *sel;           // split solves: the n coupled record indices (else null: 0..n-1)
 };
 cudaError_t launch_rdc_count(const uint8_t *lab, int64_t pitch, int H, int W, int32_t *rowcnt,
                              int32_t *rowoff, int32_t *total, cudaStream_t s);
@@ -320,6 +321,13 @@ cudaError_t launch_rdc_fill(const uint8_t *lab, int64_t pitch, int H, int W,
 cudaError_t launch_rdc_gather(const RdcSetup &a, cudaStream_t s);
 cudaError_t launch_rdc_scatter(const RdcSetup &a, const RdcIter &it, cudaStream_t s);
 cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s);
+// split of the n records into coupled (cpl, ascending) and decoupled ones (iso, ascending);
+// cnt / off: ceil(n / 1024) + 1 ints each, *n_cpl: the coupled count
+cudaError_t launch_rdc_split(const uint2 *code, int n, int32_t *cnt, int32_t *off,
+                             int32_t *n_cpl, int32_t *cpl, int32_t *iso, cudaStream_t s);
+// the K passes of the n_iso decoupled records (fixed-K solves), independent of the barrier kernel
+cudaError_t launch_rdc_iso(const RdcIter &a, const int32_t *iso, int n_iso, int n_sm,
+                           cudaStream_t s);
 
 // float64 mode (k_fp64.cu): natural-order padded double planes, same pitch as the floats
 struct F64Args {

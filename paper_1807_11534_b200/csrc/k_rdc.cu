@@ -237,28 +237,19 @@ __device__ __forceinline__ float v_of(int code, const float4 &y, float dy, int k
     return __saturatef(__fmaf_rn(y.w, -0x1p100f, __fmaf_rn(dy, -theta, y.z)));
 }
 
-// Pass k at one RD pixel (see the header comment), reading records (rho^k, v^{k-1}, c') from
-// B and writing (rho^{k+1}, v^k, c') to O -- the same float operations as K3.
-__device__ __forceinline__ void pix_pass(const PixConst &q, const float4 *B, float4 *O,
-                                         float *U, int k, int K, float tau, float theta,
-                                         float inv_theta, bool chk, bool wr_u, float &su,
-                                         float &sv) {
-    const float4 X = ld_rec(B + q.r);
+// Pass k at one RD pixel (see the header comment): from its record X = (rho^k, v^{k-1}, c')
+// and its neighbours' records in B, the new record (rho^{k+1}, v^k, c') -- the same float
+// operations as K3 -- and u^k (ux).  A decoupled pixel (no RD neighbour, k_rdc_iso) never
+// dereferences B: every neighbour is a pinned constant.
+__device__ __forceinline__ float4 pix_next(const PixConst &q, const float4 &X, const float4 *B,
+                                           int k, int K, float tau, float theta,
+                                           float inv_theta, float &ux) {
     const float4 Up = rec_at(B, q.up), Lf = rec_at(B, q.lf);
     // div p^k = (p1 - p1(x - e1)) + (p2 - p2(x - e2))
     const float dx = __fadd_rn(__fsub_rn(X.x, Up.x), __fsub_rn(X.y, Lf.y));
-    const float ux = __fmaf_rn(dx, -theta, X.z);
+    ux = __fmaf_rn(dx, -theta, X.z);
     const float vx = k == 0 ? X.z : __saturatef(__fmaf_rn(X.w, -0x1p100f, ux));
-    if (chk) {  // the stopping sums of iteration k (PAPER.md:234-238): u^k - u^{k-1}, v^k - v^{k-1}
-        const float du = ux - U[q.r], dv = vx - X.z;
-        su += du * du;
-        sv += dv * dv;
-    }
-    if (wr_u) U[q.r] = ux;  // an RD pixel reports u itself (u0 only off RD)
-    if (k == K) {           // last pass: u^K and v^K only
-        O[q.r] = make_float4(X.x, X.y, vx, X.w);
-        return;
-    }
+    if (k == K) return make_float4(X.x, X.y, vx, X.w);  // last pass: u^K and v^K only
     const float wx = __fmaf_rn(vx, -inv_theta, dx);
     float g1 = 0.0f, g2 = 0.0f;
     if (q.dn != RDC_EDGE) {  // grad_1 = 0 on row H-1
@@ -273,9 +264,100 @@ __device__ __forceinline__ void pix_pass(const PixConst &q, const float4 *B, flo
     }
     const float s = __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, fabsf(X.w)));
     const float rr = rcp_ax(__fmaf_rn(sqrt_ax(s), tau, 1.0f));
-    O[q.r] = make_float4(__fmul_rn(__fmaf_rn(g1, tau, X.x), rr),
-                         __fmul_rn(__fmaf_rn(g2, tau, X.y), rr), vx, X.w);
+    return make_float4(__fmul_rn(__fmaf_rn(g1, tau, X.x), rr),
+                       __fmul_rn(__fmaf_rn(g2, tau, X.y), rr), vx, X.w);
 }
+
+// Pass k at one RD pixel, reading records (rho^k, v^{k-1}, c') from B and writing
+// (rho^{k+1}, v^k, c') to O.
+__device__ __forceinline__ void pix_pass(const PixConst &q, const float4 *B, float4 *O,
+                                         float *U, int k, int K, float tau, float theta,
+                                         float inv_theta, bool chk, bool wr_u, float &su,
+                                         float &sv) {
+    const float4 X = ld_rec(B + q.r);
+    float ux;
+    const float4 Y = pix_next(q, X, B, k, K, tau, theta, inv_theta, ux);
+    if (chk) {  // the stopping sums of iteration k (PAPER.md:234-238): u^k - u^{k-1}, v^k - v^{k-1}
+        const float du = ux - U[q.r], dv = Y.z - X.z;
+        su += du * du;
+        sv += dv * dv;
+    }
+    if (wr_u) U[q.r] = ux;  // an RD pixel reports u itself (u0 only off RD)
+    O[q.r] = Y;
+}
+
+// Decoupled RD pixels (the split, RDS_RDC_SPLIT; fixed-K solves).  The six stencil neighbours
+// come in symmetric pairs (up/down, left/right, up-right/down-left), so a pixel none of whose
+// six neighbours is RD reads no other record and no other pixel reads its record: its K
+// iterations depend on its own state and pinned constants alone (Eq. 7-9 with rho = 0 and
+// v = u0 off RD).  At the scattered noise bands of C3 (RD density p ~ 0.1) that is about
+// (1 - p)^6 ~ half of all RD pixels.  They run as one independent thread each, the record in
+// registers for all K passes, no grid barrier; the grid-barrier kernel iterates the coupled
+// rest through an index list.  Same float operations, so the result is the same bits.
+// The one asymmetric pair is an image seam of a batch: the last column's right neighbour is
+// EDGE (grad_2 = 0) while the next image's first column still reads it as its left one, so a
+// right neighbour of class EDGE counts as coupled (also on the last column of the frame:
+// a few pixels more on the barrier path, never a wrong split).
+__device__ __forceinline__ bool rdc_coupled(uint2 w) {
+    const unsigned fa = w.x >> RDC_IDX_BITS, fb = w.y >> RDC_IDX_BITS;
+    const unsigned f = fa | (fb << 6);  // classes: up, ur, lf, dn, dl, rt (2 bits each)
+    bool any = (f >> 10) == RDC_C_EDGE;
+#pragma unroll
+    for (int e = 0; e < 6; ++e) any |= ((f >> (2 * e)) & 3u) == RDC_C_RD;
+    return any;
+}
+
+namespace {
+
+constexpr int SPLIT_CHUNK = 1024;  // records per CTA of the split (one per thread)
+
+__global__ void __launch_bounds__(SPLIT_CHUNK) k_rdc_split_count(const uint2 *code, int n,
+                                                                  int32_t *cnt) {
+    const int r = blockIdx.x * SPLIT_CHUNK + threadIdx.x;
+    const int c = __syncthreads_count(r < n && rdc_coupled(__ldg(code + r)));
+    if (threadIdx.x == 0) cnt[blockIdx.x] = c;
+}
+
+// coupled records in ascending order into cpl[off[b] ...], decoupled ones into
+// iso[b * SPLIT_CHUNK - off[b] ...] (also ascending)
+__global__ void __launch_bounds__(SPLIT_CHUNK) k_rdc_split_fill(const uint2 *code, int n,
+                                                                 const int32_t *off,
+                                                                 int32_t *cpl, int32_t *iso) {
+    __shared__ int wc[SPLIT_CHUNK / 32];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int r = blockIdx.x * SPLIT_CHUNK + t;
+    const bool in = r < n;
+    const bool c = in && rdc_coupled(__ldg(code + r));
+    const unsigned b = __ballot_sync(0xffffffffu, c);
+    if (lane == 0) wc[w] = __popc(b);
+    __syncthreads();
+    int before = 0;  // coupled records of the earlier warps of this chunk
+    for (int i = 0; i < w; ++i) before += wc[i];
+    const int pc = before + __popc(b & ((1u << lane) - 1u));  // coupled before r in the chunk
+    if (!in) return;
+    if (c)
+        cpl[off[blockIdx.x] + pc] = r;
+    else
+        iso[blockIdx.x * SPLIT_CHUNK - off[blockIdx.x] + (t - pc)] = r;
+}
+
+__global__ void __launch_bounds__(256) k_rdc_iso(const RdcIter a, const int32_t *iso, int n_iso) {
+    const float tau = a.tau, theta = a.theta, inv_theta = a.inv_theta;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_iso; i += gridDim.x * blockDim.x) {
+        const int r = iso[i];
+        const PixConst q = decode(__ldg(a.code + r), r);
+        float4 X = a.rec[0][r];  // the gathered start state (pass 0 reads rec[0])
+        float ux = 0.0f;
+        for (int k = 0; k <= a.K; ++k) X = pix_next(q, X, nullptr, k, a.K, tau, theta, inv_theta, ux);
+        // as the barrier kernel leaves it: rho^K in the buffer pass K read, v^K in the one it
+        // wrote (k_rdc_scatter), u^K in u (written from pass 1 on)
+        a.rec[0][r] = X;
+        a.rec[1][r] = X;
+        if (a.K >= 1) a.u[r] = ux;
+    }
+}
+
+}  // namespace
 
 __device__ __forceinline__ double warp_sum_d(double x) {
 #pragma unroll
@@ -354,10 +436,13 @@ __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
     const int stop = min(a.n, start + chunk);
     const float tau = a.tau, theta = a.theta, inv_theta = a.inv_theta;
     uint2 cw[NPT > 0 ? NPT : 1];  // packed codes of the owned pixels (2 registers each)
+    int ri[NPT > 0 ? NPT : 1];    // their record indices (-1: none)
+    const int32_t *sel = a.sel;   // the coupled pixels of a split solve, else every record
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
-        const int r = start + threadIdx.x + q * blockDim.x;
-        cw[q] = r < stop ? __ldg(a.code + r) : make_uint2(0u, 0u);
+        const int i = start + threadIdx.x + q * blockDim.x;
+        ri[q] = i < stop ? (sel ? __ldg(sel + i) : i) : -1;
+        cw[q] = ri[q] >= 0 ? __ldg(a.code + ri[q]) : make_uint2(0u, 0u);
     }
     __shared__ double sh[2][RDC_THREADS / 32];
     __shared__ int stop_s;
@@ -403,15 +488,16 @@ __global__ void __launch_bounds__(RDC_THREADS) k_rdc_iter(const RdcIter a) {
         if (NPT > 0) {
 #pragma unroll
             for (int q = 0; q < NPT; ++q) {
-                const int r = start + threadIdx.x + q * blockDim.x;
-                if (r < stop)
-                    pix_pass(decode(cw[q], r), B, O, a.u, k, a.K, tau, theta, inv_theta, chk,
-                             wr_u, su, sv);
+                if (ri[q] >= 0)
+                    pix_pass(decode(cw[q], ri[q]), B, O, a.u, k, a.K, tau, theta, inv_theta,
+                             chk, wr_u, su, sv);
             }
         } else {
-            for (int r = start + threadIdx.x; r < stop; r += blockDim.x)
+            for (int i = start + threadIdx.x; i < stop; i += blockDim.x) {
+                const int r = sel ? __ldg(sel + i) : i;
                 pix_pass(decode(__ldg(a.code + r), r), B, O, a.u, k, a.K, tau, theta,
                          inv_theta, chk, wr_u, su, sv);
+            }
         }
         // two buffers alternating by check parity: when checks are one pass apart no barrier
         // separates a fast CTA's write for check c+1 from a slow CTA's read for check c
@@ -515,6 +601,25 @@ cudaError_t launch_rdc_scatter(const RdcSetup &a, const RdcIter &it, cudaStream_
     return cudaGetLastError();
 }
 
+cudaError_t launch_rdc_split(const uint2 *code, int n, int32_t *cnt, int32_t *off,
+                             int32_t *n_cpl, int32_t *cpl, int32_t *iso, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    const int nb = (n + SPLIT_CHUNK - 1) / SPLIT_CHUNK;
+    k_rdc_split_count<<<nb, SPLIT_CHUNK, 0, s>>>(code, n, cnt);
+    k_rdc_scan<<<1, 1024, 0, s>>>(cnt, nb, off, n_cpl);
+    k_rdc_split_fill<<<nb, SPLIT_CHUNK, 0, s>>>(code, n, off, cpl, iso);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rdc_iso(const RdcIter &a, const int32_t *iso, int n_iso, int n_sm,
+                           cudaStream_t s) {
+    if (n_iso <= 0) return cudaSuccess;
+    int g = (n_iso + 255) / 256;
+    if (g > n_sm * 8) g = n_sm * 8;
+    k_rdc_iso<<<g, 256, 0, s>>>(a, iso, n_iso);
+    return cudaGetLastError();
+}
+
 // Can one cluster of g CTAs of fn be scheduled on this device (a g > 8 cluster needs the
 // non-portable size; MIG / MPS slices or small GPCs may not hold it)?  Cached per (fn, g).
 static bool cluster_fits(RdcFn fn, int npt_slot, int g) {
@@ -579,7 +684,7 @@ cudaError_t launch_rdc_iter(const RdcIter &a, int n_sm, cudaStream_t s) {
     // measured 3% faster at C3 delta = .1 but 1.3-4x slower at thinner bands)
     static const bool nb_env = getenv("RDS_RDC_NB") && atoi(getenv("RDS_RDC_NB"));
     // (NB needs both record buffers on 128-byte lines: ranges of whole lines, see nbr_sync)
-    const bool nb = nb_env && a.check_every <= 0 && (a.rec[1] - a.rec[0]) % 8 == 0 &&
+    const bool nb = nb_env && a.check_every <= 0 && !a.sel && (a.rec[1] - a.rec[0]) % 8 == 0 &&
                     (reinterpret_cast<uintptr_t>(a.rec[0]) & 127) == 0;
     RdcFn fn = nullptr;
     int g = 0;

@@ -103,6 +103,7 @@ struct rds_handle {
 
     int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1, opt_ctas = 0;
     int opt_norm = 0;  // stopping-rule norm: 0 Euclidean over pixels, 1 RMS (R-F2)
+    int opt_split = 1;    // coupled / decoupled split of compact fixed-K solves (RDS_OPT_RDC_SPLIT)
     int opt_compact = 2;  // f3: 0 dense stencil, 1 compacted RD iteration, 2 auto (default; RDS_OPT_COMPACT)
     int opt_wave = 0;     // temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto (RDS_OPT_WAVE)
     bool wave_ok = false; // the last solve's set-up allows the wavefront (aligned, supported kf)
@@ -332,6 +333,11 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             if (value < 0 || value > 2)
                 return fail(h, RDS_EINVAL, "rds_set_option: compact=%lld", (long long)value);
             h->opt_compact = (int)value;
+            return RDS_OK;
+        case RDS_OPT_RDC_SPLIT:
+            if (value < 0 || value > 1)
+                return fail(h, RDS_EINVAL, "rds_set_option: rdc_split=%lld", (long long)value);
+            h->opt_split = (int)value;
             return RDS_OK;
         case RDS_OPT_PROLOGUE:
             if (value < 0 || value > 2)
@@ -966,8 +972,11 @@ struct CompactPlan {
     bool use = false;
     RdcSetup su{};
     RdcIter it{};
+    const int32_t *iso = nullptr;  // split (fixed-K solves): the decoupled records
+    int n_iso = 0;
 };
-static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactPlan *cp) {
+static int compact_prepare(rds_t *h, float tau, float theta, int iters, int check_every,
+                           CompactPlan *cp) {
     cp->use = false;
     const int64_t npx = h->H * h->W;
     if (npx > INT32_MAX / 2) return RDS_OK;  // compact indices are int32: keep the dense path
@@ -991,15 +1000,18 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactP
         if (!compact_pays(n, (int64_t)act * TILE_H * TILE_W, (size_t)l2)) return RDS_OK;
     }
     if (!h->rdc_idx) CK(h, cudaMalloc(&h->rdc_idx, sizeof(int32_t) * npx));
-    // records x2 (float4), packed codes (uint2), list, u
-    const size_t nn = (size_t)(n > 0 ? n : 1);
+    // records x2 (float4), packed codes (uint2), list, u; the split's coupled and decoupled
+    // index lists and its per-chunk counts / offsets and total
+    const size_t nn = (size_t)(n > 0 ? n : 1), nch = nn / 1024 + 2;
     void *pb = h->rdc_buf;
-    CK(h, grow(&pb, &h->rdc_bytes, nn * (16 * 2 + 8 + 4 + 4)));
+    CK(h, grow(&pb, &h->rdc_bytes, nn * (16 * 2 + 8 + 4 + 4 + 4 + 4) + 4 * (2 * nch + 1)));
     h->rdc_buf = pb;
     float4 *rec0 = (float4 *)pb, *rec1 = rec0 + nn;
     uint2 *code = (uint2 *)(rec1 + nn);
     int32_t *list = (int32_t *)(code + nn);
     float *u = (float *)(list + nn);
+    int32_t *cpl = (int32_t *)(u + nn), *iso = cpl + nn, *cnt = iso + nn, *off = cnt + nch,
+            *ncpl = off + nch;
     CK(h, launch_rdc_fill(h->at(h->lab), h->pitch, (int)h->H, (int)h->W, h->rdc_row + h->H,
                           h->rdc_idx, list, h->stream));
     RdcSetup &su = cp->su;
@@ -1032,6 +1044,18 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, CompactP
     it.theta = theta;
     it.inv_theta = 1.0f / theta;
     it.bar = h->rdc_bar;
+    it.sel = nullptr;
+    // split (fixed-K solves): pixels without an RD neighbour iterate independently (k_rdc_iso)
+    if (check_every <= 0 && n >= 4096 && h->opt_split) {
+        CK(h, launch_rdc_split(code, n, cnt, off, ncpl, cpl, iso, h->stream));
+        int32_t nc = 0;
+        CK(h, cudaMemcpyAsync(&nc, ncpl, sizeof nc, cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+        it.n = nc;
+        it.sel = cpl;
+        cp->iso = iso;
+        cp->n_iso = n - nc;
+    }
     cp->use = true;
     return RDS_OK;
 }
@@ -1058,6 +1082,7 @@ static int compact_run(rds_t *h, CompactPlan *cp, int iters, const TolParams &tp
         CK(h, cudaMemcpyAsync(h->stop, &r, sizeof r, cudaMemcpyHostToDevice, h->stream));
         if (it.n == 0) CK(h, cudaStreamSynchronize(h->stream));  // r lives on this stack
     }
+    if (cp->n_iso > 0) CK(h, launch_rdc_iso(it, cp->iso, cp->n_iso, h->n_sm, h->stream));
     CK(h, launch_rdc_iter(it, h->n_sm, h->stream));
     CK(h, launch_rdc_scatter(cp->su, it, h->stream));
     return RDS_OK;
@@ -1277,7 +1302,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
 
     CompactPlan cplan;
     if (iters > 0 && h->opt_compact && !small_use && !grid_use) {
-        const int rc = compact_prepare(h, tau, theta, iters, &cplan);
+        const int rc = compact_prepare(h, tau, theta, iters, check_every, &cplan);
         if (rc) return rc;
     }
     h->warm_pending = false;
@@ -1375,6 +1400,8 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     st.k_fuse = kf;
     st.launches = (cplan.use || small_use || grid_use) ? 1 : launches;
     st.compact = cplan.use ? 1 : 0;
+    st.rdc_decoupled = cplan.use ? cplan.n_iso : 0;
+    if (cplan.use) st.launches = 1 + (cplan.n_iso > 0 ? 1 : 0);
     st.wave = (!cplan.use && !small_use && !grid_use && wave_blocks(h, kf, iters, check_every) > 0) ? 1 : 0;
     st.resident = small_use ? 1 : grid_use ? 2 : 0;
     st.persist = (!cplan.use && !small_use && !grid_use && persist_applies(h, kf, iters, check_every)) ? 1 : 0;

@@ -30,6 +30,7 @@ RDS_OPT_RESIDENT = 10  # small images as one resident cluster: 0 off, 1 / 2 (def
 RDS_OPT_PROLOGUE = 14  # plain stencil launches in the prologue form: 0 off, 1 on, 2 auto (default)
 RDS_OPT_WS = 13        # full-depth launches on the warp-specialised stencil: 0 off (default), 1 on
 RDS_OPT_PERSIST = 11   # fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto
+RDS_OPT_RDC_SPLIT = 15 # compact fixed-K solves: decoupled RD pixels iterate alone: 1 on (default), 0 off
 RDS_OPT_GRID = 12      # mid-size images resident on the whole GPU: 0 off (default), 1 / 2 on
 
 EXPORTS = (
@@ -83,7 +84,8 @@ class rds_stats_t(ctypes.Structure):
                 ("setup_ms", ctypes.c_float), ("loop_ms", ctypes.c_float),
                 ("residual", ctypes.c_float), ("check_every", ctypes.c_int32),
                 ("compact", ctypes.c_int32), ("wave", ctypes.c_int32),
-                ("resident", ctypes.c_int32), ("persist", ctypes.c_int32)]
+                ("resident", ctypes.c_int32), ("persist", ctypes.c_int32),
+                ("rdc_decoupled", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -404,7 +406,7 @@ class Solver:
 
     def __init__(self, H, W, stream=None, k_fuse=0, item_rows=0, timing=False, skip=True,
                  graph=True, batch=None, compact=None, wave=None, resident=None,
-                 persist=None, grid=None, ws=None, prologue=None):
+                 persist=None, grid=None, ws=None, prologue=None, rdc_split=None):
         self.shape = (int(H) * (int(batch) if batch else 1), int(W))
         if batch is not None:
             h = ctypes.c_void_p()
@@ -435,6 +437,8 @@ class Solver:
             rds_set_option(self.h, RDS_OPT_WS, int(ws))
         if prologue is not None:
             rds_set_option(self.h, RDS_OPT_PROLOGUE, int(prologue))
+        if rdc_split is not None:
+            rds_set_option(self.h, RDS_OPT_RDC_SPLIT, int(rdc_split))
 
     def close(self):
         if self.h is not None:

@@ -29,9 +29,9 @@ def rds():
 
 
 def _run(rds, z, delta, K, compact, batch=None, kf=0, lam=5.0, warm=None, P=None, gamma=0.0,
-         resident=None, grid=None):
+         resident=None, grid=None, rdc_split=None):
     H, W = z.shape[-2:] if batch else z.shape
-    kw = dict(compact=compact, k_fuse=kf, resident=resident, grid=grid)
+    kw = dict(compact=compact, k_fuse=kf, resident=resident, grid=grid, rdc_split=rdc_split)
     s = rds.BatchSolver(batch, H, W, **kw) if batch else rds.Solver(H, W, **kw)
     s.set_image(z)
     s.set_fitting(0.8, 0.2, gamma, P)
@@ -110,6 +110,77 @@ def test_compact_variants(rds):
     assert s3.stats()["compact"] == 1
     s3.solve(*PAR, wl.band_delta(0.2, am), 5)
     assert s3.stats()["compact"] == 0
+
+
+def _decoupled_count(lab, img_w):
+    """RD pixels none of whose six stencil neighbours (up, up-right, left, down, down-left,
+    right) is RD and which are not on an image's last column (the split's rule, RDS_OPT_RDC_SPLIT;
+    the neighbour relation of PAPER.md Eq. 7-9's forward differences / divergence)"""
+    rd = lab == 2
+    H, W = rd.shape
+    pad = np.zeros((H + 2, W + 2), bool)
+    pad[1:-1, 1:-1] = rd
+    nb = np.zeros_like(rd)
+    for di, dj in ((-1, 0), (-1, 1), (0, -1), (1, 0), (1, -1), (0, 1)):
+        nb |= pad[1 + di:H + 1 + di, 1 + dj:W + 1 + dj]
+    last = (np.arange(W) % img_w) == img_w - 1
+    return int((rd & ~nb & ~last[None, :]).sum())
+
+
+@pytest.mark.parametrize("case", ["voronoi", "noise", "batch", "warm", "K1", "K2", "P"])
+def test_compact_split_equals_unsplit(rds, orc, case):
+    """The coupled / decoupled split (RDS_OPT_RDC_SPLIT) gives the unsplit compact path's
+    values bit for bit, and its decoupled count equals the host count of RD pixels without an
+    RD neighbour."""
+    rng = np.random.default_rng(11)
+    batch, warm, P, gamma, K, dr = None, None, None, 0.0, 40, 0.1
+    if case == "noise":  # C3's recipe (cells 0.2 / 0.8, noise 0.15): a scattered band
+        z = wl.gen_voronoi(N=336, seed=9, n_sites=30)[:300, :333].copy()
+    elif case == "batch":  # image seams: the last column's right neighbour is EDGE
+        z = np.stack([wl.gen_voronoi(N=200, seed=20 + b, n_sites=8)[:, :150] for b in range(3)])
+        batch = 3
+    else:
+        z = wl.gen_voronoi(N=320, seed=5, n_sites=40)[:257, :301].copy()
+        z = (z + 0.05 * rng.standard_normal(z.shape)).astype(np.float32)
+    if case == "warm":
+        warm = wl.random_state(*z.shape, 7)
+    if case in ("K1", "K2"):
+        K = int(case[1])
+    if case == "P":
+        P = rng.uniform(0, 1, z.shape).astype(np.float32)
+        gamma, dr = 1.0, 0.2
+    zf = z.reshape(-1, z.shape[-1])
+    f = orc.fitting(zf, 0.8, 0.2, gamma, P)
+    delta = wl.band_delta(dr, orc.absmax(f))
+    s0, a = _run(rds, z, delta, K, 1, batch=batch, warm=warm, P=P, gamma=gamma, rdc_split=0)
+    s1, b = _run(rds, z, delta, K, 1, batch=batch, warm=warm, P=P, gamma=gamma, rdc_split=1)
+    st0, st1 = s0.stats(), s1.stats()
+    assert st0["compact"] == 1 and st1["compact"] == 1
+    assert st0["rdc_decoupled"] == 0
+    n_rd = int((b["labels"] == 2).sum())
+    want = _decoupled_count(b["labels"].reshape(zf.shape), z.shape[-1]) if n_rd >= 4096 else 0
+    assert st1["rdc_decoupled"] == want, (st1["rdc_decoupled"], want, n_rd)
+    if case in ("noise", "batch"):
+        assert want > 0.2 * n_rd
+    _same(a, b)
+    assert s1.energy() == s0.energy()
+    assert s1.check_frame() == 0
+
+
+def test_compact_split_oracle(rds, orc):
+    """The split path against the fp64 oracle at the north_star tolerances (a C3-like noise
+    band, about half of it decoupled)."""
+    z = wl.gen_voronoi(N=320, seed=3, n_sites=20)[:256, :320].copy()
+    f = orc.fitting(z, 0.8, 0.2)
+    delta = wl.band_delta(0.1, orc.absmax(f))
+    s, g = _run(rds, z, delta, 300, 1, rdc_split=1)
+    assert s.stats()["rdc_decoupled"] > 0
+    o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, 300)
+    assert np.array_equal(g["labels"], o["labels"])
+    for k in ("u", "v", "p1", "p2"):  # north_star: u, rho within 5e-4, mask <= 0.05%
+        err = np.abs(g[k].astype(np.float64) - o[k]).max()
+        assert err <= 5e-4, (k, err)
+    assert np.mean(g["mask"] != (o["u"] > 0.5)) <= 5e-4
 
 
 def test_compact_then_continue(rds):
