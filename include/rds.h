@@ -96,6 +96,9 @@ typedef struct {
     int32_t persist;         /* 1 if the last solve's K-loop ran as one persistent launch (RDS_OPT_PERSIST) */
     int32_t rdc_decoupled;   /* compact fixed-K solves: RD pixels with no RD neighbour, iterated
                                 independently of the grid-barrier kernel (k_rdc_iso); else 0 */
+    int32_t rdc_grouped;     /* compact fixed-K solves: coupled RD pixels in connected components of
+                                at most 1024 pixels, iterated inside one warp / CTA each
+                                (k_rdc_grp, RDS_OPT_RDC_SPLIT = 2); else 0 */
 } rds_stats_t;
 
 /* Options (rds_set_option). */
@@ -207,8 +210,14 @@ typedef struct {
                                 stencil neighbours is RD read no other record and are read by
                                 none (the neighbour relation is symmetric), so they iterate as
                                 independent threads with the record in registers (k_rdc_iso) and
-                                only the coupled rest pays the grid barrier per pass.  Same
-                                values (bit-identical).  1 (default) = on, 0 = off. */
+                                only the coupled rest pays the grid barrier per pass.  2 (default)
+                                also finds the connected components of the coupled pixels
+                                (an edge wherever one pixel's update reads another's record):
+                                a component of at most 1024 pixels runs all K passes inside one
+                                warp (<= 32 pixels) or CTA, its records exchanged through shared
+                                memory (k_rdc_grp); only larger components keep the grid
+                                barrier.  Same values (bit-identical) at every setting.
+                                0 = off, 1 = decoupled pixels only, 2 = both. */
 
 /* Create a solver for an H x W image; allocates all device state on the current device.
  * Errors: RDS_EINVAL if out == NULL, H < 1, W < 1 or H*W > 2^31; RDS_ENOMEM / RDS_ECUDA. */

@@ -329,6 +329,26 @@ cudaError_t launch_rdc_split(const uint2 *code, int n, int32_t *cnt, int32_t *of
 cudaError_t launch_rdc_iso(const RdcIter &a, const int32_t *iso, int n_iso, int n_sm,
                            cudaStream_t s);
 
+// grouped coupled records (RDS_OPT_RDC_SPLIT = 2, k_rdc.cu): connected components of the
+// coupled list that fit one warp / CTA iterate there; the rest is the fallback list
+struct GrpPlan {
+    int base[11] = {};   // first slot of class k (slot range 2^k, k = 1 .. 10)
+    int first[3] = {};   // first slot of segment 0 (warp blocks), 1 (256), 2 (1024)
+    int count[3] = {};   // slots in use per segment
+    int total = 0;       // slots allocated (segments padded to multiples of 1024)
+};
+// labels, per-label counts / flags, per-record ranks, per-root class and index; ctr: 12 ints
+// (ctr[k] = components of class k = 1 .. 10, ctr[11] = grouped records)
+cudaError_t launch_grp_label(const uint2 *code, const int32_t *cpl, int nc, int32_t *lab,
+                             int32_t *cnt, int32_t *bad, int32_t *rank, int32_t *cidx,
+                             int32_t *ctr, cudaStream_t s);
+void grp_layout(const int32_t *ctr, GrpPlan *gp);
+cudaError_t launch_grp_fill(const int32_t *cpl, int nc, const int32_t *lab, const int32_t *cidx,
+                            const int32_t *rank, const GrpPlan &gp, int32_t *slots,
+                            int32_t *lpos, int32_t *fb, int32_t *nfb, cudaStream_t s);
+cudaError_t launch_rdc_grp(const RdcIter &a, const GrpPlan &gp, const int32_t *slots,
+                           const int32_t *lpos, cudaStream_t s);
+
 // float64 mode (k_fp64.cu): natural-order padded double planes, same pitch as the floats
 struct F64Args {
     const float *z, *P;        // image and selection map (float planes; P may be null)

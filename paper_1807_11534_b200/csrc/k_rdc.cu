@@ -357,6 +357,240 @@ __global__ void __launch_bounds__(256) k_rdc_iso(const RdcIter a, const int32_t 
     }
 }
 
+
+// ---------------------------------------------------------------------------------------
+// Grouped coupled pixels (RDS_OPT_RDC_SPLIT = 2; fixed-K solves).  The coupled records form a
+// graph (an edge wherever one record reads another); at the scattered noise bands the compact
+// path serves (RD density well under the site-percolation threshold of the six-neighbour
+// lattice) its connected components are small.  A component read by no record outside it and
+// reading none can run all K passes inside ONE warp or CTA, its records exchanged through
+// shared memory with a warp / CTA barrier per pass -- no grid barrier, no L2 round trip.
+// Same float operations (pix_next), so the same bits whichever kernel owns a pixel.
+//
+// Setup: P rounds of min-label propagation over the coupled list (pull and push along every
+// read edge, one pointer jump), then every record checks that all its neighbours carry its
+// label ("settled"); a label all of whose records are settled is exactly one component (it is
+// closed under adjacency and every member reached the label's own record).  Components of up
+// to 1024 settled records get power-of-two slot ranges (classes 2 .. 1024) in a slot array
+// ordered by falling class inside three segments (warp: <= 32, CTA of 256, CTA of 1024), so
+// no range straddles its block; everything else (unsettled after P rounds, or larger) stays on
+// the grid-barrier kernel through the fallback list.  Slot order within a class comes from
+// atomic counters: it varies from run to run, the values do not.
+// ---------------------------------------------------------------------------------------
+constexpr int GRP_ROUNDS = 12;
+
+template <typename F>
+__device__ __forceinline__ void for_rd_nbrs(const PixConst &q, F f) {
+    if (q.up >= 0) f(q.up);
+    if (q.ur >= 0) f(q.ur);
+    if (q.lf >= 0) f(q.lf);
+    if (q.dn >= 0) f(q.dn);
+    if (q.dl >= 0) f(q.dl);
+    if (q.rt >= 0) f(q.rt);
+}
+
+__global__ void k_grp_init(const int32_t *cpl, int nc, int32_t *lab, int32_t *cnt, int32_t *bad,
+                           int32_t *cidx) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+        const int r = cpl[i];
+        lab[r] = r;
+        cnt[r] = 0;
+        bad[r] = 0;
+        cidx[r] = -1;  // fallback unless k_grp_class finds a settled component rooted here
+    }
+}
+
+// one round: labels only fall and always name a record of the same component
+__global__ void k_grp_prop(const uint2 *code, const int32_t *cpl, int nc, int32_t *lab) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+        const int r = cpl[i];
+        const PixConst q = decode(__ldg(code + r), r);
+        volatile int32_t *L = lab;
+        int m = L[r];
+        for_rd_nbrs(q, [&](int nb) { m = min(m, (int)L[nb]); });
+        m = min(m, (int)L[m]);
+        if (m < L[r]) atomicMin(lab + r, m);
+        for_rd_nbrs(q, [&](int nb) { if (m < L[nb]) atomicMin(lab + nb, m); });
+    }
+}
+
+__global__ void k_grp_count(const uint2 *code, const int32_t *cpl, int nc, const int32_t *lab,
+                            int32_t *cnt, int32_t *bad, int32_t *rank) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+        const int r = cpl[i];
+        const PixConst q = decode(__ldg(code + r), r);
+        const int l = lab[r];
+        for_rd_nbrs(q, [&](int nb) {
+            const int ln = lab[nb];
+            if (ln != l) {  // an edge between two labels spoils both
+                bad[l] = 1;
+                bad[ln] = 1;
+            }
+        });
+        rank[r] = atomicAdd(cnt + l, 1);
+    }
+}
+
+// roots: class k (slot range 2^k, k = 1 .. 10) and the component's index within its class,
+// packed as k << 26 | index; -1 (k_grp_init) = fallback: a spoiled or oversized label, or one
+// whose own record moved on to a smaller label.  ctr[k] = components of class k, ctr[11] =
+// grouped records.
+__global__ void k_grp_class(const int32_t *cpl, int nc, const int32_t *lab, const int32_t *cnt,
+                            const int32_t *bad, int32_t *cidx, int32_t *ctr) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+        const int r = cpl[i];
+        if (lab[r] != r) continue;
+        const int s = cnt[r];
+        if (bad[r] || s > 1024) continue;
+        int k = 1;
+        while ((1 << k) < s) ++k;
+        cidx[r] = (k << 26) | atomicAdd(ctr + k, 1);
+        atomicAdd(ctr + 11, s);
+    }
+}
+
+struct GrpBases {
+    int base[11];  // first slot of class k
+};
+
+__global__ void k_grp_fill(const int32_t *cpl, int nc, const int32_t *lab, const int32_t *cidx,
+                           const int32_t *rank, const GrpBases gb, int32_t *slots, int32_t *lpos,
+                           int32_t *fb, int32_t *nfb) {
+    const int n32 = (nc + 31) & ~31;  // whole warps: the ballot below needs every lane
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += gridDim.x * blockDim.x) {
+        const bool in = i < nc;
+        const int r = in ? cpl[i] : 0;
+        const int ci = in ? cidx[lab[r]] : 0;
+        const bool f = in && ci < 0;
+        const unsigned b = __ballot_sync(0xffffffffu, f);
+        const int lane = threadIdx.x & 31;
+        int p0 = 0;
+        if (b && lane == 0) p0 = atomicAdd(nfb, __popc(b));
+        p0 = __shfl_sync(0xffffffffu, p0, 0);
+        if (f) fb[p0 + __popc(b & ((1u << lane) - 1u))] = r;
+        if (in && ci >= 0) {
+            const int k = ci >> 26, idx = ci & ((1 << 26) - 1);
+            const int pos = gb.base[k] + (idx << k) + rank[r];
+            slots[pos] = r;
+            lpos[r] = pos & (k <= 5 ? 31 : k <= 8 ? 255 : 1023);
+        }
+    }
+}
+
+// K passes of the grouped records: block of T slots (T = 32: a warp of a 256-thread CTA),
+// records in registers, exchanged through two alternating shared-memory rows.  Passes
+// 1 .. K-1 run without class tests in the arithmetic (see the presets below); a missing
+// forward neighbour (EDGE) is a select on the difference.  Same operations in the same order
+// as pix_next.
+template <int T>
+__device__ __forceinline__ void grp_body(const RdcIter &a, const int32_t *slots,
+                                         const int32_t *lpos, int first, int nslots, int blk,
+                                         float4 (*sm)[T == 32 ? 256 : T]) {
+    constexpr int NT = T == 32 ? 256 : T;
+    const int i = blk * NT + threadIdx.x;
+    const int r = i < nslots ? slots[first + i] : -1;
+    const bool act = r >= 0;
+    const int own = threadIdx.x;
+    const int blk0 = T == 32 ? (threadIdx.x & ~31) : 0;  // first slot of this block in sm rows
+    PixConst q{};
+    float4 X = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    // passes 1 .. K-1: what the pass reads of each neighbour, preset to the pinned record
+    // (rho = 0, v = u0, c' = +inf on Bg / the frame, -inf on Fg: the FFMA.SAT of the v-step
+    // then returns u0, as K3's c' fold does) and reloaded every pass only where the neighbour
+    // is RD -- a lane's neighbour classes never change, so pinned ones cost no shared load
+    int iu = -1, iur = -1, il = -1, id = -1, idl = -1, ir = -1;  // shared-row indices (RD only)
+    float upx = 0.0f, lfy = 0.0f, dly = 0.0f, urx = 0.0f;
+    float4 D = make_float4(0.0f, 0.0f, 0.0f, INFINITY), R = D;
+    bool e1 = false, e2 = false;
+    if (act) {
+        q = decode(__ldg(a.code + r), r);
+        auto loc = [&](int c) { return c >= 0 ? blk0 + lpos[c] : c; };
+        q.up = loc(q.up);
+        q.ur = loc(q.ur);
+        q.lf = loc(q.lf);
+        q.dn = loc(q.dn);
+        q.dl = loc(q.dl);
+        q.rt = loc(q.rt);
+        iu = q.up;
+        iur = q.ur;
+        il = q.lf;
+        id = q.dn;
+        idl = q.dl;
+        ir = q.rt;
+        if (q.dn == RDC_FG) D = make_float4(0.0f, 0.0f, 1.0f, -INFINITY);
+        if (q.rt == RDC_FG) R = make_float4(0.0f, 0.0f, 1.0f, -INFINITY);
+        e1 = q.dn == RDC_EDGE;
+        e2 = q.rt == RDC_EDGE;
+        X = a.rec[0][r];
+    }
+    const float tau = a.tau, theta = a.theta, inv_theta = a.inv_theta;
+    const int K = a.K;
+    float ux = 0.0f;
+    auto pass = [&](const int k, float4 *B) {
+        if (act) B[own] = X;
+        if (T == 32)
+            __syncwarp();
+        else
+            __syncthreads();
+        if (!act) return;
+        if (k == 0 || k == K) {
+            X = pix_next(q, X, B, k, K, tau, theta, inv_theta, ux);
+            return;
+        }
+        if (iu >= 0) upx = B[iu].x;
+        if (il >= 0) lfy = B[il].y;
+        if (id >= 0) D = B[id];
+        if (idl >= 0) dly = B[idl].y;
+        if (ir >= 0) R = B[ir];
+        if (iur >= 0) urx = B[iur].x;
+        const float dx = __fadd_rn(__fsub_rn(X.x, upx), __fsub_rn(X.y, lfy));
+        ux = __fmaf_rn(dx, -theta, X.z);
+        const float vx = __saturatef(__fmaf_rn(X.w, -0x1p100f, ux));
+        const float wx = __fmaf_rn(vx, -inv_theta, dx);
+        const float dd = __fadd_rn(__fsub_rn(D.x, X.x), __fsub_rn(D.y, dly));
+        const float vd = __saturatef(__fmaf_rn(D.w, -0x1p100f, __fmaf_rn(dd, -theta, D.z)));
+        float g1 = __fsub_rn(__fmaf_rn(vd, -inv_theta, dd), wx);
+        g1 = e1 ? 0.0f : g1;
+        const float dr = __fadd_rn(__fsub_rn(R.x, urx), __fsub_rn(R.y, X.y));
+        const float vr = __saturatef(__fmaf_rn(R.w, -0x1p100f, __fmaf_rn(dr, -theta, R.z)));
+        float g2 = __fsub_rn(__fmaf_rn(vr, -inv_theta, dr), wx);
+        g2 = e2 ? 0.0f : g2;
+        const float s = __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, fabsf(X.w)));
+        const float rr = rcp_ax(__fmaf_rn(sqrt_ax(s), tau, 1.0f));
+        X = make_float4(__fmul_rn(__fmaf_rn(g1, tau, X.x), rr),
+                        __fmul_rn(__fmaf_rn(g2, tau, X.y), rr), vx, X.w);
+    };
+    int k = 0;
+    for (; k + 1 <= K; k += 2) {
+        pass(k, sm[0]);
+        pass(k + 1, sm[1]);
+    }
+    if (k <= K) pass(k, sm[0]);
+    if (act) {  // as k_rdc_iso leaves it
+        a.rec[0][r] = X;
+        a.rec[1][r] = X;
+        if (K >= 1) a.u[r] = ux;
+    }
+}
+
+// one launch for the 256-thread blocks: the first nb1 CTAs run segment 1 (components of 64 ..
+// 256 records, CTA barrier), the rest segment 0 (eight independent warp blocks per CTA)
+__global__ void __launch_bounds__(256)
+k_rdc_grp(const RdcIter a, const int32_t *slots, const int32_t *lpos, int first1, int n1, int nb1,
+          int first0, int n0) {
+    __shared__ float4 sm[2][256];
+    if ((int)blockIdx.x < nb1)
+        grp_body<256>(a, slots, lpos, first1, n1, blockIdx.x, sm);
+    else
+        grp_body<32>(a, slots, lpos, first0, n0, blockIdx.x - nb1, sm);
+}
+
+__global__ void __launch_bounds__(1024)
+k_rdc_grp_big(const RdcIter a, const int32_t *slots, const int32_t *lpos, int first, int nslots) {
+    __shared__ float4 sm[2][1024];
+    grp_body<1024>(a, slots, lpos, first, nslots, blockIdx.x, sm);
+}
+
 }  // namespace
 
 __device__ __forceinline__ double warp_sum_d(double x) {
@@ -617,6 +851,67 @@ cudaError_t launch_rdc_iso(const RdcIter &a, const int32_t *iso, int n_iso, int 
     int g = (n_iso + 255) / 256;
     if (g > n_sm * 8) g = n_sm * 8;
     k_rdc_iso<<<g, 256, 0, s>>>(a, iso, n_iso);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_grp_label(const uint2 *code, const int32_t *cpl, int nc, int32_t *lab,
+                             int32_t *cnt, int32_t *bad, int32_t *rank, int32_t *cidx,
+                             int32_t *ctr, cudaStream_t s) {
+    if (nc <= 0) return cudaSuccess;
+    int g = (nc + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(int32_t) * 12, s);
+    if (e != cudaSuccess) return e;
+    k_grp_init<<<g, 256, 0, s>>>(cpl, nc, lab, cnt, bad, cidx);
+    for (int p = 0; p < GRP_ROUNDS; ++p) k_grp_prop<<<g, 256, 0, s>>>(code, cpl, nc, lab);
+    k_grp_count<<<g, 256, 0, s>>>(code, cpl, nc, lab, cnt, bad, rank);
+    k_grp_class<<<g, 256, 0, s>>>(cpl, nc, lab, cnt, bad, cidx, ctr);
+    return cudaGetLastError();
+}
+
+// slot layout from the class counts ctr[1..10]: segment 0 = classes 32 .. 2 (warp blocks),
+// 1 = 256 .. 64, 2 = 1024, 512; every segment starts on a multiple of 1024 and holds its
+// classes by falling size, so each 2^k range is aligned to 2^k
+void grp_layout(const int32_t *ctr, GrpPlan *gp) {
+    static const int seg_hi[3] = {5, 8, 10}, seg_lo[3] = {1, 6, 9};
+    int pos = 0;
+    for (int sg = 0; sg < 3; ++sg) {
+        gp->first[sg] = pos;
+        for (int k = seg_hi[sg]; k >= seg_lo[sg]; --k) {
+            gp->base[k] = pos;
+            pos += ctr[k] << k;
+        }
+        gp->count[sg] = pos - gp->first[sg];
+        pos = (pos + 1023) & ~1023;
+    }
+    gp->total = pos;
+}
+
+cudaError_t launch_grp_fill(const int32_t *cpl, int nc, const int32_t *lab, const int32_t *cidx,
+                            const int32_t *rank, const GrpPlan &gp, int32_t *slots,
+                            int32_t *lpos, int32_t *fb, int32_t *nfb, cudaStream_t s) {
+    if (nc <= 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(slots, 0xff, sizeof(int32_t) * (size_t)(gp.total > 0 ? gp.total : 1), s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(nfb, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return e;
+    GrpBases gb;
+    for (int k = 0; k < 11; ++k) gb.base[k] = gp.base[k];
+    int g = (nc + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    k_grp_fill<<<g, 256, 0, s>>>(cpl, nc, lab, cidx, rank, gb, slots, lpos, fb, nfb);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rdc_grp(const RdcIter &a, const GrpPlan &gp, const int32_t *slots,
+                           const int32_t *lpos, cudaStream_t s) {
+    const int nb0 = (gp.count[0] + 255) / 256, nb1 = (gp.count[1] + 255) / 256;
+    if (nb0 + nb1 > 0)
+        k_rdc_grp<<<nb0 + nb1, 256, 0, s>>>(a, slots, lpos, gp.first[1], gp.count[1], nb1,
+                                            gp.first[0], gp.count[0]);
+    if (gp.count[2] > 0)
+        k_rdc_grp_big<<<(gp.count[2] + 1023) / 1024, 1024, 0, s>>>(a, slots, lpos, gp.first[2],
+                                                                   gp.count[2]);
     return cudaGetLastError();
 }
 

@@ -103,7 +103,7 @@ struct rds_handle {
 
     int opt_kf = 0, opt_rows = 0, opt_timing = 0, opt_skip = 1, opt_graph = 1, opt_ctas = 0;
     int opt_norm = 0;  // stopping-rule norm: 0 Euclidean over pixels, 1 RMS (R-F2)
-    int opt_split = 1;    // coupled / decoupled split of compact fixed-K solves (RDS_OPT_RDC_SPLIT)
+    int opt_split = 2;    // coupled / decoupled split (1) + grouped components (2) of compact fixed-K solves (RDS_OPT_RDC_SPLIT)
     int opt_compact = 2;  // f3: 0 dense stencil, 1 compacted RD iteration, 2 auto (default; RDS_OPT_COMPACT)
     int opt_wave = 0;     // temporal wavefront for fixed-K solves: 0 off (default), 1 on, 2 auto (RDS_OPT_WAVE)
     bool wave_ok = false; // the last solve's set-up allows the wavefront (aligned, supported kf)
@@ -335,7 +335,7 @@ int rds_set_option(rds_t *h, int key, int64_t value) {
             h->opt_compact = (int)value;
             return RDS_OK;
         case RDS_OPT_RDC_SPLIT:
-            if (value < 0 || value > 1)
+            if (value < 0 || value > 2)
                 return fail(h, RDS_EINVAL, "rds_set_option: rdc_split=%lld", (long long)value);
             h->opt_split = (int)value;
             return RDS_OK;
@@ -974,6 +974,9 @@ struct CompactPlan {
     RdcIter it{};
     const int32_t *iso = nullptr;  // split (fixed-K solves): the decoupled records
     int n_iso = 0;
+    GrpPlan gp{};                  // split = 2: small components of the coupled records
+    const int32_t *slots = nullptr, *lpos = nullptr;
+    int n_grp = 0;                 // records iterated by k_rdc_grp
 };
 static int compact_prepare(rds_t *h, float tau, float theta, int iters, int check_every,
                            CompactPlan *cp) {
@@ -1004,7 +1007,10 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, int chec
     // index lists and its per-chunk counts / offsets and total
     const size_t nn = (size_t)(n > 0 ? n : 1), nch = nn / 1024 + 2;
     void *pb = h->rdc_buf;
-    CK(h, grow(&pb, &h->rdc_bytes, nn * (16 * 2 + 8 + 4 + 4 + 4 + 4) + 4 * (2 * nch + 1)));
+    // (+ the grouping's labels, counts, flags, ranks, class indices, block positions and
+    // fallback list: 7 ints per record; its slots: < 2 per record + segment padding; counters)
+    CK(h, grow(&pb, &h->rdc_bytes, nn * (16 * 2 + 8 + 4 + 4 + 4 + 4 + 4 * 9) +
+                                       4 * (2 * nch + 1 + 4096 + 16)));
     h->rdc_buf = pb;
     float4 *rec0 = (float4 *)pb, *rec1 = rec0 + nn;
     uint2 *code = (uint2 *)(rec1 + nn);
@@ -1012,6 +1018,9 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, int chec
     float *u = (float *)(list + nn);
     int32_t *cpl = (int32_t *)(u + nn), *iso = cpl + nn, *cnt = iso + nn, *off = cnt + nch,
             *ncpl = off + nch;
+    int32_t *g_lab = ncpl + 1, *g_cnt = g_lab + nn, *g_bad = g_cnt + nn, *g_rank = g_bad + nn,
+            *g_cidx = g_rank + nn, *g_lpos = g_cidx + nn, *g_fb = g_lpos + nn,
+            *g_ctr = g_fb + nn, *g_slots = g_ctr + 16;
     CK(h, launch_rdc_fill(h->at(h->lab), h->pitch, (int)h->H, (int)h->W, h->rdc_row + h->H,
                           h->rdc_idx, list, h->stream));
     RdcSetup &su = cp->su;
@@ -1055,6 +1064,28 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, int chec
         it.sel = cpl;
         cp->iso = iso;
         cp->n_iso = n - nc;
+        // split = 2: the coupled records' small connected components iterate inside one warp /
+        // CTA each (k_rdc_grp); what is left keeps the grid barrier
+        if (h->opt_split >= 2 && nc > 0) {
+            CK(h, launch_grp_label(code, cpl, nc, g_lab, g_cnt, g_bad, g_rank, g_cidx, g_ctr,
+                                   h->stream));
+            int32_t ctr[12];
+            CK(h, cudaMemcpyAsync(ctr, g_ctr, sizeof ctr, cudaMemcpyDeviceToHost, h->stream));
+            CK(h, cudaStreamSynchronize(h->stream));
+            // all or nothing: while any record keeps the grid barrier, its per-pass latency is
+            // paid anyway and the barrier kernel absorbs the grouped records at no extra cost
+            // (measured at C2's connected bands: grouped + barrier 1.8 ms vs 1.2 ms)
+            if (ctr[11] == nc) {
+                grp_layout(ctr, &cp->gp);
+                CK(h, launch_grp_fill(cpl, nc, g_lab, g_cidx, g_rank, cp->gp, g_slots, g_lpos,
+                                      g_fb, g_ctr, h->stream));
+                cp->slots = g_slots;
+                cp->lpos = g_lpos;
+                cp->n_grp = ctr[11];
+                it.n = nc - ctr[11];
+                it.sel = g_fb;
+            }
+        }
     }
     cp->use = true;
     return RDS_OK;
@@ -1083,7 +1114,8 @@ static int compact_run(rds_t *h, CompactPlan *cp, int iters, const TolParams &tp
         if (it.n == 0) CK(h, cudaStreamSynchronize(h->stream));  // r lives on this stack
     }
     if (cp->n_iso > 0) CK(h, launch_rdc_iso(it, cp->iso, cp->n_iso, h->n_sm, h->stream));
-    CK(h, launch_rdc_iter(it, h->n_sm, h->stream));
+    if (cp->n_grp > 0) CK(h, launch_rdc_grp(it, cp->gp, cp->slots, cp->lpos, h->stream));
+    if (it.n > 0 || tp.check_every > 0 || !it.sel) CK(h, launch_rdc_iter(it, h->n_sm, h->stream));
     CK(h, launch_rdc_scatter(cp->su, it, h->stream));
     return RDS_OK;
 }
@@ -1401,7 +1433,10 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     st.launches = (cplan.use || small_use || grid_use) ? 1 : launches;
     st.compact = cplan.use ? 1 : 0;
     st.rdc_decoupled = cplan.use ? cplan.n_iso : 0;
-    if (cplan.use) st.launches = 1 + (cplan.n_iso > 0 ? 1 : 0);
+    st.rdc_grouped = cplan.use ? cplan.n_grp : 0;
+    if (cplan.use)
+        st.launches = (cplan.it.n > 0 || !cplan.it.sel ? 1 : 0) + (cplan.n_iso > 0 ? 1 : 0) +
+                      (cplan.gp.count[0] + cplan.gp.count[1] > 0) + (cplan.gp.count[2] > 0);
     st.wave = (!cplan.use && !small_use && !grid_use && wave_blocks(h, kf, iters, check_every) > 0) ? 1 : 0;
     st.resident = small_use ? 1 : grid_use ? 2 : 0;
     st.persist = (!cplan.use && !small_use && !grid_use && persist_applies(h, kf, iters, check_every)) ? 1 : 0;

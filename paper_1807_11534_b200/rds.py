@@ -30,7 +30,7 @@ RDS_OPT_RESIDENT = 10  # small images as one resident cluster: 0 off, 1 / 2 (def
 RDS_OPT_PROLOGUE = 14  # plain stencil launches in the prologue form: 0 off, 1 on, 2 auto (default)
 RDS_OPT_WS = 13        # full-depth launches on the warp-specialised stencil: 0 off (default), 1 on
 RDS_OPT_PERSIST = 11   # fixed-K loop as one persistent launch: 0 off (default), 1 on, 2 auto
-RDS_OPT_RDC_SPLIT = 15 # compact fixed-K solves: decoupled RD pixels iterate alone: 1 on (default), 0 off
+RDS_OPT_RDC_SPLIT = 15 # compact fixed-K solves: 1 decoupled RD pixels iterate alone, 2 (default) also small connected components inside one warp / CTA, 0 off
 RDS_OPT_GRID = 12      # mid-size images resident on the whole GPU: 0 off (default), 1 / 2 on
 
 EXPORTS = (
@@ -85,7 +85,8 @@ class rds_stats_t(ctypes.Structure):
                 ("residual", ctypes.c_float), ("check_every", ctypes.c_int32),
                 ("compact", ctypes.c_int32), ("wave", ctypes.c_int32),
                 ("resident", ctypes.c_int32), ("persist", ctypes.c_int32),
-                ("rdc_decoupled", ctypes.c_int32)]
+                ("rdc_decoupled", ctypes.c_int32),
+                ("rdc_grouped", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -1,7 +1,7 @@
 """A/B of the compact path's coupled / decoupled split (RDS_OPT_RDC_SPLIT) at the stated K:
 python scripts/split_ab.py [--config C3] [--deltas 0.02 0.05 0.1 0.2].  One JSON line per
-delta: K-loop ms (CUDA events, median of reps) with the split off / on, the decoupled
-fraction, the dense path's K-loop for reference, and whether all three gave the same u."""
+delta: K-loop ms (CUDA events, median of reps) with the split off / on (1) / on with grouped
+components (2), the decoupled and grouped fractions, the dense path's K-loop for reference, and whether all three gave the same u."""
 import argparse
 import json
 import os
@@ -25,7 +25,8 @@ z, P = wl.make_image(cfg)
 K = cfg.iters
 S = {}
 for name, kw in (("dense", dict(compact=0)), ("unsplit", dict(compact=1, rdc_split=0)),
-                 ("split", dict(compact=1, rdc_split=1))):
+                 ("split", dict(compact=1, rdc_split=1)),
+                 ("grouped", dict(compact=1, rdc_split=2))):
     s = rds.Solver(cfg.H, cfg.W, timing=True, **kw)
     s.set_image(z)
     s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
@@ -48,8 +49,15 @@ for dr in a.deltas:
         if name == "split":
             row["rd_frac"] = st["n_rd"] / (cfg.H * cfg.W)
             row["decoupled_frac"] = st["rdc_decoupled"] / max(1, st["n_rd"])
+        if name == "grouped":
+            row["grouped_frac"] = st["rdc_grouped"] / max(1, st["n_rd"])
+            row["barrier_px"] = st["n_rd"] - st["rdc_decoupled"] - st["rdc_grouped"]
     row["split_speedup"] = row["unsplit_loop_ms"] / row["split_loop_ms"]
     row["split_vs_dense"] = row["dense_loop_ms"] / row["split_loop_ms"]
+    row["grouped_vs_split"] = row["split_loop_ms"] / row["grouped_loop_ms"]
+    row["grouped_vs_dense"] = (row["dense_loop_ms"] + row["dense_setup_ms"]) / (
+        row["grouped_loop_ms"] + row["grouped_setup_ms"])
     row["same_u"] = bool(np.array_equal(us["dense"], us["split"]) and
-                         np.array_equal(us["unsplit"], us["split"]))
+                         np.array_equal(us["unsplit"], us["split"]) and
+                         np.array_equal(us["grouped"], us["split"]))
     print(json.dumps(row), flush=True)

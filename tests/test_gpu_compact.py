@@ -127,6 +127,16 @@ def _decoupled_count(lab, img_w):
     return int((rd & ~nb & ~last[None, :]).sum())
 
 
+def _component_sizes(lab, img_w):
+    """Sizes of the connected components of the RD pixels under the six-neighbour relation of
+    the stencil (scipy.ndimage.label with the hexagonal structuring element), seams of a batch
+    included as edges (the library's superset)"""
+    from scipy import ndimage
+    st = np.array([[0, 1, 1], [1, 1, 1], [1, 1, 0]])  # up, up-right, left, right, down-left, down
+    cl, n = ndimage.label(lab == 2, structure=st)
+    return np.bincount(cl.ravel())[1:]
+
+
 @pytest.mark.parametrize("case", ["voronoi", "noise", "batch", "warm", "K1", "K2", "P"])
 def test_compact_split_equals_unsplit(rds, orc, case):
     """The coupled / decoupled split (RDS_OPT_RDC_SPLIT) gives the unsplit compact path's
@@ -158,23 +168,46 @@ def test_compact_split_equals_unsplit(rds, orc, case):
     assert st0["compact"] == 1 and st1["compact"] == 1
     assert st0["rdc_decoupled"] == 0
     n_rd = int((b["labels"] == 2).sum())
-    want = _decoupled_count(b["labels"].reshape(zf.shape), z.shape[-1]) if n_rd >= 4096 else 0
+    # a batch is solved as one H x (B W) frame, the images side by side (rds.h, rds_create_batch)
+    frame = np.concatenate(list(b["labels"]), axis=1) if batch else b["labels"]
+    want = _decoupled_count(frame, z.shape[-1]) if n_rd >= 4096 else 0
     assert st1["rdc_decoupled"] == want, (st1["rdc_decoupled"], want, n_rd)
     if case in ("noise", "batch"):
         assert want > 0.2 * n_rd
     _same(a, b)
     assert s1.energy() == s0.energy()
     assert s1.check_frame() == 0
+    assert st1["rdc_grouped"] == 0
+    # split = 2: small connected components of the coupled pixels inside one warp / CTA each
+    s2, c = _run(rds, z, delta, K, 1, batch=batch, warm=warm, P=P, gamma=gamma, rdc_split=2)
+    st2 = s2.stats()
+    assert st2["compact"] == 1 and st2["rdc_decoupled"] == want
+    if n_rd >= 4096:
+        coupled = n_rd - want
+        if batch is None:  # grouped pixels lie in components of <= 1024 pixels and are coupled
+            sizes = _component_sizes(b["labels"], z.shape[-1])
+            assert sizes.sum() == n_rd
+            small = int(sizes[sizes <= 1024].sum()) - want
+            assert 0 <= st2["rdc_grouped"] <= small, (st2["rdc_grouped"], small)
+        if case in ("noise", "batch"):
+            assert st2["rdc_grouped"] > 0.9 * coupled, (st2["rdc_grouped"], coupled)
+    else:
+        assert st2["rdc_grouped"] == 0
+    _same(a, c)
+    assert s2.energy() == s0.energy()
+    assert s2.check_frame() == 0
 
 
-def test_compact_split_oracle(rds, orc):
+@pytest.mark.parametrize("split", [1, 2])
+def test_compact_split_oracle(rds, orc, split):
     """The split path against the fp64 oracle at the north_star tolerances (a C3-like noise
     band, about half of it decoupled)."""
     z = wl.gen_voronoi(N=320, seed=3, n_sites=20)[:256, :320].copy()
     f = orc.fitting(z, 0.8, 0.2)
     delta = wl.band_delta(0.1, orc.absmax(f))
-    s, g = _run(rds, z, delta, 300, 1, rdc_split=1)
+    s, g = _run(rds, z, delta, 300, 1, rdc_split=split)
     assert s.stats()["rdc_decoupled"] > 0
+    assert (s.stats()["rdc_grouped"] > 0) == (split == 2)
     o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, 300)
     assert np.array_equal(g["labels"], o["labels"])
     for k in ("u", "v", "p1", "p2"):  # north_star: u, rho within 5e-4, mask <= 0.05%
