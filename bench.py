@@ -580,9 +580,23 @@ def compact_section(cfg, zt, Pt, am, K, lam, sp, per_delta):
             # out, packed codes) against the measured L2 read bandwidth; it is latency / grid
             # barrier bound, so this fraction stays well below 1
             lm = statistics.median(ts) - st["setup_ms"]
-            gbs = RDC_BYTES_PER_RD_ITER * st["n_rd"] * K / (lm * 1e-3) / 1e9
-            row["roofline"] = {"bound": "l2", "achieved": gbs, "peak": L2_READ_GBS,
-                               "unit": "GB/s", "frac": gbs / L2_READ_GBS}
+            if st["rdc_decoupled"] + st["rdc_grouped"] == st["n_rd"]:
+                # no record goes through L2 per pass (k_rdc_iso: registers; k_rdc_grp: shared
+                # memory): bound by the two MUFU ops per RD pixel-iteration like the stencil
+                # (8 px-iter/clk/SM; one scalar instruction stream per pixel, no packed pairs,
+                # so instruction issue sits below that: DESIGN.md §6)
+                import torch
+
+                n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+                peak = (n_sm * MUFU_LANES_PER_SM / MUFU_PER_PX_ITER
+                        * _peaks().get("sm_max_mhz", 1965.0) * 1e6 / 1e9)
+                ach = st["n_rd"] * K / (lm * 1e-3) / 1e9
+                row["roofline"] = {"bound": "alu", "achieved": ach, "peak": peak,
+                                   "unit": "G RD-pixel-iter/s", "frac": ach / peak}
+            else:
+                gbs = RDC_BYTES_PER_RD_ITER * st["n_rd"] * K / (lm * 1e-3) / 1e9
+                row["roofline"] = {"bound": "l2", "achieved": gbs, "peak": L2_READ_GBS,
+                                   "unit": "GB/s", "frac": gbs / L2_READ_GBS}
         out.append(row)
     s.close()
     return {"per_delta": out, "full_dense_solve_ms": t_full,

@@ -337,7 +337,7 @@ struct GrpPlan {
     int count[3] = {};   // slots in use per segment
     int total = 0;       // slots allocated (segments padded to multiples of 1024)
 };
-// labels, per-label counts / flags, per-record ranks, per-root class and index; ctr: 12 ints
+// labels, per-label counts / flags, per-record ranks, per-root class and index; ctr: 16 ints
 // (ctr[k] = components of class k = 1 .. 10, ctr[11] = grouped records)
 cudaError_t launch_grp_label(const uint2 *code, const int32_t *cpl, int nc, int32_t *lab,
                              int32_t *cnt, int32_t *bad, int32_t *rank, int32_t *cidx,

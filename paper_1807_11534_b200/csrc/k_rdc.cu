@@ -367,17 +367,18 @@ __global__ void __launch_bounds__(256) k_rdc_iso(const RdcIter a, const int32_t 
 // shared memory with a warp / CTA barrier per pass -- no grid barrier, no L2 round trip.
 // Same float operations (pix_next), so the same bits whichever kernel owns a pixel.
 //
-// Setup: P rounds of min-label propagation over the coupled list (pull and push along every
-// read edge, one pointer jump), then every record checks that all its neighbours carry its
+// Setup: rounds of min-label propagation over the coupled list (pull and push along every
+// read edge, one pointer jump) until a round lowers no label (at most GRP_ROUNDS_MAX), then
+// every record checks that all its neighbours carry its
 // label ("settled"); a label all of whose records are settled is exactly one component (it is
 // closed under adjacency and every member reached the label's own record).  Components of up
 // to 1024 settled records get power-of-two slot ranges (classes 2 .. 1024) in a slot array
 // ordered by falling class inside three segments (warp: <= 32, CTA of 256, CTA of 1024), so
-// no range straddles its block; everything else (unsettled after P rounds, or larger) stays on
+// no range straddles its block; everything else (unsettled after the last round, or larger) stays on
 // the grid-barrier kernel through the fallback list.  Slot order within a class comes from
 // atomic counters: it varies from run to run, the values do not.
 // ---------------------------------------------------------------------------------------
-constexpr int GRP_ROUNDS = 12;
+constexpr int GRP_BATCH = 4, GRP_ROUNDS_MAX = 16;
 
 template <typename F>
 __device__ __forceinline__ void for_rd_nbrs(const PixConst &q, F f) {
@@ -400,8 +401,12 @@ __global__ void k_grp_init(const int32_t *cpl, int nc, int32_t *lab, int32_t *cn
     }
 }
 
-// one round: labels only fall and always name a record of the same component
-__global__ void k_grp_prop(const uint2 *code, const int32_t *cpl, int nc, int32_t *lab) {
+// one round: labels only fall and always name a record of the same component; *changed is
+// raised when any label fell (a round that lowers nothing is a fixed point: every edge joins
+// equal labels, so every component carries one label)
+__global__ void k_grp_prop(const uint2 *code, const int32_t *cpl, int nc, int32_t *lab,
+                           int32_t *changed) {
+    bool any = false;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
         const int r = cpl[i];
         const PixConst q = decode(__ldg(code + r), r);
@@ -409,9 +414,18 @@ __global__ void k_grp_prop(const uint2 *code, const int32_t *cpl, int nc, int32_
         int m = L[r];
         for_rd_nbrs(q, [&](int nb) { m = min(m, (int)L[nb]); });
         m = min(m, (int)L[m]);
-        if (m < L[r]) atomicMin(lab + r, m);
-        for_rd_nbrs(q, [&](int nb) { if (m < L[nb]) atomicMin(lab + nb, m); });
+        if (m < L[r]) {
+            atomicMin(lab + r, m);
+            any = true;
+        }
+        for_rd_nbrs(q, [&](int nb) {
+            if (m < L[nb]) {
+                atomicMin(lab + nb, m);
+                any = true;
+            }
+        });
     }
+    if (any) *changed = 1;
 }
 
 __global__ void k_grp_count(const uint2 *code, const int32_t *cpl, int nc, const int32_t *lab,
@@ -435,18 +449,31 @@ __global__ void k_grp_count(const uint2 *code, const int32_t *cpl, int nc, const
 // packed as k << 26 | index; -1 (k_grp_init) = fallback: a spoiled or oversized label, or one
 // whose own record moved on to a smaller label.  ctr[k] = components of class k, ctr[11] =
 // grouped records.
-__global__ void k_grp_class(const int32_t *cpl, int nc, const int32_t *lab, const int32_t *cnt,
-                            const int32_t *bad, int32_t *cidx, int32_t *ctr) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
-        const int r = cpl[i];
-        if (lab[r] != r) continue;
-        const int s = cnt[r];
-        if (bad[r] || s > 1024) continue;
-        int k = 1;
-        while ((1 << k) < s) ++k;
-        cidx[r] = (k << 26) | atomicAdd(ctr + k, 1);
-        atomicAdd(ctr + 11, s);
+__global__ void __launch_bounds__(256)
+k_grp_class(const int32_t *cpl, int nc, const int32_t *lab, const int32_t *cnt,
+            const int32_t *bad, int32_t *cidx, int32_t *ctr) {
+    // one record per thread; the class counters go through shared memory, one global atomic
+    // per class and CTA (300 K roots on eleven addresses cost 190 us at C3 delta = .1)
+    __shared__ int32_t sc[12], sb[12];
+    if (threadIdx.x < 12) sc[threadIdx.x] = 0;
+    __syncthreads();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    int r = -1, k = 0, loc = 0;
+    if (i < nc) {
+        r = cpl[i];
+        const int s = lab[r] == r ? cnt[r] : 0;
+        if (s > 0 && !bad[r] && s <= 1024) {
+            k = 1;
+            while ((1 << k) < s) ++k;
+            loc = atomicAdd(sc + k, 1);
+            atomicAdd(sc + 11, s);
+        }
     }
+    __syncthreads();
+    if (threadIdx.x >= 1 && threadIdx.x < 12 && sc[threadIdx.x] > 0)
+        sb[threadIdx.x] = atomicAdd(ctr + threadIdx.x, sc[threadIdx.x]);
+    __syncthreads();
+    if (k > 0) cidx[r] = (k << 26) | (sb[k] + loc);
 }
 
 struct GrpBases {
@@ -860,12 +887,26 @@ cudaError_t launch_grp_label(const uint2 *code, const int32_t *cpl, int nc, int3
     if (nc <= 0) return cudaSuccess;
     int g = (nc + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(int32_t) * 12, s);
+    cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(int32_t) * 16, s);
     if (e != cudaSuccess) return e;
     k_grp_init<<<g, 256, 0, s>>>(cpl, nc, lab, cnt, bad, cidx);
-    for (int p = 0; p < GRP_ROUNDS; ++p) k_grp_prop<<<g, 256, 0, s>>>(code, cpl, nc, lab);
+    // rounds in batches of GRP_BATCH with one flag read-back each, until a batch's last round
+    // lowers nothing (scattered noise bands: one or two batches) or GRP_ROUNDS_MAX is reached
+    // (a band with long connected runs: the unsettled components then stay on the barrier)
+    for (int p = 0; p < GRP_ROUNDS_MAX; p += GRP_BATCH) {
+        for (int b = 0; b < GRP_BATCH - 1; ++b) k_grp_prop<<<g, 256, 0, s>>>(code, cpl, nc, lab, ctr + 13);
+        e = cudaMemsetAsync(ctr + 12, 0, sizeof(int32_t), s);
+        if (e != cudaSuccess) return e;
+        k_grp_prop<<<g, 256, 0, s>>>(code, cpl, nc, lab, ctr + 12);
+        int32_t changed = 0;
+        e = cudaMemcpyAsync(&changed, ctr + 12, sizeof changed, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return e;
+        e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return e;
+        if (!changed) break;
+    }
     k_grp_count<<<g, 256, 0, s>>>(code, cpl, nc, lab, cnt, bad, rank);
-    k_grp_class<<<g, 256, 0, s>>>(cpl, nc, lab, cnt, bad, cidx, ctr);
+    k_grp_class<<<(nc + 255) / 256, 256, 0, s>>>(cpl, nc, lab, cnt, bad, cidx, ctr);
     return cudaGetLastError();
 }
 

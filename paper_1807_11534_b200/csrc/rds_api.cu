@@ -1066,7 +1066,11 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, int chec
         cp->n_iso = n - nc;
         // split = 2: the coupled records' small connected components iterate inside one warp /
         // CTA each (k_rdc_grp); what is left keeps the grid barrier
-        if (h->opt_split >= 2 && nc > 0) {
+        // (tried only where at least 15% of the RD pixels are decoupled: a scattered band of
+        // density p has (1 - p)^6 of them, so p below about 0.27; a connected band has few,
+        // its components are long runs that neither settle nor fit a CTA, and the label
+        // rounds would be wasted -- C2 delta = .05: 7.6% decoupled, + 0.3 ms of setup)
+        if (h->opt_split >= 2 && nc > 0 && (double)(n - nc) >= 0.15 * (double)n) {
             CK(h, launch_grp_label(code, cpl, nc, g_lab, g_cnt, g_bad, g_rank, g_cidx, g_ctr,
                                    h->stream));
             int32_t ctr[12];

@@ -18,7 +18,7 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_st
 RCMD="python scripts/small_one.py"
 $RCMD > gpurun_out/${T}_small_plain.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_small -s 1 -c 1 -o gpurun_out/${T}_small $RCMD > gpurun_out/${T}_ncu_small.log 2>&1
-CCMD="python scripts/compact_one.py --delta-rel 0.1 --iters 30"
+CCMD="python scripts/compact_one.py --delta-rel 0.1 --iters 30 --split 0"
 $CCMD > gpurun_out/${T}_compact_plain.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rdc_iter -c 1 -o gpurun_out/${T}_rdc_iter $CCMD > gpurun_out/${T}_ncu_rdc.log 2>&1
 ECMD="python scripts/energy_time.py C3"

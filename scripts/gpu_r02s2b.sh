@@ -1,8 +1,8 @@
 # Round 2, fifth session: grouped connected components of the compact path (RDS_OPT_RDC_SPLIT = 2).
-T=r02s2d
+T=r02s2f
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_compact.py -q -k "split or oracle" > gpurun_out/${T}_pytest_compact.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_compact.py -q > gpurun_out/${T}_pytest_compact.log 2>&1
 tail -5 gpurun_out/${T}_pytest_compact.log
 timeout 600 python scripts/split_ab.py --config C3 > gpurun_out/${T}_split_c3.jsonl 2> gpurun_out/${T}_split_c3.err
 tail -3 gpurun_out/${T}_split_c3.err

@@ -198,6 +198,54 @@ def test_compact_split_equals_unsplit(rds, orc, case):
     assert s2.check_frame() == 0
 
 
+def test_compact_grouped_block_sizes(rds, orc):
+    """Components of every slot class (2 ... 1024 records) so that the warp, 256-thread and
+    1024-thread forms of k_rdc_grp all run: rectangles of RD pixels (z = 0.5, f ~ 0) on a
+    pinned ground (z = 0.2 / 0.8), two pixels apart.  All of them are grouped, the result is
+    the barrier kernel's bit for bit, and it matches the fp64 oracle."""
+    rng = np.random.default_rng(5)
+    H, W = 330, 420
+    z = np.where(rng.uniform(size=(H, W)) < 0.5, 0.2, 0.8).astype(np.float32)
+    shapes = [(1, 2), (2, 3), (3, 5), (5, 8), (7, 9), (10, 20), (12, 21), (20, 30), (25, 40),
+              (32, 32), (1, 40), (60, 1), (2, 200)]
+    i0 = 2
+    n_blob = 0
+    while i0 < H - 62:
+        j0, hmax = 2, 0
+        while True:
+            h, w = shapes[n_blob % len(shapes)]
+            if j0 + w + 2 > W or i0 + h + 2 > H:
+                break
+            z[i0:i0 + h, j0:j0 + w] = 0.5 + 0.005 * rng.standard_normal((h, w))
+            j0 += w + 2
+            hmax = max(hmax, h)
+            n_blob += 1
+        i0 += hmax + 2
+    # isolated RD pixels below the rectangles: the grouping is only tried where at least 15%
+    # of the RD pixels are decoupled (the library's scattered-band gate)
+    z = np.concatenate([z, np.full((70, W), 0.2, np.float32)])
+    z[H + 4:H + 66:2, 2:W - 2:3] = 0.5
+    H = z.shape[0]
+    f = orc.fitting(z, 0.8, 0.2)
+    delta = wl.band_delta(0.1, orc.absmax(f))
+    K = 60
+    s0, a = _run(rds, z, delta, K, 1, rdc_split=0)
+    s2, c = _run(rds, z, delta, K, 1, rdc_split=2)
+    st = s2.stats()
+    sizes = _component_sizes(c["labels"], W)
+    n_rd = int((c["labels"] == 2).sum())
+    assert n_rd >= 4096 and sizes.max() <= 1024
+    assert st["rdc_decoupled"] >= 0.15 * n_rd
+    assert {int(2 ** math.ceil(math.log2(max(2, x)))) for x in sizes if x > 1} >= {2, 8, 64, 256, 1024}
+    assert st["rdc_decoupled"] + st["rdc_grouped"] == n_rd, (st, n_rd)
+    assert st["rdc_grouped"] == int(sizes[sizes > 1].sum())
+    _same(a, c)
+    o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, K)
+    assert np.array_equal(c["labels"], o["labels"])
+    for k in ("u", "v", "p1", "p2"):
+        assert np.abs(c[k].astype(np.float64) - o[k]).max() <= 5e-4, k
+
+
 @pytest.mark.parametrize("split", [1, 2])
 def test_compact_split_oracle(rds, orc, split):
     """The split path against the fp64 oracle at the north_star tolerances (a C3-like noise
