@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(256) k_rdc_iso(const RdcIter a, const int32_t 
 // atomic counters: it varies from run to run, the values do not.
 // ---------------------------------------------------------------------------------------
 constexpr int GRP_BATCH = 4, GRP_ROUNDS_MAX = 16;
+constexpr bool GRP_2PH_DEFAULT = false;  // two-phase passes (grp_body2); RDS_GRP_2PH overrides
 
 template <typename F>
 __device__ __forceinline__ void for_rd_nbrs(const PixConst &q, F f) {
@@ -598,6 +599,128 @@ __device__ __forceinline__ void grp_body(const RdcIter &a, const int32_t *slots,
         a.rec[1][r] = X;
         if (K >= 1) a.u[r] = ux;
     }
+}
+
+// Two-phase form of the same passes (RDS_GRP_2PH=1): a pass publishes w = div rho - v / theta
+// of every pixel (phase A), then takes grad w from the neighbours' published w (phase B) --
+// what K3 does with its stage state -- instead of recomputing the down / right neighbours' w
+// from their whole records.  A pinned neighbour's w is formed locally (its rho = 0, v = u0).
+// Per pass 3 shared stores and about 4 shared loads of 4 bytes instead of a 16-byte store and
+// two 16-byte loads plus four of 4 bytes; two block barriers instead of one.  Same operations
+// on the same operands in the same order, so the same bits.
+template <int T>
+__device__ __forceinline__ void grp_body2(const RdcIter &a, const int32_t *slots,
+                                          const int32_t *lpos, int first, int nslots, int blk,
+                                          float *sm) {
+    constexpr int NT = T == 32 ? 256 : T;
+    float *const p1a = sm, *const p2a = sm + NT, *const p1b = sm + 2 * NT, *const p2b = sm + 3 * NT,
+                 *const Wp = sm + 4 * NT;
+    const int i = blk * NT + threadIdx.x;
+    const int r = i < nslots ? slots[first + i] : -1;
+    const bool act = r >= 0;
+    const int own = threadIdx.x;
+    const int blk0 = T == 32 ? (threadIdx.x & ~31) : 0;
+    float4 X = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    int iu = -1, iur = -1, il = -1, id = -1, idl = -1, ir = -1;
+    float u0d = 0.0f, u0r = 0.0f;
+    bool e1 = false, e2 = false;
+    if (act) {
+        const PixConst q = decode(__ldg(a.code + r), r);
+        auto loc = [&](int c) { return c >= 0 ? blk0 + lpos[c] : -1; };
+        iu = loc(q.up);
+        iur = loc(q.ur);
+        il = loc(q.lf);
+        id = loc(q.dn);
+        idl = loc(q.dl);
+        ir = loc(q.rt);
+        u0d = q.dn == RDC_FG ? 1.0f : 0.0f;
+        u0r = q.rt == RDC_FG ? 1.0f : 0.0f;
+        e1 = q.dn == RDC_EDGE;
+        e2 = q.rt == RDC_EDGE;
+        X = a.rec[0][r];
+        p1a[own] = X.x;
+        p2a[own] = X.y;
+    }
+    auto sync = [&]() {
+        if (T == 32)
+            __syncwarp();
+        else
+            __syncthreads();
+    };
+    sync();
+    const float tau = a.tau, theta = a.theta, inv_theta = a.inv_theta;
+    const int K = a.K;
+    float ux = 0.0f;
+    auto pass = [&](const int k, const float *p1, const float *p2, float *q1, float *q2) {
+        float dx = 0.0f, vx = 0.0f, wx = 0.0f;
+        if (act) {
+            const float upx = iu >= 0 ? p1[iu] : 0.0f, lfy = il >= 0 ? p2[il] : 0.0f;
+            dx = __fadd_rn(__fsub_rn(X.x, upx), __fsub_rn(X.y, lfy));
+            ux = __fmaf_rn(dx, -theta, X.z);
+            vx = k == 0 ? X.z : __saturatef(__fmaf_rn(X.w, -0x1p100f, ux));
+            wx = __fmaf_rn(vx, -inv_theta, dx);
+            Wp[own] = wx;
+        }
+        sync();
+        if (act) {
+            float wd, wr;
+            if (id >= 0) {
+                wd = Wp[id];
+            } else {
+                const float dly = idl >= 0 ? p2[idl] : 0.0f;
+                wd = __fmaf_rn(u0d, -inv_theta, __fadd_rn(__fsub_rn(0.0f, X.x), __fsub_rn(0.0f, dly)));
+            }
+            if (ir >= 0) {
+                wr = Wp[ir];
+            } else {
+                const float urx = iur >= 0 ? p1[iur] : 0.0f;
+                wr = __fmaf_rn(u0r, -inv_theta, __fadd_rn(__fsub_rn(0.0f, urx), __fsub_rn(0.0f, X.y)));
+            }
+            const float g1 = e1 ? 0.0f : __fsub_rn(wd, wx), g2 = e2 ? 0.0f : __fsub_rn(wr, wx);
+            const float s = __fmaf_rn(g1, g1, __fmaf_rn(g2, g2, fabsf(X.w)));
+            const float rr = rcp_ax(__fmaf_rn(sqrt_ax(s), tau, 1.0f));
+            X = make_float4(__fmul_rn(__fmaf_rn(g1, tau, X.x), rr),
+                            __fmul_rn(__fmaf_rn(g2, tau, X.y), rr), vx, X.w);
+            q1[own] = X.x;
+            q2[own] = X.y;
+        }
+        sync();
+    };
+    int k = 0;
+    for (; k + 2 <= K; k += 2) {
+        pass(k, p1a, p2a, p1b, p2b);
+        pass(k + 1, p1b, p2b, p1a, p2a);
+    }
+    if (k + 1 <= K) {
+        pass(k, p1a, p2a, p1b, p2b);
+        ++k;
+    }
+    if (act) {  // pass K: u^K and v^K only (rho^K stays); k == K here, rows of parity K
+        const float *p1 = (K & 1) ? p1b : p1a, *p2 = (K & 1) ? p2b : p2a;
+        const float upx = iu >= 0 ? p1[iu] : 0.0f, lfy = il >= 0 ? p2[il] : 0.0f;
+        const float dx = __fadd_rn(__fsub_rn(X.x, upx), __fsub_rn(X.y, lfy));
+        ux = __fmaf_rn(dx, -theta, X.z);
+        X.z = K == 0 ? X.z : __saturatef(__fmaf_rn(X.w, -0x1p100f, ux));
+        a.rec[0][r] = X;
+        a.rec[1][r] = X;
+        if (K >= 1) a.u[r] = ux;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_rdc_grp2(const RdcIter a, const int32_t *slots, const int32_t *lpos, int first1, int n1, int nb1,
+           int first0, int n0) {
+    __shared__ float sm[5 * 256];
+    if ((int)blockIdx.x < nb1)
+        grp_body2<256>(a, slots, lpos, first1, n1, blockIdx.x, sm);
+    else
+        grp_body2<32>(a, slots, lpos, first0, n0, blockIdx.x - nb1, sm);
+}
+
+__global__ void __launch_bounds__(1024)
+k_rdc_grp2_big(const RdcIter a, const int32_t *slots, const int32_t *lpos, int first, int nslots) {
+    __shared__ float sm[5 * 1024];
+    grp_body2<1024>(a, slots, lpos, first, nslots, blockIdx.x, sm);
 }
 
 // one launch for the 256-thread blocks: the first nb1 CTAs run segment 1 (components of 64 ..
@@ -946,13 +1069,26 @@ cudaError_t launch_grp_fill(const int32_t *cpl, int nc, const int32_t *lab, cons
 
 cudaError_t launch_rdc_grp(const RdcIter &a, const GrpPlan &gp, const int32_t *slots,
                            const int32_t *lpos, cudaStream_t s) {
+    static const bool two_phase = [] {
+        const char *e = getenv("RDS_GRP_2PH");
+        return e ? atoi(e) != 0 : GRP_2PH_DEFAULT;
+    }();
     const int nb0 = (gp.count[0] + 255) / 256, nb1 = (gp.count[1] + 255) / 256;
-    if (nb0 + nb1 > 0)
-        k_rdc_grp<<<nb0 + nb1, 256, 0, s>>>(a, slots, lpos, gp.first[1], gp.count[1], nb1,
-                                            gp.first[0], gp.count[0]);
-    if (gp.count[2] > 0)
-        k_rdc_grp_big<<<(gp.count[2] + 1023) / 1024, 1024, 0, s>>>(a, slots, lpos, gp.first[2],
-                                                                   gp.count[2]);
+    const int nb2 = (gp.count[2] + 1023) / 1024;
+    if (nb0 + nb1 > 0) {
+        if (two_phase)
+            k_rdc_grp2<<<nb0 + nb1, 256, 0, s>>>(a, slots, lpos, gp.first[1], gp.count[1], nb1,
+                                                 gp.first[0], gp.count[0]);
+        else
+            k_rdc_grp<<<nb0 + nb1, 256, 0, s>>>(a, slots, lpos, gp.first[1], gp.count[1], nb1,
+                                                gp.first[0], gp.count[0]);
+    }
+    if (nb2 > 0) {
+        if (two_phase)
+            k_rdc_grp2_big<<<nb2, 1024, 0, s>>>(a, slots, lpos, gp.first[2], gp.count[2]);
+        else
+            k_rdc_grp_big<<<nb2, 1024, 0, s>>>(a, slots, lpos, gp.first[2], gp.count[2]);
+    }
     return cudaGetLastError();
 }
 
