@@ -725,7 +725,10 @@ k_rdc_grp2_big(const RdcIter a, const int32_t *slots, const int32_t *lpos, int f
 
 // one launch for the 256-thread blocks: the first nb1 CTAs run segment 1 (components of 64 ..
 // 256 records, CTA barrier), the rest segment 0 (eight independent warp blocks per CTA)
-__global__ void __launch_bounds__(256)
+#ifndef RDS_GRP_MINB
+#define RDS_GRP_MINB 1  // resident 256-thread CTAs per SM asked of the compiler (A/B: r02s2h)
+#endif
+__global__ void __launch_bounds__(256, RDS_GRP_MINB)
 k_rdc_grp(const RdcIter a, const int32_t *slots, const int32_t *lpos, int first1, int n1, int nb1,
           int first0, int n0) {
     __shared__ float4 sm[2][256];
