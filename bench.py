@@ -468,9 +468,10 @@ def run_ours(args, dist):
     # counts its k_rdc_iso launch)
     launches_per_step = sum(st["launches"] + 4 + 2 + (5 if st["compact"] else 0)
                             + (3 if st.get("rdc_decoupled", 0) else 0)
-                            # grouping: init, 12 label rounds, count, class, fill (st["launches"]
-                            # counts the k_rdc_grp launches)
-                            + (16 if st.get("rdc_grouped", 0) else 0) for _, st, _ in info)
+                            # grouping: init, the label rounds, count, class (+ fill when it is
+                            # kept; st["launches"] counts the k_rdc_grp launches)
+                            + ((3 + st["rdc_label_rounds"] + (1 if st["rdc_grouped"] else 0))
+                               if st.get("rdc_label_rounds", 0) else 0) for _, st, _ in info)
     line = {
         "metric": _metric(cfg), "value": value, "unit": UNIT, "n_gpus": dist.world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,

@@ -99,6 +99,8 @@ typedef struct {
     int32_t rdc_grouped;     /* compact fixed-K solves: coupled RD pixels in connected components of
                                 at most 1024 pixels, iterated inside one warp / CTA each
                                 (k_rdc_grp, RDS_OPT_RDC_SPLIT = 2); else 0 */
+    int32_t rdc_label_rounds; /* label-propagation rounds the grouping ran (k_grp_prop launches;
+                                 0 if it was not tried) */
 } rds_stats_t;
 
 /* Options (rds_set_option). */

@@ -336,12 +336,13 @@ struct GrpPlan {
     int first[3] = {};   // first slot of segment 0 (warp blocks), 1 (256), 2 (1024)
     int count[3] = {};   // slots in use per segment
     int total = 0;       // slots allocated (segments padded to multiples of 1024)
+    int rounds = 0;      // label rounds run (k_grp_prop launches)
 };
 // labels, per-label counts / flags, per-record ranks, per-root class and index; ctr: 16 ints
 // (ctr[k] = components of class k = 1 .. 10, ctr[11] = grouped records)
 cudaError_t launch_grp_label(const uint2 *code, const int32_t *cpl, int nc, int32_t *lab,
                              int32_t *cnt, int32_t *bad, int32_t *rank, int32_t *cidx,
-                             int32_t *ctr, cudaStream_t s);
+                             int32_t *ctr, int *rounds, cudaStream_t s);
 void grp_layout(const int32_t *ctr, GrpPlan *gp);
 cudaError_t launch_grp_fill(const int32_t *cpl, int nc, const int32_t *lab, const int32_t *cidx,
                             const int32_t *rank, const GrpPlan &gp, int32_t *slots,

@@ -1009,7 +1009,8 @@ cudaError_t launch_rdc_iso(const RdcIter &a, const int32_t *iso, int n_iso, int 
 
 cudaError_t launch_grp_label(const uint2 *code, const int32_t *cpl, int nc, int32_t *lab,
                              int32_t *cnt, int32_t *bad, int32_t *rank, int32_t *cidx,
-                             int32_t *ctr, cudaStream_t s) {
+                             int32_t *ctr, int *rounds, cudaStream_t s) {
+    *rounds = 0;
     if (nc <= 0) return cudaSuccess;
     int g = (nc + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
@@ -1029,6 +1030,7 @@ cudaError_t launch_grp_label(const uint2 *code, const int32_t *cpl, int nc, int3
         if (e != cudaSuccess) return e;
         e = cudaStreamSynchronize(s);
         if (e != cudaSuccess) return e;
+        *rounds += GRP_BATCH;
         if (!changed) break;
     }
     k_grp_count<<<g, 256, 0, s>>>(code, cpl, nc, lab, cnt, bad, rank);

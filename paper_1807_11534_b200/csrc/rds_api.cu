@@ -1071,8 +1071,10 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, int chec
         // its components are long runs that neither settle nor fit a CTA, and the label
         // rounds would be wasted -- C2 delta = .05: 7.6% decoupled, + 0.3 ms of setup)
         if (h->opt_split >= 2 && nc > 0 && (double)(n - nc) >= 0.15 * (double)n) {
+            int rounds = 0;
             CK(h, launch_grp_label(code, cpl, nc, g_lab, g_cnt, g_bad, g_rank, g_cidx, g_ctr,
-                                   h->stream));
+                                   &rounds, h->stream));
+            cp->gp.rounds = rounds;
             int32_t ctr[12];
             CK(h, cudaMemcpyAsync(ctr, g_ctr, sizeof ctr, cudaMemcpyDeviceToHost, h->stream));
             CK(h, cudaStreamSynchronize(h->stream));
@@ -1081,6 +1083,7 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, int chec
             // (measured at C2's connected bands: grouped + barrier 1.8 ms vs 1.2 ms)
             if (ctr[11] == nc) {
                 grp_layout(ctr, &cp->gp);
+                cp->gp.rounds = rounds;
                 CK(h, launch_grp_fill(cpl, nc, g_lab, g_cidx, g_rank, cp->gp, g_slots, g_lpos,
                                       g_fb, g_ctr, h->stream));
                 cp->slots = g_slots;
@@ -1438,6 +1441,7 @@ static int solve_impl(rds_t *h, float lambda, float theta, float tau, float delt
     st.compact = cplan.use ? 1 : 0;
     st.rdc_decoupled = cplan.use ? cplan.n_iso : 0;
     st.rdc_grouped = cplan.use ? cplan.n_grp : 0;
+    st.rdc_label_rounds = cplan.use ? cplan.gp.rounds : 0;
     if (cplan.use)
         st.launches = (cplan.it.n > 0 || !cplan.it.sel ? 1 : 0) + (cplan.n_iso > 0 ? 1 : 0) +
                       (cplan.gp.count[0] + cplan.gp.count[1] > 0) + (cplan.gp.count[2] > 0);

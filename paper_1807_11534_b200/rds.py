@@ -86,7 +86,8 @@ class rds_stats_t(ctypes.Structure):
                 ("compact", ctypes.c_int32), ("wave", ctypes.c_int32),
                 ("resident", ctypes.c_int32), ("persist", ctypes.c_int32),
                 ("rdc_decoupled", ctypes.c_int32),
-                ("rdc_grouped", ctypes.c_int32)]
+                ("rdc_grouped", ctypes.c_int32),
+                ("rdc_label_rounds", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

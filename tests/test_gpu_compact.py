@@ -239,6 +239,7 @@ def test_compact_grouped_block_sizes(rds, orc):
     assert {int(2 ** math.ceil(math.log2(max(2, x)))) for x in sizes if x > 1} >= {2, 8, 64, 256, 1024}
     assert st["rdc_decoupled"] + st["rdc_grouped"] == n_rd, (st, n_rd)
     assert st["rdc_grouped"] == int(sizes[sizes > 1].sum())
+    assert 4 <= st["rdc_label_rounds"] <= 16 and st["rdc_label_rounds"] % 4 == 0
     _same(a, c)
     o = orc.solve(f, delta, 5.0, np.float32(0.1), 0.125, K)
     assert np.array_equal(c["labels"], o["labels"])
