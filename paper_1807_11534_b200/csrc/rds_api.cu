@@ -996,11 +996,25 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, int chec
     CK(h, cudaMemcpyAsync(&act, h->counts + 0, sizeof act, cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
     if (n >= (int32_t)RDC_IDX_MASK) return RDS_OK;  // packed codes hold 26-bit indices
+    bool trial = false;  // auto mode: compact only if the grouping takes every coupled record
     if (h->opt_compact == 2) {
         int dev = 0, l2 = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-        if (!compact_pays(n, (int64_t)act * TILE_H * TILE_W, (size_t)l2)) return RDS_OK;
+        if (!compact_pays(n, (int64_t)act * TILE_H * TILE_W, (size_t)l2)) {
+            // second chance for scattered bands: if the RD density inside the active tiles
+            // predicts a band that falls apart into small components ((1 - p)^6 >= 0.3 of it
+            // decoupled, p <= 0.18) and the grouped kernels' model (0.25 us + n_rd / 4e11 /s
+            // per iteration, §6) is well under the dense one, build the compact form and keep
+            // it only if every coupled record was grouped (else back to the dense path)
+            const double apx = (double)act * TILE_H * TILE_W;
+            const double p = apx > 0.0 ? (double)n / apx : 1.0;
+            const double dense = fmax(3.0e-6, apx / 1.0e12);
+            const double grouped = 0.25e-6 + (double)n / 4.0e11;
+            trial = check_every <= 0 && h->opt_split >= 2 && n >= 4096 &&
+                    pow(1.0 - p, 6.0) >= 0.3 && grouped < 0.7 * dense;
+            if (!trial) return RDS_OK;
+        }
     }
     if (!h->rdc_idx) CK(h, cudaMalloc(&h->rdc_idx, sizeof(int32_t) * npx));
     // records x2 (float4), packed codes (uint2), list, u; the split's coupled and decoupled
@@ -1094,6 +1108,7 @@ static int compact_prepare(rds_t *h, float tau, float theta, int iters, int chec
             }
         }
     }
+    if (trial && !(it.sel && it.n == 0)) return RDS_OK;  // some records need the barrier: dense
     cp->use = true;
     return RDS_OK;
 }
