@@ -247,6 +247,31 @@ def test_compact_grouped_block_sizes(rds, orc):
         assert np.abs(c[k].astype(np.float64) - o[k]).max() <= 5e-4, k
 
 
+def test_compact_auto_second_chance(rds):
+    """Auto mode (RDS_OPT_COMPACT = 2): a scattered band the barrier kernel's cost model leaves
+    dense (C1 at delta = 0.2 max|f|, 17% RD, every tile active) is taken by the grouped compact
+    path -- every RD pixel decoupled or grouped -- with the dense path's values; with the
+    grouping off (split = 1) the same solve stays dense."""
+    cfg = wl.CONFIGS["C1"]
+    z, P = wl.make_image(cfg)
+    out = {}
+    for name, kw in (("dense", dict(compact=0)), ("auto", dict(compact=2)),
+                     ("auto_nogroup", dict(compact=2, rdc_split=1))):
+        s = rds.Solver(cfg.H, cfg.W, **kw)
+        s.set_image(z)
+        s.set_fitting(cfg.c1, cfg.c2, cfg.gamma, P)
+        s.solve(cfg.lambdas[0], cfg.theta, cfg.tau, wl.band_delta(0.2, s.absmax()), 60)
+        p1, p2 = s.p()
+        out[name] = (s.stats(), dict(u=s.u(), v=s.v(), p1=p1, p2=p2, mask=s.mask()))
+        s.close()
+    st = out["auto"][0]
+    assert out["dense"][0]["compact"] == 0 and out["auto_nogroup"][0]["compact"] == 0
+    assert st["compact"] == 1
+    assert st["rdc_decoupled"] + st["rdc_grouped"] == st["n_rd"]
+    _same(out["dense"][1], out["auto"][1])
+    _same(out["dense"][1], out["auto_nogroup"][1])
+
+
 @pytest.mark.parametrize("split", [1, 2])
 def test_compact_split_oracle(rds, orc, split):
     """The split path against the fp64 oracle at the north_star tolerances (a C3-like noise
