@@ -127,7 +127,11 @@ typedef struct {
                                 rds_solve / rds_solve_q / rds_solve_tol; 2 (default) = compact
                                 where a cost model predicts it at least 10% faster (thin
                                 scattered bands, e.g. C3 up to delta ~ 0.1 max|f|, and small
-                                images).  Same float operations per
+                                images), or -- fixed-K solves with RDS_OPT_RDC_SPLIT = 2 -- where
+                                the RD density in the active tiles is at most 0.18 and every
+                                coupled RD pixel ends up in a grouped component (the compact
+                                form is built to find out; if not, the solve runs dense).
+                                Same float operations per
                                 pixel as the dense path (results agree value for value); the
                                 solve synchronises once to size the compact arrays; tolerance
                                 solves (rds_solve_tol) evaluate the stopping rule inside the
